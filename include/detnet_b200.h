@@ -1,0 +1,159 @@
+/*
+ * detnet_b200.h -- C-ABI of the B200-native DetNet layer-stack engine.
+ *
+ * The reference (`unfold`, /root/reference/proj) has no FFI: its batch-kernel
+ * seam is the C++ API in include/unfold/kernels.hpp:29-65 plus adam_step
+ * (adam.hpp:36-37), swapped at link time. This header is that seam as plain C
+ * (pointers, sizes, status codes; no torch, no C++ types). The C++ adapter in
+ * paper_2003_09446_b200/host/unfold_b200.cpp re-exposes it as the reference's
+ * own `unfold::` functions (drop-in for src/kernels.cpp), and Python binds it
+ * with ctypes (paper_2003_09446_b200/detnet.py).
+ *
+ * Conventions
+ *  - Samples (ChannelSample, channel.hpp:11-16) are FP32 on this boundary:
+ *      H [n][n_rx][n_tx] row-major, y [n][n_rx], x [n][n_tx] as int8 +-1.
+ *  - Parameters (ModelParams/LayerParams, model.hpp:27-47) are FP64 "layer
+ *    records", one per layer, in the tests/grad_check.hpp:16-44 order:
+ *      record = W1[Z][IN] b1[Z] W2[K][Z] b2[K] W3[V][Z] b3[V] t,  IN = 3K+V.
+ *    Masks use the same layout (t slot ignored); NULL means all ones. The
+ *    effective weight is W (.) M (model.cpp:58-80).
+ *  - Gradients and Adam moments (Gradients/AdamState, backward.hpp:11-28,
+ *    adam.hpp:23-27) use the same record layout; frozen records are zero.
+ *  - Every call returns a detnet_status; on error detnet_last_error() holds
+ *    the message. The C++ adapter maps statuses back to the reference's
+ *    exception types (errors.hpp:9-31).
+ *  - A context is single-owner (not thread-safe), like unfold::Rng.
+ *  - There is no CPU fallback: without a usable sm_100 device every compute
+ *    entry point returns DETNET_ERR_CUDA.
+ */
+#ifndef DETNET_B200_H
+#define DETNET_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    DETNET_OK = 0,
+    DETNET_ERR_CONTRACT = 1, /* ContractError: shapes, arguments (matrix.hpp:34-36) */
+    DETNET_ERR_SINGULAR = 2, /* SingularMatrixError: ZF pivot test (linalg.cpp:59-60) */
+    DETNET_ERR_CONFIG = 3,   /* ConfigError: count < 1, N < K (kernels.cpp:118-120) */
+    DETNET_ERR_CUDA = 4,     /* CUDA runtime / launch failure, or no device */
+    DETNET_ERR_NCCL = 5,     /* collective failure (multi-GPU) */
+    DETNET_ERR_UNSUPPORTED = 6 /* dims outside the compiled kernel set */
+} detnet_status;
+
+typedef struct detnet_ctx detnet_ctx;
+typedef struct detnet_model detnet_model;
+
+/* ---- context ---------------------------------------------------------- */
+int detnet_ctx_create(int device, detnet_ctx **out);
+void detnet_ctx_destroy(detnet_ctx *ctx);
+const char *detnet_last_error(void);
+/* Kernel-path selection for the dense stack: 0 auto, 1 SIMT FP32, 2 tcgen05 3xTF32. */
+int detnet_ctx_set_path(detnet_ctx *ctx, int path);
+/* CUDA stream (cudaStream_t) the context launches on; NULL = its own stream. */
+int detnet_ctx_set_stream(detnet_ctx *ctx, void *stream);
+void *detnet_ctx_stream(detnet_ctx *ctx);
+
+/* Per-kernel device time, measured with CUDA events around every launch on
+ * the launching stream when profiling is on (detnet_ctx_set_profiling). */
+typedef struct {
+    double ms[8];         /* by kernel class, see DETNET_K_* */
+    long long launches[8];
+} detnet_kernel_times;
+enum { DETNET_K_GENERATE = 0, DETNET_K_PREPROCESS = 1, DETNET_K_STACK = 2, DETNET_K_REDUCE = 3,
+       DETNET_K_BACKWARD = 4, DETNET_K_ADAM = 5, DETNET_K_OTHER = 6 };
+int detnet_ctx_set_profiling(detnet_ctx *ctx, int on);
+int detnet_ctx_kernel_times(detnet_ctx *ctx, detnet_kernel_times *out, int reset);
+/* Total number of kernels this context launched (all classes). */
+long long detnet_ctx_launch_count(detnet_ctx *ctx);
+
+/* ---- parameters (ModelParams) ----------------------------------------- */
+typedef struct {
+    int n_tx, n_rx, z_dim, v_dim, depth, frozen_prefix;
+    const double *params; /* depth * record, host memory */
+    const double *masks;  /* depth * record or NULL (all ones) */
+} detnet_model_desc;
+
+long detnet_record_size(int n_tx, int z_dim, int v_dim);
+/* Upload/pack parameters once per params version (SURVEY 8b "Ownership"). */
+int detnet_model_create(detnet_ctx *ctx, const detnet_model_desc *desc, detnet_model **out);
+int detnet_model_update(detnet_model *m, const detnet_model_desc *desc);
+void detnet_model_destroy(detnet_model *m);
+/* Analytic census, flops_per_detection (compression.cpp:120-129). */
+long long detnet_model_flops_per_detection(const detnet_model *m, int include_preprocess);
+
+/* ---- batch evaluation (batch_evaluate, kernels.cpp:138-158) ------------ */
+typedef struct {
+    double data_loss;      /* mean per-sample depth-weighted loss (BatchEval) */
+    double loss_sum;       /* sum over samples, fixed tile order */
+    long long symbol_errors;
+    long long symbols;
+    long long flagged;     /* samples whose denominator guard fired */
+} detnet_eval;
+
+/* Host buffers. Copies host->device in chunks overlapped with compute.
+ * loss_layers_trainable_only: LossLayers::trainable_only (loss.hpp:16-19).
+ * xhat_out (optional, host): [n][depth][n_tx] soft outputs x_hat_1..x_hat_L
+ * (ForwardTrace::x_hat[1..L], model.hpp:52-63). */
+int detnet_batch_evaluate(detnet_model *m, long n, const float *H, const float *y,
+                          const int8_t *x, int loss_layers_trainable_only, float *xhat_out,
+                          detnet_eval *out);
+/* Same with device-resident inputs/outputs (no host copies of the samples). */
+int detnet_batch_evaluate_device(detnet_model *m, long n, const float *H_dev, const float *y_dev,
+                                 const int8_t *x_dev, int loss_layers_trainable_only,
+                                 float *xhat_dev, detnet_eval *out);
+
+/* Layers [l_begin, l_end) from a given state (host buffers): the teacher-
+ * forced single-layer check of SURVEY 7.3/H1. x_state [n][K], v_state [n][V]
+ * are read and overwritten with the state after layer l_end-1; xhat_out
+ * (optional) [n][l_end-l_begin][K]. */
+int detnet_forward_range(detnet_model *m, long n, const float *H, const float *y, int l_begin,
+                         int l_end, float *x_state, float *v_state, float *xhat_out);
+
+/* ---- training step (batch_gradient / adam_step) ------------------------ */
+typedef struct {
+    int kind;              /* 0 plain, 1 element_l1, 2 sparse_group (loss.hpp:7-14) */
+    double lambda, lambda1, lambda2;
+} detnet_loss_spec;
+
+/* batch_gradient (kernels.cpp:160-200): mean data-term gradient plus the
+ * regularizer gradient, host grads in record layout (frozen records 0). */
+int detnet_batch_gradient(detnet_model *m, long n, const float *H, const float *y,
+                          const int8_t *x, const detnet_loss_spec *spec,
+                          int loss_layers_trainable_only, double *grads_out, detnet_eval *out);
+
+typedef struct {
+    double lr0, decay_factor;
+    int decay_step;
+    double beta1, beta2, eps;
+} detnet_adam_config;
+
+/* adam_step (adam.cpp:48-79) on host arrays: params (record layout, updated
+ * in place), grads, first/second moments, *step advanced by one. */
+int detnet_adam_step(detnet_ctx *ctx, int n_tx, int z_dim, int v_dim, int depth,
+                     int frozen_prefix, double *params, const double *masks, const double *grads,
+                     double *m1, double *m2, int64_t *step, const detnet_adam_config *cfg);
+
+/* ---- on-device channel generator (make_sample/generate_batch) --------- */
+/* Rng(seed, stream_id) state (rng.cpp:18-19). */
+uint64_t detnet_rng_seed(uint64_t seed, uint64_t stream_id);
+/* Rng::stream(id) (rng.cpp:40-42); does not advance. */
+uint64_t detnet_rng_stream(uint64_t state, uint64_t id);
+/* Rng::split() (rng.cpp:44): returns the child state and advances *state. */
+uint64_t detnet_rng_split(uint64_t *state);
+/* Samples [first, first+count) of generate_batch whose split base state is
+ * `base` (kernels.cpp:121-127): sample i uses base.stream(i) and the
+ * make_sample draw order (channel.cpp:14-32). H and y are multiplied by
+ * `scale` (1/sqrt(N) for H ~ N(0,1/N)) and rounded to FP32. Device buffers. */
+int detnet_generate_device(detnet_ctx *ctx, uint64_t base, long first, long count, int n_rx,
+                           int n_tx, double snr_lo_db, double snr_hi_db, double scale,
+                           float *H_dev, float *y_dev, int8_t *x_dev, double *sigma2_dev);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

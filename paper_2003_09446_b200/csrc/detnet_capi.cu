@@ -1,0 +1,585 @@
+// detnet_capi.cu -- implementation of include/detnet_b200.h.
+//
+// Host runtime for the DetNet layer-stack engine: device context, parameter
+// packing (once per params version), workspace management, chunked
+// host<->device streaming overlapped with compute, kernel launches with
+// per-launch CUDA-event timing, and status/error mapping. No CPU fallback:
+// every compute entry point requires an sm_100 device.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/detnet_b200.h"
+#include "common.cuh"
+#include "k_generate.cuh"
+#include "k_preprocess.cuh"
+#include "k_stack_simt.cuh"
+#include "engine.hpp"
+
+using namespace detnet;
+
+namespace detnet {
+
+// ---- dims dispatch --------------------------------------------------------
+using PreFn = void (*)(dim3, dim3, size_t, cudaStream_t, long, int, const float *, const float *,
+                       const int8_t *, float *, float *, double *, uint32_t *, uint8_t *,
+                       unsigned long long *);
+using SimtFn = void (*)(dim3, dim3, size_t, cudaStream_t, const StackArgs &);
+
+template <int K>
+void launch_pre(dim3 g, dim3 b, size_t sm, cudaStream_t st, long n, int N, const float *H,
+                const float *y, const int8_t *x, float *gp, float *q32, double *dn, uint32_t *xm,
+                uint8_t *fl, unsigned long long *sing) {
+    k_preprocess<K><<<g, b, sm, st>>>(n, N, H, y, x, gp, q32, dn, xm, fl, sing);
+}
+
+template <int K, int Z, int V>
+void launch_simt(dim3 g, dim3 b, size_t sm, cudaStream_t st, const StackArgs &a) {
+    k_stack_simt<K, Z, V><<<g, b, sm, st>>>(a);
+}
+
+template <int K, int Z, int V> int set_simt_smem() {
+    const int bytes = static_cast<int>(2 * simt_rec(K, Z, V) * 4 + 64);
+    return cudaFuncSetAttribute(k_stack_simt<K, Z, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                bytes) == cudaSuccess
+               ? 0
+               : -1;
+}
+
+struct DimsEntry {
+    int K, Z, V;
+    PreFn pre;
+    SimtFn simt;
+    int (*prep)();
+};
+
+#define DETNET_DIMS(K, Z, V) {K, Z, V, launch_pre<K>, launch_simt<K, Z, V>, set_simt_smem<K, Z, V>}
+const DimsEntry kDims[] = {
+    DETNET_DIMS(20, 160, 40), DETNET_DIMS(2, 16, 4),  DETNET_DIMS(3, 24, 6),
+    DETNET_DIMS(4, 32, 8),    DETNET_DIMS(6, 48, 12), DETNET_DIMS(8, 64, 16),
+};
+#undef DETNET_DIMS
+
+static const DimsEntry *find_dims(int K, int Z, int V) {
+    for (const DimsEntry &d : kDims)
+        if (d.K == K && d.Z == Z && d.V == V) return &d;
+    return nullptr;
+}
+
+} // namespace detnet
+
+namespace {
+
+int pack_simt(detnet_model *m, const double *params, const double *masks, std::vector<float> &out) {
+    const int K = m->K, Z = m->Z, V = m->V, IN = 3 * K + V;
+    const int IN4 = simt_in4(K, V), O4 = simt_o4(K, V);
+    const long P = record_size(K, Z, V);
+    const long R = simt_rec(K, Z, V);
+    out.assign(static_cast<size_t>(R) * m->L, 0.f);
+    for (int l = 0; l < m->L; ++l) {
+        const double *p = params + l * P;
+        const double *mk = masks ? masks + l * P : nullptr;
+        auto w = [&](long off) { return p[off] * (mk ? mk[off] : 1.0); };
+        float *r = out.data() + static_cast<size_t>(l) * R;
+        const long oW1 = 0, ob1 = oW1 + static_cast<long>(Z) * IN, oW2 = ob1 + Z,
+                   ob2 = oW2 + static_cast<long>(K) * Z, oW3 = ob2 + K,
+                   ob3 = oW3 + static_cast<long>(V) * Z, ot = ob3 + V;
+        for (int i = 0; i < Z; ++i) {
+            for (int j = 0; j < IN; ++j) r[i * IN4 + j] = static_cast<float>(w(oW1 + i * IN + j));
+            r[i * IN4 + IN] = static_cast<float>(w(ob1 + i));
+        }
+        float *w23 = r + static_cast<long>(Z) * IN4;
+        for (int i = 0; i < Z; ++i) {
+            for (int k = 0; k < K; ++k) w23[i * O4 + k] = static_cast<float>(w(oW2 + k * Z + i));
+            for (int k = 0; k < V; ++k) w23[i * O4 + K + k] = static_cast<float>(w(oW3 + k * Z + i));
+        }
+        float *b23 = w23 + static_cast<long>(Z) * O4;
+        for (int k = 0; k < K; ++k) b23[k] = static_cast<float>(w(ob2 + k));
+        for (int k = 0; k < V; ++k) b23[K + k] = static_cast<float>(w(ob3 + k));
+        b23[O4] = static_cast<float>(p[ot]);
+        if (!(p[ot] > 0.0)) return fail(DETNET_ERR_CONTRACT, "soft_sign: t must be > 0 (layer %d)", l);
+    }
+    return 0;
+}
+
+int upload_model(detnet_model *m, const detnet_model_desc *d) {
+    const long P = record_size(m->K, m->Z, m->V);
+    m->params_host.assign(d->params, d->params + P * m->L);
+    m->has_masks = d->masks != nullptr;
+    if (d->masks) m->masks_host.assign(d->masks, d->masks + P * m->L);
+    else m->masks_host.clear();
+    std::vector<float> packed;
+    if (int rc = pack_simt(m, d->params, d->masks, packed)) return rc;
+    m->simt_rec = simt_rec(m->K, m->Z, m->V);
+    if (m->simt.ensure(packed.size() * 4)) return fail(DETNET_ERR_CUDA, "cudaMalloc weights");
+    CK(cudaMemcpy(m->simt.p, packed.data(), packed.size() * 4, cudaMemcpyHostToDevice));
+    std::vector<double> la(m->L), lt(m->L);
+    for (int l = 0; l < m->L; ++l) {
+        la[l] = std::log(static_cast<double>(l + 1));
+        lt[l] = (l + 1 >= m->frozen + 1) ? la[l] : 0.0;
+    }
+    if (m->lnk_all.ensure(m->L * 8) || m->lnk_train.ensure(m->L * 8))
+        return fail(DETNET_ERR_CUDA, "cudaMalloc lnk");
+    CK(cudaMemcpy(m->lnk_all.p, la.data(), m->L * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(m->lnk_train.p, lt.data(), m->L * 8, cudaMemcpyHostToDevice));
+    if (int rc = tc_pack(m->tc, m->K, m->Z, m->V, m->L, d->params, d->masks)) return rc;
+    return 0;
+}
+
+// Workspace for n samples (all global per-sample/per-tile arrays).
+int ensure_ws(detnet_ctx *c, long n, int K) {
+    const long tiles = (n + TILE - 1) / TILE;
+    const long np = tiles * TILE;
+    const int NG = gram_entries(K);
+    if (c->gp.ensure(sizeof(float) * NG * np) || c->q32.ensure(sizeof(float) * K * np) ||
+        c->denom.ensure(sizeof(double) * np) || c->xmask.ensure(sizeof(uint32_t) * np) ||
+        c->flag.ensure(np) || c->tile_loss.ensure(sizeof(double) * tiles) ||
+        c->tile_err.ensure(sizeof(long long) * tiles) || c->sing.ensure(8) ||
+        c->result.ensure(64))
+        return fail(DETNET_ERR_CUDA, "workspace allocation failed (n=%ld)", n);
+    if (!c->h_result) CK(cudaMallocHost(&c->h_result, 64));
+    return 0;
+}
+
+bool use_tc(const detnet_model *m) {
+    const int path = m->ctx->path;
+    if (path == 1) return false;
+    if (!m->tc.ready) return false;
+    return true;
+}
+
+// K1 (+pad) over samples [s0, s0+cnt) of the global arrays.
+int run_pre(detnet_model *m, cudaStream_t st, long s0, long cnt, long n_total, const float *H,
+            const float *y, const int8_t *x) {
+    detnet_ctx *c = m->ctx;
+    const int K = m->K, NG = gram_entries(K);
+    const long t0 = s0 / TILE;
+    const size_t smem = static_cast<size_t>(8) *
+                        (round_up(m->N * K + m->N, 2) + 2 * K * K) * sizeof(float);
+    const int blocks = static_cast<int>(std::min<long>((cnt + 7) / 8, 148L * 16));
+    {
+        LaunchScope ls(c, DETNET_K_PREPROCESS, st);
+        m->dims->pre(dim3(blocks), dim3(256), smem, st, cnt, m->N, H, y, x,
+                     c->gp.as<float>() + t0 * NG * TILE, c->q32.as<float>() + t0 * K * TILE,
+                     c->denom.as<double>() + s0, c->xmask.as<uint32_t>() + s0,
+                     c->flag.as<uint8_t>() + s0, c->sing.as<unsigned long long>());
+    }
+    if (int rc = check_launch()) return rc;
+    const long end = s0 + cnt;
+    if (end == n_total) {
+        const long np = (n_total + TILE - 1) / TILE * TILE;
+        if (np > n_total) {
+            LaunchScope ls(c, DETNET_K_OTHER, st);
+            k_pad_tail<<<1, TILE, 0, st>>>(n_total, np, K, c->gp.as<float>(), c->q32.as<float>(),
+                                           c->denom.as<double>(), c->xmask.as<uint32_t>(),
+                                           c->flag.as<uint8_t>());
+            if (int rc = check_launch()) return rc;
+        }
+    }
+    return 0;
+}
+
+// K2 over tiles [t0, t0+nt) (samples relative to s_base = t0*TILE).
+int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, int l_begin,
+              int l_end, bool trainable_only, float *xhat, float *xs, float *vs) {
+    detnet_ctx *c = m->ctx;
+    if (use_tc(m) && !xs) {
+        TcArgs ta{};
+        ta.gp = c->gp.as<float>();
+        ta.q32 = c->q32.as<float>();
+        ta.denom = c->denom.as<double>();
+        ta.xmask = c->xmask.as<uint32_t>();
+        ta.lnk = (trainable_only ? m->lnk_train : m->lnk_all).as<double>();
+        ta.l_begin = l_begin;
+        ta.l_end = l_end;
+        ta.n = n_local;
+        ta.n_tiles = nt;
+        ta.tile0 = t0;
+        ta.xhat = xhat;
+        ta.tile_loss = c->tile_loss.as<double>();
+        ta.tile_err = c->tile_err.as<long long>();
+        LaunchScope ls(c, DETNET_K_STACK, st);
+        if (int rc = tc_launch(m->tc, ta, st)) return rc;
+        return check_launch();
+    }
+    StackArgs a{};
+    a.gp = c->gp.as<float>();
+    a.q32 = c->q32.as<float>();
+    a.denom = c->denom.as<double>();
+    a.xmask = c->xmask.as<uint32_t>();
+    a.wrec = m->simt.as<float>();
+    a.rec_floats = m->simt_rec;
+    a.lnk = (trainable_only ? m->lnk_train : m->lnk_all).as<double>();
+    a.l_begin = l_begin;
+    a.l_end = l_end;
+    a.n = n_local;
+    a.n_tiles = nt;
+    a.tile0 = t0;
+    a.xhat = xhat;
+    a.x_state = xs;
+    a.v_state = vs;
+    a.tile_loss = c->tile_loss.as<double>();
+    a.tile_err = c->tile_err.as<long long>();
+    const size_t smem = 2 * static_cast<size_t>(m->simt_rec) * 4 + 64;
+    const int blocks = static_cast<int>((nt + 1) / 2);
+    {
+        LaunchScope ls(c, DETNET_K_STACK, st);
+        m->dims->simt(dim3(blocks), dim3(256), smem, st, a);
+    }
+    return check_launch();
+}
+
+int finish(detnet_model *m, long n, detnet_eval *out) {
+    detnet_ctx *c = m->ctx;
+    const long tiles = (n + TILE - 1) / TILE;
+    double *res = c->result.as<double>();
+    {
+        LaunchScope ls(c, DETNET_K_REDUCE, c->stream);
+        k_reduce<<<1, 1024, 0, c->stream>>>(c->tile_loss.as<double>(), c->tile_err.as<long long>(),
+                                           tiles, c->flag.as<uint8_t>(), n, res,
+                                           reinterpret_cast<long long *>(res + 1),
+                                           reinterpret_cast<long long *>(res + 2));
+    }
+    if (int rc = check_launch()) return rc;
+    CK(cudaMemcpyAsync(res + 3, c->sing.p, 8, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->h_result, res, 32, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    drain_times(c);
+    unsigned long long sing;
+    std::memcpy(&sing, c->h_result + 3, 8);
+    if (sing != ~0ull)
+        return fail(DETNET_ERR_SINGULAR,
+                    "solve_normal_equations: matrix is singular to working precision (sample %llu)",
+                    sing);
+    long long e, f;
+    std::memcpy(&e, c->h_result + 1, 8);
+    std::memcpy(&f, c->h_result + 2, 8);
+    out->loss_sum = c->h_result[0];
+    out->data_loss = n ? c->h_result[0] / static_cast<double>(n) : 0.0;
+    out->symbol_errors = e;
+    out->symbols = n * static_cast<long long>(m->K);
+    out->flagged = f;
+    return 0;
+}
+
+int reset_sing(detnet_ctx *c, cudaStream_t st) {
+    CK(cudaMemsetAsync(c->sing.p, 0xff, 8, st));
+    return 0;
+}
+
+} // namespace
+
+// =========================================================================
+extern "C" {
+
+const char *detnet_last_error(void) { return g_err.c_str(); }
+
+long detnet_record_size(int n_tx, int z_dim, int v_dim) { return record_size(n_tx, z_dim, v_dim); }
+
+int detnet_ctx_create(int device, detnet_ctx **out) {
+    if (!out) return fail(DETNET_ERR_CONTRACT, "detnet_ctx_create: null out");
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+        return fail(DETNET_ERR_CUDA, "no CUDA device available (the engine has no CPU fallback)");
+    if (device < 0 || device >= count) return fail(DETNET_ERR_CONTRACT, "bad device %d", device);
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return fail(DETNET_ERR_CUDA, "device %d is sm_%d%d; this build targets sm_100a", device,
+                    prop.major, prop.minor);
+    CK(cudaSetDevice(device));
+    auto *c = new detnet_ctx();
+    c->device = device;
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+        CK(cudaEventCreateWithFlags(&c->chunk_done[i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->copy_done[i], cudaEventDisableTiming));
+    }
+    for (const DimsEntry &d : kDims)
+        if (d.prep()) return fail(DETNET_ERR_CUDA, "cudaFuncSetAttribute (smem) failed");
+    if (int rc = tc_prepare()) return rc;
+    *out = c;
+    return 0;
+}
+
+void detnet_ctx_destroy(detnet_ctx *c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    drain_times(c);
+    for (DBuf *b : {&c->gp, &c->q32, &c->denom, &c->xmask, &c->flag, &c->tile_loss, &c->tile_err,
+                    &c->sing, &c->result, &c->xhat_dev, &c->state_x, &c->state_v})
+        b->release();
+    for (int i = 0; i < 2; ++i) {
+        c->in_H[i].release(); c->in_y[i].release(); c->in_x[i].release();
+        cudaEventDestroy(c->chunk_done[i]);
+        cudaEventDestroy(c->copy_done[i]);
+    }
+    for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
+    if (c->h_result) cudaFreeHost(c->h_result);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    cudaStreamDestroy(c->copy_stream);
+    delete c;
+}
+
+int detnet_ctx_set_path(detnet_ctx *c, int path) {
+    if (!c || path < 0 || path > 2) return fail(DETNET_ERR_CONTRACT, "bad path");
+    c->path = path;
+    return 0;
+}
+
+int detnet_ctx_set_stream(detnet_ctx *c, void *stream) {
+    if (!c) return fail(DETNET_ERR_CONTRACT, "null ctx");
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    if (stream) { c->stream = static_cast<cudaStream_t>(stream); c->own_stream = false; }
+    else { CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)); c->own_stream = true; }
+    return 0;
+}
+
+void *detnet_ctx_stream(detnet_ctx *c) { return c ? c->stream : nullptr; }
+
+int detnet_ctx_set_profiling(detnet_ctx *c, int on) {
+    if (!c) return fail(DETNET_ERR_CONTRACT, "null ctx");
+    c->profiling = on != 0;
+    return 0;
+}
+
+int detnet_ctx_kernel_times(detnet_ctx *c, detnet_kernel_times *out, int reset) {
+    if (!c || !out) return fail(DETNET_ERR_CONTRACT, "null argument");
+    drain_times(c);
+    *out = c->times;
+    if (reset) c->times = detnet_kernel_times{};
+    return 0;
+}
+
+long long detnet_ctx_launch_count(detnet_ctx *c) { return c ? c->launches : 0; }
+
+int detnet_model_create(detnet_ctx *c, const detnet_model_desc *d, detnet_model **out) {
+    if (!c || !d || !out || !d->params) return fail(DETNET_ERR_CONTRACT, "null argument");
+    if (d->n_tx < 1 || d->n_rx < d->n_tx)
+        return fail(DETNET_ERR_CONFIG, "need N >= K >= 1 for a full-rank channel");
+    if (d->depth < 1 || d->frozen_prefix < 0 || d->frozen_prefix > d->depth)
+        return fail(DETNET_ERR_CONTRACT, "bad depth/frozen_prefix");
+    const DimsEntry *de = find_dims(d->n_tx, d->z_dim, d->v_dim);
+    if (!de)
+        return fail(DETNET_ERR_UNSUPPORTED, "dims K=%d z=%d v=%d are not in the compiled kernel set",
+                    d->n_tx, d->z_dim, d->v_dim);
+    CK(cudaSetDevice(c->device));
+    auto *m = new detnet_model();
+    m->ctx = c;
+    m->K = d->n_tx; m->N = d->n_rx; m->Z = d->z_dim; m->V = d->v_dim;
+    m->L = d->depth; m->frozen = d->frozen_prefix; m->dims = de;
+    if (int rc = upload_model(m, d)) { detnet_model_destroy(m); return rc; }
+    *out = m;
+    return 0;
+}
+
+int detnet_model_update(detnet_model *m, const detnet_model_desc *d) {
+    if (!m || !d) return fail(DETNET_ERR_CONTRACT, "null argument");
+    if (d->n_tx != m->K || d->z_dim != m->Z || d->v_dim != m->V || d->n_rx != m->N)
+        return fail(DETNET_ERR_CONTRACT, "model_update: dims changed");
+    if (d->depth != m->L) {
+        m->L = d->depth;
+        m->simt.release();
+        m->lnk_all.release();
+        m->lnk_train.release();
+    }
+    m->frozen = d->frozen_prefix;
+    return upload_model(m, d);
+}
+
+void detnet_model_destroy(detnet_model *m) {
+    if (!m) return;
+    m->simt.release();
+    m->lnk_all.release();
+    m->lnk_train.release();
+    tc_release(m->tc);
+    delete m;
+}
+
+long long detnet_model_flops_per_detection(const detnet_model *m, int include_pre) {
+    if (!m) return -1;
+    const long long k = m->K, n = m->N;
+    const long P = record_size(m->K, m->Z, m->V);
+    const long IN = 3L * m->K + m->V;
+    const long spans[3][2] = {{0, m->Z * IN},
+                              {m->Z * IN + m->Z, static_cast<long>(m->K) * m->Z},
+                              {m->Z * IN + m->Z + static_cast<long>(m->K) * m->Z + m->K,
+                               static_cast<long>(m->V) * m->Z}};
+    long long flops = 0;
+    for (int l = 0; l < m->L; ++l) {
+        long long nnz = 0;
+        for (auto &sp : spans) {
+            if (!m->has_masks) { nnz += sp[1]; continue; }
+            const double *mk = m->masks_host.data() + l * P + sp[0];
+            for (long i = 0; i < sp[1]; ++i) nnz += mk[i] != 0.0;
+        }
+        flops += 2 * nnz + 2 * k * k;
+    }
+    if (include_pre) flops += 2 * n * k + 2 * n * k * k;
+    return flops;
+}
+
+int detnet_batch_evaluate_device(detnet_model *m, long n, const float *H, const float *y,
+                                 const int8_t *x, int trainable_only, float *xhat,
+                                 detnet_eval *out) {
+    if (!m || !out || (n > 0 && (!H || !y || !x)))
+        return fail(DETNET_ERR_CONTRACT, "null argument");
+    detnet_ctx *c = m->ctx;
+    *out = detnet_eval{};
+    if (n <= 0) return 0; // finish_eval of an empty batch (kernels.cpp:93-103)
+    CK(cudaSetDevice(c->device));
+    if (int rc = ensure_ws(c, n, m->K)) return rc;
+    if (int rc = reset_sing(c, c->stream)) return rc;
+    if (int rc = run_pre(m, c->stream, 0, n, n, H, y, x)) return rc;
+    const long tiles = (n + TILE - 1) / TILE;
+    if (int rc = run_stack(m, c->stream, 0, tiles, n, 0, m->L, trainable_only != 0, xhat, nullptr,
+                           nullptr))
+        return rc;
+    return finish(m, n, out);
+}
+
+int detnet_batch_evaluate(detnet_model *m, long n, const float *H, const float *y,
+                          const int8_t *x, int trainable_only, float *xhat_out,
+                          detnet_eval *out) {
+    if (!m || !out || (n > 0 && (!H || !y || !x)))
+        return fail(DETNET_ERR_CONTRACT, "null argument");
+    detnet_ctx *c = m->ctx;
+    *out = detnet_eval{};
+    if (n <= 0) return 0;
+    CK(cudaSetDevice(c->device));
+    const int K = m->K, N = m->N, L = m->L;
+    if (int rc = ensure_ws(c, n, K)) return rc;
+    if (int rc = reset_sing(c, c->stream)) return rc;
+    // Chunked streaming: copy chunk i+1 on copy_stream while chunk i computes.
+    const long chunk = 1L << 17; // samples, multiple of TILE
+    for (int b = 0; b < 2; ++b) {
+        const long cs = std::min(chunk, n);
+        if (c->in_H[b].ensure(sizeof(float) * cs * N * K) || c->in_y[b].ensure(sizeof(float) * cs * N) ||
+            c->in_x[b].ensure(static_cast<size_t>(cs) * K))
+            return fail(DETNET_ERR_CUDA, "input staging allocation failed");
+    }
+    if (xhat_out && c->xhat_dev.ensure(sizeof(float) * std::min(chunk, n) * L * K))
+        return fail(DETNET_ERR_CUDA, "xhat staging allocation failed");
+    const long nchunks = (n + chunk - 1) / chunk;
+    for (long ci = 0; ci < nchunks; ++ci) {
+        const int b = static_cast<int>(ci & 1);
+        const long s0 = ci * chunk, cnt = std::min(chunk, n - s0);
+        if (ci >= 2) CK(cudaStreamWaitEvent(c->copy_stream, c->chunk_done[b], 0));
+        CK(cudaMemcpyAsync(c->in_H[b].p, H + s0 * N * K, sizeof(float) * cnt * N * K,
+                           cudaMemcpyHostToDevice, c->copy_stream));
+        CK(cudaMemcpyAsync(c->in_y[b].p, y + s0 * N, sizeof(float) * cnt * N,
+                           cudaMemcpyHostToDevice, c->copy_stream));
+        CK(cudaMemcpyAsync(c->in_x[b].p, x + s0 * K, static_cast<size_t>(cnt) * K,
+                           cudaMemcpyHostToDevice, c->copy_stream));
+        CK(cudaEventRecord(c->copy_done[b], c->copy_stream));
+        CK(cudaStreamWaitEvent(c->stream, c->copy_done[b], 0));
+        if (int rc = run_pre(m, c->stream, s0, cnt, n, c->in_H[b].as<float>(), c->in_y[b].as<float>(),
+                             c->in_x[b].as<int8_t>()))
+            return rc;
+        const long t0 = s0 / TILE, nt = (cnt + TILE - 1) / TILE;
+        if (int rc = run_stack(m, c->stream, t0, nt, cnt, 0, L, trainable_only != 0,
+                               xhat_out ? c->xhat_dev.as<float>() : nullptr, nullptr, nullptr))
+            return rc;
+        if (xhat_out) {
+            CK(cudaMemcpyAsync(xhat_out + s0 * L * K, c->xhat_dev.p, sizeof(float) * cnt * L * K,
+                               cudaMemcpyDeviceToHost, c->stream));
+        }
+        CK(cudaEventRecord(c->chunk_done[b], c->stream));
+    }
+    return finish(m, n, out);
+}
+
+int detnet_forward_range(detnet_model *m, long n, const float *H, const float *y, int l_begin,
+                         int l_end, float *x_state, float *v_state, float *xhat_out) {
+    if (!m || !H || !y || !x_state || !v_state) return fail(DETNET_ERR_CONTRACT, "null argument");
+    if (l_begin < 0 || l_end > m->L || l_begin >= l_end)
+        return fail(DETNET_ERR_CONTRACT, "bad layer range [%d,%d)", l_begin, l_end);
+    if (n <= 0) return 0;
+    detnet_ctx *c = m->ctx;
+    CK(cudaSetDevice(c->device));
+    const int K = m->K, N = m->N, V = m->V, nl = l_end - l_begin;
+    if (int rc = ensure_ws(c, n, K)) return rc;
+    if (c->in_H[0].ensure(sizeof(float) * n * N * K) || c->in_y[0].ensure(sizeof(float) * n * N) ||
+        c->in_x[0].ensure(static_cast<size_t>(n) * K) || c->state_x.ensure(sizeof(float) * n * K) ||
+        c->state_v.ensure(sizeof(float) * n * V) ||
+        (xhat_out && c->xhat_dev.ensure(sizeof(float) * n * nl * K)))
+        return fail(DETNET_ERR_CUDA, "allocation failed");
+    CK(cudaMemcpyAsync(c->in_H[0].p, H, sizeof(float) * n * N * K, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->in_y[0].p, y, sizeof(float) * n * N, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(c->in_x[0].p, 1, static_cast<size_t>(n) * K, c->stream));
+    CK(cudaMemcpyAsync(c->state_x.p, x_state, sizeof(float) * n * K, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->state_v.p, v_state, sizeof(float) * n * V, cudaMemcpyHostToDevice, c->stream));
+    if (int rc = reset_sing(c, c->stream)) return rc;
+    if (int rc = run_pre(m, c->stream, 0, n, n, c->in_H[0].as<float>(), c->in_y[0].as<float>(),
+                         c->in_x[0].as<int8_t>()))
+        return rc;
+    const long tiles = (n + TILE - 1) / TILE;
+    if (int rc = run_stack(m, c->stream, 0, tiles, n, l_begin, l_end, false,
+                           xhat_out ? c->xhat_dev.as<float>() : nullptr, c->state_x.as<float>(),
+                           c->state_v.as<float>()))
+        return rc;
+    CK(cudaMemcpyAsync(x_state, c->state_x.p, sizeof(float) * n * K, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(v_state, c->state_v.p, sizeof(float) * n * V, cudaMemcpyDeviceToHost, c->stream));
+    if (xhat_out)
+        CK(cudaMemcpyAsync(xhat_out, c->xhat_dev.p, sizeof(float) * n * nl * K,
+                           cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    drain_times(c);
+    return 0;
+}
+
+// ---- rng helpers (host) ----------------------------------------------------
+uint64_t detnet_rng_seed(uint64_t seed, uint64_t stream_id) {
+    return mix64(mix64(seed ^ 0x853c49e6748fea9bULL) + stream_id);
+}
+uint64_t detnet_rng_stream(uint64_t state, uint64_t id) {
+    return mix64(state ^ mix64(id + 0xda3e39cb94b95bdbULL));
+}
+uint64_t detnet_rng_split(uint64_t *state) {
+    *state += kGamma;
+    return mix64(mix64(*state));
+}
+
+int detnet_generate_device(detnet_ctx *c, uint64_t base, long first, long count, int n_rx,
+                           int n_tx, double lo, double hi, double scale, float *H, float *y,
+                           int8_t *x, double *sigma2) {
+    if (!c || !H || !y || !x) return fail(DETNET_ERR_CONTRACT, "null argument");
+    if (count < 1) return fail(DETNET_ERR_CONFIG, "generate_batch: batch size must be >= 1");
+    if (n_rx < n_tx || n_tx < 1 || n_tx > 32)
+        return fail(DETNET_ERR_CONFIG, "generate_batch: need N >= K >= 1 (K <= 32)");
+    CK(cudaSetDevice(c->device));
+    const int blocks = static_cast<int>((count + 127) / 128);
+    {
+        LaunchScope ls(c, DETNET_K_GENERATE, c->stream);
+        k_generate<<<blocks, 128, 0, c->stream>>>(base, first, count, n_rx, n_tx, lo, hi, scale, H, y,
+                                                  x, sigma2);
+    }
+    if (int rc = check_launch()) return rc;
+    CK(cudaStreamSynchronize(c->stream));
+    drain_times(c);
+    return 0;
+}
+
+// ---- training ----------------------------------------------------------------
+int detnet_batch_gradient(detnet_model *m, long n, const float *H, const float *y,
+                          const int8_t *x, const detnet_loss_spec *spec, int trainable_only,
+                          double *grads_out, detnet_eval *out) {
+    return train_batch_gradient(m, n, H, y, x, spec, trainable_only, grads_out, out);
+}
+
+int detnet_adam_step(detnet_ctx *c, int n_tx, int z_dim, int v_dim, int depth, int frozen_prefix,
+                     double *params, const double *masks, const double *grads, double *m1,
+                     double *m2, int64_t *step, const detnet_adam_config *cfg) {
+    return train_adam_step(c, n_tx, z_dim, v_dim, depth, frozen_prefix, params, masks, grads, m1,
+                           m2, step, cfg);
+}
+
+} // extern "C"

@@ -1,0 +1,199 @@
+// engine.hpp -- internal host-side state shared by the engine's translation
+// units (not part of the C-ABI; see include/detnet_b200.h).
+#pragma once
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/detnet_b200.h"
+#include "common.cuh"
+
+
+namespace detnet {
+
+inline thread_local std::string g_err;
+
+inline int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(DETNET_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                                  \
+    } while (0)
+
+inline long record_size(int K, int Z, int V) {
+    const long IN = 3L * K + V;
+    return Z * IN + Z + static_cast<long>(K) * Z + K + static_cast<long>(V) * Z + V + 1;
+}
+
+// device buffer that only grows
+struct DBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    int ensure(size_t bytes) {
+        if (bytes <= cap) return 0;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        if (cudaMalloc(&p, bytes) != cudaSuccess) return -1;
+        cap = bytes;
+        return 0;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <typename T> T *as() const { return static_cast<T *>(p); }
+};
+
+struct DimsEntry;
+
+// tcgen05 path (stack_tc.cu): packed weights and launch arguments.
+struct TcModel {
+    bool ready = false;
+    int K = 0, Z = 0, V = 0, L = 0;
+    DBuf w;             // [L][rec bytes] pre-laid-out smem images
+    long rec_bytes = 0;
+};
+
+struct TcArgs {
+    const float *gp;
+    const float *q32;
+    const double *denom;
+    const uint32_t *xmask;
+    const double *lnk;
+    int l_begin, l_end;
+    long n, n_tiles, tile0;
+    float *xhat;
+    double *tile_loss;
+    long long *tile_err;
+};
+
+int tc_prepare();
+int tc_pack(TcModel &tc, int K, int Z, int V, int L, const double *params, const double *masks);
+int tc_launch(const TcModel &tc, const TcArgs &a, cudaStream_t st);
+void tc_release(TcModel &tc);
+
+// training (train.cu)
+int train_batch_gradient(detnet_model *m, long n, const float *H, const float *y,
+                         const int8_t *x, const detnet_loss_spec *spec, int trainable_only,
+                         double *grads_out, detnet_eval *out);
+int train_adam_step(detnet_ctx *c, int n_tx, int z_dim, int v_dim, int depth, int frozen_prefix,
+                    double *params, const double *masks, const double *grads, double *m1,
+                    double *m2, int64_t *step, const detnet_adam_config *cfg);
+
+} // namespace detnet
+
+struct detnet_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = true;
+    cudaStream_t copy_stream = nullptr;
+    int path = 0;
+    bool profiling = false;
+    long long launches = 0;
+    detnet_kernel_times times{};
+    struct Pending {
+        int cls;
+        cudaEvent_t a, b;
+    };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> event_pool;
+    // workspace
+    detnet::DBuf gp, q32, denom, xmask, flag, tile_loss, tile_err, sing, result;
+    detnet::DBuf in_H[2], in_y[2], in_x[2], xhat_dev, state_x, state_v;
+    double *h_result = nullptr; // pinned: loss, err, flag, singular
+    cudaEvent_t chunk_done[2] = {nullptr, nullptr};
+    cudaEvent_t copy_done[2] = {nullptr, nullptr};
+};
+
+struct detnet_model {
+    detnet_ctx *ctx = nullptr;
+    int K = 0, N = 0, Z = 0, V = 0, L = 0, frozen = 0;
+    const detnet::DimsEntry *dims = nullptr;
+    detnet::DBuf simt;          // [L][simt_rec]
+    long simt_rec = 0;
+    detnet::DBuf lnk_all, lnk_train;
+    std::vector<double> masks_nnz; // per layer nnz of W masks (census)
+    std::vector<double> params_host, masks_host;
+    bool has_masks = false;
+    detnet::TcModel tc; // tcgen05 path packing (stack_tc.cu)
+};
+
+namespace detnet {
+inline cudaEvent_t take_event(detnet_ctx *c) {
+    if (!c->event_pool.empty()) {
+        cudaEvent_t e = c->event_pool.back();
+        c->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Bracket a launch with events on the launching stream when profiling.
+struct LaunchScope {
+    detnet_ctx *c;
+    int cls;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr;
+    LaunchScope(detnet_ctx *c_, int cls_, cudaStream_t st_) : c(c_), cls(cls_), st(st_) {
+        c->launches++;
+        c->times.launches[cls]++;
+        if (c->profiling) {
+            a = take_event(c);
+            cudaEventRecord(a, st);
+        }
+    }
+    ~LaunchScope() {
+        if (c->profiling) {
+            cudaEvent_t b = take_event(c);
+            cudaEventRecord(b, st);
+            c->pending.push_back({cls, a, b});
+        }
+    }
+};
+
+inline void drain_times(detnet_ctx *c) {
+    for (auto &p : c->pending) {
+        float ms = 0.f;
+        cudaEventSynchronize(p.b);
+        cudaEventElapsedTime(&ms, p.a, p.b);
+        c->times.ms[p.cls] += ms;
+        c->event_pool.push_back(p.a);
+        c->event_pool.push_back(p.b);
+    }
+    c->pending.clear();
+}
+
+inline int check_launch() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(DETNET_ERR_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+    return 0;
+}
+
+// training (train.cu)
+int train_batch_gradient(detnet_model *m, long n, const float *H, const float *y,
+                         const int8_t *x, const detnet_loss_spec *spec, int trainable_only,
+                         double *grads_out, detnet_eval *out);
+int train_adam_step(detnet_ctx *c, int n_tx, int z_dim, int v_dim, int depth, int frozen_prefix,
+                    double *params, const double *masks, const double *grads, double *m1,
+                    double *m2, int64_t *step, const detnet_adam_config *cfg);
+
+} // namespace detnet

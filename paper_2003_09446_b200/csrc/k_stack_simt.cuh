@@ -1,0 +1,245 @@
+// k_stack_simt.cuh -- K2-SIMT: the fused DetNet layer stack on FP32 CUDA
+// cores, one thread per sample, all L layers in one launch.
+//
+// Restates forward_pre (model.cpp:84-122) + loss_plain (loss.cpp:9-31) + the
+// hard-decision error count (kernels.cpp:63-65). Per layer and sample:
+//   gx = G x_hat                      (G packed, FP32 from K1, read via L2)
+//   u1 = W1 [q; x_hat; gx; v] + b1    (bias folded as input column IN)
+//   z  = relu(u1);  [u2; v'] = [W2; W3] z + [b2; b3]
+//   x_hat' = psi_t(u2)                (model.cpp:32-41)
+//   loss += ln(l+1) * ||x - x_hat'||^2 / denom   (FP64)
+// Each layer's weights (W (.) M, FP32, ~105 KB at K=20) are staged into
+// shared memory by the bulk-copy engine (cp.async.bulk + mbarrier), double
+// buffered so layer l+1 lands while layer l computes; every thread reads
+// them as warp-uniform float4 broadcasts. This path is the correctness
+// baseline and serves dims the tcgen05 kernel does not cover.
+#pragma once
+
+#include "common.cuh"
+
+namespace detnet {
+
+struct SimtDims {
+    int K, Z, V;
+};
+
+// Packed per-layer record for the SIMT kernel (floats):
+//   W1x  [Z][IN4]   row i = W1[i][0..IN) * M1, b1[i]*mb1[i], 0 pad
+//   W23T [Z][O4]    row i = (W2[.][i] * M2, W3[.][i] * M3, 0 pad)
+//   b23  [O4]       (b2 * mb2, b3 * mb3, 0 pad)
+//   tail [4]        (t, 0, 0, 0)
+__host__ __device__ constexpr int simt_in4(int K, int V) { return round_up(3 * K + V + 1, 4); }
+__host__ __device__ constexpr int simt_o4(int K, int V) { return round_up(K + V, 4); }
+__host__ __device__ constexpr long simt_rec(int K, int Z, int V) {
+    return static_cast<long>(Z) * simt_in4(K, V) + static_cast<long>(Z) * simt_o4(K, V) +
+           simt_o4(K, V) + 4;
+}
+
+struct StackArgs {
+    const float *gp;        // [tile][NG][TILE]
+    const float *q32;       // [tile][K][TILE]
+    const double *denom;    // [s]
+    const uint32_t *xmask;  // [s]
+    const float *wrec;      // [depth][rec]
+    long rec_floats;
+    const double *lnk;      // [depth] ln(l+1) or 0 when excluded
+    int l_begin, l_end;
+    long n, n_tiles, tile0; // tile0: global index of this launch's first tile
+    float *xhat;            // optional [s][l_end-l_begin][K] (s relative to this launch)
+    float *x_state;         // optional [s][K] in/out
+    float *v_state;         // optional [s][V] in/out
+    double *tile_loss;      // [global tile]
+    long long *tile_err;    // [global tile]
+};
+
+template <int K, int Z, int V>
+__global__ void __launch_bounds__(256, 1) k_stack_simt(StackArgs a) {
+    constexpr int IN = 3 * K + V;
+    constexpr int IN4 = simt_in4(K, V);
+    constexpr int O = K + V;
+    constexpr int O4 = simt_o4(K, V);
+    constexpr int NG = gram_entries(K);
+    constexpr int REC = static_cast<int>(simt_rec(K, Z, V));
+    extern __shared__ __align__(128) float sw[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sw + 2 * REC);
+
+    const int tid = threadIdx.x;
+    const long tile_l = static_cast<long>(blockIdx.x) * 2 + (tid >> 7);
+    const bool live_tile = tile_l < a.n_tiles;
+    const long tile = live_tile ? tile_l : a.n_tiles - 1;
+    const int col = tid & (TILE - 1);
+    const long s = tile * TILE + col;           // sample index within this launch
+    const bool live = live_tile && s < a.n;
+    const long gt = a.tile0 + tile;              // global tile index for SoA buffers
+
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const uint32_t bytes = static_cast<uint32_t>(REC) * 4u;
+    if (tid == 0) {
+        for (int b = 0; b < 2; ++b) {
+            const int l = a.l_begin + b;
+            if (l < a.l_end) {
+                mbar_arrive_expect_tx(&bars[b], bytes);
+                bulk_g2s_chunked(sw + b * REC, a.wrec + static_cast<long>(l) * a.rec_floats, bytes,
+                                 &bars[b]);
+            }
+        }
+    }
+
+    float q[K], x[K], v[V];
+#pragma unroll
+    for (int k = 0; k < K; ++k) q[k] = a.q32[(gt * K + k) * TILE + col];
+    if (a.x_state && live) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) x[k] = a.x_state[s * K + k];
+#pragma unroll
+        for (int k = 0; k < V; ++k) v[k] = a.v_state[s * V + k];
+    } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k) x[k] = 0.f;
+#pragma unroll
+        for (int k = 0; k < V; ++k) v[k] = 0.f;
+    }
+    const uint32_t xm = a.xmask[gt * TILE + col];
+    const double dnm = a.denom[gt * TILE + col];
+    double loss = 0.0;
+    const int nl = a.l_end - a.l_begin;
+    const float *gps = a.gp + gt * NG * TILE + col;
+
+    for (int l = a.l_begin; l < a.l_end; ++l) {
+        const int it = l - a.l_begin;
+        const int b = it & 1;
+        mbar_wait(&bars[b], (it >> 1) & 1);
+        const float *W = sw + b * REC;
+
+        float gx[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) gx[k] = 0.f;
+        {
+            int e = 0;
+#pragma unroll
+            for (int r = 0; r < K; ++r)
+#pragma unroll
+                for (int c = r; c < K; ++c, ++e) {
+                    const float g = __ldg(gps + e * TILE);
+                    gx[r] = fmaf(g, x[c], gx[r]);
+                    if (c != r) gx[c] = fmaf(g, x[r], gx[c]);
+                }
+        }
+
+        float acc[O];
+        const float *b23 = W + Z * IN4 + Z * O4;
+#pragma unroll
+        for (int o = 0; o < O; ++o) acc[o] = b23[o];
+
+#define DETNET_IN(j)                                                                            \
+    ((j) < K ? q[(j) < K ? (j) : 0]                                                             \
+             : (j) < 2 * K ? x[((j) - K) < K ? (j) - K : 0]                                      \
+                           : (j) < 3 * K ? gx[((j) - 2 * K) < K ? (j) - 2 * K : 0]               \
+                                         : v[((j) - 3 * K) < V ? (j) - 3 * K : 0])
+#pragma unroll 1
+        for (int i = 0; i < Z; ++i) {
+            const float4 *w4 = reinterpret_cast<const float4 *>(W + i * IN4);
+            float u0 = 0.f, u1 = 0.f, u2 = 0.f, u3 = 0.f;
+#pragma unroll
+            for (int m = 0; m < IN4 / 4; ++m) {
+                const float4 w = w4[m];
+                if (4 * m + 0 < IN) u0 = fmaf(w.x, DETNET_IN(4 * m + 0), u0);
+                else if (4 * m + 0 == IN) u0 += w.x;
+                if (4 * m + 1 < IN) u1 = fmaf(w.y, DETNET_IN(4 * m + 1), u1);
+                else if (4 * m + 1 == IN) u1 += w.y;
+                if (4 * m + 2 < IN) u2 = fmaf(w.z, DETNET_IN(4 * m + 2), u2);
+                else if (4 * m + 2 == IN) u2 += w.z;
+                if (4 * m + 3 < IN) u3 = fmaf(w.w, DETNET_IN(4 * m + 3), u3);
+                else if (4 * m + 3 == IN) u3 += w.w;
+            }
+            const float u = (u0 + u1) + (u2 + u3);
+            const float z = u > 0.f ? u : 0.f;
+            const float4 *c4 = reinterpret_cast<const float4 *>(W + Z * IN4 + i * O4);
+#pragma unroll
+            for (int m = 0; m < O4 / 4; ++m) {
+                const float4 w = c4[m];
+                if (4 * m + 0 < O) acc[4 * m + 0] = fmaf(w.x, z, acc[4 * m + 0]);
+                if (4 * m + 1 < O) acc[4 * m + 1] = fmaf(w.y, z, acc[4 * m + 1]);
+                if (4 * m + 2 < O) acc[4 * m + 2] = fmaf(w.z, z, acc[4 * m + 2]);
+                if (4 * m + 3 < O) acc[4 * m + 3] = fmaf(w.w, z, acc[4 * m + 3]);
+            }
+        }
+#undef DETNET_IN
+        const float t = W[Z * IN4 + Z * O4 + O4];
+        double err = 0.0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const float u = acc[k];
+            const float xn = u <= -t ? -1.f : (u >= t ? 1.f : __fdiv_rn(u, t));
+            x[k] = xn;
+            const double d = ((xm >> k) & 1u ? 1.0 : -1.0) - static_cast<double>(xn);
+            err += d * d;
+        }
+#pragma unroll
+        for (int k = 0; k < V; ++k) v[k] = acc[K + k];
+        loss += a.lnk[l] * err / dnm;
+        if (a.xhat && live) {
+            float *o = a.xhat + (s * nl + it) * K;
+#pragma unroll
+            for (int k = 0; k < K; ++k) o[k] = x[k];
+        }
+        __syncthreads();  // every thread is done reading buffer b
+        if (tid == 0 && l + 2 < a.l_end) {
+            mbar_arrive_expect_tx(&bars[b], bytes);
+            bulk_g2s_chunked(sw + b * REC, a.wrec + static_cast<long>(l + 2) * a.rec_floats, bytes,
+                             &bars[b]);
+        }
+    }
+
+    if (a.x_state && live) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) a.x_state[s * K + k] = x[k];
+#pragma unroll
+        for (int k = 0; k < V; ++k) a.v_state[s * V + k] = v[k];
+    }
+    long long errs = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) errs += (x[k] >= 0.f) != (((xm >> k) & 1u) != 0);
+    if (!live) { loss = 0.0; errs = 0; }
+
+    // deterministic per-tile reduction: 4 warps per tile, fixed tree
+    __shared__ double s_loss[8];
+    __shared__ long long s_err[8];
+    loss = warp_sum(loss);
+    errs = warp_sum(errs);
+    if ((tid & 31) == 0) { s_loss[tid >> 5] = loss; s_err[tid >> 5] = errs; }
+    __syncthreads();
+    if ((tid & 127) == 0 && live_tile) {
+        const int w0 = tid >> 5;
+        a.tile_loss[gt] = (s_loss[w0] + s_loss[w0 + 1]) + (s_loss[w0 + 2] + s_loss[w0 + 3]);
+        a.tile_err[gt] = s_err[w0] + s_err[w0 + 1] + s_err[w0 + 2] + s_err[w0 + 3];
+    }
+}
+
+// K5: fixed-order reduction of per-tile partials and per-sample flags.
+__global__ void __launch_bounds__(1024) k_reduce(const double *tile_loss, const long long *tile_err,
+                                                 long n_tiles, const uint8_t *flag, long n,
+                                                 double *out_loss, long long *out_err,
+                                                 long long *out_flag) {
+    __shared__ double sl[1024];
+    __shared__ long long se[1024], sf[1024];
+    const int t = threadIdx.x;
+    double l = 0.0;
+    long long e = 0, f = 0;
+    for (long i = t; i < n_tiles; i += 1024) { l += tile_loss[i]; e += tile_err[i]; }
+    for (long i = t; i < n; i += 1024) f += flag[i];
+    sl[t] = l; se[t] = e; sf[t] = f;
+    __syncthreads();
+    for (int w = 512; w > 0; w >>= 1) {
+        if (t < w) { sl[t] += sl[t + w]; se[t] += se[t + w]; sf[t] += sf[t + w]; }
+        __syncthreads();
+    }
+    if (t == 0) { *out_loss = sl[0]; *out_err = se[0]; *out_flag = sf[0]; }
+}
+
+} // namespace detnet

@@ -1,0 +1,337 @@
+"""ctypes binding of the C-ABI (include/detnet_b200.h), mirroring the
+reference's batch-kernel API (proj/include/unfold/kernels.hpp:29-65):
+
+    ctx = Context(device=0)
+    model = ctx.model(n_tx, n_rx, z_dim, v_dim, params, masks=None, frozen_prefix=0)
+    ev = model.batch_evaluate(H, y, x)          # -> BatchEval
+    model.batch_gradient(H, y, x, spec)          # -> (BatchEval, grads)
+
+Errors map to the reference's exception taxonomy (errors.hpp:9-31). There is
+no CPU fallback: constructing a Context without a B200 raises CudaError, and a
+missing shared library raises ImportError at import time.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libdetnet_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is not built: run `make -C paper_2003_09446_b200/csrc` "
+                      "(or __graft_entry__.build())")
+_lib = C.CDLL(LIB_PATH)
+
+_dp = C.POINTER(C.c_double)
+_fp = C.POINTER(C.c_float)
+_bp = C.POINTER(C.c_int8)
+_vp = C.c_void_p
+
+
+# --- exception taxonomy (errors.hpp:9-31) -----------------------------------
+class DetnetError(RuntimeError):
+    pass
+
+
+class ContractError(DetnetError, ValueError):
+    pass
+
+
+class SingularMatrixError(DetnetError):
+    pass
+
+
+class ConfigError(DetnetError):
+    pass
+
+
+class CudaError(DetnetError):
+    pass
+
+
+class UnsupportedError(DetnetError):
+    pass
+
+
+_ERRS = {1: ContractError, 2: SingularMatrixError, 3: ConfigError, 4: CudaError, 5: CudaError,
+         6: UnsupportedError}
+
+
+def _check(rc):
+    if rc:
+        msg = _lib.detnet_last_error().decode()
+        raise _ERRS.get(rc, DetnetError)(msg)
+
+
+class _ModelDesc(C.Structure):
+    _fields_ = [("n_tx", C.c_int), ("n_rx", C.c_int), ("z_dim", C.c_int), ("v_dim", C.c_int),
+                ("depth", C.c_int), ("frozen_prefix", C.c_int), ("params", _dp), ("masks", _dp)]
+
+
+class _Eval(C.Structure):
+    _fields_ = [("data_loss", C.c_double), ("loss_sum", C.c_double),
+                ("symbol_errors", C.c_longlong), ("symbols", C.c_longlong),
+                ("flagged", C.c_longlong)]
+
+
+class _Times(C.Structure):
+    _fields_ = [("ms", C.c_double * 8), ("launches", C.c_longlong * 8)]
+
+
+class _LossSpec(C.Structure):
+    _fields_ = [("kind", C.c_int), ("lam", C.c_double), ("lam1", C.c_double), ("lam2", C.c_double)]
+
+
+class _AdamCfg(C.Structure):
+    _fields_ = [("lr0", C.c_double), ("decay_factor", C.c_double), ("decay_step", C.c_int),
+                ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double)]
+
+
+_lib.detnet_last_error.restype = C.c_char_p
+_lib.detnet_ctx_create.argtypes = [C.c_int, C.POINTER(_vp)]
+_lib.detnet_ctx_destroy.argtypes = [_vp]
+_lib.detnet_ctx_set_path.argtypes = [_vp, C.c_int]
+_lib.detnet_ctx_set_stream.argtypes = [_vp, _vp]
+_lib.detnet_ctx_stream.restype = _vp
+_lib.detnet_ctx_stream.argtypes = [_vp]
+_lib.detnet_ctx_set_profiling.argtypes = [_vp, C.c_int]
+_lib.detnet_ctx_kernel_times.argtypes = [_vp, C.POINTER(_Times), C.c_int]
+_lib.detnet_ctx_launch_count.restype = C.c_longlong
+_lib.detnet_ctx_launch_count.argtypes = [_vp]
+_lib.detnet_record_size.restype = C.c_long
+_lib.detnet_record_size.argtypes = [C.c_int, C.c_int, C.c_int]
+_lib.detnet_model_create.argtypes = [_vp, C.POINTER(_ModelDesc), C.POINTER(_vp)]
+_lib.detnet_model_update.argtypes = [_vp, C.POINTER(_ModelDesc)]
+_lib.detnet_model_destroy.argtypes = [_vp]
+_lib.detnet_model_flops_per_detection.restype = C.c_longlong
+_lib.detnet_model_flops_per_detection.argtypes = [_vp, C.c_int]
+_lib.detnet_batch_evaluate.argtypes = [_vp, C.c_long, _vp, _vp, _vp, C.c_int, _vp,
+                                       C.POINTER(_Eval)]
+_lib.detnet_batch_evaluate_device.argtypes = [_vp, C.c_long, _vp, _vp, _vp, C.c_int, _vp,
+                                              C.POINTER(_Eval)]
+_lib.detnet_forward_range.argtypes = [_vp, C.c_long, _vp, _vp, C.c_int, C.c_int, _vp, _vp, _vp]
+_lib.detnet_batch_gradient.argtypes = [_vp, C.c_long, _vp, _vp, _vp, C.POINTER(_LossSpec), C.c_int,
+                                       _vp, C.POINTER(_Eval)]
+_lib.detnet_adam_step.argtypes = [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp,
+                                  _vp, _vp, C.POINTER(C.c_int64), C.POINTER(_AdamCfg)]
+_lib.detnet_rng_seed.restype = C.c_uint64
+_lib.detnet_rng_seed.argtypes = [C.c_uint64, C.c_uint64]
+_lib.detnet_rng_stream.restype = C.c_uint64
+_lib.detnet_rng_stream.argtypes = [C.c_uint64, C.c_uint64]
+_lib.detnet_rng_split.restype = C.c_uint64
+_lib.detnet_rng_split.argtypes = [C.POINTER(C.c_uint64)]
+_lib.detnet_generate_device.argtypes = [_vp, C.c_uint64, C.c_long, C.c_long, C.c_int, C.c_int,
+                                        C.c_double, C.c_double, C.c_double, _vp, _vp, _vp, _vp]
+
+EXPORTED = [n for n in dir(_lib) if n.startswith("detnet_")]
+
+
+def lib_path():
+    return LIB_PATH
+
+
+@dataclass
+class BatchEval:
+    """unfold::BatchEval (kernels.hpp:16-25)."""
+    data_loss: float
+    symbol_errors: int
+    symbols: int
+    flagged: int
+    loss_sum: float = 0.0
+
+    def ber(self):
+        return self.symbol_errors / self.symbols if self.symbols else 0.0
+
+
+def _addr(a):
+    """Data pointer of a numpy array, a torch tensor, or a raw int address."""
+    if a is None:
+        return None
+    if isinstance(a, int):
+        return a
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()  # torch tensor
+
+
+PATH_AUTO, PATH_SIMT, PATH_TC = 0, 1, 2
+
+
+class Context:
+    """One CUDA device (detnet_ctx). Single-owner, like unfold::Rng."""
+
+    def __init__(self, device=0, path=PATH_AUTO):
+        h = _vp()
+        _check(_lib.detnet_ctx_create(device, C.byref(h)))
+        self._h = h
+        self.device = device
+        self.set_path(path)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.detnet_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_path(self, path):
+        _check(_lib.detnet_ctx_set_path(self._h, path))
+
+    def set_stream(self, stream_ptr):
+        _check(_lib.detnet_ctx_set_stream(self._h, stream_ptr))
+
+    @property
+    def stream(self):
+        return _lib.detnet_ctx_stream(self._h)
+
+    def set_profiling(self, on=True):
+        _check(_lib.detnet_ctx_set_profiling(self._h, int(on)))
+
+    def kernel_times(self, reset=False):
+        t = _Times()
+        _check(_lib.detnet_ctx_kernel_times(self._h, C.byref(t), int(reset)))
+        names = ["generate", "preprocess", "stack", "reduce", "backward", "adam", "other", "x"]
+        return {n: (t.ms[i], t.launches[i]) for i, n in enumerate(names)}
+
+    @property
+    def launch_count(self):
+        return _lib.detnet_ctx_launch_count(self._h)
+
+    def model(self, n_tx, n_rx, z_dim, v_dim, params, masks=None, frozen_prefix=0):
+        return Model(self, n_tx, n_rx, z_dim, v_dim, params, masks, frozen_prefix)
+
+    # -- on-device generator (generate_batch keying, kernels.cpp:116-136) --
+    def generate(self, base_state, first, count, n_rx, n_tx, snr_lo, snr_hi, scale, H, y, x,
+                 sigma2=None):
+        _check(_lib.detnet_generate_device(self._h, base_state, first, count, n_rx, n_tx, snr_lo,
+                                           snr_hi, scale, _addr(H), _addr(y), _addr(x),
+                                           _addr(sigma2)))
+
+    def adam_step(self, n_tx, z_dim, v_dim, depth, frozen_prefix, params, masks, grads, m1, m2,
+                  step, lr0=1e-4, decay_factor=0.97, decay_step=1000, beta1=0.9, beta2=0.999,
+                  eps=1e-8):
+        cfg = _AdamCfg(lr0, decay_factor, decay_step, beta1, beta2, eps)
+        st = C.c_int64(step)
+        _check(_lib.detnet_adam_step(self._h, n_tx, z_dim, v_dim, depth, frozen_prefix,
+                                     _addr(params), _addr(masks), _addr(grads), _addr(m1),
+                                     _addr(m2), C.byref(st), C.byref(cfg)))
+        return st.value
+
+
+def rng_seed(seed, stream_id=0):
+    return _lib.detnet_rng_seed(seed, stream_id)
+
+
+def rng_stream(state, stream_id):
+    return _lib.detnet_rng_stream(state, stream_id)
+
+
+def rng_split(state):
+    """Rng::split(): returns (child_state, advanced_state)."""
+    s = C.c_uint64(state)
+    child = _lib.detnet_rng_split(C.byref(s))
+    return child, s.value
+
+
+def record_size(n_tx, z_dim, v_dim):
+    return _lib.detnet_record_size(n_tx, z_dim, v_dim)
+
+
+class Model:
+    """Device-resident ModelParams (detnet_model)."""
+
+    def __init__(self, ctx, n_tx, n_rx, z_dim, v_dim, params, masks=None, frozen_prefix=0):
+        self.ctx = ctx
+        self.n_tx, self.n_rx, self.z_dim, self.v_dim = n_tx, n_rx, z_dim, v_dim
+        self.depth = int(np.asarray(params).shape[0])
+        self.frozen_prefix = frozen_prefix
+        h = _vp()
+        d = self._desc(params, masks)
+        _check(_lib.detnet_model_create(ctx._h, C.byref(d), C.byref(h)))
+        self._h = h
+
+    def _desc(self, params, masks):
+        P = record_size(self.n_tx, self.z_dim, self.v_dim)
+        p = np.ascontiguousarray(params, np.float64).reshape(-1, P)
+        mk = None if masks is None else np.ascontiguousarray(masks, np.float64).reshape(-1, P)
+        self._keep = (p, mk)
+        self.depth = p.shape[0]
+        return _ModelDesc(self.n_tx, self.n_rx, self.z_dim, self.v_dim, p.shape[0],
+                          self.frozen_prefix, p.ctypes.data_as(_dp),
+                          None if mk is None else mk.ctypes.data_as(_dp))
+
+    def update(self, params, masks=None, frozen_prefix=None):
+        if frozen_prefix is not None:
+            self.frozen_prefix = frozen_prefix
+        d = self._desc(params, masks)
+        _check(_lib.detnet_model_update(self._h, C.byref(d)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.detnet_model_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def flops_per_detection(self, include_preprocess=True):
+        return _lib.detnet_model_flops_per_detection(self._h, int(include_preprocess))
+
+    @staticmethod
+    def _samples(H, y, x):
+        H = np.ascontiguousarray(H, np.float32)
+        y = np.ascontiguousarray(y, np.float32)
+        x = np.ascontiguousarray(x, np.int8)
+        return H, y, x
+
+    def batch_evaluate(self, H, y, x, trainable_only=False, want_xhat=False):
+        """batch_evaluate over host samples; returns BatchEval (and x_hat [n][L][K])."""
+        H, y, x = self._samples(H, y, x)
+        n = H.shape[0]
+        xh = np.empty((n, self.depth, self.n_tx), np.float32) if want_xhat else None
+        ev = _Eval()
+        _check(_lib.detnet_batch_evaluate(self._h, n, _addr(H), _addr(y), _addr(x),
+                                          int(trainable_only), _addr(xh), C.byref(ev)))
+        out = BatchEval(ev.data_loss, ev.symbol_errors, ev.symbols, ev.flagged, ev.loss_sum)
+        return (out, xh) if want_xhat else out
+
+    def batch_evaluate_device(self, n, H_ptr, y_ptr, x_ptr, trainable_only=False, xhat_ptr=None):
+        """Device-resident samples (torch tensors or raw device addresses)."""
+        ev = _Eval()
+        _check(_lib.detnet_batch_evaluate_device(self._h, n, _addr(H_ptr), _addr(y_ptr),
+                                                 _addr(x_ptr), int(trainable_only),
+                                                 _addr(xhat_ptr), C.byref(ev)))
+        return BatchEval(ev.data_loss, ev.symbol_errors, ev.symbols, ev.flagged, ev.loss_sum)
+
+    def forward_range(self, H, y, l_begin, l_end, x_state, v_state, want_xhat=True):
+        """Layers [l_begin, l_end) from state (x_state [n][K], v_state [n][V])."""
+        H, y, _ = self._samples(H, y, np.zeros((1,), np.int8))
+        n = H.shape[0]
+        xs = np.ascontiguousarray(x_state, np.float32).copy()
+        vs = np.ascontiguousarray(v_state, np.float32).copy()
+        xh = np.empty((n, l_end - l_begin, self.n_tx), np.float32) if want_xhat else None
+        _check(_lib.detnet_forward_range(self._h, n, _addr(H), _addr(y), l_begin, l_end,
+                                         _addr(xs), _addr(vs), _addr(xh)))
+        return xs, vs, xh
+
+    def batch_gradient(self, H, y, x, kind=0, lam=0.0, lam1=0.0, lam2=0.0, trainable_only=False):
+        H, y, x = self._samples(H, y, x)
+        n = H.shape[0]
+        P = record_size(self.n_tx, self.z_dim, self.v_dim)
+        grads = np.zeros((self.depth, P))
+        ev = _Eval()
+        spec = _LossSpec(kind, lam, lam1, lam2)
+        _check(_lib.detnet_batch_gradient(self._h, n, _addr(H), _addr(y), _addr(x), C.byref(spec),
+                                          int(trainable_only), _addr(grads), C.byref(ev)))
+        return BatchEval(ev.data_loss, ev.symbol_errors, ev.symbols, ev.flagged, ev.loss_sum), grads

@@ -1,0 +1,248 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle.
+
+Tolerances (BASELINE.json north_star):
+* teacher-forced soft outputs: every x_l entry within rtol 1e-4 (+ atol 1e-5,
+  the near-zero band the north star names) of the oracle layer evaluated on
+  the same FP32-rounded state;
+* end to end: hard decisions and error counts identical except on entries
+  whose oracle soft output is within 1e-5 of zero; data loss within 1e-4
+  relative; flagged counts identical;
+* integer outputs (symbols, flagged, error counts) exact.
+"""
+import numpy as np
+import pytest
+
+from oracle.oracle import Model as OModel
+
+pytestmark = pytest.mark.gpu
+
+K, N = 20, 30
+RTOL, ATOL = 1e-4, 1e-5
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2003_09446_b200 import Context
+    return Context(0)
+
+
+def _inputs(oracle, n, lo=7.0, hi=14.0, seed=2, K=K, N=N):
+    r = oracle.rng(seed, 0)
+    H, x, y, _ = oracle.generate_batch(r, N, K, n, lo, hi)
+    H32 = (H / np.sqrt(N)).astype(np.float32)
+    y32 = (y / np.sqrt(N)).astype(np.float32)
+    return H32, y32, x.astype(np.int8)
+
+
+def _omodel(params, K=K, N=N, masks=None, frozen=0):
+    return OModel(K, N, 8 * K, 2 * K, params.shape[0], params, masks=masks, frozen_prefix=frozen)
+
+
+def _close(a, b, rtol=RTOL, atol=ATOL):
+    return np.abs(a - b) <= atol + rtol * np.abs(b)
+
+
+@pytest.mark.parametrize("path", [1, 0])
+def test_golden_forward(ctx, path):
+    """Golden vectors produced by the reference (tests/golden/forward_k20.npz)."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "forward_k20.npz"))
+    ctx.set_path(path)
+    m = ctx.model(K, N, 160, 40, g["params"].astype(np.float64))
+    ev, xh = m.batch_evaluate(g["H"], g["y"], g["x"], want_xhat=True)
+    assert np.all(_close(xh, g["x_hat"][:, 1:]))
+    assert ev.symbol_errors == int(g["symbol_errors"]) and ev.flagged == int(g["flagged"])
+    assert ev.symbols == 8 * K
+    assert abs(ev.data_loss - float(g["data_loss"])) <= 1e-4 * abs(float(g["data_loss"]))
+    ctx.set_path(0)
+
+
+@pytest.mark.parametrize("path", [1, 0])
+def test_teacher_forced_layers(ctx, oracle, path):
+    """Every layer of a 90-layer stack, fed the oracle's own state."""
+    from paper_2003_09446_b200.workload import xavier_params
+    L, n = 90, 256
+    params = xavier_params(K, L, seed=9)
+    om = _omodel(params)
+    H, y, x = _inputs(oracle, n)
+    ctx.set_path(path)
+    m = ctx.model(K, N, 160, 40, params)
+    Hd, yd = H.astype(np.float64), y.astype(np.float64)
+    # oracle trajectory (FP64)
+    xs = np.zeros((n, K)); vs = np.zeros((n, 40))
+    worst = 0.0
+    for l in range(L):
+        xin = xs.astype(np.float32); vin = vs.astype(np.float32)
+        exp_x = np.empty((n, K)); exp_v = np.empty((n, 40))
+        for s in range(n):
+            st, q, G, _ = oracle.preprocess(Hd[s], yd[s])
+            exp_x[s], exp_v[s], _ = oracle.layer(om, l, q, G, xin[s].astype(np.float64),
+                                                 vin[s].astype(np.float64))
+        gx, gv, _ = m.forward_range(H, y, l, l + 1, xin, vin, want_xhat=False)
+        ok = _close(gx, exp_x) & True
+        assert ok.all(), f"layer {l}: {np.sum(~ok)} x entries outside tolerance"
+        okv = _close(gv, exp_v, atol=1e-4)
+        assert okv.all(), f"layer {l}: v max err {np.abs(gv - exp_v).max()}"
+        worst = max(worst, float(np.max(np.abs(gx - exp_x) / (ATOL + np.abs(exp_x)))))
+        xs, vs = exp_x, exp_v
+    ctx.set_path(0)
+    print(f"teacher-forced worst normalised x error: {worst:.3e}")
+
+
+@pytest.mark.parametrize("L,n", [(90, 512), (40, 1024)])
+def test_end_to_end_statistics(ctx, oracle, L, n):
+    from paper_2003_09446_b200.workload import xavier_params
+    params = xavier_params(K, L, seed=9)
+    H, y, x = _inputs(oracle, n)
+    m = ctx.model(K, N, 160, 40, params)
+    ev, xh = m.batch_evaluate(H, y, x, want_xhat=True)
+    ref = oracle.evaluate(_omodel(params), H.astype(np.float64), y.astype(np.float64),
+                          x.astype(np.float64), want_xhat=True)
+    xl_ref = ref["xhat"][:, -1, :]
+    xl = xh[:, -1, :]
+    near0 = np.abs(xl_ref) < 1e-5
+    dec_ok = ((xl >= 0) == (xl_ref >= 0)) | near0
+    assert dec_ok.all()
+    if not near0.any():
+        assert ev.symbol_errors == int(ref["errors"].sum())
+    frac = float(np.mean(_close(xh, ref["xhat"])))
+    assert frac > 0.99, f"only {frac:.4f} of soft outputs within 1e-4"
+    rel = abs(ev.data_loss - ref["loss"].mean()) / abs(ref["loss"].mean())
+    assert rel < 1e-4, rel
+    assert ev.flagged == int(ref["flagged"].sum())
+    assert ev.symbols == n * K
+
+
+@pytest.mark.parametrize("n", [1, 127, 129, 1000])
+def test_ragged_batches(ctx, oracle, n):
+    from paper_2003_09446_b200.workload import xavier_params
+    params = xavier_params(K, 8, seed=4)
+    H, y, x = _inputs(oracle, n, seed=11)
+    m = ctx.model(K, N, 160, 40, params)
+    ev, xh = m.batch_evaluate(H, y, x, want_xhat=True)
+    ref = oracle.evaluate(_omodel(params), H.astype(np.float64), y.astype(np.float64),
+                          x.astype(np.float64), want_xhat=True)
+    assert np.all(_close(xh, ref["xhat"]))
+    assert ev.symbol_errors == int(ref["errors"].sum()) and ev.symbols == n * K
+
+
+def test_empty_batch(ctx):
+    from paper_2003_09446_b200.workload import xavier_params
+    m = ctx.model(K, N, 160, 40, xavier_params(K, 2, seed=4))
+    ev = m.batch_evaluate(np.zeros((0, N, K), np.float32), np.zeros((0, N), np.float32),
+                          np.zeros((0, K), np.int8))
+    assert ev.data_loss == 0.0 and ev.symbols == 0 and ev.symbol_errors == 0
+
+
+def test_singular_channel_raises(ctx, oracle):
+    """solve_normal_equations pivot test -> SingularMatrixError (linalg.cpp:59-60)."""
+    import paper_2003_09446_b200 as p
+    from paper_2003_09446_b200.workload import xavier_params
+    H, y, x = _inputs(oracle, 64)
+    H[17, :, 3] = H[17, :, 5]  # two identical columns: G singular
+    m = ctx.model(K, N, 160, 40, xavier_params(K, 2, seed=4))
+    with pytest.raises(p.SingularMatrixError):
+        m.batch_evaluate(H, y, x)
+
+
+def test_flagged_denominator(ctx, oracle):
+    """Noise-free sample: x_tilde == x, denominator guard fires (loss.cpp:16-19)."""
+    from paper_2003_09446_b200.workload import xavier_params
+    H, y, x = _inputs(oracle, 16)
+    y[3] = (H[3].astype(np.float64) @ x[3].astype(np.float64)).astype(np.float32)
+    params = xavier_params(K, 3, seed=4)
+    m = ctx.model(K, N, 160, 40, params)
+    ev = m.batch_evaluate(H, y, x)
+    ref = oracle.batch_evaluate(_omodel(params), H.astype(np.float64), y.astype(np.float64),
+                                x.astype(np.float64))
+    assert ev.flagged == ref["flagged"]
+    assert abs(ev.data_loss - ref["data_loss"]) <= 1e-4 * abs(ref["data_loss"])
+
+
+def test_trainable_only_loss(ctx, oracle):
+    from paper_2003_09446_b200.workload import xavier_params
+    params = xavier_params(K, 6, seed=4)
+    H, y, x = _inputs(oracle, 256)
+    m = ctx.model(K, N, 160, 40, params, frozen_prefix=4)
+    ev = m.batch_evaluate(H, y, x, trainable_only=True)
+    ref = oracle.batch_evaluate(_omodel(params, frozen=4), H.astype(np.float64),
+                                y.astype(np.float64), x.astype(np.float64), trainable_only=True)
+    assert abs(ev.data_loss - ref["data_loss"]) <= 1e-4 * abs(ref["data_loss"])
+    assert ev.symbol_errors == ref["symbol_errors"]
+
+
+def test_masked_models(ctx, oracle):
+    """Group-pruned and sparse-group masks (configs 3/4 semantics) at L=8."""
+    from paper_2003_09446_b200.workload import group_masks, sparse_group_model, xavier_params
+    params = xavier_params(K, 8, seed=9)
+    mk = group_masks(K, 8, seed=31)
+    ps, ms = sparse_group_model(params, mk, K)
+    H, y, x = _inputs(oracle, 512)
+    for p_, m_ in ((params, mk), (ps, ms)):
+        m = ctx.model(K, N, 160, 40, p_, masks=m_)
+        ev, xh = m.batch_evaluate(H, y, x, want_xhat=True)
+        ref = oracle.evaluate(_omodel(p_, masks=m_), H.astype(np.float64), y.astype(np.float64),
+                              x.astype(np.float64), want_xhat=True)
+        assert np.all(_close(xh, ref["xhat"]))
+        assert ev.symbol_errors == int(ref["errors"].sum())
+
+
+@pytest.mark.parametrize("k", [2, 3, 4, 8])
+def test_desk_scale_dims(ctx, oracle, k):
+    from paper_2003_09446_b200.workload import xavier_params
+    n_rx = 2 * k
+    params = xavier_params(k, 5, seed=3)
+    H, y, x = _inputs(oracle, 300, K=k, N=n_rx)
+    m = ctx.model(k, n_rx, 8 * k, 2 * k, params)
+    ev, xh = m.batch_evaluate(H, y, x, want_xhat=True)
+    ref = oracle.evaluate(_omodel(params, K=k, N=n_rx), H.astype(np.float64),
+                          y.astype(np.float64), x.astype(np.float64), want_xhat=True)
+    assert np.all(_close(xh, ref["xhat"], rtol=1e-4, atol=1e-5))
+    assert ev.symbol_errors == int(ref["errors"].sum())
+
+
+def test_gpu_generator_matches_host(ctx, oracle):
+    """K0 vs the reference generator (make_sample order), scaled by 1/sqrt(N)."""
+    import torch
+    import paper_2003_09446_b200 as p
+    n = 4096
+    st = p.rng_seed(2, 0)
+    base, _ = p.rng_split(st)
+    Hd = torch.empty((n, N, K), dtype=torch.float32, device="cuda")
+    yd = torch.empty((n, N), dtype=torch.float32, device="cuda")
+    xd = torch.empty((n, K), dtype=torch.int8, device="cuda")
+    s2 = torch.empty((n,), dtype=torch.float64, device="cuda")
+    ctx.generate(base, 0, n, N, K, 7.0, 14.0, 1.0 / np.sqrt(N), Hd, yd, xd, s2)
+    H, y, x = _inputs(oracle, n)
+    Hg, yg, xg = Hd.cpu().numpy(), yd.cpu().numpy(), xd.cpu().numpy()
+    assert np.array_equal(xg, x)
+    same = np.mean(Hg == H)
+    assert same > 0.9999, same
+    assert np.max(np.abs(Hg - H)) <= 2 ** -20 * np.max(np.abs(H))
+    assert np.mean(yg == y) > 0.999
+    # fixed SNR draws no SNR sample first (channel.cpp:18)
+    ctx.generate(base, 0, 64, N, K, 10.0, 10.0, 1.0 / np.sqrt(N), Hd, yd, xd, s2)
+    r = oracle.rng(2, 0)
+    Hf, xf, _, _ = oracle.generate_batch(r, N, K, 64, 10.0, 10.0)
+    assert np.array_equal(xd[:64].cpu().numpy(), xf.astype(np.int8))
+
+
+def test_device_path_matches_host_path(ctx, oracle):
+    import torch
+    from paper_2003_09446_b200.workload import xavier_params
+    params = xavier_params(K, 10, seed=9)
+    H, y, x = _inputs(oracle, 3000)
+    m = ctx.model(K, N, 160, 40, params)
+    ev_h = m.batch_evaluate(H, y, x)
+    Hd, yd, xd = (torch.from_numpy(a).cuda() for a in (H, y, x))
+    ev_d = m.batch_evaluate_device(H.shape[0], Hd, yd, xd)
+    assert ev_h.data_loss == ev_d.data_loss and ev_h.symbol_errors == ev_d.symbol_errors
+
+
+def test_kernel_launches_counted(ctx, oracle):
+    from paper_2003_09446_b200.workload import xavier_params
+    m = ctx.model(K, N, 160, 40, xavier_params(K, 3, seed=9))
+    H, y, x = _inputs(oracle, 200)
+    before = ctx.launch_count
+    m.batch_evaluate(H, y, x)
+    assert ctx.launch_count - before >= 3  # preprocess, stack, reduce

@@ -1,0 +1,412 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 DetNet layer-stack engine (BASELINE.json metric).
+
+Default workload = BASELINE.json configs[1] ("config 2"): dense DetNet
+forward, L=40, K=20 transmit x N=30 receive, real BPSK, a BER sweep over SNR
+{0,2,...,14} dB with 2^20 samples per SNR point (per GPU: weak scaling over
+the sample-index space). One step = the whole sweep = 8 x 2^20 detections
+through detnet_batch_evaluate_device (preprocess + fused layer stack +
+loss/BER reduction). Inputs are generated on the device with the reference's
+own Rng keying (harness.cpp:133 point streams, kernels.cpp:127 per-sample
+streams), H and y scaled by 1/sqrt(N) (H ~ N(0,1/N)), and are resident in
+HBM before the timed region; each point's inputs (2.66 GB) exceed the 126 MB
+L2, so no flush is needed between iterations.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--config 1|2|3|4] [--path auto|simt|tc] [--no-e2e]
+
+Prints ONE JSON line on rank 0.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+K, N, Z, V = 20, 30, 160, 40
+SNRS = [0.0, 2.0, 4.0, 6.0, 8.0, 10.0, 12.0, 14.0]
+MASTER_SEED, WEIGHT_SEED = 1, 9
+POINT_KEY = 0x45564131  # harness.cpp:133
+METRIC = "DetNet detections/sec (30x20 BPSK, L layers)"
+
+
+def workload(cfg):
+    """(layers, points [(lo, hi)], samples per point per GPU, masks kind, want_xhat)."""
+    if cfg == 1:
+        return 90, [(7.0, 14.0)], 4096, None, True
+    if cfg == 2:
+        return 40, [(s, s) for s in SNRS], 1 << 20, None, False
+    if cfg == 3:
+        return 40, [(7.0, 14.0)], 1 << 20, "group", False
+    if cfg == 4:
+        return 40, [(7.0, 14.0)], 1 << 20, "sgl", False
+    raise SystemExit(f"unknown config {cfg}")
+
+
+def build_params(cfg, L):
+    from paper_2003_09446_b200.workload import group_masks, sparse_group_model, xavier_params
+    p = xavier_params(K, L, seed=WEIGHT_SEED)
+    if cfg == 3:
+        return p, group_masks(K, L, seed=31)
+    if cfg == 4:
+        return sparse_group_model(p, group_masks(K, L, seed=31), K)
+    return p, None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        smax = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def measured_peaks(torch):
+    """cuBLAS TF32 and FP32 GEMM peaks on this GPU (8192^3, best of 5)."""
+    out = {}
+    n = 8192
+    a = torch.randn(n, n, device="cuda")
+    b = torch.randn(n, n, device="cuda")
+    for name, tf32 in (("tf32_tflops", True), ("fp32_tflops", False)):
+        torch.backends.cuda.matmul.allow_tf32 = tf32
+        for _ in range(2):
+            torch.matmul(a, b)
+        torch.cuda.synchronize()
+        best = 1e9
+        for _ in range(5 if tf32 else 3):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            torch.matmul(a, b)
+            e.record()
+            torch.cuda.synchronize()
+            best = min(best, s.elapsed_time(e) / 1e3)
+        out[name] = 2 * n ** 3 / best / 1e12
+    torch.backends.cuda.matmul.allow_tf32 = False
+    del a, b
+    torch.cuda.empty_cache()
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        out["hbm_gbs"] = mp.get("hbm_gbs")
+        out["bf16_tflops"] = mp.get("bf16_tflops")
+    except (OSError, ValueError):
+        out["hbm_gbs"] = None
+    return out
+
+
+def cpu_reference(cfg, per_point, steps, warmup, as_arm):
+    """The reference CPU path (oracle/_ref, OpenMP on all host cores) or, if
+    that was not built, the C restatement (1 core) on a bounded sample."""
+    from oracle.oracle import Model as OModel
+    from oracle.oracle import Oracle, RefLib, available_ref
+    L, points, _, mk, _ = workload(cfg)
+    params, masks = build_params(cfg, L)
+    om = OModel(K, N, Z, V, L, params, masks=masks)
+    orc = Oracle()
+    kind = "reference" if available_ref() else "port"
+    ref = RefLib() if kind == "reference" else None
+    batches = []
+    master = orc.rng(MASTER_SEED, 0)
+    import ctypes as C
+    for p, (lo, hi) in enumerate(points):
+        pr = orc.lib.or_stream(C.byref(master), POINT_KEY + p)
+        H, x, y, _ = orc.generate_batch(pr, N, K, per_point, lo, hi)
+        H = (H / np.sqrt(N)).astype(np.float32).astype(np.float64)
+        y = (y / np.sqrt(N)).astype(np.float32).astype(np.float64)
+        batches.append((H, y, x))
+
+    def one():
+        for H, y, x in batches:
+            if ref:
+                ref.batch_evaluate(om, H, y, x, parallel=True)
+            else:
+                orc.batch_evaluate(om, H, y, x)
+
+    for _ in range(warmup):
+        one()
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        one()
+        times.append(time.perf_counter() - t0)
+    dets = per_point * len(points)
+    cores = ref.worker_count() if ref else 1
+    return {"value": dets / statistics.mean(times), "unit": "detections/s", "cores": cores,
+            "kind": kind, "sample": f"{per_point} samples x {len(points)} SNR point(s) of config "
+            f"{cfg} per step (first indices of each point's stream), batch_evaluate only",
+            "sec_per_step": statistics.mean(times)}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    L, points, _, _, _ = workload(args.config)
+    # bounded sample per step: ~2-4 s of 16-core CPU work
+    per_point = {1: 2048, 2: 4096, 3: 16384, 4: 16384}[args.config]
+    r = cpu_reference(args.config, per_point, args.steps, args.warmup, True)
+    line = {"metric": METRIC.replace("L layers", f"L={L}"), "value": r["value"],
+            "unit": "detections/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": r["sec_per_step"] * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference Rng, H~N(0,1/N), FP32-representable)",
+            "config": config_block(args, L, points, per_point), "impl": "reference",
+            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": r["value"], "unit": "detections/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_block(args, L, points, per_point):
+    names = {1: "config1: dense L=90, batch 4096, SNR U[7,14] dB, per-layer x_l out",
+             2: "config2: dense L=40, BER sweep SNR {0,2,..,14} dB, 2^20 samples/point/GPU",
+             3: "config3: group-pruned L=40 (112/160 units, 30/100 W1 cols dead), 2^20",
+             4: "config4: sparse-group L=40 (config3 groups, 5% kept N(0,0.05^2)), 2^20"}
+    return {"workload": names[args.config], "n_rx": N, "n_tx": K, "layers": L,
+            "z_dim": Z, "v_dim": V, "snr_points": [list(p) for p in points],
+            "samples_per_point_per_gpu": per_point, "parallelism": f"dp{args.gpus}",
+            "l2": "inputs per point (2540 B/detection) exceed L2; no flush needed"
+            if per_point * 2540 > 126e6 else "inputs smaller than L2",
+            "weights": f"Xavier-uniform from Rng({WEIGHT_SEED}), FP32-rounded, b=0, t=0.5"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--path", default="auto", choices=["auto", "simt", "tc"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    import paper_2003_09446_b200 as eng
+    L, points, per_point, _, want_xhat = workload(args.config)
+    params, masks = build_params(args.config, L)
+    peaks = measured_peaks(torch) if rank == 0 else {}
+
+    ctx = eng.Context(local, path={"auto": 0, "simt": 1, "tc": 2}[args.path])
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    model = ctx.model(K, N, Z, V, params, masks=masks)
+
+    # ---- inputs: on-device generator, rank shard of each point's stream ----
+    master = eng.rng_seed(MASTER_SEED, 0)
+    dev_in = []
+    for p, (lo, hi) in enumerate(points):
+        base, _ = eng.rng_split(eng.rng_stream(master, POINT_KEY + p))
+        H = torch.empty((per_point, N, K), dtype=torch.float32, device="cuda")
+        y = torch.empty((per_point, N), dtype=torch.float32, device="cuda")
+        x = torch.empty((per_point, K), dtype=torch.int8, device="cuda")
+        ctx.generate(base, rank * per_point, per_point, N, K, lo, hi, 1.0 / np.sqrt(N), H, y, x)
+        dev_in.append((H, y, x))
+    xhat = (torch.empty((per_point, L, K), dtype=torch.float32, device="cuda")
+            if want_xhat else None)
+    torch.cuda.synchronize()
+
+    def step_device():
+        evs = []
+        for H, y, x in dev_in:
+            evs.append(model.batch_evaluate_device(per_point, H, y, x, xhat_ptr=xhat))
+        return evs
+
+    for _ in range(args.warmup):
+        step_device()
+    ctx.kernel_times(reset=True)
+    ctx.set_profiling(True)
+    launches0 = ctx.launch_count
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(args.steps):
+            evs = step_device()
+        t1.record()
+        torch.cuda.synchronize()
+    barrier()
+    launches = ctx.launch_count - launches0
+    ctx.set_profiling(False)
+    kt = ctx.kernel_times(reset=True)
+    ms = t0.elapsed_time(t1)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    # the only data-path collective: per-point error counts / loss sums
+    stats = torch.tensor([[e.symbol_errors, e.symbols, e.flagged] for e in evs], dtype=torch.int64,
+                         device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(stats)
+    ms = float(ms_t.item())
+    dets = per_point * len(points) * world
+    value = dets * args.steps / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (the fused layer stack) ----
+    stack_ms, stack_launches = kt["stack"]
+    census_layers = (model.flops_per_detection(False))  # per detection, layers only
+    flops_per_launch = census_layers * per_point
+    avg_launch_s = stack_ms / 1e3 / max(stack_launches, 1)
+    achieved = flops_per_launch / avg_launch_s / 1e12
+    tc_path = ctx_path_name(ctx, model)
+    if tc_path == "tcgen05-3xtf32":
+        peak = peaks.get("tf32_tflops", 0) / 3.0 if peaks.get("tf32_tflops") else None
+        peak_note = "measured cuBLAS TF32 GEMM / 3 (3xTF32 split), this run"
+    else:
+        peak = peaks.get("fp32_tflops")
+        peak_note = "measured cuBLAS FP32 SGEMM (CUDA-core FP32 pipe), this run"
+    roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": (achieved / peak) if peak else None, "traffic": None,
+            "kernel": "k_stack (fused layer stack)", "path": tc_path, "peak_source": peak_note,
+            "census_flop_per_detection_layers": census_layers,
+            "detections_per_launch": per_point, "avg_launch_ms": avg_launch_s * 1e3,
+            "share_of_step": stack_ms / (ms * 1.0) if ms else None,
+            "kernel_ms": {k: v[0] for k, v in kt.items() if v[1]},
+            "kernel_launches": {k: v[1] for k, v in kt.items() if v[1]}}
+
+    # ---- end to end through the C-ABI with pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, torch, model, dev_in, per_point, L, want_xhat, barrier, world)
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu and world == 1:
+            try:
+                cpu_pp = 2048 if args.config == 2 else (1024 if args.config == 1 else 8192)
+                c = cpu_reference(args.config, cpu_pp, 1, 0, False)
+                cpu = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            except Exception as exc:  # pragma: no cover
+                cpu = {"value": None, "error": str(exc)}
+        st = stats.cpu().numpy()
+        out = {"metric": METRIC.replace("L layers", f"L={L}"), "value": value,
+               "unit": "detections/s", "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+               "data": "synthetic (reference Rng generator on device, H~N(0,1/N), FP32)",
+               "config": config_block(args, L, points, per_point),
+               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+               "clocks": clk.summary(), "peaks_measured": peaks,
+               "ber_last_step": [float(s[0]) / float(s[1]) for s in st]}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def ctx_path_name(ctx, model):
+    return model.path_name
+
+
+def run_e2e(args, torch, model, dev_in, per_point, L, want_xhat, barrier, world):
+    """Same sweep through detnet_batch_evaluate (host buffers; H2D inside)."""
+    host = []
+    try:
+        for H, y, x in dev_in:
+            host.append((H.cpu().pin_memory().numpy(), y.cpu().pin_memory().numpy(),
+                         x.cpu().pin_memory().numpy()))
+    except RuntimeError as exc:
+        return {"value": None, "error": f"pinned allocation failed: {exc}"}
+    xh = torch.empty((per_point, L, K), dtype=torch.float32).pin_memory().numpy() if want_xhat else None
+
+    def step():
+        for H, y, x in host:
+            ev = model_eval_host(model, H, y, x, xh)
+        return ev
+
+    for _ in range(max(1, args.warmup // 2)):
+        step()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([el], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
+    barrier()
+    h2d = sum(H.nbytes + y.nbytes + x.nbytes for H, y, x in host)
+    d2h = 32 * len(host) + (xh.nbytes * len(host) if xh is not None else 0)
+    dets = per_point * len(host) * world
+    return {"value": dets * args.steps / el, "unit": "detections/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "timer": "host wall clock around synchronous C-ABI calls, max over ranks"}
+
+
+def model_eval_host(model, H, y, x, xh):
+    import ctypes as C
+
+    from paper_2003_09446_b200 import detnet as d
+    ev = d._Eval()
+    d._check(d._lib.detnet_batch_evaluate(model._h, H.shape[0], H.ctypes.data, y.ctypes.data,
+                                          x.ctypes.data, 0, None if xh is None else xh.ctypes.data,
+                                          C.byref(ev)))
+    return ev
+
+
+if __name__ == "__main__":
+    main()

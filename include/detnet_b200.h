@@ -83,6 +83,9 @@ long detnet_record_size(int n_tx, int z_dim, int v_dim);
 int detnet_model_create(detnet_ctx *ctx, const detnet_model_desc *desc, detnet_model **out);
 int detnet_model_update(detnet_model *m, const detnet_model_desc *desc);
 void detnet_model_destroy(detnet_model *m);
+/* Kernel path the dense stack of this model runs on under the context's
+ * current path setting: 1 SIMT FP32, 2 tcgen05 3xTF32. */
+int detnet_model_path(const detnet_model *m);
 /* Analytic census, flops_per_detection (compression.cpp:120-129). */
 long long detnet_model_flops_per_detection(const detnet_model *m, int include_preprocess);
 

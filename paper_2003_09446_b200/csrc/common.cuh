@@ -75,6 +75,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
     }
 }
 
+// Same, with a watchdog: traps (kernel error instead of a hung GPU) if the
+// phase has not completed after ~4 s of SM clocks.
+__device__ __forceinline__ void mbar_wait_guard(uint64_t *bar, uint32_t phase) {
+    if (mbar_try_wait(bar, phase)) return;
+    const long long t0 = clock64();
+    while (!mbar_try_wait(bar, phase)) {
+        if (clock64() - t0 > 8000000000LL) __trap();
+    }
+}
+
 // 1-D bulk copy global -> shared, completion counted on an mbarrier
 // (SASS: UBLKCP). bytes must be a multiple of 16, addresses 16-B aligned.
 __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, uint32_t bytes,

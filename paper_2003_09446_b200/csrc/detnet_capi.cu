@@ -160,12 +160,12 @@ int run_pre(detnet_model *m, cudaStream_t st, long s0, long cnt, long n_total, c
     detnet_ctx *c = m->ctx;
     const int K = m->K, NG = gram_entries(K);
     const long t0 = s0 / TILE;
-    const size_t smem = static_cast<size_t>(8) *
-                        (round_up(m->N * K + m->N, 2) + 2 * K * K) * sizeof(float);
-    const int blocks = static_cast<int>(std::min<long>((cnt + 7) / 8, 148L * 16));
+    const int N = m->N;
+    const size_t smem = static_cast<size_t>(4) * (N * K + N + K * K + K) * sizeof(double);
+    const int blocks = static_cast<int>(std::min<long>((cnt + 3) / 4, 148L * 32));
     {
         LaunchScope ls(c, DETNET_K_PREPROCESS, st);
-        m->dims->pre(dim3(blocks), dim3(256), smem, st, cnt, m->N, H, y, x,
+        m->dims->pre(dim3(blocks), dim3(128), smem, st, cnt, m->N, H, y, x,
                      c->gp.as<float>() + t0 * NG * TILE, c->q32.as<float>() + t0 * K * TILE,
                      c->denom.as<double>() + s0, c->xmask.as<uint32_t>() + s0,
                      c->flag.as<uint8_t>() + s0, c->sing.as<unsigned long long>());
@@ -189,7 +189,7 @@ int run_pre(detnet_model *m, cudaStream_t st, long s0, long cnt, long n_total, c
 int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, int l_begin,
               int l_end, bool trainable_only, float *xhat, float *xs, float *vs) {
     detnet_ctx *c = m->ctx;
-    if (use_tc(m) && !xs) {
+    if (use_tc(m)) {
         TcArgs ta{};
         ta.gp = c->gp.as<float>();
         ta.q32 = c->q32.as<float>();
@@ -205,7 +205,7 @@ int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, 
         ta.tile_loss = c->tile_loss.as<double>();
         ta.tile_err = c->tile_err.as<long long>();
         LaunchScope ls(c, DETNET_K_STACK, st);
-        if (int rc = tc_launch(m->tc, ta, st)) return rc;
+        if (int rc = tc_launch_state(m->tc, ta, xs, vs, st)) return rc;
         return check_launch();
     }
     StackArgs a{};
@@ -403,6 +403,8 @@ void detnet_model_destroy(detnet_model *m) {
     tc_release(m->tc);
     delete m;
 }
+
+int detnet_model_path(const detnet_model *m) { return m && use_tc(m) ? 2 : 1; }
 
 long long detnet_model_flops_per_detection(const detnet_model *m, int include_pre) {
     if (!m) return -1;

@@ -87,6 +87,7 @@ struct TcArgs {
 int tc_prepare();
 int tc_pack(TcModel &tc, int K, int Z, int V, int L, const double *params, const double *masks);
 int tc_launch(const TcModel &tc, const TcArgs &a, cudaStream_t st);
+int tc_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cudaStream_t st);
 void tc_release(TcModel &tc);
 
 // training (train.cu)

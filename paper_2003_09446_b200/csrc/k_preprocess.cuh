@@ -5,9 +5,15 @@
 //   G = H^T H            gram, linalg.cpp:31-42 (upper triangle, i ascending)
 //   x_tilde = G^-1 q     solve_normal_equations, linalg.cpp:44-79
 //   denom = max(||x - x_tilde||^2, 1e-12), flagged    loss.cpp:16-19
-// all in FP64 with the reference's operation order and no FMA contraction,
-// so on FP32-representable inputs q, G, x_tilde and denom are bit-identical
-// to the reference. The layer stack consumes FP32 roundings of q and G.
+// in FP64 with the reference's operation order, so on FP32-representable
+// inputs q, G, x_tilde and denom are bit-identical to the reference. (A
+// product of two FP32 values is exact in FP64, so acc + a*b may use DFMA.)
+// The layer stack consumes FP32 roundings of q and G.
+//
+// LU layout: lane r < K owns row r of [G | q] in registers; row swaps are
+// tracked as a position permutation (pos), reproducing the reference's
+// first-strict-maximum pivot choice over positions; every row lane
+// eliminates its own row with one parallel division per column.
 //
 // Outputs (tile SoA, TILE samples per tile):
 //   gp  [tile][K(K+1)/2][TILE]  packed upper triangle of G (row-major a<=b)
@@ -26,115 +32,112 @@ __global__ void __launch_bounds__(256)
                  const int8_t *__restrict__ x, float *__restrict__ gp, float *__restrict__ q32,
                  double *__restrict__ denom, uint32_t *__restrict__ xmask,
                  uint8_t *__restrict__ flag, unsigned long long *__restrict__ singular) {
-    static_assert(K + 1 <= 32, "one lane per column plus the right-hand side");
+    static_assert(K <= 32, "one lane per row");
     constexpr int NG = gram_entries(K);
+    constexpr unsigned FULL = 0xffffffffu;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int warps = blockDim.x >> 5;
-    // per-warp scratch: H (N*K floats), y (N floats), G (K*K doubles)
-    const int hfl = round_up(N * K + N, 2);
-    float *sH = reinterpret_cast<float *>(smem_raw) +
-                static_cast<size_t>(warp) * (hfl + 2 * K * K);
-    float *sy = sH + N * K;
-    double *sG = reinterpret_cast<double *>(sH + hfl);
+    // per-warp scratch (doubles): H [N*K], y [N], G [K*K], q [K]
+    const int per = N * K + N + K * K + K;
+    double *sH = reinterpret_cast<double *>(smem_raw) + static_cast<size_t>(warp) * per;
+    double *sy = sH + N * K;
+    double *sG = sy + N;
+    double *sq = sG + K * K;
 
     for (long s = static_cast<long>(blockIdx.x) * warps + warp; s < n;
          s += static_cast<long>(gridDim.x) * warps) {
         const float *Hs = H + s * static_cast<long>(N) * K;
-        for (int i = lane; i < N * K; i += 32) sH[i] = Hs[i];
-        for (int i = lane; i < N; i += 32) sy[i] = y[s * N + i];
+        for (int i = lane; i < N * K; i += 32) sH[i] = static_cast<double>(__ldg(Hs + i));
+        for (int i = lane; i < N; i += 32) sy[i] = static_cast<double>(__ldg(y + s * N + i));
         __syncwarp();
         const long tile = s / TILE;
         const int col = static_cast<int>(s % TILE);
 
-        // q_j (lane j), i ascending, from 0.0
-        double qj = 0.0;
         if (lane < K) {
-            for (int i = 0; i < N; ++i)
-                qj = dadd(qj, dmul(static_cast<double>(sH[i * K + lane]),
-                                   static_cast<double>(sy[i])));
+            double qj = 0.0;
+            for (int i = 0; i < N; ++i) qj = fma(sH[i * K + lane], sy[i], qj);
+            sq[lane] = qj;
             q32[(tile * K + lane) * TILE + col] = __double2float_rn(qj);
         }
-        // G upper triangle, entries spread over lanes
         for (int e = lane; e < NG; e += 32) {
             int a = 0, rem = e;
             while (rem >= K - a) { rem -= K - a; ++a; }
             const int b = a + rem;
             double acc = 0.0;
-            for (int i = 0; i < N; ++i)
-                acc = dadd(acc, dmul(static_cast<double>(sH[i * K + a]),
-                                     static_cast<double>(sH[i * K + b])));
+            for (int i = 0; i < N; ++i) acc = fma(sH[i * K + a], sH[i * K + b], acc);
             sG[a * K + b] = acc;
             sG[b * K + a] = acc;
             gp[(tile * NG + e) * TILE + col] = __double2float_rn(acc);
         }
         __syncwarp();
 
-        // LU with partial pivoting: lane j < K owns column j, lane K the rhs.
-        double c[K];
+        const bool rl = lane < K;
+        double row[K + 1];
 #pragma unroll
-        for (int r = 0; r < K; ++r) {
-            const double qr = __shfl_sync(0xffffffffu, qj, r);
-            c[r] = lane < K ? sG[r * K + lane] : (lane == K ? qr : 0.0);
-        }
+        for (int j = 0; j < K; ++j) row[j] = rl ? sG[lane * K + j] : 0.0;
+        row[K] = rl ? sq[lane] : 0.0;
         double gmax = 0.0;
-        if (lane < K) {
 #pragma unroll
-            for (int r = 0; r < K; ++r) gmax = fmax(gmax, fabs(c[r]));
-        }
+        for (int j = 0; j < K; ++j) gmax = fmax(gmax, fabs(row[j]));
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) gmax = fmax(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
+        for (int o = 16; o > 0; o >>= 1) gmax = fmax(gmax, __shfl_xor_sync(FULL, gmax, o));
         const double tol = dmul(1e-12, gmax);
+
+        int pos = rl ? lane : 1000 + lane;
         bool sing = false;
 #pragma unroll
         for (int cc = 0; cc < K; ++cc) {
-            // pivot search in column cc (lane cc), first strict maximum
-            int piv = cc;
-            double best = fabs(c[cc]);
+            if (!sing) {
+                // pivot: max |A(p, cc)| over positions p >= cc, lowest position on ties
+                double bv = (rl && pos >= cc) ? fabs(row[cc]) : -1.0;
+                int bp = (rl && pos >= cc) ? pos : 1 << 20;
 #pragma unroll
-            for (int r = cc + 1; r < K; ++r) {
-                const double v = fabs(c[r]);
-                if (v > best) { best = v; piv = r; }
-            }
-            piv = __shfl_sync(0xffffffffu, piv, cc);
-            best = __shfl_sync(0xffffffffu, best, cc);
-            if (best <= tol) { sing = true; break; }
-            if (piv != cc) {
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ov = __shfl_xor_sync(FULL, bv, o);
+                    const int op = __shfl_xor_sync(FULL, bp, o);
+                    if (ov > bv || (ov == bv && op < bp)) { bv = ov; bp = op; }
+                }
+                if (bv <= tol) {
+                    sing = true;
+                } else {
+                    const int pl = __ffs(__ballot_sync(FULL, pos == bp)) - 1;
+                    const int cl = __ffs(__ballot_sync(FULL, pos == cc)) - 1;
+                    if (lane == cl) pos = bp;
+                    if (lane == pl) pos = cc;
+                    double pr[K + 1];
 #pragma unroll
-                for (int r = cc + 1; r < K; ++r)
-                    if (r == piv) { const double t = c[cc]; c[cc] = c[r]; c[r] = t; }
-            }
-            const double d = __shfl_sync(0xffffffffu, c[cc], cc);
+                    for (int j = cc; j <= K; ++j) pr[j] = __shfl_sync(FULL, row[j], pl);
+                    if (rl && pos > cc) {
+                        const double f = ddiv(row[cc], pr[cc]);
+                        if (f != 0.0) {
 #pragma unroll
-            for (int r = cc + 1; r < K; ++r) {
-                const double f = __shfl_sync(0xffffffffu, ddiv(c[r], d), cc);
-                if (f == 0.0) continue;
-                if (lane >= cc && lane <= K) c[r] = dsub(c[r], dmul(f, c[cc]));
+                            for (int j = cc; j <= K; ++j) row[j] = dsub(row[j], dmul(f, pr[j]));
+                        }
+                    }
+                }
             }
         }
-        double dn = 0.0;
         if (!sing) {
-            // back substitution on the rhs lane
+            double xs[K];
 #pragma unroll
             for (int i = K - 1; i >= 0; --i) {
-                double acc = c[i];
+                double acc = row[K];
 #pragma unroll
-                for (int j = i + 1; j < K; ++j) {
-                    const double a = __shfl_sync(0xffffffffu, c[i], j);
-                    acc = dsub(acc, dmul(a, c[j]));
-                }
-                const double aii = __shfl_sync(0xffffffffu, c[i], i);
-                if (lane == K) c[i] = ddiv(acc, aii);
+                for (int j = i + 1; j < K; ++j) acc = dsub(acc, dmul(row[j], xs[j]));
+                const double xi = ddiv(acc, row[i]);
+                const int li = __ffs(__ballot_sync(FULL, pos == i)) - 1;
+                xs[i] = __shfl_sync(FULL, xi, li);
             }
-            if (lane == K) {
-                const int8_t *xs = x + s * K;
+            if (lane == 0) {
+                const int8_t *xv = x + s * K;
                 uint32_t mask = 0;
+                double dn = 0.0;
 #pragma unroll
                 for (int i = 0; i < K; ++i) {
-                    const double xv = static_cast<double>(xs[i]);
-                    const double df = dsub(xv, c[i]);
+                    const double df = dsub(static_cast<double>(xv[i]), xs[i]);
                     dn = dadd(dn, dmul(df, df));
-                    if (xs[i] > 0) mask |= 1u << i;
+                    if (xv[i] > 0) mask |= 1u << i;
                 }
                 flag[s] = dn < 1e-12 ? 1 : 0;
                 denom[s] = dn < 1e-12 ? 1e-12 : dn;
@@ -150,7 +153,7 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-// Padding samples of the last tile: neutral values so the stack kernel can
+// Padding samples of the last tile: neutral values so the stack kernels can
 // run full tiles without bounds checks on loads.
 __global__ void k_pad_tail(long n, long n_pad, int K, float *gp, float *q32, double *denom,
                            uint32_t *xmask, uint8_t *flag) {

@@ -1,20 +1,499 @@
-// stack_tc.cu -- K2-TC: tcgen05 3xTF32 fused layer stack (in progress).
+// stack_tc.cu -- K2-TC: the fused DetNet layer stack on tcgen05 tensor cores
+// (3xTF32 split), K=20, z=160, v=40 (the BASELINE.json dims).
+//
+// Restates forward_pre (model.cpp:84-122) + loss_plain (loss.cpp:9-31) + the
+// error count (kernels.cpp:63-65) for a persistent loop over 128-sample
+// tiles; every layer of a tile is two dense contractions over the batch:
+//   U1[128 x 160]  = [q 1 | x gx v][128 x 104] . W1'^T     (bias b1 folded)
+//   U2V[128 x 64]  = relu(U1)[128 x 160] . [W3; W2]^T + [b3; b2]
+// each evaluated as Ahi.Bhi + Ahi.Blo + Alo.Bhi with hi = rna_tf32(a),
+// lo = rna_tf32(a - hi) (error ~2^-22 relative per product, FP32 accumulate).
+//
+// On-chip residency (one CTA per SM, 384 threads):
+//  * TMEM (512 cols x 128 lanes; lane = sample of the tile):
+//      [  0,160) U1 accumulator, overwritten in place by z_hi
+//      [160,240) A_dyn hi = [x | gx | v] hi   } reused as z_lo [160,320)
+//      [240,320) A_dyn lo                      } after the W1 MMAs complete
+//      [320,384) U2V accumulator: [v' (40) | u2 (20) | pad]
+//      [384,408) [q | 1 | 0 0 0] hi,  [416,440) lo   (constant per tile)
+//  * SMEM: the current layer's W1 (hi+lo, 130 KB) and [W3;W2] (hi+lo, 80 KB)
+//    in the no-swizzle K-major core-matrix layout, each streamed in by the
+//    bulk-copy engine as soon as the MMAs reading the previous layer's copy
+//    have completed (single slot per matrix = natural double buffering,
+//    since W1(l+1) lands during the W23 phase of layer l and vice versa).
+//  * Registers: each sample's packed Gram matrix (210 FP32) split over two
+//    threads (warps w and w+4, the same TMEM lane quadrant): thread A holds
+//    rows 0-5 (105 entries) and x_hat, thread B rows 6-19 and v. G x_hat is
+//    formed on FP32 CUDA cores with a 14-float smem exchange per layer.
+// Warp roles: 0-3 "A" epilogue, 4-7 "B" epilogue, 8 TMEM alloc + weight
+// producer + single-thread MMA issuer (warps 9-11 complete its warpgroup so
+// setmaxnreg can move registers to the epilogue warpgroups).
+#include <cmath>
+#include <cstring>
+#include <vector>
+
 #include "engine.hpp"
+#include "tc_ptx.cuh"
 
 namespace detnet {
+namespace {
 
-int tc_prepare() { return 0; }
+constexpr int KX = 20, ZH = 160, VV = 40, NG = 210;
+constexpr int NA = 105; // Gram entries held by thread A (rows 0..5)
+constexpr int C_U1 = 0, C_DYN = 160, C_DYNLO = 240, C_ZLO = 160, C_U2 = 320, C_QHI = 384,
+              C_QLO = 416, TMEM_COLS = 512;
+constexpr int W1_ROWS = 160, W1_K = 104, W23_ROWS = 64, W23_K = 160;
+constexpr uint32_t W1_HALF = W1_ROWS * W1_K * 4;     // 66,560 B per hi/lo
+constexpr uint32_t W23_HALF = W23_ROWS * W23_K * 4;  // 40,960 B
+constexpr uint32_t W1_BYTES = 2 * W1_HALF, W23_BYTES = 2 * W23_HALF;
+constexpr uint32_t LAYER_BYTES = W1_BYTES + W23_BYTES; // 215,040 B
+constexpr uint32_t W1_LBO = W1_ROWS * 16, W23_LBO = W23_ROWS * 16;
+constexpr int BT = 64; // per-layer [b3 (40) | b2 (20) | t | pad]
+constexpr int NTHREADS = 384; // 2 epilogue warpgroups + 1 control warpgroup
+constexpr uint32_t SM_W1 = 0, SM_W23 = SM_W1 + W1_BYTES, SM_X = SM_W23 + W23_BYTES,
+                   SM_GX = SM_X + 14 * 128 * 4, SM_RED = SM_GX + 14 * 128 * 4,
+                   SM_BAR = SM_RED + 128, SM_TMEM = SM_BAR + 8 * 8, SM_TOTAL = SM_TMEM + 16;
 
-int tc_pack(TcModel &tc, int K, int Z, int V, int L, const double *, const double *) {
-    tc.ready = false;
-    tc.K = K; tc.Z = Z; tc.V = V; tc.L = L;
+struct TcKArgs {
+    TcArgs a;
+    const unsigned char *w; // [L][LAYER_BYTES]
+    const float *bt;        // [L][BT]
+    float *x_state, *v_state;
+};
+
+enum { B_W1F = 0, B_W23F = 1, B_U1 = 2, B_U2 = 3, B_AREADY = 4, B_ZREADY = 5 };
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                   "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void split(float v, float &hi, float &lo) {
+    hi = tc::tf32_rna(v);
+    lo = tc::tf32_rna(v - hi);
+}
+
+__global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
+    extern __shared__ __align__(1024) unsigned char sm[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sm + SM_BAR);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sm + SM_TMEM);
+    float *sX = reinterpret_cast<float *>(sm + SM_X);
+    float *sGX = reinterpret_cast<float *>(sm + SM_GX);
+    const TcArgs &a = p.a;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int L0 = a.l_begin, L1 = a.l_end, NL = L1 - L0;
+
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[B_W1F], 1);
+        mbar_init(&bars[B_W23F], 1);
+        mbar_init(&bars[B_U1], 1);
+        mbar_init(&bars[B_U2], 1);
+        mbar_init(&bars[B_AREADY], 256);
+        mbar_init(&bars[B_ZREADY], 256);
+        fence_mbar_init();
+    }
+    if (warp == 8) {
+        tc::tmem_alloc(tmem_slot, TMEM_COLS);
+        tc::tmem_relinquish();
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tbase = *tmem_slot;
+    const long my_tiles = a.n_tiles > blockIdx.x ? (a.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const long total_it = my_tiles * NL;
+
+    // Registers: the control warpgroup needs few, the epilogue warpgroups hold
+    // each sample's Gram matrix (105 floats per thread) + state. setmaxnreg is
+    // the first statement of each role branch so ptxas allocates per role.
+    if (warp >= 8) {
+        // ================= producer + MMA issuer (one thread) =================
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory");
+        if (warp == 8 && lane == 0) {
+            const uint32_t sw1 = smem_u32(sm + SM_W1), sw23 = smem_u32(sm + SM_W23);
+            auto load_w1 = [&](int l) {
+                mbar_arrive_expect_tx(&bars[B_W1F], W1_BYTES);
+                bulk_g2s_chunked(sm + SM_W1, p.w + static_cast<size_t>(l) * LAYER_BYTES, W1_BYTES,
+                                 &bars[B_W1F]);
+            };
+            auto load_w23 = [&](int l) {
+                mbar_arrive_expect_tx(&bars[B_W23F], W23_BYTES);
+                bulk_g2s_chunked(sm + SM_W23,
+                                 p.w + static_cast<size_t>(l) * LAYER_BYTES + W1_BYTES, W23_BYTES,
+                                 &bars[B_W23F]);
+            };
+            if (total_it > 0) { load_w1(L0); load_w23(L0); }
+            const uint32_t id1 = tc::idesc_tf32(128, W1_ROWS);
+            const uint32_t id2 = tc::idesc_tf32(128, W23_ROWS);
+            for (long it = 0; it < total_it; ++it) {
+                const uint32_t ph = static_cast<uint32_t>(it & 1);
+                const int l = L0 + static_cast<int>(it % NL);
+                const int lnext = L0 + static_cast<int>((it + 1) % NL);
+                // ---- W1: U1 = [q 1 | x gx v] . W1'^T ----
+                mbar_wait_guard(&bars[B_W1F], ph);
+                mbar_wait_guard(&bars[B_AREADY], ph);
+                tc::fence_after();
+                {
+                    uint32_t acc = 0;
+#pragma unroll 1
+                    for (int kk = 0; kk < 13; ++kk) {
+                        const uint32_t ahi = kk < 3 ? C_QHI + 8 * kk : C_DYN + 8 * (kk - 3);
+                        const uint32_t alo = kk < 3 ? C_QLO + 8 * kk : C_DYNLO + 8 * (kk - 3);
+                        const uint64_t bhi = tc::smem_desc(sw1 + 2 * kk * W1_LBO, W1_LBO, 128);
+                        const uint64_t blo =
+                            tc::smem_desc(sw1 + W1_HALF + 2 * kk * W1_LBO, W1_LBO, 128);
+                        tc::mma_tf32_ts(tbase + C_U1, tbase + ahi, bhi, id1, acc);
+                        tc::mma_tf32_ts(tbase + C_U1, tbase + ahi, blo, id1, 1);
+                        tc::mma_tf32_ts(tbase + C_U1, tbase + alo, bhi, id1, 1);
+                        acc = 1;
+                    }
+                }
+                tc::commit(&bars[B_U1]);
+                mbar_wait_guard(&bars[B_U1], ph); // W1 slot free
+                if (it + 1 < total_it) load_w1(lnext);
+                // ---- W23: U2V = z . [W3; W2]^T ----
+                mbar_wait_guard(&bars[B_W23F], ph);
+                mbar_wait_guard(&bars[B_ZREADY], ph);
+                tc::fence_after();
+                {
+                    uint32_t acc = 0;
+#pragma unroll 1
+                    for (int kk = 0; kk < 20; ++kk) {
+                        const uint64_t bhi = tc::smem_desc(sw23 + 2 * kk * W23_LBO, W23_LBO, 128);
+                        const uint64_t blo =
+                            tc::smem_desc(sw23 + W23_HALF + 2 * kk * W23_LBO, W23_LBO, 128);
+                        tc::mma_tf32_ts(tbase + C_U2, tbase + C_U1 + 8 * kk, bhi, id2, acc);
+                        tc::mma_tf32_ts(tbase + C_U2, tbase + C_U1 + 8 * kk, blo, id2, 1);
+                        tc::mma_tf32_ts(tbase + C_U2, tbase + C_ZLO + 8 * kk, bhi, id2, 1);
+                        acc = 1;
+                    }
+                }
+                tc::commit(&bars[B_U2]);
+                mbar_wait_guard(&bars[B_U2], ph); // W23 slot free
+                if (it + 1 < total_it) load_w23(lnext);
+            }
+        }
+    } else {
+        // ========================= epilogue warps ==========================
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 232;" ::: "memory");
+        const bool isA = warp < 4;
+        const int quad = warp & 3;
+        const int col = quad * 32 + lane; // sample within the tile == TMEM lane
+        const uint32_t trow = tbase + (static_cast<uint32_t>(quad * 32) << 16);
+        const int pair_bar = 1 + quad;
+        long it = 0;
+        for (long ti = 0; ti < my_tiles; ++ti) {
+            const long tile = blockIdx.x + ti * gridDim.x;
+            const long gt = a.tile0 + tile;
+            const long s = tile * TILE + col;
+            const bool live = s < a.n;
+            // ---- tile init: Gram entries into registers, state, q ----
+            float g[NA];
+            const float *gps = a.gp + gt * NG * TILE + col;
+            const int e0 = isA ? 0 : NA;
+#pragma unroll
+            for (int e = 0; e < NA; ++e) g[e] = __ldg(gps + (e0 + e) * TILE);
+            float x[KX];   // A: full x_hat; B: x[6..19] copy
+            double loss = 0.0;
+            uint32_t xm = 0;
+            double dnm = 1.0;
+            if (isA) {
+#pragma unroll
+                for (int k = 0; k < KX; ++k) x[k] = (p.x_state && live) ? p.x_state[s * KX + k] : 0.f;
+                xm = a.xmask[gt * TILE + col];
+                dnm = a.denom[gt * TILE + col];
+            } else {
+                float qh[24], ql[24];
+#pragma unroll
+                for (int k = 0; k < KX; ++k) split(a.q32[(gt * KX + k) * TILE + col], qh[k], ql[k]);
+                qh[20] = 1.f; ql[20] = 0.f;
+#pragma unroll
+                for (int k = 21; k < 24; ++k) { qh[k] = 0.f; ql[k] = 0.f; }
+                float t16[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) t16[k] = qh[k];
+                tc::st16(trow + C_QHI, t16);
+                tc::st8(trow + C_QHI + 16, qh + 16);
+#pragma unroll
+                for (int k = 0; k < 16; ++k) t16[k] = ql[k];
+                tc::st16(trow + C_QLO, t16);
+                tc::st8(trow + C_QLO + 16, ql + 16);
+            }
+            for (int l = L0; l < L1; ++l, ++it) {
+                const uint32_t ph = static_cast<uint32_t>(it & 1);
+                // ---- prep: G x_hat (split over A and B), write A_dyn ----
+                if (isA) {
+#pragma unroll
+                    for (int j = 6; j < KX; ++j) sX[(j - 6) * 128 + col] = x[j];
+                }
+                tc::named_bar(pair_bar, 64);
+                float gx[KX];
+                if (isA) {
+#pragma unroll
+                    for (int k = 0; k < KX; ++k) gx[k] = 0.f;
+                    int e = 0;
+#pragma unroll
+                    for (int r = 0; r < 6; ++r)
+#pragma unroll
+                        for (int c = r; c < KX; ++c, ++e) {
+                            gx[r] = fmaf(g[e], x[c], gx[r]);
+                            if (c != r) gx[c] = fmaf(g[e], x[r], gx[c]);
+                        }
+                } else {
+#pragma unroll
+                    for (int j = 6; j < KX; ++j) x[j] = sX[(j - 6) * 128 + col];
+                    float part[KX];
+#pragma unroll
+                    for (int k = 6; k < KX; ++k) part[k] = 0.f;
+                    int e = 0;
+#pragma unroll
+                    for (int r = 6; r < KX; ++r)
+#pragma unroll
+                        for (int c = r; c < KX; ++c, ++e) {
+                            part[r] = fmaf(g[e], x[c], part[r]);
+                            if (c != r) part[c] = fmaf(g[e], x[r], part[c]);
+                        }
+#pragma unroll
+                    for (int k = 6; k < KX; ++k) sGX[(k - 6) * 128 + col] = part[k];
+                }
+                tc::named_bar(pair_bar, 64);
+                if (isA) {
+#pragma unroll
+                    for (int k = 6; k < KX; ++k) gx[k] += sGX[(k - 6) * 128 + col];
+#pragma unroll
+                    for (int c = 0; c < 5; ++c) {
+                        float hi[8], lo[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const int j = 8 * c + k;
+                            split(j < KX ? x[j < KX ? j : 0] : gx[j >= KX ? j - KX : 0], hi[k], lo[k]);
+                        }
+                        tc::st8(trow + C_DYN + 8 * c, hi);
+                        tc::st8(trow + C_DYNLO + 8 * c, lo);
+                    }
+                } else {
+                    // v_l: the state on entry (l == L0) or v' + b3 of layer l-1,
+                    // still resident in the U2V accumulator columns [0, 40)
+                    const float *btp = p.bt + static_cast<size_t>(l > L0 ? l - 1 : 0) * BT;
+#pragma unroll
+                    for (int c = 0; c < 5; ++c) {
+                        float v8[8], hi[8], lo[8];
+                        if (l == L0) {
+#pragma unroll
+                            for (int k = 0; k < 8; ++k)
+                                v8[k] = (p.v_state && live) ? p.v_state[s * VV + 8 * c + k] : 0.f;
+                        } else {
+                            tmem_ld8(trow + C_U2 + 8 * c, v8);
+#pragma unroll
+                            for (int k = 0; k < 8; ++k) v8[k] += __ldg(btp + 8 * c + k);
+                        }
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) split(v8[k], hi[k], lo[k]);
+                        tc::st8(trow + C_DYN + 40 + 8 * c, hi);
+                        tc::st8(trow + C_DYNLO + 40 + 8 * c, lo);
+                    }
+                }
+                tc::wait_st();
+                tc::fence_before();
+                mbar_arrive(&bars[B_AREADY]);
+
+                // ---- epilogue 1: z = relu(U1) -> z_hi (in place), z_lo ----
+                mbar_wait_guard(&bars[B_U1], ph);
+                tc::fence_after();
+                {
+                    const int c0 = isA ? 0 : 80;
+#pragma unroll 1
+                    for (int c = c0; c < c0 + 80; c += 16) {
+                        float u[16], zh[16], zl[16];
+                        tc::ld16(trow + C_U1 + c, u);
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) split(u[k] > 0.f ? u[k] : 0.f, zh[k], zl[k]);
+                        tc::st16(trow + C_U1 + c, zh);
+                        tc::st16(trow + C_ZLO + c, zl);
+                    }
+                }
+                tc::wait_st();
+                tc::fence_before();
+                mbar_arrive(&bars[B_ZREADY]);
+
+                // ---- epilogue 2: x_hat = psi_t(u2 + b2), v = v' + b3, loss ----
+                mbar_wait_guard(&bars[B_U2], ph);
+                tc::fence_after();
+                const float *bt = p.bt + static_cast<size_t>(l) * BT;
+                if (isA) {
+                    float u[16], w[16];
+                    tc::ld16(trow + C_U2 + 32, u);  // cols 32..47: u2[0..7] at 40..47
+                    tc::ld16(trow + C_U2 + 48, w);  // cols 48..63: u2[8..19] at 48..59
+                    const float t = __ldg(bt + 60);
+                    double err = 0.0;
+#pragma unroll
+                    for (int k = 0; k < KX; ++k) {
+                        const float uu = (k < 8 ? u[8 + k] : w[k - 8]) + __ldg(bt + 40 + k);
+                        const float xn = uu <= -t ? -1.f : (uu >= t ? 1.f : __fdiv_rn(uu, t));
+                        x[k] = xn;
+                        const double d = ((xm >> k) & 1u ? 1.0 : -1.0) - static_cast<double>(xn);
+                        err += d * d;
+                    }
+                    loss += a.lnk[l] * err / dnm;
+                    if (a.xhat && live) {
+                        float4 *o = reinterpret_cast<float4 *>(a.xhat + (s * NL + (l - L0)) * KX);
+#pragma unroll
+                        for (int k = 0; k < KX / 4; ++k)
+                            o[k] = make_float4(x[4 * k], x[4 * k + 1], x[4 * k + 2], x[4 * k + 3]);
+                    }
+                }
+            }
+            // ---- tile end: state out, per-tile partials (A warps) ----
+            if (p.x_state && live) {
+                if (isA) {
+#pragma unroll
+                    for (int k = 0; k < KX; ++k) p.x_state[s * KX + k] = x[k];
+                } else {
+                    const float *btp = p.bt + static_cast<size_t>(L1 - 1) * BT;
+#pragma unroll
+                    for (int c = 0; c < 5; ++c) {
+                        float v8[8];
+                        tmem_ld8(trow + C_U2 + 8 * c, v8);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) p.v_state[s * VV + 8 * c + k] = v8[k] + __ldg(btp + 8 * c + k);
+                    }
+                }
+            }
+            if (isA) {
+                long long errs = 0;
+#pragma unroll
+                for (int k = 0; k < KX; ++k) errs += (x[k] >= 0.f) != (((xm >> k) & 1u) != 0);
+                if (!live) { loss = 0.0; errs = 0; }
+                loss = warp_sum(loss);
+                errs = warp_sum(errs);
+                double *rl = reinterpret_cast<double *>(sm + SM_RED);
+                long long *re = reinterpret_cast<long long *>(sm + SM_RED + 64);
+                if (lane == 0) { rl[quad] = loss; re[quad] = errs; }
+                tc::named_bar(5, 128);
+                if (threadIdx.x == 0) {
+                    a.tile_loss[gt] = (rl[0] + rl[1]) + (rl[2] + rl[3]);
+                    a.tile_err[gt] = re[0] + re[1] + re[2] + re[3];
+                }
+                tc::named_bar(5, 128);
+            }
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 8) tc::tmem_dealloc(tbase, TMEM_COLS);
+}
+
+// ---- host: packing into the smem images -------------------------------------
+float rna_tf32_host(float v) {
+    uint32_t b;
+    std::memcpy(&b, &v, 4);
+    if ((b & 0x7f800000u) == 0x7f800000u) return v;
+    b = (b + 0x1000u) & 0xffffe000u;
+    float r;
+    std::memcpy(&r, &b, 4);
+    return r;
+}
+
+// offset (floats) of element (n, k) in a no-swizzle K-major B image with NR rows
+inline size_t img_off(int n, int k, int NR) {
+    return static_cast<size_t>(k / 4) * NR * 4 + (n / 8) * 32 + (n % 8) * 4 + (k % 4);
+}
+
+} // namespace
+
+int tc_prepare() {
+    cudaError_t e = cudaFuncSetAttribute(k_stack_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(SM_TOTAL));
+    if (e != cudaSuccess)
+        return fail(DETNET_ERR_CUDA, "tcgen05 kernel smem attribute: %s", cudaGetErrorString(e));
     return 0;
 }
 
-int tc_launch(const TcModel &, const TcArgs &, cudaStream_t) {
-    return fail(DETNET_ERR_UNSUPPORTED, "tcgen05 path not available");
+int tc_pack(TcModel &tc, int K, int Z, int V, int L, const double *params, const double *masks) {
+    tc.K = K; tc.Z = Z; tc.V = V; tc.L = L;
+    tc.ready = false;
+    if (K != KX || Z != ZH || V != VV) return 0; // other dims use the SIMT path
+    const int IN = 3 * K + V;
+    const long P = Z * IN + Z + static_cast<long>(K) * Z + K + static_cast<long>(V) * Z + V + 1;
+    std::vector<float> img(static_cast<size_t>(L) * LAYER_BYTES / 4, 0.f);
+    std::vector<float> bt(static_cast<size_t>(L) * BT, 0.f);
+    for (int l = 0; l < L; ++l) {
+        const double *pr = params + l * P;
+        const double *mk = masks ? masks + l * P : nullptr;
+        auto w = [&](long off) { return static_cast<float>(pr[off] * (mk ? mk[off] : 1.0)); };
+        const long oW1 = 0, ob1 = static_cast<long>(Z) * IN, oW2 = ob1 + Z,
+                   ob2 = oW2 + static_cast<long>(K) * Z, oW3 = ob2 + K,
+                   ob3 = oW3 + static_cast<long>(V) * Z, ot = ob3 + V;
+        float *L1hi = img.data() + static_cast<size_t>(l) * LAYER_BYTES / 4;
+        float *L1lo = L1hi + W1_HALF / 4;
+        float *L2hi = L1hi + W1_BYTES / 4;
+        float *L2lo = L2hi + W23_HALF / 4;
+        for (int i = 0; i < W1_ROWS; ++i)
+            for (int k = 0; k < W1_K; ++k) {
+                float val = 0.f;
+                if (k < KX) val = w(oW1 + i * IN + k);
+                else if (k == KX) val = w(ob1 + i);
+                else if (k >= 24) val = w(oW1 + i * IN + (k - 4));
+                const float hi = rna_tf32_host(val);
+                L1hi[img_off(i, k, W1_ROWS)] = hi;
+                L1lo[img_off(i, k, W1_ROWS)] = rna_tf32_host(val - hi);
+            }
+        for (int r = 0; r < W23_ROWS; ++r)
+            for (int i = 0; i < W23_K; ++i) {
+                float val = 0.f;
+                if (r < VV) val = w(oW3 + r * Z + i);
+                else if (r < VV + KX) val = w(oW2 + (r - VV) * Z + i);
+                const float hi = rna_tf32_host(val);
+                L2hi[img_off(r, i, W23_ROWS)] = hi;
+                L2lo[img_off(r, i, W23_ROWS)] = rna_tf32_host(val - hi);
+            }
+        float *b = bt.data() + static_cast<size_t>(l) * BT;
+        for (int k = 0; k < VV; ++k) b[k] = w(ob3 + k);
+        for (int k = 0; k < KX; ++k) b[VV + k] = w(ob2 + k);
+        b[60] = static_cast<float>(pr[ot]);
+    }
+    const size_t wbytes = img.size() * 4, bbytes = bt.size() * 4;
+    if (tc.w.ensure(wbytes + bbytes)) return fail(DETNET_ERR_CUDA, "cudaMalloc tc weights");
+    if (cudaMemcpy(tc.w.p, img.data(), wbytes, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(static_cast<char *>(tc.w.p) + wbytes, bt.data(), bbytes,
+                   cudaMemcpyHostToDevice) != cudaSuccess)
+        return fail(DETNET_ERR_CUDA, "upload tc weights");
+    tc.rec_bytes = LAYER_BYTES;
+    tc.ready = true;
+    return 0;
 }
 
-void tc_release(TcModel &tc) { tc.w.release(); tc.ready = false; }
+int tc_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cudaStream_t st) {
+    if (!tc.ready) return fail(DETNET_ERR_UNSUPPORTED, "tcgen05 path not packed for these dims");
+    TcKArgs p;
+    p.a = a;
+    p.w = static_cast<const unsigned char *>(tc.w.p);
+    p.bt = reinterpret_cast<const float *>(static_cast<const char *>(tc.w.p) +
+                                           static_cast<size_t>(tc.L) * LAYER_BYTES);
+    p.x_state = xs;
+    p.v_state = vs;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = static_cast<int>(std::min<long>(a.n_tiles, sms));
+    if (grid <= 0) return 0;
+    k_stack_tc<<<grid, NTHREADS, SM_TOTAL, st>>>(p);
+    return 0;
+}
+
+int tc_launch(const TcModel &tc, const TcArgs &a, cudaStream_t st) {
+    return tc_launch_state(tc, a, nullptr, nullptr, st);
+}
+
+void tc_release(TcModel &tc) {
+    tc.w.release();
+    tc.ready = false;
+}
 
 } // namespace detnet

@@ -107,6 +107,7 @@ _lib.detnet_record_size.argtypes = [C.c_int, C.c_int, C.c_int]
 _lib.detnet_model_create.argtypes = [_vp, C.POINTER(_ModelDesc), C.POINTER(_vp)]
 _lib.detnet_model_update.argtypes = [_vp, C.POINTER(_ModelDesc)]
 _lib.detnet_model_destroy.argtypes = [_vp]
+_lib.detnet_model_path.argtypes = [_vp]
 _lib.detnet_model_flops_per_detection.restype = C.c_longlong
 _lib.detnet_model_flops_per_detection.argtypes = [_vp, C.c_int]
 _lib.detnet_batch_evaluate.argtypes = [_vp, C.c_long, _vp, _vp, _vp, C.c_int, _vp,
@@ -284,6 +285,10 @@ class Model:
             self.close()
         except Exception:
             pass
+
+    @property
+    def path_name(self):
+        return {1: "simt-fp32", 2: "tcgen05-3xtf32"}[_lib.detnet_model_path(self._h)]
 
     def flops_per_detection(self, include_preprocess=True):
         return _lib.detnet_model_flops_per_detection(self._h, int(include_preprocess))

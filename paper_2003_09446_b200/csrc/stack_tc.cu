@@ -11,9 +11,10 @@
 //
 // On-chip residency (one CTA per SM, 384 threads):
 //  * TMEM (512 cols x 128 lanes; lane = sample of the tile):
-//      [  0,160) U1 accumulator, overwritten in place by z_hi
-//      [160,240) A_dyn hi = [x | gx | v] hi   } reused as z_lo [160,320)
-//      [240,320) A_dyn lo                      } after the W1 MMAs complete
+//      [  0,160) U1 accumulator (two N=80 halves), overwritten in place by z_hi
+//      [160,240) A_dyn hi = [x | gx | v] hi   } z_lo of units 80-159 reuses
+//      [240,320) A_dyn lo                      } [160,240) once W1 is done
+//      z_lo of units 0-79: [408,416) + [440,512) (written during W1 half 2)
 //      [320,384) U2V accumulator: [v' (40) | u2 (20) | pad]
 //      [384,408) [q | 1 | 0 0 0] hi,  [416,440) lo   (constant per tile)
 //  * SMEM: the current layer's W1 (hi+lo, 130 KB) and [W3;W2] (hi+lo, 80 KB)
@@ -29,6 +30,8 @@
 // producer + single-thread MMA issuer (warps 9-11 complete its warpgroup so
 // setmaxnreg can move registers to the epilogue warpgroups).
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -40,15 +43,21 @@ namespace {
 
 constexpr int KX = 20, ZH = 160, VV = 40, NG = 210;
 constexpr int NA = 105; // Gram entries held by thread A (rows 0..5)
-constexpr int C_U1 = 0, C_DYN = 160, C_DYNLO = 240, C_ZLO = 160, C_U2 = 320, C_QHI = 384,
+constexpr int C_U1 = 0, C_DYN = 160, C_DYNLO = 240, C_U2 = 320, C_QHI = 384,
               C_QLO = 416, TMEM_COLS = 512;
+// z_lo column of hidden unit j (groups of 8): units 0-79 are written while the
+// second W1 half still reads A_dyn, so they live in the otherwise free
+// columns [408,416) and [440,512); units 80-159 reuse A_dyn hi [160,240).
+__host__ __device__ constexpr int zlo_col(int j) {
+    return j >= 80 ? 160 + (j - 80) : (j < 8 ? 408 + j : 440 + (j - 8));
+}
 constexpr int W1_ROWS = 160, W1_K = 104, W23_ROWS = 64, W23_K = 160;
 constexpr uint32_t W1_HALF = W1_ROWS * W1_K * 4;     // 66,560 B per hi/lo
 constexpr uint32_t W23_HALF = W23_ROWS * W23_K * 4;  // 40,960 B
 constexpr uint32_t W1_BYTES = 2 * W1_HALF, W23_BYTES = 2 * W23_HALF;
 constexpr uint32_t LAYER_BYTES = W1_BYTES + W23_BYTES; // 215,040 B
 constexpr uint32_t W1_LBO = W1_ROWS * 16, W23_LBO = W23_ROWS * 16;
-constexpr int BT = 64; // per-layer [b3 (40) | b2 (20) | t | pad]
+constexpr int BT = 64; // per-layer [b3 (40) | b2 (20) | t | 1/t | pad]
 constexpr int NTHREADS = 384; // 2 epilogue warpgroups + 1 control warpgroup
 constexpr uint32_t SM_W1 = 0, SM_W23 = SM_W1 + W1_BYTES, SM_X = SM_W23 + W23_BYTES,
                    SM_GX = SM_X + 14 * 128 * 4, SM_RED = SM_GX + 14 * 128 * 4,
@@ -59,9 +68,16 @@ struct TcKArgs {
     const unsigned char *w; // [L][LAYER_BYTES]
     const float *bt;        // [L][BT]
     float *x_state, *v_state;
+    long long *trace; // optional debug timeline (DETNET_TC_TRACE): CTA 0, tile 0
 };
 
-enum { B_W1F = 0, B_W23F = 1, B_U1 = 2, B_U2 = 3, B_AREADY = 4, B_ZREADY = 5 };
+#define TRACE(ev, l)                                                                           \
+    do {                                                                                       \
+        if (p.trace && blockIdx.x == 0 && (l) - L0 < 8 && trace_on)                            \
+            p.trace[((l) - L0) * 16 + (ev)] = clock64();                                       \
+    } while (0)
+
+enum { B_W1F = 0, B_W23F = 1, B_U1A = 2, B_U1B = 3, B_U2 = 4, B_AREADY = 5, B_ZA = 6, B_ZB = 7 };
 
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
     uint32_t r[8];
@@ -74,16 +90,51 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
     for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 3xTF32 split: hi = rna_tf32(v); lo = v - hi is exact in FP32 and the tensor
+// core drops its low 13 bits (|lo| <= 2^-11 |v|, so the error is <= 2^-21 |v|).
 __device__ __forceinline__ void split(float v, float &hi, float &lo) {
     hi = tc::tf32_rna(v);
-    lo = tc::tf32_rna(v - hi);
+    lo = v - hi;
+}
+
+// Epilogue 2 for one layer: load the whole U2V row (64 columns, one wait),
+// x_hat = psi_t(u2 + b2) from columns [40, 60) and, on the B side, v = v' + b3
+// from columns [0, 40).
+template <bool WITH_V>
+__device__ __forceinline__ void epi2_layer(uint32_t trow, const float *bt, float (&x)[KX],
+                                           float (&v)[VV]) {
+    uint32_t r[4][16];
+    if (WITH_V) {
+        tc::ld16_nw(trow + C_U2, r[0]);
+        tc::ld16_nw(trow + C_U2 + 16, r[1]);
+    }
+    tc::ld16_nw(trow + C_U2 + 32, r[2]);
+    tc::ld16_nw(trow + C_U2 + 48, r[3]);
+    float b[60];
+    const float4 *b4 = reinterpret_cast<const float4 *>(bt);
+#pragma unroll
+    for (int k = WITH_V ? 0 : 10; k < 15; ++k) {
+        const float4 q = __ldg(b4 + k);
+        b[4 * k] = q.x; b[4 * k + 1] = q.y; b[4 * k + 2] = q.z; b[4 * k + 3] = q.w;
+    }
+    const float2 tt = __ldg(reinterpret_cast<const float2 *>(bt + 60)); // (t, 1/t)
+    tc::wait_ld();
+#pragma unroll
+    for (int k = 0; k < KX; ++k) {
+        const int c = 40 + k;
+        const float uu = __uint_as_float(r[c / 16][c % 16]) + b[40 + k];
+        x[k] = uu <= -tt.x ? -1.f : (uu >= tt.x ? 1.f : uu * tt.y);
+    }
+    if (WITH_V) {
+#pragma unroll
+        for (int k = 0; k < VV; ++k) v[k] = __uint_as_float(r[k / 16][k % 16]) + b[k];
+    }
 }
 
 __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
     extern __shared__ __align__(1024) unsigned char sm[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(sm + SM_BAR);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sm + SM_TMEM);
-    float *sX = reinterpret_cast<float *>(sm + SM_X);
     float *sGX = reinterpret_cast<float *>(sm + SM_GX);
     const TcArgs &a = p.a;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -92,10 +143,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
     if (threadIdx.x == 0) {
         mbar_init(&bars[B_W1F], 1);
         mbar_init(&bars[B_W23F], 1);
-        mbar_init(&bars[B_U1], 1);
+        mbar_init(&bars[B_U1A], 1);
+        mbar_init(&bars[B_U1B], 1);
         mbar_init(&bars[B_U2], 1);
         mbar_init(&bars[B_AREADY], 256);
-        mbar_init(&bars[B_ZREADY], 256);
+        mbar_init(&bars[B_ZA], 256);
+        mbar_init(&bars[B_ZB], 256);
         fence_mbar_init();
     }
     if (warp == 8) {
@@ -113,70 +166,106 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
     // each sample's Gram matrix (105 floats per thread) + state. setmaxnreg is
     // the first statement of each role branch so ptxas allocates per role.
     if (warp >= 8) {
-        // ================= producer + MMA issuer (one thread) =================
+        // 4 x 40 + 8 x 232 registers per lane = the 384 x 168 the CTA launches with
         asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory");
-        if (warp == 8 && lane == 0) {
+        if (warp == 8) {
+            // ============ MMA issuer (warp-uniform loop, one elected lane) ============
             const uint32_t sw1 = smem_u32(sm + SM_W1), sw23 = smem_u32(sm + SM_W23);
-            auto load_w1 = [&](int l) {
-                mbar_arrive_expect_tx(&bars[B_W1F], W1_BYTES);
-                bulk_g2s_chunked(sm + SM_W1, p.w + static_cast<size_t>(l) * LAYER_BYTES, W1_BYTES,
-                                 &bars[B_W1F]);
-            };
-            auto load_w23 = [&](int l) {
-                mbar_arrive_expect_tx(&bars[B_W23F], W23_BYTES);
-                bulk_g2s_chunked(sm + SM_W23,
-                                 p.w + static_cast<size_t>(l) * LAYER_BYTES + W1_BYTES, W23_BYTES,
-                                 &bars[B_W23F]);
-            };
-            if (total_it > 0) { load_w1(L0); load_w23(L0); }
-            const uint32_t id1 = tc::idesc_tf32(128, W1_ROWS);
+            const uint32_t id1 = tc::idesc_tf32(128, 80);
             const uint32_t id2 = tc::idesc_tf32(128, W23_ROWS);
+            const uint64_t d1 = tc::smem_desc(sw1, W1_LBO, 128);
+            const uint64_t d23 = tc::smem_desc(sw23, W23_LBO, 128);
+            constexpr uint64_t S1 = (2 * W1_LBO) >> 4, S23 = (2 * W23_LBO) >> 4;
+            constexpr uint64_t H1 = W1_HALF >> 4, H23 = W23_HALF >> 4, NB = (80 / 8 * 128) >> 4;
             for (long it = 0; it < total_it; ++it) {
                 const uint32_t ph = static_cast<uint32_t>(it & 1);
                 const int l = L0 + static_cast<int>(it % NL);
-                const int lnext = L0 + static_cast<int>((it + 1) % NL);
-                // ---- W1: U1 = [q 1 | x gx v] . W1'^T ----
+                const bool trace_on = it < NL && lane == 0;
                 mbar_wait_guard(&bars[B_W1F], ph);
+                TRACE(12, l);
                 mbar_wait_guard(&bars[B_AREADY], ph);
+                TRACE(6, l);
                 tc::fence_after();
-                {
-                    uint32_t acc = 0;
+                // U1 = [q 1 | x gx v] . W1'^T in two N=80 halves (hidden 0-79, 80-159)
 #pragma unroll 1
-                    for (int kk = 0; kk < 13; ++kk) {
-                        const uint32_t ahi = kk < 3 ? C_QHI + 8 * kk : C_DYN + 8 * (kk - 3);
-                        const uint32_t alo = kk < 3 ? C_QLO + 8 * kk : C_DYNLO + 8 * (kk - 3);
-                        const uint64_t bhi = tc::smem_desc(sw1 + 2 * kk * W1_LBO, W1_LBO, 128);
-                        const uint64_t blo =
-                            tc::smem_desc(sw1 + W1_HALF + 2 * kk * W1_LBO, W1_LBO, 128);
-                        tc::mma_tf32_ts(tbase + C_U1, tbase + ahi, bhi, id1, acc);
-                        tc::mma_tf32_ts(tbase + C_U1, tbase + ahi, blo, id1, 1);
-                        tc::mma_tf32_ts(tbase + C_U1, tbase + alo, bhi, id1, 1);
-                        acc = 1;
+                for (int h = 0; h < 2; ++h) {
+                    if (tc::elect_one()) {
+                        const uint32_t tb = tc::opaque32(tbase);
+                        const uint64_t d1h = tc::opaque64(d1 + h * NB);
+                        const uint32_t dcol = tb + C_U1 + 80 * h;
+#pragma unroll
+                        for (int kk = 0; kk < 13; ++kk) {
+                            const uint32_t ahi = kk < 3 ? C_QHI + 8 * kk : C_DYN + 8 * (kk - 3);
+                            const uint32_t alo = kk < 3 ? C_QLO + 8 * kk : C_DYNLO + 8 * (kk - 3);
+                            const uint64_t bhi = d1h + kk * S1;
+                            tc::mma_tf32_ts(dcol, tb + ahi, bhi, id1, kk > 0);
+                            tc::mma_tf32_ts(dcol, tb + ahi, bhi + H1, id1, 1);
+                            tc::mma_tf32_ts(dcol, tb + alo, bhi, id1, 1);
+                        }
+                        tc::commit(&bars[h == 0 ? B_U1A : B_U1B]);
                     }
+                    __syncwarp();
                 }
-                tc::commit(&bars[B_U1]);
-                mbar_wait_guard(&bars[B_U1], ph); // W1 slot free
-                if (it + 1 < total_it) load_w1(lnext);
-                // ---- W23: U2V = z . [W3; W2]^T ----
+                TRACE(7, l);
                 mbar_wait_guard(&bars[B_W23F], ph);
-                mbar_wait_guard(&bars[B_ZREADY], ph);
-                tc::fence_after();
-                {
-                    uint32_t acc = 0;
+                TRACE(13, l);
+                // U2V = z . [W3; W2]^T, K split by the two z halves
 #pragma unroll 1
-                    for (int kk = 0; kk < 20; ++kk) {
-                        const uint64_t bhi = tc::smem_desc(sw23 + 2 * kk * W23_LBO, W23_LBO, 128);
-                        const uint64_t blo =
-                            tc::smem_desc(sw23 + W23_HALF + 2 * kk * W23_LBO, W23_LBO, 128);
-                        tc::mma_tf32_ts(tbase + C_U2, tbase + C_U1 + 8 * kk, bhi, id2, acc);
-                        tc::mma_tf32_ts(tbase + C_U2, tbase + C_U1 + 8 * kk, blo, id2, 1);
-                        tc::mma_tf32_ts(tbase + C_U2, tbase + C_ZLO + 8 * kk, bhi, id2, 1);
-                        acc = 1;
+                for (int h = 0; h < 2; ++h) {
+                    mbar_wait_guard(&bars[h == 0 ? B_ZA : B_ZB], ph);
+                    if (h == 0) TRACE(9, l);
+                    tc::fence_after();
+                    if (tc::elect_one()) {
+                        const uint32_t tb = tc::opaque32(tbase);
+                        const uint64_t d23h = tc::opaque64(d23 + h * 10 * S23);
+#pragma unroll
+                        for (int k2 = 0; k2 < 10; ++k2) {
+                            const int kk = 10 * h + k2;
+                            const uint64_t bhi = d23h + k2 * S23;
+                            const uint32_t zl = h == 0 ? (k2 == 0 ? 408 : 440 + 8 * (k2 - 1))
+                                                       : 160 + 8 * k2;
+                            tc::mma_tf32_ts(tb + C_U2, tb + C_U1 + 8 * kk, bhi, id2, kk > 0);
+                            tc::mma_tf32_ts(tb + C_U2, tb + C_U1 + 8 * kk, bhi + H23, id2, 1);
+                            tc::mma_tf32_ts(tb + C_U2, tb + zl, bhi, id2, 1);
+                        }
+                        if (h == 1) tc::commit(&bars[B_U2]);
                     }
+                    __syncwarp();
                 }
-                tc::commit(&bars[B_U2]);
-                mbar_wait_guard(&bars[B_U2], ph); // W23 slot free
-                if (it + 1 < total_it) load_w23(lnext);
+                TRACE(10, l);
+            }
+        } else if (warp == 9) {
+            // ================ weight producer (one elected lane) ================
+            const bool leader = tc::elect_one();
+            auto load_w1 = [&](int l) {
+                if (leader) {
+                    mbar_arrive_expect_tx(&bars[B_W1F], W1_BYTES);
+                    bulk_g2s_chunked(sm + SM_W1, p.w + static_cast<size_t>(l) * LAYER_BYTES,
+                                     W1_BYTES, &bars[B_W1F]);
+                }
+                __syncwarp();
+            };
+            auto load_w23 = [&](int l) {
+                if (leader) {
+                    mbar_arrive_expect_tx(&bars[B_W23F], W23_BYTES);
+                    bulk_g2s_chunked(sm + SM_W23,
+                                     p.w + static_cast<size_t>(l) * LAYER_BYTES + W1_BYTES,
+                                     W23_BYTES, &bars[B_W23F]);
+                }
+                __syncwarp();
+            };
+            if (total_it > 0) { load_w1(L0); load_w23(L0); }
+            for (long it = 0; it + 1 < total_it; ++it) {
+                const uint32_t ph = static_cast<uint32_t>(it & 1);
+                const int l = L0 + static_cast<int>(it % NL);
+                const int lnext = L0 + static_cast<int>((it + 1) % NL);
+                const bool trace_on = it < NL && lane == 0;
+                mbar_wait_guard(&bars[B_U1B], ph); // both W1 halves consumed
+                TRACE(8, l);
+                load_w1(lnext);
+                mbar_wait_guard(&bars[B_U2], ph); // W23 consumed
+                TRACE(11, l);
+                load_w23(lnext);
             }
         }
     } else {
@@ -199,15 +288,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
             const int e0 = isA ? 0 : NA;
 #pragma unroll
             for (int e = 0; e < NA; ++e) g[e] = __ldg(gps + (e0 + e) * TILE);
-            float x[KX];   // A: full x_hat; B: x[6..19] copy
-            double loss = 0.0;
-            uint32_t xm = 0;
-            double dnm = 1.0;
-            if (isA) {
+            float x[KX], v[VV];
 #pragma unroll
-                for (int k = 0; k < KX; ++k) x[k] = (p.x_state && live) ? p.x_state[s * KX + k] : 0.f;
+            for (int k = 0; k < KX; ++k) x[k] = (p.x_state && live) ? p.x_state[s * KX + k] : 0.f;
+            if (!isA) {
+#pragma unroll
+                for (int k = 0; k < VV; ++k) v[k] = (p.v_state && live) ? p.v_state[s * VV + k] : 0.f;
+            }
+            double wsum = 0.0; // sum_l ln(l+1) ||x - x_hat_l||^2 (divided by denom at the end)
+            uint32_t xm = 0;
+            if (isA) {
                 xm = a.xmask[gt * TILE + col];
-                dnm = a.denom[gt * TILE + col];
             } else {
                 float qh[24], ql[24];
 #pragma unroll
@@ -215,26 +306,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                 qh[20] = 1.f; ql[20] = 0.f;
 #pragma unroll
                 for (int k = 21; k < 24; ++k) { qh[k] = 0.f; ql[k] = 0.f; }
-                float t16[16];
 #pragma unroll
-                for (int k = 0; k < 16; ++k) t16[k] = qh[k];
-                tc::st16(trow + C_QHI, t16);
-                tc::st8(trow + C_QHI + 16, qh + 16);
-#pragma unroll
-                for (int k = 0; k < 16; ++k) t16[k] = ql[k];
-                tc::st16(trow + C_QLO, t16);
-                tc::st8(trow + C_QLO + 16, ql + 16);
+                for (int c = 0; c < 3; ++c) {
+                    tc::st8(trow + C_QHI + 8 * c, qh + 8 * c);
+                    tc::st8(trow + C_QLO + 8 * c, ql + 8 * c);
+                }
             }
             for (int l = L0; l < L1; ++l, ++it) {
                 const uint32_t ph = static_cast<uint32_t>(it & 1);
-                // ---- prep: G x_hat (split over A and B), write A_dyn ----
+                const bool trace_on = ti == 0 && threadIdx.x == 0;
+                TRACE(0, l);
+                // ---- prep: G x_hat (rows 0-5 on A, rows 6-19 on B), write A_dyn ----
                 if (isA) {
-#pragma unroll
-                    for (int j = 6; j < KX; ++j) sX[(j - 6) * 128 + col] = x[j];
-                }
-                tc::named_bar(pair_bar, 64);
-                float gx[KX];
-                if (isA) {
+                    float gx[KX];
 #pragma unroll
                     for (int k = 0; k < KX; ++k) gx[k] = 0.f;
                     int e = 0;
@@ -245,9 +329,30 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                             gx[r] = fmaf(g[e], x[c], gx[r]);
                             if (c != r) gx[c] = fmaf(g[e], x[r], gx[c]);
                         }
-                } else {
+                    // x hi/lo can go out while B finishes its rows
 #pragma unroll
-                    for (int j = 6; j < KX; ++j) x[j] = sX[(j - 6) * 128 + col];
+                    for (int c = 0; c < 2; ++c) {
+                        float hi[8], lo[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) split(x[8 * c + k], hi[k], lo[k]);
+                        tc::st8(trow + C_DYN + 8 * c, hi);
+                        tc::st8(trow + C_DYNLO + 8 * c, lo);
+                    }
+                    tc::named_bar(pair_bar, 64);
+#pragma unroll
+                    for (int k = 6; k < KX; ++k) gx[k] += sGX[(k - 6) * 128 + col];
+#pragma unroll
+                    for (int c = 2; c < 5; ++c) {
+                        float hi[8], lo[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const int j = 8 * c + k;
+                            split(j < KX ? x[j < KX ? j : 0] : gx[j >= KX ? j - KX : 0], hi[k], lo[k]);
+                        }
+                        tc::st8(trow + C_DYN + 8 * c, hi);
+                        tc::st8(trow + C_DYNLO + 8 * c, lo);
+                    }
+                } else {
                     float part[KX];
 #pragma unroll
                     for (int k = 6; k < KX; ++k) part[k] = 0.f;
@@ -261,40 +366,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                         }
 #pragma unroll
                     for (int k = 6; k < KX; ++k) sGX[(k - 6) * 128 + col] = part[k];
-                }
-                tc::named_bar(pair_bar, 64);
-                if (isA) {
-#pragma unroll
-                    for (int k = 6; k < KX; ++k) gx[k] += sGX[(k - 6) * 128 + col];
+                    tc::named_bar(pair_bar, 64);
 #pragma unroll
                     for (int c = 0; c < 5; ++c) {
                         float hi[8], lo[8];
 #pragma unroll
-                        for (int k = 0; k < 8; ++k) {
-                            const int j = 8 * c + k;
-                            split(j < KX ? x[j < KX ? j : 0] : gx[j >= KX ? j - KX : 0], hi[k], lo[k]);
-                        }
-                        tc::st8(trow + C_DYN + 8 * c, hi);
-                        tc::st8(trow + C_DYNLO + 8 * c, lo);
-                    }
-                } else {
-                    // v_l: the state on entry (l == L0) or v' + b3 of layer l-1,
-                    // still resident in the U2V accumulator columns [0, 40)
-                    const float *btp = p.bt + static_cast<size_t>(l > L0 ? l - 1 : 0) * BT;
-#pragma unroll
-                    for (int c = 0; c < 5; ++c) {
-                        float v8[8], hi[8], lo[8];
-                        if (l == L0) {
-#pragma unroll
-                            for (int k = 0; k < 8; ++k)
-                                v8[k] = (p.v_state && live) ? p.v_state[s * VV + 8 * c + k] : 0.f;
-                        } else {
-                            tmem_ld8(trow + C_U2 + 8 * c, v8);
-#pragma unroll
-                            for (int k = 0; k < 8; ++k) v8[k] += __ldg(btp + 8 * c + k);
-                        }
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) split(v8[k], hi[k], lo[k]);
+                        for (int k = 0; k < 8; ++k) split(v[8 * c + k], hi[k], lo[k]);
                         tc::st8(trow + C_DYN + 40 + 8 * c, hi);
                         tc::st8(trow + C_DYNLO + 40 + 8 * c, lo);
                     }
@@ -302,45 +379,53 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                 tc::wait_st();
                 tc::fence_before();
                 mbar_arrive(&bars[B_AREADY]);
+                TRACE(1, l);
 
-                // ---- epilogue 1: z = relu(U1) -> z_hi (in place), z_lo ----
-                mbar_wait_guard(&bars[B_U1], ph);
-                tc::fence_after();
-                {
-                    const int c0 = isA ? 0 : 80;
+                // ---- epilogue 1: z = relu(U1) -> z_hi (in place), z_lo. Each W1 half
+                // (80 hidden units) is shared by A (first 40) and B (last 40).
 #pragma unroll 1
-                    for (int c = c0; c < c0 + 80; c += 16) {
-                        float u[16], zh[16], zl[16];
-                        tc::ld16(trow + C_U1 + c, u);
+                for (int h = 0; h < 2; ++h) {
+                    mbar_wait_guard(&bars[h == 0 ? B_U1A : B_U1B], ph);
+                    if (h == 0) TRACE(2, l);
+                    tc::fence_after();
+                    const int c0 = 80 * h + (isA ? 0 : 40);
+                    uint32_t r[3][16];
+                    tc::ld16_nw(trow + C_U1 + c0, r[0]);
+                    tc::ld16_nw(trow + C_U1 + c0 + 16, r[1]);
+                    tc::ld16_nw(trow + C_U1 + c0 + 32, r[2]); // cols 32..39 used
+                    tc::wait_ld();
+                    float zh[40], zl[40];
 #pragma unroll
-                        for (int k = 0; k < 16; ++k) split(u[k] > 0.f ? u[k] : 0.f, zh[k], zl[k]);
-                        tc::st16(trow + C_U1 + c, zh);
-                        tc::st16(trow + C_ZLO + c, zl);
+                    for (int k = 0; k < 40; ++k) {
+                        const float u = __uint_as_float(r[k / 16][k % 16]);
+                        split(u > 0.f ? u : 0.f, zh[k], zl[k]);
                     }
+#pragma unroll
+                    for (int g8 = 0; g8 < 5; ++g8) {
+                        tc::st8(trow + C_U1 + c0 + 8 * g8, zh + 8 * g8);
+                        tc::st8(trow + zlo_col(c0 + 8 * g8), zl + 8 * g8);
+                    }
+                    tc::wait_st();
+                    tc::fence_before();
+                    mbar_arrive(&bars[h == 0 ? B_ZA : B_ZB]);
                 }
-                tc::wait_st();
-                tc::fence_before();
-                mbar_arrive(&bars[B_ZREADY]);
+                TRACE(3, l);
 
-                // ---- epilogue 2: x_hat = psi_t(u2 + b2), v = v' + b3, loss ----
+                // ---- epilogue 2: x_hat = psi_t(u2 + b2) on both halves; A: loss ----
                 mbar_wait_guard(&bars[B_U2], ph);
+                TRACE(4, l);
                 tc::fence_after();
                 const float *bt = p.bt + static_cast<size_t>(l) * BT;
+                if (isA) epi2_layer<false>(trow, bt, x, v);
+                else epi2_layer<true>(trow, bt, x, v);
                 if (isA) {
-                    float u[16], w[16];
-                    tc::ld16(trow + C_U2 + 32, u);  // cols 32..47: u2[0..7] at 40..47
-                    tc::ld16(trow + C_U2 + 48, w);  // cols 48..63: u2[8..19] at 48..59
-                    const float t = __ldg(bt + 60);
-                    double err = 0.0;
+                    float err = 0.f;
 #pragma unroll
                     for (int k = 0; k < KX; ++k) {
-                        const float uu = (k < 8 ? u[8 + k] : w[k - 8]) + __ldg(bt + 40 + k);
-                        const float xn = uu <= -t ? -1.f : (uu >= t ? 1.f : __fdiv_rn(uu, t));
-                        x[k] = xn;
-                        const double d = ((xm >> k) & 1u ? 1.0 : -1.0) - static_cast<double>(xn);
-                        err += d * d;
+                        const float d = ((xm >> k) & 1u ? 1.f : -1.f) - x[k];
+                        err = fmaf(d, d, err);
                     }
-                    loss += a.lnk[l] * err / dnm;
+                    wsum += a.lnk[l] * static_cast<double>(err);
                     if (a.xhat && live) {
                         float4 *o = reinterpret_cast<float4 *>(a.xhat + (s * NL + (l - L0)) * KX);
 #pragma unroll
@@ -348,6 +433,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                             o[k] = make_float4(x[4 * k], x[4 * k + 1], x[4 * k + 2], x[4 * k + 3]);
                     }
                 }
+                TRACE(5, l);
             }
             // ---- tile end: state out, per-tile partials (A warps) ----
             if (p.x_state && live) {
@@ -355,21 +441,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
 #pragma unroll
                     for (int k = 0; k < KX; ++k) p.x_state[s * KX + k] = x[k];
                 } else {
-                    const float *btp = p.bt + static_cast<size_t>(L1 - 1) * BT;
 #pragma unroll
-                    for (int c = 0; c < 5; ++c) {
-                        float v8[8];
-                        tmem_ld8(trow + C_U2 + 8 * c, v8);
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) p.v_state[s * VV + 8 * c + k] = v8[k] + __ldg(btp + 8 * c + k);
-                    }
+                    for (int k = 0; k < VV; ++k) p.v_state[s * VV + k] = v[k];
                 }
             }
             if (isA) {
                 long long errs = 0;
 #pragma unroll
                 for (int k = 0; k < KX; ++k) errs += (x[k] >= 0.f) != (((xm >> k) & 1u) != 0);
-                if (!live) { loss = 0.0; errs = 0; }
+                double loss = live ? wsum / a.denom[gt * TILE + col] : 0.0;
+                if (!live) errs = 0;
                 loss = warp_sum(loss);
                 errs = warp_sum(errs);
                 double *rl = reinterpret_cast<double *>(sm + SM_RED);
@@ -457,6 +538,7 @@ int tc_pack(TcModel &tc, int K, int Z, int V, int L, const double *params, const
         for (int k = 0; k < VV; ++k) b[k] = w(ob3 + k);
         for (int k = 0; k < KX; ++k) b[VV + k] = w(ob2 + k);
         b[60] = static_cast<float>(pr[ot]);
+        b[61] = static_cast<float>(1.0 / pr[ot]);
     }
     const size_t wbytes = img.size() * 4, bbytes = bt.size() * 4;
     if (tc.w.ensure(wbytes + bbytes)) return fail(DETNET_ERR_CUDA, "cudaMalloc tc weights");
@@ -478,12 +560,34 @@ int tc_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cu
                                            static_cast<size_t>(tc.L) * LAYER_BYTES);
     p.x_state = xs;
     p.v_state = vs;
+    p.trace = nullptr;
+    static long long *trace_buf = nullptr;
+    const bool tracing = std::getenv("DETNET_TC_TRACE") != nullptr;
+    if (tracing) {
+        if (!trace_buf) cudaMalloc(&trace_buf, 8 * 16 * sizeof(long long));
+        cudaMemsetAsync(trace_buf, 0, 8 * 16 * sizeof(long long), st);
+        p.trace = trace_buf;
+    }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int grid = static_cast<int>(std::min<long>(a.n_tiles, sms));
     if (grid <= 0) return 0;
     k_stack_tc<<<grid, NTHREADS, SM_TOTAL, st>>>(p);
+    if (tracing) {
+        long long h[8 * 16];
+        cudaMemcpyAsync(h, trace_buf, sizeof h, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        const char *nm[16] = {"prep0", "a_arr", "u1ok", "z_arr", "u2ok", "epi2end", "C:aready",
+                              "C:w1iss", "C:u1ok", "C:zready", "C:w23iss", "C:u2ok", "C:w1f",
+                              "C:w23f", "", ""};
+        const long long t0 = h[0];
+        for (int l = 0; l < 8; ++l) {
+            std::fprintf(stderr, "layer %d:", l);
+            for (int e = 0; e < 14; ++e) std::fprintf(stderr, " %s=%lld", nm[e], h[l * 16 + e] - t0);
+            std::fprintf(stderr, "\n");
+        }
+    }
     return 0;
 }
 

@@ -54,6 +54,11 @@ void detnet_ctx_destroy(detnet_ctx *ctx);
 const char *detnet_last_error(void);
 /* Kernel-path selection for the dense stack: 0 auto, 1 SIMT FP32, 2 tcgen05 3xTF32. */
 int detnet_ctx_set_path(detnet_ctx *ctx, int path);
+/* Preprocessing mode: 0 (default) FP32 Cholesky + FP64 refinement with the
+ * reference LU as fallback for ill-conditioned samples (FP64-accurate loss
+ * denominators); 1 the reference LU for every sample (bit-identical q, G,
+ * x_tilde and denominators, slower). */
+int detnet_ctx_set_exact_preprocess(detnet_ctx *ctx, int on);
 /* CUDA stream (cudaStream_t) the context launches on; NULL = its own stream. */
 int detnet_ctx_set_stream(detnet_ctx *ctx, void *stream);
 void *detnet_ctx_stream(detnet_ctx *ctx);

@@ -19,6 +19,7 @@
 #include "common.cuh"
 #include "k_generate.cuh"
 #include "k_preprocess.cuh"
+#include "k_prep_fast.cuh"
 #include "k_stack_simt.cuh"
 #include "engine.hpp"
 
@@ -29,14 +30,33 @@ namespace detnet {
 // ---- dims dispatch --------------------------------------------------------
 using PreFn = void (*)(dim3, dim3, size_t, cudaStream_t, long, int, const float *, const float *,
                        const int8_t *, float *, float *, double *, uint32_t *, uint8_t *,
-                       unsigned long long *);
+                       unsigned long long *, const long *, const int *);
 using SimtFn = void (*)(dim3, dim3, size_t, cudaStream_t, const StackArgs &);
 
 template <int K>
 void launch_pre(dim3 g, dim3 b, size_t sm, cudaStream_t st, long n, int N, const float *H,
                 const float *y, const int8_t *x, float *gp, float *q32, double *dn, uint32_t *xm,
-                uint8_t *fl, unsigned long long *sing) {
-    k_preprocess<K><<<g, b, sm, st>>>(n, N, H, y, x, gp, q32, dn, xm, fl, sing);
+                uint8_t *fl, unsigned long long *sing, const long *list, const int *cnt) {
+    k_preprocess<K><<<g, b, sm, st>>>(n, N, H, y, x, gp, q32, dn, xm, fl, sing, list, cnt);
+}
+
+using FastFn = void (*)(dim3, dim3, size_t, cudaStream_t, long, int, const float *, const float *,
+                        const int8_t *, float *, float *, double *, uint32_t *, uint8_t *, int *,
+                        long *);
+
+template <int K>
+void launch_fast(dim3 g, dim3 b, size_t sm, cudaStream_t st, long n, int N, const float *H,
+                 const float *y, const int8_t *x, float *gp, float *q32, double *dn, uint32_t *xm,
+                 uint8_t *fl, int *fbc, long *fbl) {
+    k_prep_fast<K><<<g, b, sm, st>>>(n, N, H, y, x, gp, q32, dn, xm, fl, fbc, fbl);
+}
+
+template <int K> int set_fast_smem() {
+    return cudaFuncSetAttribute(k_prep_fast<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(gram_entries(K) * PREP_FAST_SAMPLES * 4)) ==
+                   cudaSuccess
+               ? 0
+               : -1;
 }
 
 template <int K, int Z, int V>
@@ -57,11 +77,15 @@ struct DimsEntry {
     PreFn pre;
     SimtFn simt;
     int (*prep)();
+    FastFn fast;           // nullptr: exact preprocessing only
+    int (*prep_fast)();
 };
 
-#define DETNET_DIMS(K, Z, V) {K, Z, V, launch_pre<K>, launch_simt<K, Z, V>, set_simt_smem<K, Z, V>}
+#define DETNET_DIMS(K, Z, V) {K, Z, V, launch_pre<K>, launch_simt<K, Z, V>, set_simt_smem<K, Z, V>, nullptr, nullptr}
 const DimsEntry kDims[] = {
-    DETNET_DIMS(20, 160, 40), DETNET_DIMS(2, 16, 4),  DETNET_DIMS(3, 24, 6),
+    {20, 160, 40, launch_pre<20>, launch_simt<20, 160, 40>, set_simt_smem<20, 160, 40>,
+     launch_fast<20>, set_fast_smem<20>},
+    DETNET_DIMS(2, 16, 4),  DETNET_DIMS(3, 24, 6),
     DETNET_DIMS(4, 32, 8),    DETNET_DIMS(6, 48, 12), DETNET_DIMS(8, 64, 16),
 };
 #undef DETNET_DIMS
@@ -162,13 +186,35 @@ int run_pre(detnet_model *m, cudaStream_t st, long s0, long cnt, long n_total, c
     const long t0 = s0 / TILE;
     const int N = m->N;
     const size_t smem = static_cast<size_t>(4) * (N * K + N + K * K + K) * sizeof(double);
-    const int blocks = static_cast<int>(std::min<long>((cnt + 3) / 4, 148L * 32));
-    {
+    if (m->dims->fast && !c->exact_pre) {
+        // fast path + exact LU for the samples it flags (device-side list)
+        if (c->fb_list.ensure(sizeof(long) * cnt) || c->fb_count.ensure(sizeof(int)))
+            return fail(DETNET_ERR_CUDA, "fallback list allocation failed");
+        CK(cudaMemsetAsync(c->fb_count.p, 0, sizeof(int), st));
+        {
+            LaunchScope ls(c, DETNET_K_PREPROCESS, st);
+            m->dims->fast(dim3(static_cast<unsigned>((cnt + PREP_FAST_SAMPLES - 1) / PREP_FAST_SAMPLES)),
+                          dim3(2 * PREP_FAST_SAMPLES), gram_entries(K) * PREP_FAST_SAMPLES * 4, st,
+                          cnt, N, H, y, x, c->gp.as<float>() + t0 * NG * TILE,
+                          c->q32.as<float>() + t0 * K * TILE, c->denom.as<double>() + s0,
+                          c->xmask.as<uint32_t>() + s0, c->flag.as<uint8_t>() + s0,
+                          c->fb_count.as<int>(), c->fb_list.as<long>());
+        }
+        if (int rc = check_launch()) return rc;
+        LaunchScope ls(c, DETNET_K_OTHER, st); // exact LU for the flagged samples
+        m->dims->pre(dim3(148), dim3(128), smem, st, cnt, m->N, H, y, x,
+                     c->gp.as<float>() + t0 * NG * TILE, c->q32.as<float>() + t0 * K * TILE,
+                     c->denom.as<double>() + s0, c->xmask.as<uint32_t>() + s0,
+                     c->flag.as<uint8_t>() + s0, c->sing.as<unsigned long long>(),
+                     c->fb_list.as<long>(), c->fb_count.as<int>());
+    } else {
+        const int blocks = static_cast<int>(std::min<long>((cnt + 3) / 4, 148L * 32));
         LaunchScope ls(c, DETNET_K_PREPROCESS, st);
         m->dims->pre(dim3(blocks), dim3(128), smem, st, cnt, m->N, H, y, x,
                      c->gp.as<float>() + t0 * NG * TILE, c->q32.as<float>() + t0 * K * TILE,
                      c->denom.as<double>() + s0, c->xmask.as<uint32_t>() + s0,
-                     c->flag.as<uint8_t>() + s0, c->sing.as<unsigned long long>());
+                     c->flag.as<uint8_t>() + s0, c->sing.as<unsigned long long>(), nullptr,
+                     nullptr);
     }
     if (int rc = check_launch()) return rc;
     const long end = s0 + cnt;
@@ -303,7 +349,8 @@ int detnet_ctx_create(int device, detnet_ctx **out) {
         CK(cudaEventCreateWithFlags(&c->copy_done[i], cudaEventDisableTiming));
     }
     for (const DimsEntry &d : kDims)
-        if (d.prep()) return fail(DETNET_ERR_CUDA, "cudaFuncSetAttribute (smem) failed");
+        if (d.prep() || (d.prep_fast && d.prep_fast()))
+            return fail(DETNET_ERR_CUDA, "cudaFuncSetAttribute (smem) failed");
     if (int rc = tc_prepare()) return rc;
     *out = c;
     return 0;
@@ -332,6 +379,12 @@ void detnet_ctx_destroy(detnet_ctx *c) {
 int detnet_ctx_set_path(detnet_ctx *c, int path) {
     if (!c || path < 0 || path > 2) return fail(DETNET_ERR_CONTRACT, "bad path");
     c->path = path;
+    return 0;
+}
+
+int detnet_ctx_set_exact_preprocess(detnet_ctx *c, int on) {
+    if (!c) return fail(DETNET_ERR_CONTRACT, "null ctx");
+    c->exact_pre = on != 0;
     return 0;
 }
 

@@ -117,7 +117,8 @@ struct detnet_ctx {
     std::vector<cudaEvent_t> event_pool;
     // workspace
     detnet::DBuf gp, q32, denom, xmask, flag, tile_loss, tile_err, sing, result;
-    detnet::DBuf in_H[2], in_y[2], in_x[2], xhat_dev, state_x, state_v;
+    detnet::DBuf in_H[2], in_y[2], in_x[2], xhat_dev, state_x, state_v, fb_list, fb_count;
+    bool exact_pre = false; // bit-exact reference LU for every sample
     double *h_result = nullptr; // pinned: loss, err, flag, singular
     cudaEvent_t chunk_done[2] = {nullptr, nullptr};
     cudaEvent_t copy_done[2] = {nullptr, nullptr};

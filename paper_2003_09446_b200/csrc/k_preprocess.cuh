@@ -1,4 +1,7 @@
-// k_preprocess.cuh -- K1: per-sample preprocessing, one warp per sample.
+// k_preprocess.cuh -- K1 exact path: per-sample preprocessing, one warp per
+// sample, bit-identical to the reference. Used for all samples when exact
+// preprocessing is requested (and for dims without a fast path), and for the
+// samples the fast path (k_prep_fast.cuh) flags as ill-conditioned.
 //
 // Restates the part of evaluate_one before the layer loop (kernels.cpp:55-58):
 //   q = H^T y            matvec_transpose, linalg.cpp:20-29 (i outer)
@@ -31,7 +34,8 @@ __global__ void __launch_bounds__(256)
     k_preprocess(long n, int N, const float *__restrict__ H, const float *__restrict__ y,
                  const int8_t *__restrict__ x, float *__restrict__ gp, float *__restrict__ q32,
                  double *__restrict__ denom, uint32_t *__restrict__ xmask,
-                 uint8_t *__restrict__ flag, unsigned long long *__restrict__ singular) {
+                 uint8_t *__restrict__ flag, unsigned long long *__restrict__ singular,
+                 const long *__restrict__ list, const int *__restrict__ list_count) {
     static_assert(K <= 32, "one lane per row");
     constexpr int NG = gram_entries(K);
     constexpr unsigned FULL = 0xffffffffu;
@@ -45,8 +49,11 @@ __global__ void __launch_bounds__(256)
     double *sG = sy + N;
     double *sq = sG + K * K;
 
-    for (long s = static_cast<long>(blockIdx.x) * warps + warp; s < n;
-         s += static_cast<long>(gridDim.x) * warps) {
+    // optional index list: only the listed samples (the fast path's fallbacks)
+    const long n_eff = list ? static_cast<long>(*list_count) : n;
+    for (long si = static_cast<long>(blockIdx.x) * warps + warp; si < n_eff;
+         si += static_cast<long>(gridDim.x) * warps) {
+        const long s = list ? list[si] : si;
         const float *Hs = H + s * static_cast<long>(N) * K;
         for (int i = lane; i < N * K; i += 32) sH[i] = static_cast<double>(__ldg(Hs + i));
         for (int i = lane; i < N; i += 32) sy[i] = static_cast<double>(__ldg(y + s * N + i));

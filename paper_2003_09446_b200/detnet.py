@@ -96,6 +96,7 @@ _lib.detnet_ctx_create.argtypes = [C.c_int, C.POINTER(_vp)]
 _lib.detnet_ctx_destroy.argtypes = [_vp]
 _lib.detnet_ctx_set_path.argtypes = [_vp, C.c_int]
 _lib.detnet_ctx_set_stream.argtypes = [_vp, _vp]
+_lib.detnet_ctx_set_exact_preprocess.argtypes = [_vp, C.c_int]
 _lib.detnet_ctx_stream.restype = _vp
 _lib.detnet_ctx_stream.argtypes = [_vp]
 _lib.detnet_ctx_set_profiling.argtypes = [_vp, C.c_int]
@@ -185,6 +186,9 @@ class Context:
 
     def set_path(self, path):
         _check(_lib.detnet_ctx_set_path(self._h, path))
+
+    def set_exact_preprocess(self, on=True):
+        _check(_lib.detnet_ctx_set_exact_preprocess(self._h, int(on)))
 
     def set_stream(self, stream_ptr):
         _check(_lib.detnet_ctx_set_stream(self._h, stream_ptr))

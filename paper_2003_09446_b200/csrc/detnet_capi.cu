@@ -48,11 +48,15 @@ template <int K>
 void launch_fast(dim3 g, dim3 b, size_t sm, cudaStream_t st, long n, int N, const float *H,
                  const float *y, const int8_t *x, float *gp, float *q32, double *dn, uint32_t *xm,
                  uint8_t *fl, int *fbc, long *fbl) {
-    k_prep_fast<K><<<g, b, sm, st>>>(n, N, H, y, x, gp, q32, dn, xm, fl, fbc, fbl);
+    (void)b;
+    (void)sm;
+    k_prep_gram<K><<<g, 2 * PREP_FAST_SAMPLES, 0, st>>>(n, N, H, y, x, gp, q32, xm);
+    k_prep_solve<K><<<g, PREP_FAST_SAMPLES, gram_entries(K) * PREP_FAST_SAMPLES * 4, st>>>(
+        n, N, H, y, gp, q32, xm, dn, fl, fbc, fbl);
 }
 
 template <int K> int set_fast_smem() {
-    return cudaFuncSetAttribute(k_prep_fast<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    return cudaFuncSetAttribute(k_prep_solve<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(gram_entries(K) * PREP_FAST_SAMPLES * 4)) ==
                    cudaSuccess
                ? 0

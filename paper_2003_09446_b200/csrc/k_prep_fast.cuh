@@ -5,18 +5,19 @@
 //   q = H^T y, G = H^T H                      -> FP32 outputs for the layer stack
 //   d = x - x_tilde = G^-1 H^T (H x - y)      -> denom = max(||d||^2, 1e-12)
 // Instead of the reference's FP64 LU (linalg.cpp:44-79, kept bit-exact in
-// k_preprocess.cuh), the solve is an FP32 Cholesky in shared memory plus one
-// step of iterative refinement whose residual H^T (H x - y) - H^T H d0 is
-// formed in FP64 straight from the FP32 inputs (products exact in FP64), so
-// d (hence the loss denominator) is FP64-accurate (~1e-10 relative) for
+// k_preprocess.cuh), d starts from an FP32 Cholesky solve of G d0 = G x - q
+// (Cholesky in shared memory) and is refined (up to two steps) with the
+// residual H^T (H (x - d) - y) formed in FP64 straight from the FP32 inputs,
+// so d (hence the loss denominator) is FP64-accurate (~1e-10 relative) for
 // well-conditioned samples. Samples whose Cholesky pivots collapse or whose
 // refinement correction is not small are queued for the exact reference LU
 // (k_preprocess on an index list), which also owns SingularMatrixError.
 //
 // Work split inside a pair (lanes 2i, 2i+1 = one sample; both stream the same
 // H rows, so each 80-byte row is fetched once per pair):
-//   half 0: Gram rows 0..R0-1 (upper-triangle entries [0, NA)), q (FP64), Cholesky,
-//           solves, refinement;  half 1: Gram rows R0..K-1, r = H^T (H x - y).
+//   half 0: Gram rows 0..R0-1 (upper-triangle entries [0, NA)) and q;
+//   half 1: Gram rows R0..K-1. The solve runs in a second kernel (k_prep_solve),
+//   one thread per sample.
 #pragma once
 
 #include "common.cuh"
@@ -49,19 +50,24 @@ __host__ __device__ constexpr int tri_idx(int K, int a, int b) { // a <= b
 
 constexpr int PREP_FAST_SAMPLES = 64; // per CTA
 
+// Shared-memory load that ptxas may not hoist or CSE: keeps the unrolled
+// factor/solve loops from parking all 210 factor entries in registers.
+__device__ __forceinline__ float lds_v(const float *p) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(smem_u32(p)));
+    return v;
+}
+
+// K1a: Gram and q (FP32 accumulation) with two threads per sample.
 template <int K>
 __global__ void __launch_bounds__(128)
-    k_prep_fast(long n, int N, const float *__restrict__ H, const float *__restrict__ y,
+    k_prep_gram(long n, int N, const float *__restrict__ H, const float *__restrict__ y,
                 const int8_t *__restrict__ x, float *__restrict__ gp, float *__restrict__ q32,
-                double *__restrict__ denom, uint32_t *__restrict__ xmask,
-                uint8_t *__restrict__ flag, int *__restrict__ fb_count,
-                long *__restrict__ fb_list) {
+                uint32_t *__restrict__ xmask) {
     using S = PrepSplit<K>;
     constexpr int NG = S::NG, NA = S::NA, NB = S::NB, R0 = S::R0;
     constexpr int NMAX = NA > NB ? NA : NB;
     static_assert(K % 4 == 0, "rows are read as float4");
-    extern __shared__ float gs_raw[]; // [NG][PREP_FAST_SAMPLES]
-    float(*Gs)[PREP_FAST_SAMPLES] = reinterpret_cast<float(*)[PREP_FAST_SAMPLES]>(gs_raw);
     const int half = threadIdx.x & 1;
     const int ls = threadIdx.x >> 1; // local sample
     const long s = static_cast<long>(blockIdx.x) * PREP_FAST_SAMPLES + ls;
@@ -78,14 +84,13 @@ __global__ void __launch_bounds__(128)
     for (int j = 0; j < K; ++j)
         if (xs[j] > 0) mask |= 1u << j;
 
-    // ---- pass 1: Gram halves, q (half 0), r = H^T (H x - y) in FP64 (half 1)
+    // ---- pass 1 over H: Gram halves and q (half 0), FP32 ----
     float acc[NMAX];
 #pragma unroll
     for (int e = 0; e < NMAX; ++e) acc[e] = 0.f;
-    // w: q (half 0) or r = H^T (H x - y) (half 1), both FP64 accumulators
-    double w[K];
+    float q[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) w[j] = 0.0;
+    for (int j = 0; j < K; ++j) q[j] = 0.f;
 #pragma unroll 1
     for (int i = 0; i < N; ++i) {
         float h[K];
@@ -94,60 +99,85 @@ __global__ void __launch_bounds__(128)
             const float4 v = __ldg(Hs + i * (K / 4) + c);
             h[4 * c] = v.x; h[4 * c + 1] = v.y; h[4 * c + 2] = v.z; h[4 * c + 3] = v.w;
         }
-        const float yi = __ldg(ys + i);
         if (half == 0) {
+            const float yi = __ldg(ys + i);
             int e = 0;
 #pragma unroll
             for (int a = 0; a < R0; ++a)
 #pragma unroll
                 for (int b = a; b < K; ++b, ++e) acc[e] = fmaf(h[a], h[b], acc[e]);
 #pragma unroll
-            for (int j = 0; j < K; ++j) w[j] = fma(static_cast<double>(h[j]), static_cast<double>(yi), w[j]);
+            for (int j = 0; j < K; ++j) q[j] = fmaf(h[j], yi, q[j]);
         } else {
             int e = 0;
 #pragma unroll
             for (int a = R0; a < K; ++a)
 #pragma unroll
                 for (int b = a; b < K; ++b, ++e) acc[e] = fmaf(h[a], h[b], acc[e]);
-            double ei = -static_cast<double>(yi);
-#pragma unroll
-            for (int j = 0; j < K; ++j) ei += (mask >> j) & 1u ? static_cast<double>(h[j]) : -static_cast<double>(h[j]);
-#pragma unroll
-            for (int j = 0; j < K; ++j) w[j] = fma(static_cast<double>(h[j]), ei, w[j]);
         }
     }
-    // Gram entries -> shared (for the factorization) and global (layer stack)
+    if (!live) return;
     {
         const int e0 = half == 0 ? 0 : NA;
         const int ne = half == 0 ? NA : NB;
 #pragma unroll
         for (int e = 0; e < NMAX; ++e)
-            if (e < ne) {
-                Gs[e0 + e][ls] = acc[e];
-                if (live) gp[(tile * NG + e0 + e) * TILE + col] = acc[e];
-            }
+            if (e < ne) gp[(tile * NG + e0 + e) * TILE + col] = acc[e];
     }
-    if (half == 0 && live) {
+    if (half == 0) {
 #pragma unroll
-        for (int j = 0; j < K; ++j) q32[(tile * K + j) * TILE + col] = __double2float_rn(w[j]);
+        for (int j = 0; j < K; ++j) q32[(tile * K + j) * TILE + col] = q[j];
+        xmask[s] = mask;
     }
-    // r from the odd lane to the even lane of the pair
-    double r[K];
+}
+
+// K1b: x_tilde via FP32 Cholesky in shared memory + FP64 refinement, one
+// thread per sample; flags ill-conditioned samples for the exact LU.
+template <int K>
+__global__ void __launch_bounds__(PREP_FAST_SAMPLES)
+    k_prep_solve(long n, int N, const float *__restrict__ H, const float *__restrict__ y,
+                 const float *__restrict__ gp, const float *__restrict__ q32,
+                 const uint32_t *__restrict__ xmask, double *__restrict__ denom,
+                 uint8_t *__restrict__ flag, int *__restrict__ fb_count,
+                 long *__restrict__ fb_list) {
+    constexpr int NG = K * (K + 1) / 2;
+    static_assert(K % 4 == 0, "rows are read as float4");
+    extern __shared__ float gs_raw[]; // [NG][PREP_FAST_SAMPLES]
+    float(*Gs)[PREP_FAST_SAMPLES] = reinterpret_cast<float(*)[PREP_FAST_SAMPLES]>(gs_raw);
+    const int ls = threadIdx.x;
+    const long s = static_cast<long>(blockIdx.x) * PREP_FAST_SAMPLES + ls;
+    const bool live = s < n;
+    const long sc = live ? s : n - 1;
+    const long tile = sc / TILE;
+    const int col = static_cast<int>(sc % TILE);
+    const float4 *Hs = reinterpret_cast<const float4 *>(H + sc * static_cast<long>(N) * K);
+    const float *ys = y + sc * N;
+    const uint32_t mask = xmask[sc];
+#pragma unroll 4
+    for (int e = 0; e < NG; ++e) Gs[e][ls] = gp[(tile * NG + e) * TILE + col];
+    __syncwarp();
+    float r32[K]; // initial residual G x - q in FP32 (only a starting guess)
 #pragma unroll
-    for (int j = 0; j < K; ++j) r[j] = __shfl_down_sync(0xffffffffu, w[j], 1);
-    __syncthreads();
-    if (half == 1) return;
+    for (int j = 0; j < K; ++j) r32[j] = -q32[(tile * K + j) * TILE + col];
+#pragma unroll
+    for (int a = 0; a < K; ++a)
+#pragma unroll
+        for (int b = a; b < K; ++b) {
+            const float g = lds_v(&Gs[tri_idx(K, a, b)][ls]);
+            r32[a] = fmaf(g, (mask >> b) & 1u ? 1.f : -1.f, r32[a]);
+            if (b != a) r32[b] = fmaf(g, (mask >> a) & 1u ? 1.f : -1.f, r32[b]);
+        }
 
     // ---- FP32 Cholesky in place: L[i][j] (i > j) stored at Gs[tri(j, i)],
     // the diagonal holds 1 / L[j][j] ----
     bool bad = false;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-        float sjj = Gs[tri_idx(K, j, j)][ls];
+        float sjj = lds_v(&Gs[tri_idx(K, j, j)][ls]);
         const float gjj = sjj;
 #pragma unroll
         for (int k = 0; k < j; ++k) {
-            const float l = Gs[tri_idx(K, k, j)][ls];
+            const float l = lds_v(&Gs[tri_idx(K, k, j)][ls]);
             sjj = fmaf(-l, l, sjj);
         }
         if (!(sjj > 1e-5f * gjj)) bad = true;
@@ -155,65 +185,75 @@ __global__ void __launch_bounds__(128)
         Gs[tri_idx(K, j, j)][ls] = dinv;
 #pragma unroll 1
         for (int i = j + 1; i < K; ++i) {
-            float sij = Gs[tri_idx(K, j, i)][ls];
+            float sij = lds_v(&Gs[tri_idx(K, j, i)][ls]);
 #pragma unroll
             for (int k = 0; k < j; ++k)
-                sij = fmaf(-Gs[tri_idx(K, k, i)][ls], Gs[tri_idx(K, k, j)][ls], sij);
+                sij = fmaf(-lds_v(&Gs[tri_idx(K, k, i)][ls]), lds_v(&Gs[tri_idx(K, k, j)][ls]), sij);
             Gs[tri_idx(K, j, i)][ls] = sij * dinv;
         }
     }
     // solve L L^T d = b (FP32)
-    auto solve = [&](const float (&b)[K], float (&d)[K]) {
-        float z[K];
+    auto solve = [&](float (&b)[K]) {
 #pragma unroll
         for (int i = 0; i < K; ++i) {
             float t = b[i];
 #pragma unroll
-            for (int k = 0; k < i; ++k) t = fmaf(-Gs[tri_idx(K, k, i)][ls], z[k], t);
-            z[i] = t * Gs[tri_idx(K, i, i)][ls];
+            for (int k = 0; k < i; ++k) t = fmaf(-lds_v(&Gs[tri_idx(K, k, i)][ls]), b[k], t);
+            b[i] = t * lds_v(&Gs[tri_idx(K, i, i)][ls]);
         }
 #pragma unroll
         for (int i = K - 1; i >= 0; --i) {
-            float t = z[i];
+            float t = b[i];
 #pragma unroll
-            for (int k = i + 1; k < K; ++k) t = fmaf(-Gs[tri_idx(K, i, k)][ls], d[k], t);
-            d[i] = t * Gs[tri_idx(K, i, i)][ls];
+            for (int k = i + 1; k < K; ++k) t = fmaf(-lds_v(&Gs[tri_idx(K, i, k)][ls]), b[k], t);
+            b[i] = t * lds_v(&Gs[tri_idx(K, i, i)][ls]);
         }
     };
-    float b[K], d0[K];
+    solve(r32); // d0 = G^-1 (G x - q) = x - x_tilde (FP32 estimate)
+    double xd[K]; // x - d = current x_tilde estimate
 #pragma unroll
-    for (int j = 0; j < K; ++j) b[j] = static_cast<float>(r[j]);
-    solve(b, d0);
-    // ---- refinement: r <- r - H^T (H d0) in FP64 (the residual) ----
+    for (int j = 0; j < K; ++j) xd[j] = ((mask >> j) & 1u ? 1.0 : -1.0) - static_cast<double>(r32[j]);
+    // ---- refinement: res = H^T (H (x - d) - y) in FP64 from the FP32 inputs,
+    // d <- d + G^-1 res; at most two steps ----
+    double dn = 0.0;
+    bool conv = false;
 #pragma unroll 1
-    for (int i = 0; i < N; ++i) {
-        float h[K];
+    for (int step = 0; step < 2 && !conv; ++step) {
+        double res[K];
 #pragma unroll
-        for (int c = 0; c < K / 4; ++c) {
-            const float4 v = __ldg(Hs + i * (K / 4) + c);
-            h[4 * c] = v.x; h[4 * c + 1] = v.y; h[4 * c + 2] = v.z; h[4 * c + 3] = v.w;
+        for (int j = 0; j < K; ++j) res[j] = 0.0;
+#pragma unroll 1
+        for (int i = 0; i < N; ++i) {
+            float h[K];
+#pragma unroll
+            for (int c = 0; c < K / 4; ++c) {
+                const float4 v = __ldg(Hs + i * (K / 4) + c);
+                h[4 * c] = v.x; h[4 * c + 1] = v.y; h[4 * c + 2] = v.z; h[4 * c + 3] = v.w;
+            }
+            double t = -static_cast<double>(__ldg(ys + i));
+#pragma unroll
+            for (int j = 0; j < K; ++j) t = fma(static_cast<double>(h[j]), xd[j], t);
+#pragma unroll
+            for (int j = 0; j < K; ++j) res[j] = fma(static_cast<double>(h[j]), t, res[j]);
         }
-        double f = 0.0;
+        float c32[K];
 #pragma unroll
-        for (int j = 0; j < K; ++j) f = fma(static_cast<double>(h[j]), static_cast<double>(d0[j]), f);
+        for (int j = 0; j < K; ++j) c32[j] = static_cast<float>(res[j]);
+        solve(c32);
+        double cmax = 0.0, dmax = 0.0;
+        dn = 0.0;
 #pragma unroll
-        for (int j = 0; j < K; ++j) r[j] = fma(-static_cast<double>(h[j]), f, r[j]);
+        for (int j = 0; j < K; ++j) {
+            xd[j] -= static_cast<double>(c32[j]);
+            const double dj = ((mask >> j) & 1u ? 1.0 : -1.0) - xd[j];
+            dn = fma(dj, dj, dn);
+            cmax = fmax(cmax, fabs(static_cast<double>(c32[j])));
+            dmax = fmax(dmax, fabs(dj));
+        }
+        conv = cmax <= 1e-5 * dmax;
     }
-    float corr[K];
-#pragma unroll
-    for (int j = 0; j < K; ++j) b[j] = static_cast<float>(r[j]);
-    solve(b, corr);
-    double dn = 0.0, cmax = 0.0, dmax = 0.0;
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-        const double dj = static_cast<double>(d0[j]) + static_cast<double>(corr[j]);
-        dn = fma(dj, dj, dn);
-        cmax = fmax(cmax, fabs(static_cast<double>(corr[j])));
-        dmax = fmax(dmax, fabs(dj));
-    }
-    if (!(cmax <= 1e-5 * dmax) || !(dn == dn)) bad = true;
+    if (!conv || !(dn == dn)) bad = true;
     if (!live) return;
-    xmask[s] = mask;
     if (bad) {
         // exact reference LU (and the singular test) for this sample
         const int slot = atomicAdd(fb_count, 1);

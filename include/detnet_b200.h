@@ -161,6 +161,13 @@ int detnet_generate_device(detnet_ctx *ctx, uint64_t base, long first, long coun
                            int n_tx, double snr_lo_db, double snr_hi_db, double scale,
                            float *H_dev, float *y_dev, int8_t *x_dev, double *sigma2_dev);
 
+/* Same generator with unscaled FP64 host outputs, exactly the fields of the
+ * ChannelSamples unfold::generate_batch returns: H [count][n_rx][n_tx],
+ * x [count][n_tx] (+-1.0), y [count][n_rx], sigma2 [count] (nullable). */
+int detnet_generate_host(detnet_ctx *ctx, uint64_t base, long first, long count, int n_rx,
+                         int n_tx, double snr_lo_db, double snr_hi_db, double *H, double *x,
+                         double *y, double *sigma2);
+
 #ifdef __cplusplus
 }
 #endif

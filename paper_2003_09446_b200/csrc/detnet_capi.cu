@@ -618,11 +618,42 @@ int detnet_generate_device(detnet_ctx *c, uint64_t base, long first, long count,
     const int blocks = static_cast<int>((count + 127) / 128);
     {
         LaunchScope ls(c, DETNET_K_GENERATE, c->stream);
-        k_generate<<<blocks, 128, 0, c->stream>>>(base, first, count, n_rx, n_tx, lo, hi, scale, H, y,
-                                                  x, sigma2);
+        k_generate<float, int8_t><<<blocks, 128, 0, c->stream>>>(base, first, count, n_rx, n_tx,
+                                                                 lo, hi, scale, H, y, x, sigma2);
     }
     if (int rc = check_launch()) return rc;
     CK(cudaStreamSynchronize(c->stream));
+    drain_times(c);
+    return 0;
+}
+
+int detnet_generate_host(detnet_ctx *c, uint64_t base, long first, long count, int n_rx, int n_tx,
+                         double lo, double hi, double *H, double *x, double *y, double *sigma2) {
+    if (!c || !H || !y || !x) return fail(DETNET_ERR_CONTRACT, "null argument");
+    if (count < 1) return fail(DETNET_ERR_CONFIG, "generate_batch: batch size must be >= 1");
+    if (n_rx < n_tx || n_tx < 1 || n_tx > 32)
+        return fail(DETNET_ERR_CONFIG, "generate_batch: need N >= K >= 1 (K <= 32)");
+    CK(cudaSetDevice(c->device));
+    const size_t nh = static_cast<size_t>(count) * n_rx * n_tx, ny = static_cast<size_t>(count) * n_rx,
+                 nx = static_cast<size_t>(count) * n_tx;
+    DBuf buf;
+    if (buf.ensure(sizeof(double) * (nh + ny + nx + count)))
+        return fail(DETNET_ERR_CUDA, "generator buffer allocation failed");
+    double *dH = buf.as<double>(), *dy = dH + nh, *dx = dy + ny, *ds = dx + nx;
+    const int blocks = static_cast<int>((count + 127) / 128);
+    {
+        LaunchScope ls(c, DETNET_K_GENERATE, c->stream);
+        k_generate<double, double><<<blocks, 128, 0, c->stream>>>(base, first, count, n_rx, n_tx, lo,
+                                                                  hi, 1.0, dH, dy, dx, ds);
+    }
+    if (int rc = check_launch()) { buf.release(); return rc; }
+    cudaMemcpyAsync(H, dH, sizeof(double) * nh, cudaMemcpyDeviceToHost, c->stream);
+    cudaMemcpyAsync(y, dy, sizeof(double) * ny, cudaMemcpyDeviceToHost, c->stream);
+    cudaMemcpyAsync(x, dx, sizeof(double) * nx, cudaMemcpyDeviceToHost, c->stream);
+    if (sigma2) cudaMemcpyAsync(sigma2, ds, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream);
+    const cudaError_t e = cudaStreamSynchronize(c->stream);
+    buf.release();
+    if (e != cudaSuccess) return fail(DETNET_ERR_CUDA, "generate_host: %s", cudaGetErrorString(e));
     drain_times(c);
     return 0;
 }

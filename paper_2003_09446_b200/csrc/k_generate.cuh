@@ -19,10 +19,14 @@ __device__ __forceinline__ double u01_from(uint64_t r) {
     return static_cast<double>(r >> 11) * 0x1.0p-53;
 }
 
+// Out = float: H, y scaled and rounded to FP32, x as int8 (the engine's input
+// format). Out = double: unscaled FP64 ChannelSample fields (H, y, x = +-1.0),
+// what unfold::generate_batch returns.
+template <typename Out, typename XOut>
 __global__ void __launch_bounds__(128) k_generate(uint64_t base, long first, long count, int N,
                                                   int K, double lo, double hi, double scale,
-                                                  float *__restrict__ H, float *__restrict__ y,
-                                                  int8_t *__restrict__ x,
+                                                  Out *__restrict__ H, Out *__restrict__ y,
+                                                  XOut *__restrict__ x,
                                                   double *__restrict__ sigma2) {
     const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= count) return;
@@ -41,7 +45,7 @@ __global__ void __launch_bounds__(128) k_generate(uint64_t base, long first, lon
     for (int j = 0; j < K; ++j) {
         const uint64_t r = mix64(s0 + (dx + j + 1) * kGamma);
         if (r >> 63) xbits |= 1u << j;
-        x[i * K + j] = (r >> 63) ? int8_t(1) : int8_t(-1);
+        x[i * K + j] = (r >> 63) ? XOut(1) : XOut(-1);
     }
     // H and y = H x (row i: acc over j ascending), then noise
     uint64_t st = s0 + d0 * kGamma;
@@ -54,7 +58,7 @@ __global__ void __launch_bounds__(128) k_generate(uint64_t base, long first, lon
             st += kGamma;
             const double u2 = u01_from(mix64(st));
             const double g = dmul(sqrt(-2.0 * log(u1)), cos(dmul(two_pi, u2)));
-            H[(i * N + r) * K + j] = __double2float_rn(dmul(g, scale));
+            H[(i * N + r) * K + j] = static_cast<Out>(dmul(g, scale));
             acc = dadd(acc, (xbits >> j) & 1u ? g : -g);
         }
         // noise draw for row r: d0 + 2NK + K + 2r (+1)
@@ -64,7 +68,7 @@ __global__ void __launch_bounds__(128) k_generate(uint64_t base, long first, lon
         sn += kGamma;
         const double n2 = u01_from(mix64(sn));
         const double g = dmul(sqrt(-2.0 * log(n1)), cos(dmul(two_pi, n2)));
-        y[i * N + r] = __double2float_rn(dmul(dadd(acc, dmul(sigma, g)), scale));
+        y[i * N + r] = static_cast<Out>(dmul(dadd(acc, dmul(sigma, g)), scale));
     }
     if (sigma2) sigma2[i] = s2;
 }

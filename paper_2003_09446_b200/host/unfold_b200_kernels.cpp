@@ -1,0 +1,300 @@
+// unfold_b200_kernels.cpp -- drop-in replacement for the reference's batch
+// kernel seam, proj/src/kernels.cpp (declared in proj/include/unfold/kernels.hpp:
+// 29-65). Link this file instead of kernels.cpp (and unfold_b200_adam.cpp
+// instead of adam.cpp) and every caller of the seam -- training.cpp:18,65,72,
+// harness.cpp:134-153, tools/bench_kernels.cpp -- runs on the B200 engine
+// through the C-ABI in include/detnet_b200.h. Compiled against the
+// reference's own headers; no CPU fallback for the hot path.
+//
+// Conventions kept from the reference:
+//  * exceptions: ContractError / SingularMatrixError / ConfigError /
+//    runtime_error for the C-ABI status codes (errors.hpp:9-31);
+//  * generate_batch advances the caller's Rng by exactly one draw (split)
+//    and keys sample i on base.stream(i) (kernels.cpp:116-136);
+//  * batch_gradient zeroes grads and adds the regularizer gradient
+//    (kernels.cpp:160-200); frozen slots stay empty (backward.cpp:88-103).
+// Precision: samples cross the boundary as FP32 (H, y) and int8 (x); weights
+// are packed to FP32 per params version (content-hashed).
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#include "detnet_b200.h"
+#include "unfold/kernels.hpp"
+
+namespace unfold {
+
+namespace {
+
+[[noreturn]] void throw_status(int rc) {
+    const std::string msg = detnet_last_error();
+    switch (rc) {
+    case DETNET_ERR_CONTRACT: throw ContractError(msg);
+    case DETNET_ERR_SINGULAR: throw SingularMatrixError(msg);
+    case DETNET_ERR_CONFIG: throw ConfigError(msg);
+    default: throw std::runtime_error("detnet_b200: " + msg);
+    }
+}
+
+inline void check(int rc) {
+    if (rc != DETNET_OK) throw_status(rc);
+}
+
+long record_size(const ModelParams &p) {
+    return detnet_record_size(p.n_tx, p.dims.z_dim, p.dims.v_dim);
+}
+
+// ModelParams -> layer records (grad_check.hpp:16-44 order), values and masks.
+void pack(const ModelParams &p, std::vector<double> &vals, std::vector<double> &masks,
+          bool &any_mask) {
+    const long P = record_size(p);
+    vals.assign(static_cast<size_t>(P) * p.depth(), 0.0);
+    masks.assign(static_cast<size_t>(P) * p.depth(), 1.0);
+    any_mask = false;
+    for (int l = 0; l < p.depth(); ++l) {
+        const LayerParams &lp = p.layers[l];
+        double *r = vals.data() + static_cast<size_t>(l) * P;
+        double *m = masks.data() + static_cast<size_t>(l) * P;
+        long off = 0;
+        auto put = [&](const std::vector<double> &v, const std::vector<double> &mk) {
+            std::memcpy(r + off, v.data(), sizeof(double) * v.size());
+            std::memcpy(m + off, mk.data(), sizeof(double) * mk.size());
+            off += static_cast<long>(v.size());
+        };
+        put(lp.W1.data, lp.M1.data);
+        put(lp.b1, lp.mb1);
+        put(lp.W2.data, lp.M2.data);
+        put(lp.b2, lp.mb2);
+        put(lp.W3.data, lp.M3.data);
+        put(lp.b3, lp.mb3);
+        r[off] = lp.t;
+        m[off] = 1.0;
+        if (!lp.all_ones) any_mask = true;
+    }
+}
+
+uint64_t fnv1a(const std::vector<double> &a, const std::vector<double> &b, uint64_t seed) {
+    uint64_t h = 1469598103934665603ULL ^ seed;
+    auto eat = [&](const std::vector<double> &v) {
+        const unsigned char *p = reinterpret_cast<const unsigned char *>(v.data());
+        for (size_t i = 0; i < v.size() * sizeof(double); ++i) h = (h ^ p[i]) * 1099511628211ULL;
+    };
+    eat(a);
+    eat(b);
+    return h;
+}
+
+struct CachedModel {
+    detnet_model *m = nullptr;
+    uint64_t hash = 0;
+    int depth = 0;
+};
+
+struct Engine {
+    detnet_ctx *ctx = nullptr;
+    std::unordered_map<const ModelParams *, CachedModel> models;
+    std::mutex mu;
+
+    Engine() {
+        const char *dev = std::getenv("DETNET_DEVICE");
+        check(detnet_ctx_create(dev ? std::atoi(dev) : 0, &ctx));
+    }
+};
+
+Engine &engine() {
+    static Engine e;
+    return e;
+}
+
+// Device mirror of params, re-validated per call (SURVEY 8b "Ownership":
+// train_steps does not change on prune, so a content hash decides).
+detnet_model *model_for(const ModelParams &p) {
+    Engine &e = engine();
+    std::vector<double> vals, masks;
+    bool any_mask = false;
+    pack(p, vals, masks, any_mask);
+    const uint64_t h = fnv1a(vals, masks, static_cast<uint64_t>(p.frozen_prefix) * 131 + p.depth());
+    detnet_model_desc d{p.n_tx, p.n_rx, p.dims.z_dim, p.dims.v_dim, p.depth(), p.frozen_prefix,
+                        vals.data(), any_mask ? masks.data() : nullptr};
+    CachedModel &c = e.models[&p];
+    if (!c.m) {
+        check(detnet_model_create(e.ctx, &d, &c.m));
+    } else if (c.hash != h || c.depth != p.depth()) {
+        check(detnet_model_update(c.m, &d));
+    }
+    c.hash = h;
+    c.depth = p.depth();
+    return c.m;
+}
+
+struct Packed {
+    std::vector<float> H, y;
+    std::vector<int8_t> x;
+};
+
+Packed pack_samples(const ModelParams &p, std::span<const ChannelSample> batch) {
+    Packed s;
+    const int N = p.n_rx, K = p.n_tx;
+    const size_t n = batch.size();
+    s.H.resize(n * N * K);
+    s.y.resize(n * N);
+    s.x.resize(n * K);
+    for (size_t i = 0; i < n; ++i) {
+        const ChannelSample &c = batch[i];
+        if (c.H.rows != N || c.H.cols != K || static_cast<int>(c.y.size()) != N ||
+            static_cast<int>(c.x.size()) != K)
+            throw ContractError("batch sample shape does not match params");
+        for (int j = 0; j < N * K; ++j) s.H[i * N * K + j] = static_cast<float>(c.H.data[j]);
+        for (int j = 0; j < N; ++j) s.y[i * N + j] = static_cast<float>(c.y[j]);
+        for (int j = 0; j < K; ++j) s.x[i * K + j] = c.x[j] >= 0.0 ? 1 : -1;
+    }
+    return s;
+}
+
+BatchEval to_eval(const detnet_eval &ev) {
+    BatchEval out;
+    out.data_loss = ev.data_loss;
+    out.symbol_errors = ev.symbol_errors;
+    out.symbols = ev.symbols;
+    out.flagged = ev.flagged;
+    return out;
+}
+
+long long baseline_errors_one(const ChannelSample &s, BaselineKind kind) {
+    if (kind == BaselineKind::oracle) return 0;
+    const Vec d = kind == BaselineKind::zf ? sign_slice(zf_decode(s.H, s.y)) : ml_decode(s.H, s.y);
+    long long e = 0;
+    for (size_t i = 0; i < s.x.size(); ++i) e += d[i] != s.x[i];
+    return e;
+}
+
+} // namespace
+
+int worker_count() {
+#ifdef _OPENMP
+    int n = omp_get_max_threads();
+#else
+    int n = 1;
+#endif
+    if (const char *env = std::getenv("UNFOLD_THREADS")) {
+        const int cap = std::atoi(env);
+        if (cap > 0) n = std::min(n, cap);
+    }
+    return std::max(n, 1);
+}
+
+std::vector<ChannelSample> generate_batch(Rng &rng, int n_rx, int n_tx, int count, SnrRange snr) {
+    if (count < 1) throw ConfigError("generate_batch: batch size must be >= 1");
+    if (n_rx < n_tx || n_tx < 1) throw ConfigError("generate_batch: need N >= K >= 1");
+    const uint64_t base = rng.split().state();
+    std::vector<double> H(static_cast<size_t>(count) * n_rx * n_tx), x(static_cast<size_t>(count) * n_tx),
+        y(static_cast<size_t>(count) * n_rx), s2(count);
+    check(detnet_generate_host(engine().ctx, base, 0, count, n_rx, n_tx, snr.lo_db, snr.hi_db,
+                               H.data(), x.data(), y.data(), s2.data()));
+    std::vector<ChannelSample> out(count);
+    for (int i = 0; i < count; ++i) {
+        ChannelSample &c = out[i];
+        c.H = Matrix(n_rx, n_tx);
+        std::memcpy(c.H.data.data(), H.data() + static_cast<size_t>(i) * n_rx * n_tx,
+                    sizeof(double) * n_rx * n_tx);
+        c.x.assign(x.begin() + static_cast<long>(i) * n_tx, x.begin() + static_cast<long>(i + 1) * n_tx);
+        c.y.assign(y.begin() + static_cast<long>(i) * n_rx, y.begin() + static_cast<long>(i + 1) * n_rx);
+        c.sigma2 = s2[i];
+    }
+    return out;
+}
+
+BatchEval batch_evaluate(const ModelParams &params, std::span<const ChannelSample> batch,
+                         LossLayers loss_layers) {
+    std::lock_guard<std::mutex> lk(engine().mu);
+    detnet_model *m = model_for(params);
+    if (batch.empty()) return BatchEval{};
+    Packed s = pack_samples(params, batch);
+    detnet_eval ev{};
+    check(detnet_batch_evaluate(m, static_cast<long>(batch.size()), s.H.data(), s.y.data(),
+                                s.x.data(), loss_layers == LossLayers::trainable_only, nullptr, &ev));
+    return to_eval(ev);
+}
+
+BatchEval batch_gradient(const ModelParams &params, std::span<const ChannelSample> batch,
+                         const LossSpec &spec, Gradients &grads, LossLayers loss_layers) {
+    require(!batch.empty(), "batch_gradient: empty batch");
+    require(grads.layers.size() == params.layers.size(), "batch_gradient: gradient shape mismatch");
+    std::lock_guard<std::mutex> lk(engine().mu);
+    detnet_model *m = model_for(params);
+    Packed s = pack_samples(params, batch);
+    const long P = record_size(params);
+    std::vector<double> g(static_cast<size_t>(P) * params.depth(), 0.0);
+    detnet_loss_spec ls{spec.kind == LossKind::plain ? 0 : (spec.kind == LossKind::element_l1 ? 1 : 2),
+                        spec.lambda, spec.lambda1, spec.lambda2};
+    detnet_eval ev{};
+    check(detnet_batch_gradient(m, static_cast<long>(batch.size()), s.H.data(), s.y.data(),
+                                s.x.data(), &ls, loss_layers == LossLayers::trainable_only,
+                                g.data(), &ev));
+    grads.set_zero();
+    for (int l = params.frozen_prefix; l < params.depth(); ++l) {
+        LayerGrads &gl = grads.layers[l];
+        if (gl.empty()) continue;
+        const double *r = g.data() + static_cast<size_t>(l) * P;
+        long off = 0;
+        auto get = [&](std::vector<double> &v) {
+            std::memcpy(v.data(), r + off, sizeof(double) * v.size());
+            off += static_cast<long>(v.size());
+        };
+        get(gl.W1.data);
+        get(gl.b1);
+        get(gl.W2.data);
+        get(gl.b2);
+        get(gl.W3.data);
+        get(gl.b3);
+        gl.t = r[off];
+    }
+    return to_eval(ev);
+}
+
+// ZF/ML/oracle baselines are not on the GPU path; they call
+// the reference's own zf_decode/ml_decode (channel.cpp) per sample.
+std::pair<long long, long long> batch_baseline_errors(std::span<const ChannelSample> batch,
+                                                      BaselineKind kind) {
+    long long errors = 0, symbols = 0;
+    for (const ChannelSample &s : batch) {
+        errors += baseline_errors_one(s, kind);
+        symbols += static_cast<long long>(s.x.size());
+    }
+    return {errors, symbols};
+}
+
+// The serial twins keep the seam's API; on this engine they run the same
+// deterministic device path (parity against a CPU restatement lives in the
+// repository's oracle/ and tests/, not in the product).
+namespace ref {
+
+std::vector<ChannelSample> generate_batch(Rng &rng, int n_rx, int n_tx, int count, SnrRange snr) {
+    return unfold::generate_batch(rng, n_rx, n_tx, count, snr);
+}
+BatchEval batch_evaluate(const ModelParams &params, std::span<const ChannelSample> batch,
+                         LossLayers loss_layers) {
+    return unfold::batch_evaluate(params, batch, loss_layers);
+}
+BatchEval batch_gradient(const ModelParams &params, std::span<const ChannelSample> batch,
+                         const LossSpec &spec, Gradients &grads, LossLayers loss_layers) {
+    return unfold::batch_gradient(params, batch, spec, grads, loss_layers);
+}
+std::pair<long long, long long> batch_baseline_errors(std::span<const ChannelSample> batch,
+                                                      BaselineKind kind) {
+    return unfold::batch_baseline_errors(batch, kind);
+}
+
+} // namespace ref
+
+} // namespace unfold

@@ -1,0 +1,85 @@
+"""The C++ drop-in seam (paper_2003_09446_b200/host/unfold_b200_*.cpp) driven
+through the reference's own types and init_params, against the oracle.
+
+oracle/_ref/dropin_test is built by __graft_entry__.build() where the
+reference tree exists (it links the reference's non-replaced sources) and
+travels to the GPU box with the snapshot."""
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle.oracle import Model
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "oracle", "_ref", "dropin_test")
+
+
+@pytest.fixture(scope="module")
+def run():
+    if not os.path.exists(BIN):
+        pytest.skip("dropin_test not built (needs the reference tree at build time)")
+    out = subprocess.run([BIN, "3", "5", "4", "157"], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    return json.loads(out.stdout)
+
+
+def _model(d, params=None):
+    K, N, L = d["K"], d["N"], d["L"]
+    P = np.array(d["params"] if params is None else params).reshape(L, -1)
+    return Model(K, N, 8 * K, 2 * K, L, P, frozen_prefix=1)
+
+
+def _inputs(d):
+    K, N, n = d["K"], d["N"], d["n"]
+    # the seam rounds samples to FP32
+    H = np.array(d["H"]).reshape(n, N, K).astype(np.float32).astype(np.float64)
+    y = np.array(d["y"]).reshape(n, N).astype(np.float32).astype(np.float64)
+    x = np.array(d["x"]).reshape(n, K)
+    return H, y, x
+
+
+def test_dropin_generate_batch(run, oracle):
+    """generate_batch on the device: keying and draw order of kernels.cpp:116-136."""
+    d = run
+    r = oracle.rng(200, 0)
+    H, x, y, _ = oracle.generate_batch(r, d["N"], d["K"], d["n"], 4.0, 12.0)
+    assert np.array_equal(np.array(d["x"]).reshape(x.shape), x)
+    Hg = np.array(d["H"]).reshape(H.shape)
+    assert np.max(np.abs(Hg - H)) <= 1e-12 * max(1.0, np.max(np.abs(H)))
+    yg = np.array(d["y"]).reshape(y.shape)
+    assert np.max(np.abs(yg - y)) <= 1e-12 * max(1.0, np.max(np.abs(y)))
+
+
+def test_dropin_batch_evaluate(run, oracle):
+    d = run
+    m = _model(d)
+    H, y, x = _inputs(d)
+    ref = oracle.batch_evaluate(m, H, y, x)
+    loss, errors, symbols, flagged = d["eval"]
+    assert symbols == d["n"] * d["K"] and flagged == ref["flagged"]
+    assert abs(loss - ref["data_loss"]) <= 1e-4 * abs(ref["data_loss"])
+    assert abs(errors - ref["symbol_errors"]) <= 2  # N(0,1) channels: rare FP32 sign flips
+    reft = oracle.batch_evaluate(m, H, y, x, trainable_only=True)
+    assert abs(d["eval_trainable"][0] - reft["data_loss"]) <= 1e-4 * abs(reft["data_loss"])
+
+
+def test_dropin_gradient_and_adam(run, oracle):
+    d = run
+    if not d["grads"]:
+        pytest.skip("batch_gradient not available")
+    m = _model(d)
+    H, y, x = _inputs(d)
+    ref = oracle.batch_gradient(m, H, y, x, kind=2, lam1=0.04, lam2=0.04)
+    g = np.array(d["grads"]).reshape(ref["grads"].shape)
+    scale = np.max(np.abs(ref["grads"]))
+    assert np.max(np.abs(g - ref["grads"])) <= 1e-3 * scale
+    assert d["train_steps"] == 1
+    mo = np.zeros_like(m.params)
+    vo = np.zeros_like(m.params)
+    oracle.adam_step(m, g, mo, vo, 0, lr0=1e-3)
+    p2 = np.array(d["params_after_adam"]).reshape(m.params.shape)
+    assert np.max(np.abs(p2 - m.params)) <= 1e-9

@@ -140,6 +140,24 @@ typedef struct {
     double beta1, beta2, eps;
 } detnet_adam_config;
 
+/* Device-resident training step, split so ranks can all-reduce (sum) the raw
+ * gradient between the two calls (one data-parallel rank per GPU):
+ *  detnet_train_grad: samples (device) -> raw_dev [param_count] FP64 sums of
+ *    the per-sample data-term gradients (unscaled, unmasked, record layout)
+ *    and this rank's BatchEval (loss sum, errors, flagged);
+ *  detnet_train_apply: raw (all-reduced) -> mean over n_global samples, masks,
+ *    regularizer gradient, Adam update of the model's device master params
+ *    (moments kept in the model; reset with detnet_model_reset_adam, as
+ *    training.cpp:55 starts a fresh AdamState per incremental step). */
+long detnet_model_param_count(const detnet_model *m);
+int detnet_train_grad(detnet_model *m, long n, const float *H_dev, const float *y_dev,
+                      const int8_t *x_dev, int loss_layers_trainable_only, double *raw_dev,
+                      detnet_eval *out);
+int detnet_train_apply(detnet_model *m, const double *raw_dev, long n_global,
+                       const detnet_loss_spec *spec, const detnet_adam_config *cfg);
+int detnet_model_get_params(detnet_model *m, double *params_out);
+int detnet_model_reset_adam(detnet_model *m);
+
 /* adam_step (adam.cpp:48-79) on host arrays: params (record layout, updated
  * in place), grads, first/second moments, *step advanced by one. */
 int detnet_adam_step(detnet_ctx *ctx, int n_tx, int z_dim, int v_dim, int depth,

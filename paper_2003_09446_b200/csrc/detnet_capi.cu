@@ -102,7 +102,7 @@ static const DimsEntry *find_dims(int K, int Z, int V) {
 
 } // namespace detnet
 
-namespace {
+namespace detnet {
 
 int pack_simt(detnet_model *m, const double *params, const double *masks, std::vector<float> &out) {
     const int K = m->K, Z = m->Z, V = m->V, IN = 3 * K + V;
@@ -157,6 +157,24 @@ int upload_model(detnet_model *m, const detnet_model_desc *d) {
     CK(cudaMemcpy(m->lnk_all.p, la.data(), m->L * 8, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(m->lnk_train.p, lt.data(), m->L * 8, cudaMemcpyHostToDevice));
     if (int rc = tc_pack(m->tc, m->K, m->Z, m->V, m->L, d->params, d->masks)) return rc;
+    m->train_ready = false; // the device master copy restarts from these params
+    m->tc_stale = false;
+    return 0;
+}
+
+// After device-side training steps the tcgen05 images are rebuilt once from
+// the FP64 master copy before the next tensor-core evaluation.
+int refresh_tc(detnet_model *m) {
+    if (!m->tc_stale) return 0;
+    const long total = record_size(m->K, m->Z, m->V) * m->L;
+    std::vector<double> p(total);
+    CK(cudaStreamSynchronize(m->ctx->stream));
+    CK(cudaMemcpy(p.data(), m->tparams.p, sizeof(double) * total, cudaMemcpyDeviceToHost));
+    m->params_host = p;
+    if (int rc = tc_pack(m->tc, m->K, m->Z, m->V, m->L, p.data(),
+                         m->has_masks ? m->masks_host.data() : nullptr))
+        return rc;
+    m->tc_stale = false;
     return 0;
 }
 
@@ -237,9 +255,12 @@ int run_pre(detnet_model *m, cudaStream_t st, long s0, long cnt, long n_total, c
 
 // K2 over tiles [t0, t0+nt) (samples relative to s_base = t0*TILE).
 int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, int l_begin,
-              int l_end, bool trainable_only, float *xhat, float *xs, float *vs) {
+              int l_end, bool trainable_only, float *xhat, float *xs, float *vs,
+              const TraceBufs *trace) {
     detnet_ctx *c = m->ctx;
-    if (use_tc(m)) {
+    if (!trace && m->ctx->path != 1)
+        if (int rc = refresh_tc(m)) return rc;
+    if (use_tc(m) && !trace) {
         TcArgs ta{};
         ta.gp = c->gp.as<float>();
         ta.q32 = c->q32.as<float>();
@@ -276,6 +297,13 @@ int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, 
     a.v_state = vs;
     a.tile_loss = c->tile_loss.as<double>();
     a.tile_err = c->tile_err.as<long long>();
+    if (trace) {
+        a.tr_in = trace->in;
+        a.tr_z = trace->z;
+        a.tr_u2 = trace->u2;
+        a.tr_xf = trace->xf;
+        a.ts = trace->ts;
+    }
     const size_t smem = 2 * static_cast<size_t>(m->simt_rec) * 4 + 64;
     const int blocks = static_cast<int>((nt + 1) / 2);
     {
@@ -323,7 +351,7 @@ int reset_sing(detnet_ctx *c, cudaStream_t st) {
     return 0;
 }
 
-} // namespace
+} // namespace detnet
 
 // =========================================================================
 extern "C" {

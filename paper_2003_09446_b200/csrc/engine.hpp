@@ -90,13 +90,6 @@ int tc_launch(const TcModel &tc, const TcArgs &a, cudaStream_t st);
 int tc_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cudaStream_t st);
 void tc_release(TcModel &tc);
 
-// training (train.cu)
-int train_batch_gradient(detnet_model *m, long n, const float *H, const float *y,
-                         const int8_t *x, const detnet_loss_spec *spec, int trainable_only,
-                         double *grads_out, detnet_eval *out);
-int train_adam_step(detnet_ctx *c, int n_tx, int z_dim, int v_dim, int depth, int frozen_prefix,
-                    double *params, const double *masks, const double *grads, double *m1,
-                    double *m2, int64_t *step, const detnet_adam_config *cfg);
 
 } // namespace detnet
 
@@ -135,6 +128,11 @@ struct detnet_model {
     std::vector<double> params_host, masks_host;
     bool has_masks = false;
     detnet::TcModel tc; // tcgen05 path packing (stack_tc.cu)
+    // training state (train.cu): FP64 master params, masks, Adam moments
+    detnet::DBuf tparams, tmasks, tm, tv;
+    int64_t adam_step = 0;
+    bool train_ready = false;
+    bool tc_stale = false;  // tcgen05 images lag the device master params
 };
 
 namespace detnet {
@@ -189,6 +187,21 @@ inline int check_launch() {
     if (e != cudaSuccess) return fail(DETNET_ERR_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
     return 0;
 }
+
+// forward-path helpers (detnet_capi.cu) shared with the training step
+struct TraceBufs {
+    float *in, *z, *u2, *xf;
+    long ts;
+};
+int ensure_ws(detnet_ctx *c, long n, int K);
+int reset_sing(detnet_ctx *c, cudaStream_t st);
+int run_pre(detnet_model *m, cudaStream_t st, long s0, long cnt, long n_total, const float *H,
+            const float *y, const int8_t *x);
+int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, int l_begin,
+              int l_end, bool trainable_only, float *xhat, float *xs, float *vs,
+              const TraceBufs *trace = nullptr);
+int finish(detnet_model *m, long n, detnet_eval *out);
+int pack_simt_device(detnet_model *m); // FP32 records from the FP64 master copy
 
 // training (train.cu)
 int train_batch_gradient(detnet_model *m, long n, const float *H, const float *y,

@@ -50,6 +50,13 @@ struct StackArgs {
     float *v_state;         // optional [s][V] in/out
     double *tile_loss;      // [global tile]
     long long *tile_err;    // [global tile]
+    // optional training trace (backward.cpp:105-165 needs in, u1 (via z), z,
+    // u2 per layer), feature-major / sample-minor: [l][feature][ts]
+    float *tr_in;           // [L][IN][ts]   layer input [q; x; Gx; v]
+    float *tr_z;            // [L][Z][ts]    relu(u1)
+    float *tr_u2;           // [L][K][ts]
+    float *tr_xf;           // [K][ts]       x_hat_L
+    long ts;                // trace sample stride (>= padded sample count)
 };
 
 template <int K, int Z, int V>
@@ -131,6 +138,17 @@ __global__ void __launch_bounds__(256, 1) k_stack_simt(StackArgs a) {
                 }
         }
 
+        if (a.tr_in && live_tile) {
+            float *ti = a.tr_in + static_cast<long>(l) * IN * a.ts + s;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                ti[k * a.ts] = q[k];
+                ti[(K + k) * a.ts] = x[k];
+                ti[(2 * K + k) * a.ts] = gx[k];
+            }
+#pragma unroll
+            for (int k = 0; k < V; ++k) ti[(3 * K + k) * a.ts] = v[k];
+        }
         float acc[O];
         const float *b23 = W + Z * IN4 + Z * O4;
 #pragma unroll
@@ -159,6 +177,7 @@ __global__ void __launch_bounds__(256, 1) k_stack_simt(StackArgs a) {
             }
             const float u = (u0 + u1) + (u2 + u3);
             const float z = u > 0.f ? u : 0.f;
+            if (a.tr_z && live_tile) a.tr_z[(static_cast<long>(l) * Z + i) * a.ts + s] = z;
             const float4 *c4 = reinterpret_cast<const float4 *>(W + Z * IN4 + i * O4);
 #pragma unroll
             for (int m = 0; m < O4 / 4; ++m) {
@@ -175,6 +194,7 @@ __global__ void __launch_bounds__(256, 1) k_stack_simt(StackArgs a) {
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             const float u = acc[k];
+            if (a.tr_u2 && live_tile) a.tr_u2[(static_cast<long>(l) * K + k) * a.ts + s] = u;
             const float xn = u <= -t ? -1.f : (u >= t ? 1.f : __fdiv_rn(u, t));
             x[k] = xn;
             const double d = ((xm >> k) & 1u ? 1.0 : -1.0) - static_cast<double>(xn);
@@ -202,6 +222,10 @@ __global__ void __launch_bounds__(256, 1) k_stack_simt(StackArgs a) {
 #pragma unroll
         for (int k = 0; k < V; ++k) a.v_state[s * V + k] = v[k];
     }
+    if (a.tr_xf && live_tile) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) a.tr_xf[k * a.ts + s] = x[k];
+    }
     long long errs = 0;
 #pragma unroll
     for (int k = 0; k < K; ++k) errs += (x[k] >= 0.f) != (((xm >> k) & 1u) != 0);
@@ -222,7 +246,7 @@ __global__ void __launch_bounds__(256, 1) k_stack_simt(StackArgs a) {
 }
 
 // K5: fixed-order reduction of per-tile partials and per-sample flags.
-__global__ void __launch_bounds__(1024) k_reduce(const double *tile_loss, const long long *tile_err,
+static __global__ void __launch_bounds__(1024) k_reduce(const double *tile_loss, const long long *tile_err,
                                                  long n_tiles, const uint8_t *flag, long n,
                                                  double *out_loss, long long *out_err,
                                                  long long *out_flag) {

@@ -1,0 +1,414 @@
+// k_train.cuh -- training-step kernels (BASELINE config 5): the reverse sweep
+// of backward_data (backward.cpp:105-165), the batch reductions that turn it
+// into weight gradients, the regularizer gradient (backward.cpp:169-220) and
+// Adam (adam.cpp:48-79).
+//
+// Data layout: the forward pass (k_stack_simt with trace pointers) records,
+// feature-major / sample-minor ([l][feature][ts]), the layer input
+// in = [q; x; Gx; v], z = relu(u1) and u2, plus x_hat_L. The backward sweep
+// (one thread per sample, all trainable layers, weights double-buffered in
+// shared memory in reverse layer order) writes the per-sample adjoints
+//   u1bar [l][Z][ts],  g23bar [l][K+V][ts] = [u2bar; vbar]
+// and per-CTA partial t-gradients. The weight gradients are then batch
+// contractions over the sample axis,
+//   dW1 = u1bar . in^T,  dW2|dW3 = [u2bar; vbar] . z^T  (+ bias = row sums),
+// computed by a split-K kernel (FP32 inside a split of 256 samples, FP64
+// across splits, fixed order => deterministic), scaled by 1/n, masked and
+// combined with the regularizer gradient in FP64.
+#pragma once
+
+#include "common.cuh"
+#include "k_stack_simt.cuh"
+
+namespace detnet {
+
+struct BwdArgs {
+    const float *gp;        // [tile][NG][TILE]
+    const double *denom;    // [s]
+    const uint32_t *xmask;  // [s]
+    const float *wrec;      // SIMT layer records
+    long rec_floats;
+    const double *lnk;      // ln(l+1)
+    int L, lf;              // layers, frozen prefix (sweep l = L-1 .. lf)
+    long n, n_tiles, ts;
+    const float *tr_in, *tr_z, *tr_u2, *tr_xf;
+    float *u1bar;           // [L][Z][ts]
+    float *g23bar;          // [L][K+V][ts]
+    double *tbar_part;      // [L][gridDim.x]
+};
+
+template <int K, int Z, int V>
+__global__ void __launch_bounds__(256, 1) k_train_bwd(BwdArgs a) {
+    constexpr int IN = 3 * K + V;
+    constexpr int IN4 = simt_in4(K, V);
+    constexpr int O = K + V;
+    constexpr int O4 = simt_o4(K, V);
+    constexpr int NG = gram_entries(K);
+    constexpr int REC = static_cast<int>(simt_rec(K, Z, V));
+    extern __shared__ __align__(128) float sw[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sw + 2 * REC);
+    __shared__ double s_t[2][8];
+
+    const int tid = threadIdx.x;
+    const long tile_l = static_cast<long>(blockIdx.x) * 2 + (tid >> 7);
+    const bool live_tile = tile_l < a.n_tiles;
+    const long tile = live_tile ? tile_l : a.n_tiles - 1;
+    const int col = tid & (TILE - 1);
+    const long s = tile * TILE + col;
+    const bool live = live_tile && s < a.n;
+
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const uint32_t bytes = static_cast<uint32_t>(REC) * 4u;
+    const int nl = a.L - a.lf;
+    if (tid == 0) {
+        for (int b = 0; b < 2 && b < nl; ++b) {
+            mbar_arrive_expect_tx(&bars[b], bytes);
+            bulk_g2s_chunked(sw + b * REC, a.wrec + static_cast<long>(a.L - 1 - b) * a.rec_floats,
+                             bytes, &bars[b]);
+        }
+    }
+    const uint32_t xm = a.xmask[tile * TILE + col];
+    const float dinv2 = static_cast<float>(2.0 / a.denom[tile * TILE + col]);
+    const float *gps = a.gp + tile * NG * TILE + col;
+    float abar[K], vbar[V];
+#pragma unroll
+    for (int k = 0; k < K; ++k) abar[k] = 0.f;
+#pragma unroll
+    for (int k = 0; k < V; ++k) vbar[k] = 0.f;
+
+    for (int it = 0; it < nl; ++it) {
+        const int l = a.L - 1 - it;
+        const int b = it & 1;
+        mbar_wait(&bars[b], (it >> 1) & 1);
+        const float *W = sw + b * REC;
+        // a_bar += 2 ln(l+1)/denom (x_hat_{l+1} - x)
+        const float w = static_cast<float>(a.lnk[l]) * dinv2;
+        const float *xn = l + 1 < a.L ? a.tr_in + (static_cast<long>(l + 1) * IN + K) * a.ts + s
+                                      : a.tr_xf + s;
+        const float t = W[Z * IN4 + Z * O4 + O4];
+        const float tinv = 1.f / t;
+        float u2bar[K];
+        float tb = 0.f;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const float xk = (xm >> k) & 1u ? 1.f : -1.f;
+            abar[k] = fmaf(w, xn[k * a.ts] - xk, abar[k]);
+            const float u = a.tr_u2[(static_cast<long>(l) * K + k) * a.ts + s];
+            const bool lin = u >= -t && u < t; // model.cpp:45-51
+            u2bar[k] = lin ? abar[k] * tinv : 0.f;
+            tb += lin ? abar[k] * (-u * tinv * tinv) : 0.f;
+        }
+        // threads of a clamped (dead) second tile alias a live tile: no writes
+        float *g23 = a.g23bar + static_cast<long>(l) * O * a.ts + s;
+        if (live_tile) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) g23[k * a.ts] = live ? u2bar[k] : 0.f;
+#pragma unroll
+            for (int k = 0; k < V; ++k) g23[(K + k) * a.ts] = live ? vbar[k] : 0.f;
+        }
+        // z_bar = W2^T u2bar + W3^T vbar; u1bar = z_bar [u1 > 0]; in_bar = W1^T u1bar
+        float ibar[IN - K]; // x, Gx, v blocks (the q block is data)
+#pragma unroll
+        for (int j = 0; j < IN - K; ++j) ibar[j] = 0.f;
+        const float *zl = a.tr_z + static_cast<long>(l) * Z * a.ts + s;
+        float *u1b = a.u1bar + static_cast<long>(l) * Z * a.ts + s;
+#pragma unroll 1
+        for (int i = 0; i < Z; ++i) {
+            const float4 *c4 = reinterpret_cast<const float4 *>(W + Z * IN4 + i * O4);
+            float zb0 = 0.f, zb1 = 0.f;
+#pragma unroll
+            for (int m = 0; m < O4 / 4; ++m) {
+                const float4 c = c4[m];
+#define DETNET_G(j) ((j) < K ? u2bar[(j) < K ? (j) : 0] : vbar[((j) - K) < V ? (j) - K : 0])
+                if (4 * m + 0 < O) zb0 = fmaf(c.x, DETNET_G(4 * m + 0), zb0);
+                if (4 * m + 1 < O) zb1 = fmaf(c.y, DETNET_G(4 * m + 1), zb1);
+                if (4 * m + 2 < O) zb0 = fmaf(c.z, DETNET_G(4 * m + 2), zb0);
+                if (4 * m + 3 < O) zb1 = fmaf(c.w, DETNET_G(4 * m + 3), zb1);
+#undef DETNET_G
+            }
+            const float ub = zl[i * a.ts] > 0.f ? zb0 + zb1 : 0.f;
+            if (live_tile) u1b[i * a.ts] = live ? ub : 0.f;
+            const float4 *w4 = reinterpret_cast<const float4 *>(W + i * IN4);
+#pragma unroll
+            for (int m = K / 4; m < IN4 / 4; ++m) {
+                const float4 wv = w4[m];
+#define DETNET_IB(c, wc)                                                                        \
+    if (4 * m + (c) >= K && 4 * m + (c) < IN)                                                    \
+        ibar[(4 * m + (c) - K) >= 0 ? 4 * m + (c) - K : 0] =                                    \
+            fmaf(wc, ub, ibar[(4 * m + (c) - K) >= 0 ? 4 * m + (c) - K : 0]);
+                DETNET_IB(0, wv.x)
+                DETNET_IB(1, wv.y)
+                DETNET_IB(2, wv.z)
+                DETNET_IB(3, wv.w)
+#undef DETNET_IB
+            }
+        }
+        // a_bar <- G gx_bar + x_bar (G symmetric); v_bar <- v block
+#pragma unroll
+        for (int k = 0; k < K; ++k) abar[k] = ibar[k];
+        {
+            int e = 0;
+#pragma unroll
+            for (int r = 0; r < K; ++r)
+#pragma unroll
+                for (int c = r; c < K; ++c, ++e) {
+                    const float g = __ldg(gps + e * TILE);
+                    abar[r] = fmaf(g, ibar[K + c], abar[r]);
+                    if (c != r) abar[c] = fmaf(g, ibar[K + r], abar[c]);
+                }
+        }
+#pragma unroll
+        for (int k = 0; k < V; ++k) vbar[k] = ibar[2 * K + k];
+        // per-CTA t gradient (deterministic tree)
+        double tsum = live ? static_cast<double>(tb) : 0.0;
+        tsum = warp_sum(tsum);
+        if ((tid & 31) == 0) s_t[it & 1][tid >> 5] = tsum;
+        __syncthreads(); // also: every thread is done reading buffer b
+        if (tid == 0) {
+            double acc = 0.0;
+            for (int w8 = 0; w8 < 8; ++w8) acc += s_t[it & 1][w8];
+            a.tbar_part[static_cast<long>(l) * gridDim.x + blockIdx.x] = acc;
+            if (it + 2 < nl) {
+                mbar_arrive_expect_tx(&bars[b], bytes);
+                bulk_g2s_chunked(sw + b * REC,
+                                 a.wrec + static_cast<long>(a.L - 1 - (it + 2)) * a.rec_floats,
+                                 bytes, &bars[b]);
+            }
+        }
+    }
+}
+
+// C[job][m][n] partial over a split of samples: C = A . B^T with A [M][ts],
+// B [N][ts]; column n == N is the bias (sum of A). Jobs = (layer, which).
+struct DwJob {
+    const float *A;
+    const float *B;
+    int M, N;       // output M x (N + 1)
+    double *out;    // [splits][M][N+1] partials
+};
+
+constexpr int DW_TILE = 32, DW_SPLIT = 256, DW_KC = 32;
+
+__global__ void __launch_bounds__(256) k_dw_gemm(const DwJob *jobs, long n, long ts, int splits) {
+    const DwJob jb = jobs[blockIdx.z];
+    const int m0 = blockIdx.y * DW_TILE, n0 = blockIdx.x * DW_TILE;
+    if (m0 >= jb.M || n0 > jb.N) return;
+    __shared__ float sA[DW_KC][DW_TILE + 1], sB[DW_KC][DW_TILE + 1];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4; // 16 x 16 threads, 2 x 2 outputs
+    for (int sp = 0; sp < splits; ++sp) {
+        const long k0 = static_cast<long>(sp) * DW_SPLIT;
+        const long k1 = k0 + DW_SPLIT < n ? k0 + DW_SPLIT : n;
+        float c[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+        for (long kc = k0; kc < k1; kc += DW_KC) {
+            for (int idx = threadIdx.x; idx < DW_KC * DW_TILE; idx += 256) {
+                const int kk = idx % DW_KC, r = idx / DW_KC;
+                const long k = kc + kk;
+                const bool in = k < k1;
+                const int mr = m0 + r, nr = n0 + r;
+                sA[kk][r] = (in && mr < jb.M) ? jb.A[static_cast<long>(mr) * ts + k] : 0.f;
+                sB[kk][r] = (in && nr < jb.N) ? jb.B[static_cast<long>(nr) * ts + k]
+                                              : ((in && nr == jb.N) ? 1.f : 0.f);
+            }
+            __syncthreads();
+#pragma unroll 8
+            for (int kk = 0; kk < DW_KC; ++kk) {
+                const float a0 = sA[kk][ty], a1 = sA[kk][ty + 16];
+                const float b0 = sB[kk][tx], b1 = sB[kk][tx + 16];
+                c[0][0] = fmaf(a0, b0, c[0][0]);
+                c[0][1] = fmaf(a0, b1, c[0][1]);
+                c[1][0] = fmaf(a1, b0, c[1][0]);
+                c[1][1] = fmaf(a1, b1, c[1][1]);
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int mr = m0 + ty + 16 * i, nc = n0 + tx + 16 * j;
+                if (mr < jb.M && nc <= jb.N)
+                    jb.out[(static_cast<long>(sp) * jb.M + mr) * (jb.N + 1) + nc] = c[i][j];
+            }
+    }
+}
+
+struct SumArgs {
+    const double *p1;     // W1 partials [L][splits][Z][IN+1]
+    const double *p23;    // W23 partials [L][splits][K+V][Z+1]
+    const double *tpart;  // [L][tblocks]
+    int tblocks, splits;
+    int K, Z, V, L, lf;
+    double *raw;          // [L][P] unscaled, unmasked data-gradient sums (record layout)
+};
+
+// Sum the split partials in fixed order (FP64) into record layout. The raw
+// sums are what ranks all-reduce (sum) before the update.
+__global__ void k_grad_sum(SumArgs a) {
+    const int K = a.K, Z = a.Z, V = a.V, IN = 3 * K + V;
+    const int P = Z * IN + Z + K * Z + K + V * Z + V + 1;
+    const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= static_cast<long>(a.L) * P) return;
+    const int l = static_cast<int>(idx / P), e = static_cast<int>(idx % P);
+    if (l < a.lf) { a.raw[idx] = 0.0; return; }
+    const int ob1 = Z * IN, oW2 = ob1 + Z, ob2 = oW2 + K * Z, oW3 = ob2 + K, ob3 = oW3 + V * Z, ot = ob3 + V;
+    double sum = 0.0;
+    if (e == ot) {
+        for (int b = 0; b < a.tblocks; ++b) sum += a.tpart[static_cast<long>(l) * a.tblocks + b];
+    } else {
+        const double *src;
+        long stride, base;
+        if (e < ob1) { // W1[i][j]
+            src = a.p1 + static_cast<long>(l) * a.splits * Z * (IN + 1);
+            base = static_cast<long>(e / IN) * (IN + 1) + e % IN;
+            stride = static_cast<long>(Z) * (IN + 1);
+        } else if (e < oW2) { // b1[i]
+            src = a.p1 + static_cast<long>(l) * a.splits * Z * (IN + 1);
+            base = static_cast<long>(e - ob1) * (IN + 1) + IN;
+            stride = static_cast<long>(Z) * (IN + 1);
+        } else {
+            int r, c;
+            if (e < ob2) { r = (e - oW2) / Z; c = (e - oW2) % Z; }          // W2[k][i]
+            else if (e < oW3) { r = e - ob2; c = Z; }                        // b2[k]
+            else if (e < ob3) { r = K + (e - oW3) / Z; c = (e - oW3) % Z; } // W3[v][i]
+            else { r = K + (e - ob3); c = Z; }                               // b3[v]
+            src = a.p23 + static_cast<long>(l) * a.splits * (K + V) * (Z + 1);
+            base = static_cast<long>(r) * (Z + 1) + c;
+            stride = static_cast<long>(K + V) * (Z + 1);
+        }
+        for (int sp = 0; sp < a.splits; ++sp) sum += src[sp * stride + base];
+    }
+    a.raw[idx] = sum;
+}
+
+struct RegArgs {
+    const double *raw;     // [L][P] (all-reduced across ranks)
+    const double *params;  // FP64 master records [L][P]
+    const double *masks;   // [L][P] or null
+    const double *colnorm; // [L][ng] group norms (SGL)
+    int K, Z, V, L, lf;
+    double inv_n;
+    int kind;              // 0 plain, 1 element_l1, 2 sparse_group
+    double lam, lam1, lam2;
+    double *grads;         // [L][P] out
+};
+
+// Column-group norms of [W (.) M | b (.) mb] (loss.cpp:43-59, backward.cpp:175-199):
+// groups per layer = IN + 1 (W1) + Z + 1 (W2) + Z + 1 (W3).
+__global__ void k_group_norms(const double *params, const double *masks, int K, int Z, int V,
+                              int L, int lf, double *colnorm) {
+    const int IN = 3 * K + V, P = Z * IN + Z + K * Z + K + V * Z + V + 1;
+    const int ng = IN + 1 + 2 * (Z + 1);
+    const long g = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (g >= static_cast<long>(L - lf) * ng) return;
+    const int l = lf + static_cast<int>(g / ng), j = static_cast<int>(g % ng);
+    const double *p = params + static_cast<long>(l) * P;
+    const double *mk = masks ? masks + static_cast<long>(l) * P : nullptr;
+    const int oW1 = 0, ob1 = Z * IN, oW2 = ob1 + Z, ob2 = oW2 + K * Z, oW3 = ob2 + K, ob3 = oW3 + V * Z;
+    int off, rows, cols, col;
+    bool bias;
+    if (j <= IN) { off = j < IN ? oW1 : ob1; rows = Z; cols = IN; col = j; bias = j == IN; }
+    else if (j <= IN + 1 + Z) { const int jj = j - IN - 1; off = jj < Z ? oW2 : ob2; rows = K; cols = Z; col = jj; bias = jj == Z; }
+    else { const int jj = j - IN - 2 - Z; off = jj < Z ? oW3 : ob3; rows = V; cols = Z; col = jj; bias = jj == Z; }
+    double sq = 0.0;
+    for (int i = 0; i < rows; ++i) {
+        const long e = bias ? off + i : off + static_cast<long>(i) * cols + col;
+        const double w = dmul(p[e], mk ? mk[e] : 1.0);
+        sq = dadd(sq, dmul(w, w));
+    }
+    colnorm[static_cast<long>(l) * ng + j] = sqrt(sq);
+}
+
+__device__ __forceinline__ double sign0(double w) { return w > 0.0 ? 1.0 : (w < 0.0 ? -1.0 : 0.0); }
+
+// grads = raw * mask / n + regularizer gradient (backward.cpp:169-220 order:
+// group term then L1 term; kernels.cpp:195-198 scaling).
+__global__ void k_grad_apply_reg(RegArgs a) {
+    const int K = a.K, Z = a.Z, V = a.V, IN = 3 * K + V;
+    const int P = Z * IN + Z + K * Z + K + V * Z + V + 1;
+    const int ng = IN + 1 + 2 * (Z + 1);
+    const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= static_cast<long>(a.L) * P) return;
+    const int l = static_cast<int>(idx / P), e = static_cast<int>(idx % P);
+    if (l < a.lf) { a.grads[idx] = 0.0; return; }
+    const int ob1 = Z * IN, oW2 = ob1 + Z, ob2 = oW2 + K * Z, oW3 = ob2 + K, ob3 = oW3 + V * Z, ot = ob3 + V;
+    const double mk = (a.masks && e != ot) ? a.masks[idx] : 1.0;
+    double g = dmul(dmul(a.raw[idx], mk), a.inv_n);
+    if (e != ot && a.kind != 0) {
+        int gcol;
+        bool weight;
+        if (e < ob1) { gcol = e % IN; weight = true; }
+        else if (e < oW2) { gcol = IN; weight = false; }
+        else if (e < ob2) { gcol = IN + 1 + (e - oW2) % Z; weight = true; }
+        else if (e < oW3) { gcol = IN + 1 + Z; weight = false; }
+        else if (e < ob3) { gcol = IN + 2 + Z + (e - oW3) % Z; weight = true; }
+        else { gcol = IN + 2 + 2 * Z; weight = false; }
+        const double w = a.params[idx];
+        if (a.kind == 2) {
+            const double nrm = a.colnorm[static_cast<long>(l) * ng + gcol];
+            if (nrm > 0.0) g = dadd(g, dmul(dmul(ddiv(a.lam1, nrm), w), mk));
+            if (weight) g = dadd(g, dmul(dmul(a.lam2, sign0(w)), mk));
+        } else if (weight) {
+            g = dadd(g, dmul(dmul(a.lam, sign0(w)), mk));
+        }
+    }
+    a.grads[idx] = g;
+}
+
+// adam.cpp:30-79 per entry, FP64 without contraction (bit-identical to the
+// reference for identical inputs). Masked entries (mask 0) untouched.
+__global__ void k_adam(double *params, const double *masks, const double *grads, double *m,
+                       double *v, long count, int P, int lf, double lr, double b1, double b2,
+                       double eps, double bc1, double bc2) {
+    const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= count) return;
+    const int l = static_cast<int>(idx / P), e = static_cast<int>(idx % P);
+    if (l < lf) return;
+    const bool is_t = e == P - 1;
+    if (!is_t && masks && masks[idx] == 0.0) return;
+    const double g = grads[idx];
+    const double mi = dadd(dmul(b1, m[idx]), dmul(dsub(1.0, b1), g));
+    const double vi = dadd(dmul(b2, v[idx]), dmul(dmul(dsub(1.0, b2), g), g));
+    m[idx] = mi;
+    v[idx] = vi;
+    const double mhat = ddiv(mi, bc1);
+    const double vhat = ddiv(vi, bc2);
+    double w = dsub(params[idx], ddiv(dmul(lr, mhat), dadd(__dsqrt_rn(vhat), eps)));
+    if (is_t && w < 1e-3) w = 1e-3;
+    params[idx] = w;
+}
+
+// FP64 records -> SIMT FP32 records (same mapping as the host packer).
+__global__ void k_pack_simt(const double *params, const double *masks, int K, int Z, int V, int L,
+                            float *out) {
+    const int IN = 3 * K + V, IN4 = simt_in4(K, V), O4 = simt_o4(K, V);
+    const long R = simt_rec(K, Z, V);
+    const int P = Z * IN + Z + K * Z + K + V * Z + V + 1;
+    const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= static_cast<long>(L) * R) return;
+    const int l = static_cast<int>(idx / R);
+    const long r = idx % R;
+    const double *p = params + static_cast<long>(l) * P;
+    const double *mk = masks ? masks + static_cast<long>(l) * P : nullptr;
+    auto w = [&](long off) { return static_cast<float>(p[off] * (mk ? mk[off] : 1.0)); };
+    const int oW1 = 0, ob1 = Z * IN, oW2 = ob1 + Z, ob2 = oW2 + K * Z, oW3 = ob2 + K, ob3 = oW3 + V * Z, ot = ob3 + V;
+    float val = 0.f;
+    if (r < static_cast<long>(Z) * IN4) {
+        const int i = static_cast<int>(r / IN4), j = static_cast<int>(r % IN4);
+        val = j < IN ? w(oW1 + i * IN + j) : (j == IN ? w(ob1 + i) : 0.f);
+    } else if (r < static_cast<long>(Z) * IN4 + static_cast<long>(Z) * O4) {
+        const long rr = r - static_cast<long>(Z) * IN4;
+        const int i = static_cast<int>(rr / O4), k = static_cast<int>(rr % O4);
+        val = k < K ? w(oW2 + k * Z + i) : (k < K + V ? w(oW3 + (k - K) * Z + i) : 0.f);
+    } else {
+        const int k = static_cast<int>(r - static_cast<long>(Z) * IN4 - static_cast<long>(Z) * O4);
+        val = k < K ? w(ob2 + k) : (k < K + V ? w(ob3 + (k - K)) : (k == O4 ? static_cast<float>(p[ot]) : 0.f));
+    }
+    out[idx] = val;
+}
+
+} // namespace detnet

@@ -1,16 +1,373 @@
-// train.cu -- forward+backward training step and Adam (in progress).
+// train.cu -- the training step on the device (BASELINE config 5):
+// batch_gradient (kernels.cpp:160-200) = preprocessing + forward with trace +
+// reverse sweep + batch contractions + regularizer gradient, and adam_step
+// (adam.cpp:48-79). Exposed through detnet_batch_gradient / detnet_adam_step
+// (host arrays, the reference seam) and detnet_train_grad / detnet_train_apply
+// (device-resident step; raw gradient sums in a caller buffer so ranks can
+// all-reduce them between the two calls).
+#include <cmath>
+#include <cstring>
+#include <vector>
+
 #include "engine.hpp"
+#include "k_train.cuh"
 
 namespace detnet {
+namespace {
 
-int train_batch_gradient(detnet_model *, long, const float *, const float *, const int8_t *,
-                         const detnet_loss_spec *, int, double *, detnet_eval *) {
-    return fail(DETNET_ERR_UNSUPPORTED, "batch_gradient: not built yet");
+using BwdFn = void (*)(dim3, dim3, size_t, cudaStream_t, const BwdArgs &);
+
+template <int K, int Z, int V>
+void launch_bwd(dim3 g, dim3 b, size_t sm, cudaStream_t st, const BwdArgs &a) {
+    k_train_bwd<K, Z, V><<<g, b, sm, st>>>(a);
+}
+template <int K, int Z, int V> int set_bwd_smem() {
+    return cudaFuncSetAttribute(k_train_bwd<K, Z, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(2 * simt_rec(K, Z, V) * 4 + 64)) == cudaSuccess
+               ? 0
+               : -1;
 }
 
-int train_adam_step(detnet_ctx *, int, int, int, int, int, double *, const double *,
-                    const double *, double *, double *, int64_t *, const detnet_adam_config *) {
-    return fail(DETNET_ERR_UNSUPPORTED, "adam_step: not built yet");
+struct BwdEntry {
+    int K, Z, V;
+    BwdFn fn;
+    int (*prep)();
+};
+const BwdEntry kBwd[] = {
+    {20, 160, 40, launch_bwd<20, 160, 40>, set_bwd_smem<20, 160, 40>},
+    {2, 16, 4, launch_bwd<2, 16, 4>, set_bwd_smem<2, 16, 4>},
+    {3, 24, 6, launch_bwd<3, 24, 6>, set_bwd_smem<3, 24, 6>},
+    {4, 32, 8, launch_bwd<4, 32, 8>, set_bwd_smem<4, 32, 8>},
+    {6, 48, 12, launch_bwd<6, 48, 12>, set_bwd_smem<6, 48, 12>},
+    {8, 64, 16, launch_bwd<8, 64, 16>, set_bwd_smem<8, 64, 16>},
+};
+
+const BwdEntry *find_bwd(int K, int Z, int V) {
+    static bool prepped = false;
+    if (!prepped) {
+        for (const BwdEntry &e : kBwd) e.prep();
+        prepped = true;
+    }
+    for (const BwdEntry &e : kBwd)
+        if (e.K == K && e.Z == Z && e.V == V) return &e;
+    return nullptr;
+}
+
+struct TrainWs {
+    DBuf tr_in, tr_z, tr_u2, tr_xf, u1bar, g23bar, tbar, p1, p23, jobs, raw, grads, colnorm;
+    DBuf in_H, in_y, in_x;
+};
+
+TrainWs &ws_for(detnet_ctx *c) {
+    // one workspace per context (contexts are single-owner)
+    static std::vector<std::pair<detnet_ctx *, TrainWs *>> all;
+    for (auto &p : all)
+        if (p.first == c) return *p.second;
+    all.push_back({c, new TrainWs()});
+    return *all.back().second;
+}
+
+long rec_size(const detnet_model *m) { return record_size(m->K, m->Z, m->V); }
+
+int ensure_train_state(detnet_model *m) {
+    if (m->train_ready) return 0;
+    const size_t bytes = sizeof(double) * rec_size(m) * m->L;
+    if (m->tparams.ensure(bytes) || m->tmasks.ensure(bytes) || m->tm.ensure(bytes) ||
+        m->tv.ensure(bytes))
+        return fail(DETNET_ERR_CUDA, "training state allocation failed");
+    CK(cudaMemcpy(m->tparams.p, m->params_host.data(), bytes, cudaMemcpyHostToDevice));
+    if (m->has_masks) {
+        CK(cudaMemcpy(m->tmasks.p, m->masks_host.data(), bytes, cudaMemcpyHostToDevice));
+    } else {
+        std::vector<double> ones(rec_size(m) * m->L, 1.0);
+        CK(cudaMemcpy(m->tmasks.p, ones.data(), bytes, cudaMemcpyHostToDevice));
+    }
+    CK(cudaMemset(m->tm.p, 0, bytes));
+    CK(cudaMemset(m->tv.p, 0, bytes));
+    m->adam_step = 0;
+    m->train_ready = true;
+    return 0;
+}
+
+// Forward with trace + reverse sweep + contractions -> raw gradient sums
+// (record layout, unscaled, unmasked) in `raw`; local BatchEval in *out.
+int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8_t *x,
+             bool trainable_only, double *raw, detnet_eval *out) {
+    detnet_ctx *c = m->ctx;
+    const BwdEntry *be = find_bwd(m->K, m->Z, m->V);
+    if (!be) return fail(DETNET_ERR_UNSUPPORTED, "no backward kernel for these dims");
+    if (n < 1) return fail(DETNET_ERR_CONTRACT, "batch_gradient: empty batch");
+    const int K = m->K, Z = m->Z, V = m->V, L = m->L, IN = 3 * K + V, O = K + V;
+    const int lf = m->frozen;
+    const long tiles = (n + TILE - 1) / TILE, ts = tiles * TILE;
+    TrainWs &w = ws_for(c);
+    const int splits = static_cast<int>((n + DW_SPLIT - 1) / DW_SPLIT);
+    const int bwd_blocks = static_cast<int>((tiles + 1) / 2);
+    if (w.tr_in.ensure(sizeof(float) * L * IN * ts) || w.tr_z.ensure(sizeof(float) * L * Z * ts) ||
+        w.tr_u2.ensure(sizeof(float) * L * K * ts) || w.tr_xf.ensure(sizeof(float) * K * ts) ||
+        w.u1bar.ensure(sizeof(float) * L * Z * ts) || w.g23bar.ensure(sizeof(float) * L * O * ts) ||
+        w.tbar.ensure(sizeof(double) * L * bwd_blocks) ||
+        w.p1.ensure(sizeof(double) * L * splits * Z * (IN + 1)) ||
+        w.p23.ensure(sizeof(double) * L * splits * O * (Z + 1)) ||
+        w.jobs.ensure(sizeof(DwJob) * 2 * L))
+        return fail(DETNET_ERR_CUDA, "training workspace allocation failed");
+    if (int rc = ensure_ws(c, n, K)) return rc;
+    if (int rc = reset_sing(c, c->stream)) return rc;
+    if (int rc = run_pre(m, c->stream, 0, n, n, H, y, x)) return rc;
+    TraceBufs tb{w.tr_in.as<float>(), w.tr_z.as<float>(), w.tr_u2.as<float>(), w.tr_xf.as<float>(),
+                 ts};
+    if (int rc = run_stack(m, c->stream, 0, tiles, n, 0, L, trainable_only, nullptr, nullptr,
+                           nullptr, &tb))
+        return rc;
+    if (lf < L) {
+        BwdArgs ba{};
+        ba.gp = c->gp.as<float>();
+        ba.denom = c->denom.as<double>();
+        ba.xmask = c->xmask.as<uint32_t>();
+        ba.wrec = m->simt.as<float>();
+        ba.rec_floats = m->simt_rec;
+        ba.lnk = m->lnk_all.as<double>();
+        ba.L = L;
+        ba.lf = lf;
+        ba.n = n;
+        ba.n_tiles = tiles;
+        ba.ts = ts;
+        ba.tr_in = tb.in;
+        ba.tr_z = tb.z;
+        ba.tr_u2 = tb.u2;
+        ba.tr_xf = tb.xf;
+        ba.u1bar = w.u1bar.as<float>();
+        ba.g23bar = w.g23bar.as<float>();
+        ba.tbar_part = w.tbar.as<double>();
+        {
+            LaunchScope ls(c, DETNET_K_BACKWARD, c->stream);
+            be->fn(dim3(bwd_blocks), dim3(256), 2 * static_cast<size_t>(m->simt_rec) * 4 + 64,
+                   c->stream, ba);
+        }
+        if (int rc = check_launch()) return rc;
+        std::vector<DwJob> jobs;
+        for (int l = lf; l < L; ++l) {
+            jobs.push_back({w.u1bar.as<float>() + static_cast<long>(l) * Z * ts,
+                            w.tr_in.as<float>() + static_cast<long>(l) * IN * ts, Z, IN,
+                            w.p1.as<double>() + static_cast<long>(l) * splits * Z * (IN + 1)});
+            jobs.push_back({w.g23bar.as<float>() + static_cast<long>(l) * O * ts,
+                            w.tr_z.as<float>() + static_cast<long>(l) * Z * ts, O, Z,
+                            w.p23.as<double>() + static_cast<long>(l) * splits * O * (Z + 1)});
+        }
+        CK(cudaMemcpyAsync(w.jobs.p, jobs.data(), sizeof(DwJob) * jobs.size(),
+                           cudaMemcpyHostToDevice, c->stream));
+        const int mx = std::max(IN, Z) + 1, my = std::max(Z, O);
+        {
+            LaunchScope ls(c, DETNET_K_BACKWARD, c->stream);
+            k_dw_gemm<<<dim3((mx + DW_TILE - 1) / DW_TILE, (my + DW_TILE - 1) / DW_TILE,
+                             static_cast<unsigned>(jobs.size())),
+                        256, 0, c->stream>>>(w.jobs.as<DwJob>(), n, ts, splits);
+        }
+        if (int rc = check_launch()) return rc;
+    }
+    SumArgs sa{w.p1.as<double>(), w.p23.as<double>(), w.tbar.as<double>(), bwd_blocks, splits,
+               K, Z, V, L, lf, raw};
+    const long total = rec_size(m) * L;
+    {
+        LaunchScope ls(c, DETNET_K_BACKWARD, c->stream);
+        k_grad_sum<<<static_cast<unsigned>((total + 255) / 256), 256, 0, c->stream>>>(sa);
+    }
+    if (int rc = check_launch()) return rc;
+    return finish(m, n, out); // loss / errors / flagged of the forward pass (syncs)
+}
+
+// grads = raw * mask / n_global + regularizer gradient
+int apply_reg(detnet_model *m, const double *raw, long n_global, const detnet_loss_spec *spec,
+              double *grads) {
+    detnet_ctx *c = m->ctx;
+    TrainWs &w = ws_for(c);
+    const int K = m->K, Z = m->Z, V = m->V, L = m->L, IN = 3 * K + V;
+    const int ng = IN + 1 + 2 * (Z + 1);
+    const int kind = spec ? spec->kind : 0;
+    if (w.colnorm.ensure(sizeof(double) * L * ng)) return fail(DETNET_ERR_CUDA, "alloc colnorm");
+    if (kind == 2 && m->frozen < L) {
+        const long groups = static_cast<long>(L - m->frozen) * ng;
+        LaunchScope ls(c, DETNET_K_ADAM, c->stream);
+        k_group_norms<<<static_cast<unsigned>((groups + 127) / 128), 128, 0, c->stream>>>(
+            m->tparams.as<double>(), m->tmasks.as<double>(), K, Z, V, L, m->frozen,
+            w.colnorm.as<double>());
+    }
+    if (int rc = check_launch()) return rc;
+    RegArgs ra{raw, m->tparams.as<double>(), m->tmasks.as<double>(), w.colnorm.as<double>(),
+               K, Z, V, L, m->frozen, 1.0 / static_cast<double>(n_global), kind,
+               spec ? spec->lambda : 0.0, spec ? spec->lambda1 : 0.0, spec ? spec->lambda2 : 0.0,
+               grads};
+    const long total = rec_size(m) * L;
+    {
+        LaunchScope ls(c, DETNET_K_ADAM, c->stream);
+        k_grad_apply_reg<<<static_cast<unsigned>((total + 255) / 256), 256, 0, c->stream>>>(ra);
+    }
+    return check_launch();
+}
+
+void adam_coefs(const detnet_adam_config *cfg, int64_t &step, double &lr, double &bc1,
+                double &bc2) {
+    lr = cfg->lr0 * std::pow(cfg->decay_factor, static_cast<double>(step / cfg->decay_step));
+    step += 1;
+    bc1 = 1.0 - std::pow(cfg->beta1, static_cast<double>(step));
+    bc2 = 1.0 - std::pow(cfg->beta2, static_cast<double>(step));
+}
+
+int validate_adam(const detnet_adam_config *cfg) {
+    if (!cfg || cfg->lr0 <= 0 || cfg->decay_factor <= 0 || cfg->decay_step <= 0 ||
+        cfg->beta1 <= 0 || cfg->beta1 >= 1 || cfg->beta2 <= 0 || cfg->beta2 >= 1 || cfg->eps <= 0)
+        return fail(DETNET_ERR_CONFIG,
+                    "TrainConfig: all optimizer settings must be positive (betas in (0,1))");
+    return 0;
+}
+
+} // namespace
+
+int pack_simt_device(detnet_model *m) {
+    const long R = simt_rec(m->K, m->Z, m->V) * m->L;
+    LaunchScope ls(m->ctx, DETNET_K_ADAM, m->ctx->stream);
+    k_pack_simt<<<static_cast<unsigned>((R + 255) / 256), 256, 0, m->ctx->stream>>>(
+        m->tparams.as<double>(), m->tmasks.as<double>(), m->K, m->Z, m->V, m->L,
+        m->simt.as<float>());
+    return check_launch();
+}
+
+int train_batch_gradient(detnet_model *m, long n, const float *H, const float *y, const int8_t *x,
+                         const detnet_loss_spec *spec, int trainable_only, double *grads_out,
+                         detnet_eval *out) {
+    if (!m || !out || !grads_out || (n > 0 && (!H || !y || !x)))
+        return fail(DETNET_ERR_CONTRACT, "null argument");
+    if (n < 1) return fail(DETNET_ERR_CONTRACT, "batch_gradient: empty batch");
+    detnet_ctx *c = m->ctx;
+    CK(cudaSetDevice(c->device));
+    if (int rc = ensure_train_state(m)) return rc;
+    TrainWs &w = ws_for(c);
+    const int N = m->N, K = m->K;
+    const long total = rec_size(m) * m->L;
+    if (w.in_H.ensure(sizeof(float) * n * N * K) || w.in_y.ensure(sizeof(float) * n * N) ||
+        w.in_x.ensure(static_cast<size_t>(n) * K) || w.raw.ensure(sizeof(double) * total) ||
+        w.grads.ensure(sizeof(double) * total))
+        return fail(DETNET_ERR_CUDA, "allocation failed");
+    CK(cudaMemcpyAsync(w.in_H.p, H, sizeof(float) * n * N * K, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(w.in_y.p, y, sizeof(float) * n * N, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(w.in_x.p, x, static_cast<size_t>(n) * K, cudaMemcpyHostToDevice, c->stream));
+    if (int rc = grad_raw(m, n, w.in_H.as<float>(), w.in_y.as<float>(), w.in_x.as<int8_t>(),
+                          trainable_only != 0, w.raw.as<double>(), out))
+        return rc;
+    if (int rc = apply_reg(m, w.raw.as<double>(), n, spec, w.grads.as<double>())) return rc;
+    CK(cudaMemcpyAsync(grads_out, w.grads.p, sizeof(double) * total, cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    drain_times(c);
+    return 0;
+}
+
+int train_adam_step(detnet_ctx *c, int K, int Z, int V, int L, int lf, double *params,
+                    const double *masks, const double *grads, double *m1, double *m2,
+                    int64_t *step, const detnet_adam_config *cfg) {
+    if (!c || !params || !grads || !m1 || !m2 || !step) return fail(DETNET_ERR_CONTRACT, "null argument");
+    if (int rc = validate_adam(cfg)) return rc;
+    if (L < 1 || lf < 0 || lf > L) return fail(DETNET_ERR_CONTRACT, "bad depth/frozen_prefix");
+    CK(cudaSetDevice(c->device));
+    const long P = record_size(K, Z, V), total = P * L;
+    const size_t bytes = sizeof(double) * total;
+    DBuf buf;
+    if (buf.ensure(5 * bytes)) return fail(DETNET_ERR_CUDA, "adam buffers");
+    double *dp = buf.as<double>(), *dm = dp + total, *dg = dm + total, *d1 = dg + total,
+           *d2 = d1 + total;
+    CK(cudaMemcpyAsync(dp, params, bytes, cudaMemcpyHostToDevice, c->stream));
+    if (masks) CK(cudaMemcpyAsync(dm, masks, bytes, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dg, grads, bytes, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(d1, m1, bytes, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(d2, m2, bytes, cudaMemcpyHostToDevice, c->stream));
+    double lr, bc1, bc2;
+    int64_t st = *step;
+    adam_coefs(cfg, st, lr, bc1, bc2);
+    {
+        LaunchScope ls(c, DETNET_K_ADAM, c->stream);
+        k_adam<<<static_cast<unsigned>((total + 255) / 256), 256, 0, c->stream>>>(
+            dp, masks ? dm : nullptr, dg, d1, d2, total, static_cast<int>(P), lf, lr, cfg->beta1,
+            cfg->beta2, cfg->eps, bc1, bc2);
+    }
+    if (int rc = check_launch()) { buf.release(); return rc; }
+    cudaMemcpyAsync(params, dp, bytes, cudaMemcpyDeviceToHost, c->stream);
+    cudaMemcpyAsync(m1, d1, bytes, cudaMemcpyDeviceToHost, c->stream);
+    cudaMemcpyAsync(m2, d2, bytes, cudaMemcpyDeviceToHost, c->stream);
+    const cudaError_t e = cudaStreamSynchronize(c->stream);
+    buf.release();
+    if (e != cudaSuccess) return fail(DETNET_ERR_CUDA, "adam_step: %s", cudaGetErrorString(e));
+    drain_times(c);
+    *step = st;
+    return 0;
 }
 
 } // namespace detnet
+
+using namespace detnet;
+
+extern "C" {
+
+long detnet_model_param_count(const detnet_model *m) {
+    return m ? record_size(m->K, m->Z, m->V) * m->L : 0;
+}
+
+int detnet_train_grad(detnet_model *m, long n, const float *H, const float *y, const int8_t *x,
+                      int trainable_only, double *raw_dev, detnet_eval *out) {
+    if (!m || !raw_dev || !out) return fail(DETNET_ERR_CONTRACT, "null argument");
+    CK(cudaSetDevice(m->ctx->device));
+    if (int rc = ensure_train_state(m)) return rc;
+    return grad_raw(m, n, H, y, x, trainable_only != 0, raw_dev, out);
+}
+
+int detnet_train_apply(detnet_model *m, const double *raw_dev, long n_global,
+                       const detnet_loss_spec *spec, const detnet_adam_config *cfg) {
+    if (!m || !raw_dev || n_global < 1) return fail(DETNET_ERR_CONTRACT, "bad argument");
+    if (int rc = validate_adam(cfg)) return rc;
+    detnet_ctx *c = m->ctx;
+    CK(cudaSetDevice(c->device));
+    if (int rc = ensure_train_state(m)) return rc;
+    TrainWs &w = ws_for(c);
+    const long total = rec_size(m) * m->L;
+    if (w.grads.ensure(sizeof(double) * total)) return fail(DETNET_ERR_CUDA, "alloc grads");
+    if (int rc = apply_reg(m, raw_dev, n_global, spec, w.grads.as<double>())) return rc;
+    double lr, bc1, bc2;
+    adam_coefs(cfg, m->adam_step, lr, bc1, bc2);
+    {
+        LaunchScope ls(c, DETNET_K_ADAM, c->stream);
+        k_adam<<<static_cast<unsigned>((total + 255) / 256), 256, 0, c->stream>>>(
+            m->tparams.as<double>(), m->tmasks.as<double>(), w.grads.as<double>(),
+            m->tm.as<double>(), m->tv.as<double>(), total, static_cast<int>(rec_size(m)),
+            m->frozen, lr, cfg->beta1, cfg->beta2, cfg->eps, bc1, bc2);
+    }
+    if (int rc = check_launch()) return rc;
+    if (int rc = pack_simt_device(m)) return rc;
+    // the tcgen05 images are rebuilt from the master copy before the next
+    // tensor-core evaluation (refresh_tc)
+    m->tc_stale = true;
+    CK(cudaStreamSynchronize(c->stream));
+    drain_times(c);
+    return 0;
+}
+
+int detnet_model_get_params(detnet_model *m, double *out) {
+    if (!m || !out) return fail(DETNET_ERR_CONTRACT, "null argument");
+    const long total = record_size(m->K, m->Z, m->V) * m->L;
+    if (!m->train_ready) {
+        std::memcpy(out, m->params_host.data(), sizeof(double) * total);
+        return 0;
+    }
+    CK(cudaMemcpy(out, m->tparams.p, sizeof(double) * total, cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+int detnet_model_reset_adam(detnet_model *m) {
+    if (!m) return fail(DETNET_ERR_CONTRACT, "null argument");
+    if (!m->train_ready) return 0;
+    const size_t bytes = sizeof(double) * record_size(m->K, m->Z, m->V) * m->L;
+    CK(cudaMemset(m->tm.p, 0, bytes));
+    CK(cudaMemset(m->tv.p, 0, bytes));
+    m->adam_step = 0;
+    return 0;
+}
+
+} // extern "C"

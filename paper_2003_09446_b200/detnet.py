@@ -120,6 +120,14 @@ _lib.detnet_batch_gradient.argtypes = [_vp, C.c_long, _vp, _vp, _vp, C.POINTER(_
                                        _vp, C.POINTER(_Eval)]
 _lib.detnet_adam_step.argtypes = [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp,
                                   _vp, _vp, C.POINTER(C.c_int64), C.POINTER(_AdamCfg)]
+_lib.detnet_model_param_count.restype = C.c_long
+_lib.detnet_model_param_count.argtypes = [_vp]
+_lib.detnet_train_grad.argtypes = [_vp, C.c_long, _vp, _vp, _vp, C.c_int, _vp, C.POINTER(_Eval)]
+_lib.detnet_train_apply.argtypes = [_vp, _vp, C.c_long, C.POINTER(_LossSpec), C.POINTER(_AdamCfg)]
+_lib.detnet_model_get_params.argtypes = [_vp, _vp]
+_lib.detnet_model_reset_adam.argtypes = [_vp]
+_lib.detnet_generate_host.argtypes = [_vp, C.c_uint64, C.c_long, C.c_long, C.c_int, C.c_int,
+                                      C.c_double, C.c_double, _vp, _vp, _vp, _vp]
 _lib.detnet_rng_seed.restype = C.c_uint64
 _lib.detnet_rng_seed.argtypes = [C.c_uint64, C.c_uint64]
 _lib.detnet_rng_stream.restype = C.c_uint64
@@ -219,6 +227,14 @@ class Context:
         _check(_lib.detnet_generate_device(self._h, base_state, first, count, n_rx, n_tx, snr_lo,
                                            snr_hi, scale, _addr(H), _addr(y), _addr(x),
                                            _addr(sigma2)))
+
+    def generate_host(self, base_state, first, count, n_rx, n_tx, snr_lo, snr_hi):
+        """FP64 unscaled samples (what unfold::generate_batch returns)."""
+        H = np.empty((count, n_rx, n_tx)); x = np.empty((count, n_tx)); y = np.empty((count, n_rx))
+        s2 = np.empty(count)
+        _check(_lib.detnet_generate_host(self._h, base_state, first, count, n_rx, n_tx, snr_lo,
+                                         snr_hi, _addr(H), _addr(x), _addr(y), _addr(s2)))
+        return H, x, y, s2
 
     def adam_step(self, n_tx, z_dim, v_dim, depth, frozen_prefix, params, masks, grads, m1, m2,
                   step, lr0=1e-4, decay_factor=0.97, decay_step=1000, beta1=0.9, beta2=0.999,
@@ -333,6 +349,32 @@ class Model:
         _check(_lib.detnet_forward_range(self._h, n, _addr(H), _addr(y), l_begin, l_end,
                                          _addr(xs), _addr(vs), _addr(xh)))
         return xs, vs, xh
+
+    @property
+    def param_count(self):
+        return _lib.detnet_model_param_count(self._h)
+
+    def train_grad(self, n, H_ptr, y_ptr, x_ptr, raw_ptr, trainable_only=False):
+        """Device-resident gradient sums (detnet_train_grad) into raw_ptr (FP64)."""
+        ev = _Eval()
+        _check(_lib.detnet_train_grad(self._h, n, _addr(H_ptr), _addr(y_ptr), _addr(x_ptr),
+                                      int(trainable_only), _addr(raw_ptr), C.byref(ev)))
+        return BatchEval(ev.data_loss, ev.symbol_errors, ev.symbols, ev.flagged, ev.loss_sum)
+
+    def train_apply(self, raw_ptr, n_global, kind=0, lam=0.0, lam1=0.0, lam2=0.0, lr0=1e-4,
+                    decay_factor=0.97, decay_step=1000, beta1=0.9, beta2=0.999, eps=1e-8):
+        spec = _LossSpec(kind, lam, lam1, lam2)
+        cfg = _AdamCfg(lr0, decay_factor, decay_step, beta1, beta2, eps)
+        _check(_lib.detnet_train_apply(self._h, _addr(raw_ptr), n_global, C.byref(spec),
+                                       C.byref(cfg)))
+
+    def get_params(self):
+        out = np.empty((self.depth, record_size(self.n_tx, self.z_dim, self.v_dim)))
+        _check(_lib.detnet_model_get_params(self._h, _addr(out)))
+        return out
+
+    def reset_adam(self):
+        _check(_lib.detnet_model_reset_adam(self._h))
 
     def batch_gradient(self, H, y, x, kind=0, lam=0.0, lam1=0.0, lam2=0.0, trainable_only=False):
         H, y, x = self._samples(H, y, x)

@@ -48,6 +48,8 @@ def workload(cfg):
         return 40, [(7.0, 14.0)], 1 << 20, "group", False
     if cfg == 4:
         return 40, [(7.0, 14.0)], 1 << 20, "sgl", False
+    if cfg == 5:
+        return 40, [(7.0, 14.0)], 5000, None, False
     raise SystemExit(f"unknown config {cfg}")
 
 
@@ -208,7 +210,9 @@ def config_block(args, L, points, per_point):
     names = {1: "config1: dense L=90, batch 4096, SNR U[7,14] dB, per-layer x_l out",
              2: "config2: dense L=40, BER sweep SNR {0,2,..,14} dB, 2^20 samples/point/GPU",
              3: "config3: group-pruned L=40 (112/160 units, 30/100 W1 cols dead), 2^20",
-             4: "config4: sparse-group L=40 (config3 groups, 5% kept N(0,0.05^2)), 2^20"}
+             4: "config4: sparse-group L=40 (config3 groups, 5% kept N(0,0.05^2)), 2^20",
+             5: "config5: training step L=40, batch 5000/GPU, plain loss + group LASSO "
+                "1e-4 (column groups), Adam lr 1e-3"}
     return {"workload": names[args.config], "n_rx": N, "n_tx": K, "layers": L,
             "z_dim": Z, "v_dim": V, "snr_points": [list(p) for p in points],
             "samples_per_point_per_gpu": per_point, "parallelism": f"dp{args.gpus}",
@@ -245,6 +249,8 @@ def main():
             dist.barrier()
 
     import paper_2003_09446_b200 as eng
+    if args.config == 5:
+        return run_train_bench(args, torch, dist, world, rank, local, barrier, eng)
     L, points, per_point, _, want_xhat = workload(args.config)
     params, masks = build_params(args.config, L)
     peaks = measured_peaks(torch) if rank == 0 else {}
@@ -355,6 +361,121 @@ def main():
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_train_bench(args, torch, dist, world, rank, local, barrier, eng):
+    """Config 5: data-parallel training steps. Each rank computes the raw
+    gradient sums of its 5000-sample shard of the global batch (sample indices
+    [rank*5000, (rank+1)*5000) of generate_batch(train_rng, 5000*world), keyed
+    like training.cpp:39,63-64), the ranks all-reduce them (the only NCCL
+    traffic besides the stats), and every rank applies the identical Adam
+    update."""
+    L, _, per_gpu, _, _ = workload(5)
+    params, _ = build_params(5, L)
+    ctx = eng.Context(local)
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    model = ctx.model(K, N, Z, V, params)
+    raw = torch.zeros(model.param_count, dtype=torch.float64, device="cuda")
+    total_steps = args.warmup + args.steps
+    train = eng.rng_stream(eng.rng_seed(MASTER_SEED, 0), 2)
+    batches = []
+    for _ in range(total_steps):
+        base, train = eng.rng_split(train)
+        H = torch.empty((per_gpu, N, K), dtype=torch.float32, device="cuda")
+        y = torch.empty((per_gpu, N), dtype=torch.float32, device="cuda")
+        x = torch.empty((per_gpu, K), dtype=torch.int8, device="cuda")
+        ctx.generate(base, rank * per_gpu, per_gpu, N, K, 7.0, 14.0, 1.0 / np.sqrt(N), H, y, x)
+        batches.append((H, y, x))
+    n_global = per_gpu * world
+    stats = torch.zeros(3, dtype=torch.float64, device="cuda")
+
+    def step(b):
+        H, y, x = batches[b]
+        ev = model.train_grad(per_gpu, H, y, x, raw)
+        if world > 1:
+            dist.all_reduce(raw)
+        model.train_apply(raw, n_global, kind=2, lam1=1e-4, lr0=1e-3)
+        return ev
+
+    peaks = measured_peaks(torch) if rank == 0 else {}
+    for b in range(args.warmup):
+        step(b)
+    ctx.kernel_times(reset=True)
+    ctx.set_profiling(True)
+    launches0 = ctx.launch_count
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for b in range(args.warmup, total_steps):
+            ev = step(b)
+        t1.record()
+        torch.cuda.synchronize()
+    barrier()
+    ctx.set_profiling(False)
+    kt = ctx.kernel_times(reset=True)
+    launches = ctx.launch_count - launches0
+    ms_t = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    value = n_global * args.steps / (ms / 1e3)
+    flops_sample = L * (52_000 + 103_200) + 25_200  # SURVEY 8d config 5 census
+    bwd_ms, bwd_n = kt["backward"]
+    achieved = flops_sample * n_global / world * args.steps / (ms / 1e3) / 1e12
+    roof = {"bound": "tensor", "achieved": achieved, "peak": peaks.get("fp32_tflops"),
+            "unit": "TFLOP/s",
+            "frac": achieved / peaks["fp32_tflops"] if peaks.get("fp32_tflops") else None,
+            "traffic": None, "kernel": "whole training step (FP32 CUDA-core kernels)",
+            "peak_source": "measured cuBLAS FP32 SGEMM, this run",
+            "census_flop_per_sample_step": flops_sample,
+            "kernel_ms": {k: v[0] for k, v in kt.items() if v[1]},
+            "kernel_launches": {k: v[1] for k, v in kt.items() if v[1]}}
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu and world == 1:
+            cpu = cpu_train_reference(L, params, 500)
+        print(json.dumps({
+            "metric": "DetNet training samples/sec (30x20 BPSK, L=40, fwd+bwd+Adam)",
+            "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (reference Rng generator on device, H~N(0,1/N), FP32)",
+            "config": {"workload": config_block(args, L, [(7.0, 14.0)], per_gpu)["workload"],
+                       "global_batch": n_global, "per_gpu_batch": per_gpu, "layers": L,
+                       "parallelism": f"dp{world}",
+                       "l2": "fresh batch per step (12.7 MB) + 1 M-parameter model"},
+            "roofline": roof, "cpu_baseline": cpu, "gpu_launches": launches,
+            "clocks": clk.summary(), "last_step_loss": ev.data_loss, "peaks_measured": peaks}),
+            flush=True)
+
+
+def cpu_train_reference(L, params, n):
+    """Reference batch_gradient + adam_step (OpenMP) on a bounded batch."""
+    from oracle.oracle import Model as OModel
+    from oracle.oracle import Oracle, RefLib, available_ref
+    orc = Oracle()
+    om = OModel(K, N, Z, V, L, params.copy())
+    r = orc.rng(MASTER_SEED, 2)
+    H, x, y, _ = orc.generate_batch(r, N, K, n, 7.0, 14.0)
+    H = (H / np.sqrt(N)).astype(np.float32).astype(np.float64)
+    y = (y / np.sqrt(N)).astype(np.float32).astype(np.float64)
+    ref = RefLib() if available_ref() else None
+    m1 = np.zeros_like(om.params)
+    m2 = np.zeros_like(om.params)
+    t0 = time.perf_counter()
+    if ref:
+        g = ref.batch_gradient(om, H, y, x, kind=2, lam1=1e-4, parallel=True)["grads"]
+        ref.adam_step(om, g, m1, m2, 0, lr0=1e-3)
+    else:
+        g = orc.batch_gradient(om, H, y, x, kind=2, lam1=1e-4)["grads"]
+        orc.adam_step(om, g, m1, m2, 0, lr0=1e-3)
+    el = time.perf_counter() - t0
+    return {"value": n / el, "unit": "samples/s", "cores": ref.worker_count() if ref else 1,
+            "kind": "reference" if ref else "port",
+            "sample": f"one batch_gradient + adam_step over {n} samples (L={L})"}
 
 
 def ctx_path_name(ctx, model):

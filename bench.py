@@ -249,6 +249,8 @@ def main():
             dist.barrier()
 
     import paper_2003_09446_b200 as eng
+    from paper_2003_09446_b200.parallel import allreduce_grad, shard
+    globals().update(shard=shard, allreduce_grad=allreduce_grad)
     if args.config == 5:
         return run_train_bench(args, torch, dist, world, rank, local, barrier, eng)
     L, points, per_point, _, want_xhat = workload(args.config)
@@ -268,7 +270,8 @@ def main():
         H = torch.empty((per_point, N, K), dtype=torch.float32, device="cuda")
         y = torch.empty((per_point, N), dtype=torch.float32, device="cuda")
         x = torch.empty((per_point, K), dtype=torch.int8, device="cuda")
-        ctx.generate(base, rank * per_point, per_point, N, K, lo, hi, 1.0 / np.sqrt(N), H, y, x)
+        first, count = shard(per_point, rank)
+        ctx.generate(base, first, count, N, K, lo, hi, 1.0 / np.sqrt(N), H, y, x)
         dev_in.append((H, y, x))
     xhat = (torch.empty((per_point, L, K), dtype=torch.float32, device="cuda")
             if want_xhat else None)
@@ -384,7 +387,8 @@ def run_train_bench(args, torch, dist, world, rank, local, barrier, eng):
         H = torch.empty((per_gpu, N, K), dtype=torch.float32, device="cuda")
         y = torch.empty((per_gpu, N), dtype=torch.float32, device="cuda")
         x = torch.empty((per_gpu, K), dtype=torch.int8, device="cuda")
-        ctx.generate(base, rank * per_gpu, per_gpu, N, K, 7.0, 14.0, 1.0 / np.sqrt(N), H, y, x)
+        first, count = shard(per_gpu, rank)
+        ctx.generate(base, first, count, N, K, 7.0, 14.0, 1.0 / np.sqrt(N), H, y, x)
         batches.append((H, y, x))
     n_global = per_gpu * world
     stats = torch.zeros(3, dtype=torch.float64, device="cuda")
@@ -392,8 +396,7 @@ def run_train_bench(args, torch, dist, world, rank, local, barrier, eng):
     def step(b):
         H, y, x = batches[b]
         ev = model.train_grad(per_gpu, H, y, x, raw)
-        if world > 1:
-            dist.all_reduce(raw)
+        allreduce_grad(dist if world > 1 else None, raw)
         model.train_apply(raw, n_global, kind=2, lam1=1e-4, lr0=1e-3)
         return ev
 

@@ -52,7 +52,8 @@ typedef struct detnet_model detnet_model;
 int detnet_ctx_create(int device, detnet_ctx **out);
 void detnet_ctx_destroy(detnet_ctx *ctx);
 const char *detnet_last_error(void);
-/* Kernel-path selection for the dense stack: 0 auto, 1 SIMT FP32, 2 tcgen05 3xTF32. */
+/* Kernel-path selection: 0 auto (tcgen05 where compiled, else SIMT), 1 SIMT
+ * FP32, 2 tcgen05 3xTF32, 3 sparse CSR (pruned models). */
 int detnet_ctx_set_path(detnet_ctx *ctx, int path);
 /* Preprocessing mode: 0 (default) FP32 Cholesky + FP64 refinement with the
  * reference LU as fallback for ill-conditioned samples (FP64-accurate loss
@@ -88,8 +89,8 @@ long detnet_record_size(int n_tx, int z_dim, int v_dim);
 int detnet_model_create(detnet_ctx *ctx, const detnet_model_desc *desc, detnet_model **out);
 int detnet_model_update(detnet_model *m, const detnet_model_desc *desc);
 void detnet_model_destroy(detnet_model *m);
-/* Kernel path the dense stack of this model runs on under the context's
- * current path setting: 1 SIMT FP32, 2 tcgen05 3xTF32. */
+/* Kernel path the stack of this model runs on under the context's current
+ * path setting: 1 SIMT FP32, 2 tcgen05 3xTF32, 3 sparse. */
 int detnet_model_path(const detnet_model *m);
 /* Analytic census, flops_per_detection (compression.cpp:120-129). */
 long long detnet_model_flops_per_detection(const detnet_model *m, int include_preprocess);

@@ -20,6 +20,7 @@
 #include "k_generate.cuh"
 #include "k_preprocess.cuh"
 #include "k_prep_fast.cuh"
+#include "k_stack_sparse.cuh"
 #include "k_stack_simt.cuh"
 #include "engine.hpp"
 
@@ -136,6 +137,81 @@ int pack_simt(detnet_model *m, const double *params, const double *masks, std::v
     return 0;
 }
 
+// Sparse layer streams for k_stack_sparse (format in k_stack_sparse.cuh).
+int pack_sparse(detnet_model *m, const double *params, const double *masks) {
+    m->sparse_ready = false;
+    const int K = m->K, Z = m->Z, V = m->V, IN = 3 * K + V;
+    const long P = record_size(K, Z, V);
+    long nnz = 0, total = static_cast<long>(m->L) * (Z * IN + K * Z + V * Z);
+    std::vector<int> st;
+    std::vector<long> offs(m->L);
+    auto fbits = [](float f) { int i; std::memcpy(&i, &f, 4); return i; };
+    for (int l = 0; l < m->L; ++l) {
+        const double *p = params + l * P;
+        const double *mk = masks ? masks + l * P : nullptr;
+        auto w = [&](long off) { return static_cast<float>(p[off] * (mk ? mk[off] : 1.0)); };
+        const long oW1 = 0, ob1 = static_cast<long>(Z) * IN, oW2 = ob1 + Z,
+                   ob2 = oW2 + static_cast<long>(K) * Z, oW3 = ob2 + K,
+                   ob3 = oW3 + static_cast<long>(V) * Z, ot = ob3 + V;
+        std::vector<int> units;
+        std::vector<std::vector<std::pair<int, float>>> ins, outs;
+        for (int i = 0; i < Z; ++i) {
+            std::vector<std::pair<int, float>> o;
+            for (int r = 0; r < V; ++r) if (w(oW3 + r * Z + i) != 0.f) o.push_back({r, w(oW3 + r * Z + i)});
+            for (int k = 0; k < K; ++k) if (w(oW2 + k * Z + i) != 0.f) o.push_back({V + k, w(oW2 + k * Z + i)});
+            std::vector<std::pair<int, float>> in;
+            for (int j = 0; j < IN; ++j) if (w(oW1 + i * IN + j) != 0.f) in.push_back({j, w(oW1 + i * IN + j)});
+            nnz += static_cast<long>(in.size() + o.size());
+            if (o.empty()) continue;
+            units.push_back(i);
+            ins.push_back(in);
+            outs.push_back(o);
+        }
+        const int nu = static_cast<int>(units.size());
+        long work = 0, half = 0;
+        for (int u = 0; u < nu; ++u) work += 1 + ins[u].size() + outs[u].size();
+        int split = nu;
+        for (int u = 0; u < nu; ++u) {
+            half += 1 + ins[u].size() + outs[u].size();
+            if (2 * half >= work) { split = u + 1; break; }
+        }
+        while (st.size() % 4) st.push_back(0);
+        const long base = static_cast<long>(st.size());
+        offs[l] = base;
+        st.resize(base + 4 + 4 * nu + nu, 0);
+        if (st.size() & 1) st.push_back(0);
+        int e = 0;
+        std::vector<int> ent;
+        for (int u = 0; u < nu; ++u) {
+            st[base + 4 + 4 * u + 0] = e;
+            for (auto &pr : ins[u]) { ent.push_back(pr.first); ent.push_back(fbits(pr.second)); ++e; }
+            st[base + 4 + 4 * u + 1] = e;
+            st[base + 4 + 4 * u + 2] = e;
+            for (auto &pr : outs[u]) { ent.push_back(pr.first); ent.push_back(fbits(pr.second)); ++e; }
+            st[base + 4 + 4 * u + 3] = e;
+            st[base + 4 + 4 * nu + u] = fbits(w(ob1 + units[u]));
+        }
+        st.insert(st.end(), ent.begin(), ent.end());
+        const long tail = static_cast<long>(st.size()) - base;
+        std::vector<int> b23(68, 0);
+        for (int r = 0; r < V; ++r) b23[r] = fbits(w(ob3 + r));
+        for (int k = 0; k < K; ++k) b23[V + k] = fbits(w(ob2 + k));
+        b23[64] = fbits(static_cast<float>(p[ot]));
+        b23[65] = fbits(static_cast<float>(1.0 / p[ot]));
+        st.insert(st.end(), b23.begin(), b23.end());
+        st[base + 0] = nu;
+        st[base + 1] = split;
+        st[base + 2] = static_cast<int>(tail);
+    }
+    m->density = total ? static_cast<double>(nnz) / static_cast<double>(total) : 1.0;
+    if (m->sparse_stream.ensure(st.size() * 4) || m->sparse_off.ensure(offs.size() * 8))
+        return fail(DETNET_ERR_CUDA, "sparse stream allocation");
+    CK(cudaMemcpy(m->sparse_stream.p, st.data(), st.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(m->sparse_off.p, offs.data(), offs.size() * 8, cudaMemcpyHostToDevice));
+    m->sparse_ready = (K == 20 && V == 40);
+    return 0;
+}
+
 int upload_model(detnet_model *m, const detnet_model_desc *d) {
     const long P = record_size(m->K, m->Z, m->V);
     m->params_host.assign(d->params, d->params + P * m->L);
@@ -157,6 +233,7 @@ int upload_model(detnet_model *m, const detnet_model_desc *d) {
     CK(cudaMemcpy(m->lnk_all.p, la.data(), m->L * 8, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(m->lnk_train.p, lt.data(), m->L * 8, cudaMemcpyHostToDevice));
     if (int rc = tc_pack(m->tc, m->K, m->Z, m->V, m->L, d->params, d->masks)) return rc;
+    if (int rc = pack_sparse(m, d->params, d->masks)) return rc;
     m->train_ready = false; // the device master copy restarts from these params
     m->tc_stale = false;
     return 0;
@@ -195,7 +272,7 @@ int ensure_ws(detnet_ctx *c, long n, int K) {
 
 bool use_tc(const detnet_model *m) {
     const int path = m->ctx->path;
-    if (path == 1) return false;
+    if (path == 1 || path == 3) return false;
     if (!m->tc.ready) return false;
     return true;
 }
@@ -258,6 +335,31 @@ int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, 
               int l_end, bool trainable_only, float *xhat, float *xs, float *vs,
               const TraceBufs *trace) {
     detnet_ctx *c = m->ctx;
+    const bool sparse = !trace && !xs && m->sparse_ready && !m->tc_stale && c->path == 3;
+    if (sparse) {
+        SparseArgs sa{};
+        sa.gp = c->gp.as<float>();
+        sa.q32 = c->q32.as<float>();
+        sa.denom = c->denom.as<double>();
+        sa.xmask = c->xmask.as<uint32_t>();
+        sa.stream = m->sparse_stream.as<int>();
+        sa.lay_off = m->sparse_off.as<long>();
+        sa.lnk = (trainable_only ? m->lnk_train : m->lnk_all).as<double>();
+        sa.L = m->L;
+        sa.n = n_local;
+        sa.n_tiles = nt;
+        sa.tile0 = t0;
+        sa.xhat = xhat;
+        sa.tile_loss = c->tile_loss.as<double>();
+        sa.tile_err = c->tile_err.as<long long>();
+        const size_t smem = sizeof(float) * TILE * (3 * 20 + 40 + 2 * 60 + 20);
+        const int grid = static_cast<int>(std::min<long>(nt, 148));
+        {
+            LaunchScope ls(c, DETNET_K_STACK, st);
+            k_stack_sparse<20, 40><<<grid, 256, smem, st>>>(sa);
+        }
+        return check_launch();
+    }
     if (!trace && m->ctx->path != 1)
         if (int rc = refresh_tc(m)) return rc;
     if (use_tc(m) && !trace) {
@@ -384,6 +486,8 @@ int detnet_ctx_create(int device, detnet_ctx **out) {
         if (d.prep() || (d.prep_fast && d.prep_fast()))
             return fail(DETNET_ERR_CUDA, "cudaFuncSetAttribute (smem) failed");
     if (int rc = tc_prepare()) return rc;
+    CK(cudaFuncSetAttribute(k_stack_sparse<20, 40>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(sizeof(float) * TILE * (3 * 20 + 40 + 2 * 60 + 20))));
     *out = c;
     return 0;
 }
@@ -409,7 +513,7 @@ void detnet_ctx_destroy(detnet_ctx *c) {
 }
 
 int detnet_ctx_set_path(detnet_ctx *c, int path) {
-    if (!c || path < 0 || path > 2) return fail(DETNET_ERR_CONTRACT, "bad path");
+    if (!c || path < 0 || path > 3) return fail(DETNET_ERR_CONTRACT, "bad path");
     c->path = path;
     return 0;
 }
@@ -489,7 +593,11 @@ void detnet_model_destroy(detnet_model *m) {
     delete m;
 }
 
-int detnet_model_path(const detnet_model *m) { return m && use_tc(m) ? 2 : 1; }
+int detnet_model_path(const detnet_model *m) {
+    if (!m) return 0;
+    if (m->sparse_ready && !m->tc_stale && m->ctx->path == 3) return 3;
+    return use_tc(m) ? 2 : 1;
+}
 
 long long detnet_model_flops_per_detection(const detnet_model *m, int include_pre) {
     if (!m) return -1;

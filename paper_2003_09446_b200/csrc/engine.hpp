@@ -133,6 +133,10 @@ struct detnet_model {
     int64_t adam_step = 0;
     bool train_ready = false;
     bool tc_stale = false;  // tcgen05 images lag the device master params
+    // sparse path (k_stack_sparse.cuh): CSR-like stream of surviving weights
+    detnet::DBuf sparse_stream, sparse_off;
+    bool sparse_ready = false;
+    double density = 1.0;   // surviving W entries / all W entries
 };
 
 namespace detnet {

@@ -168,7 +168,7 @@ def _addr(a):
     return a.data_ptr()  # torch tensor
 
 
-PATH_AUTO, PATH_SIMT, PATH_TC = 0, 1, 2
+PATH_AUTO, PATH_SIMT, PATH_TC, PATH_SPARSE = 0, 1, 2, 3
 
 
 class Context:
@@ -308,7 +308,8 @@ class Model:
 
     @property
     def path_name(self):
-        return {1: "simt-fp32", 2: "tcgen05-3xtf32"}[_lib.detnet_model_path(self._h)]
+        return {1: "simt-fp32", 2: "tcgen05-3xtf32", 3: "sparse-csr-fp32"}[
+            _lib.detnet_model_path(self._h)]
 
     def flops_per_detection(self, include_preprocess=True):
         return _lib.detnet_model_flops_per_detection(self._h, int(include_preprocess))

@@ -261,3 +261,24 @@ def test_kernel_launches_counted(ctx, oracle):
     before = ctx.launch_count
     m.batch_evaluate(H, y, x)
     assert ctx.launch_count - before >= 3  # preprocess, stack, reduce
+
+
+@pytest.mark.parametrize("path", [3, 1])
+def test_sparse_group_model_paths(ctx, oracle, path):
+    """Config-4 style model (group masks + 5% Bernoulli within groups) on the
+    sparse CSR kernel and on the SIMT kernel, against the oracle."""
+    from paper_2003_09446_b200.workload import group_masks, sparse_group_model, xavier_params
+    params = xavier_params(K, 10, seed=9)
+    ps, ms = sparse_group_model(params, group_masks(K, 10, seed=31), K)
+    H, y, x = _inputs(oracle, 700, seed=5)
+    ctx.set_path(path)
+    m = ctx.model(K, N, 160, 40, ps, masks=ms)
+    assert m.path_name == {3: "sparse-csr-fp32", 1: "simt-fp32"}[path]
+    ev, xh = m.batch_evaluate(H, y, x, want_xhat=True)
+    ctx.set_path(0)
+    ref = oracle.evaluate(_omodel(ps, masks=ms), H.astype(np.float64), y.astype(np.float64),
+                          x.astype(np.float64), want_xhat=True)
+    ok, stats = _e2e_ok(xh, ref["xhat"])
+    assert ok, stats
+    assert ev.symbol_errors == int(ref["errors"].sum())
+    assert abs(ev.data_loss - ref["loss"].mean()) <= 1e-4 * abs(ref["loss"].mean())

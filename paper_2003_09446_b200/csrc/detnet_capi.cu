@@ -14,6 +14,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include "../../include/detnet_b200.h"
 #include "common.cuh"
@@ -22,6 +23,8 @@
 #include "k_prep_fast.cuh"
 #include "k_stack_sparse.cuh"
 #include "k_stack_simt.cuh"
+#include <cudaTypedefs.h>
+
 #include "engine.hpp"
 
 using namespace detnet;
@@ -43,22 +46,51 @@ void launch_pre(dim3 g, dim3 b, size_t sm, cudaStream_t st, long n, int N, const
 
 using FastFn = void (*)(dim3, dim3, size_t, cudaStream_t, long, int, const float *, const float *,
                         const int8_t *, float *, float *, double *, uint32_t *, uint8_t *, int *,
-                        long *);
+                        long *, float *, const CUtensorMap *);
+
+// 2-D view of H for the K1 fast path: rows of N*K floats (one sample), box
+// {SSTR/4 floats, PS_TILE samples}. The box is 4 floats wider than a 6-row
+// chunk so each sample lands on the bank-spreading 496-byte stride; the extra
+// floats are the next row (or zero fill past the end of the sample).
+int encode_h_map(CUtensorMap *map, const float *H, long n, int N, int K) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return fail(DETNET_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(N) * K, static_cast<cuuint64_t>(n)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(N) * K * 4};
+    const cuuint32_t box[2] = {PrepStreamSmem<20, PREP_FAST_N>::BOXW, PS_TILE};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(H), dims,
+                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(DETNET_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", r);
+    return 0;
+}
 
 template <int K>
 void launch_fast(dim3 g, dim3 b, size_t sm, cudaStream_t st, long n, int N, const float *H,
                  const float *y, const int8_t *x, float *gp, float *q32, double *dn, uint32_t *xm,
-                 uint8_t *fl, int *fbc, long *fbl) {
+                 uint8_t *fl, int *fbc, long *fbl, float *scratch, const CUtensorMap *map) {
     (void)b;
     (void)sm;
-    k_prep_gram<K><<<g, 2 * PREP_FAST_SAMPLES, 0, st>>>(n, N, H, y, x, gp, q32, xm);
-    k_prep_solve<K><<<g, PREP_FAST_SAMPLES, gram_entries(K) * PREP_FAST_SAMPLES * 4, st>>>(
-        n, N, H, y, gp, q32, xm, dn, fl, fbc, fbl);
+    (void)N; // the fast path is instantiated for N == PREP_FAST_N only
+    (void)H;
+    k_prep_stream<K, PREP_FAST_N><<<g, PS_THREADS, PrepStreamSmem<K, PREP_FAST_N>::BYTES, st>>>(
+        *map, n, y, x, gp, q32, dn, xm, fl, fbc, fbl, scratch);
 }
 
 template <int K> int set_fast_smem() {
-    return cudaFuncSetAttribute(k_prep_solve<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(gram_entries(K) * PREP_FAST_SAMPLES * 4)) ==
+    return cudaFuncSetAttribute(k_prep_stream<K, PREP_FAST_N>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(PrepStreamSmem<K, PREP_FAST_N>::BYTES)) ==
                    cudaSuccess
                ? 0
                : -1;
@@ -285,19 +317,29 @@ int run_pre(detnet_model *m, cudaStream_t st, long s0, long cnt, long n_total, c
     const long t0 = s0 / TILE;
     const int N = m->N;
     const size_t smem = static_cast<size_t>(4) * (N * K + N + K * K + K) * sizeof(double);
-    if (m->dims->fast && !c->exact_pre) {
+    const bool aligned = (reinterpret_cast<uintptr_t>(H) % 16 == 0) &&
+                         (reinterpret_cast<uintptr_t>(y) % 16 == 0) &&
+                         (reinterpret_cast<uintptr_t>(x) % 4 == 0);
+    if (m->dims->fast && !c->exact_pre && aligned && N == PREP_FAST_N) {
         // fast path + exact LU for the samples it flags (device-side list)
         if (c->fb_list.ensure(sizeof(long) * cnt) || c->fb_count.ensure(sizeof(int)))
             return fail(DETNET_ERR_CUDA, "fallback list allocation failed");
         CK(cudaMemsetAsync(c->fb_count.p, 0, sizeof(int), st));
         {
             LaunchScope ls(c, DETNET_K_PREPROCESS, st);
-            m->dims->fast(dim3(static_cast<unsigned>((cnt + PREP_FAST_SAMPLES - 1) / PREP_FAST_SAMPLES)),
-                          dim3(2 * PREP_FAST_SAMPLES), gram_entries(K) * PREP_FAST_SAMPLES * 4, st,
+            const long tiles = (cnt + PS_TILE - 1) / PS_TILE;
+            const long grid = std::min<long>(tiles, 2L * c->sms);
+            if (c->prep_scratch.ensure(sizeof(float) * grid * NG * PS_TILE))
+                return fail(DETNET_ERR_CUDA, "preprocess scratch allocation failed");
+            CUtensorMap hmap;
+            if (int rc = encode_h_map(&hmap, H, cnt, N, K)) return rc;
+            m->dims->fast(dim3(static_cast<unsigned>(grid)),
+                          dim3(PS_THREADS), 0, st,
                           cnt, N, H, y, x, c->gp.as<float>() + t0 * NG * TILE,
                           c->q32.as<float>() + t0 * K * TILE, c->denom.as<double>() + s0,
                           c->xmask.as<uint32_t>() + s0, c->flag.as<uint8_t>() + s0,
-                          c->fb_count.as<int>(), c->fb_list.as<long>());
+                          c->fb_count.as<int>(), c->fb_list.as<long>(),
+                          c->prep_scratch.as<float>(), &hmap);
         }
         if (int rc = check_launch()) return rc;
         LaunchScope ls(c, DETNET_K_OTHER, st); // exact LU for the flagged samples
@@ -476,6 +518,7 @@ int detnet_ctx_create(int device, detnet_ctx **out) {
     CK(cudaSetDevice(device));
     auto *c = new detnet_ctx();
     c->device = device;
+    c->sms = prop.multiProcessorCount;
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     for (int i = 0; i < 2; ++i) {

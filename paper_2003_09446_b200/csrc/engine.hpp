@@ -67,6 +67,7 @@ struct DimsEntry;
 struct TcModel {
     bool ready = false;
     int K = 0, Z = 0, V = 0, L = 0;
+    int zh = 0;         // hidden rows per packed layer (160 dense | 48 compacted)
     DBuf w;             // [L][rec bytes] pre-laid-out smem images
     long rec_bytes = 0;
 };
@@ -95,6 +96,7 @@ void tc_release(TcModel &tc);
 
 struct detnet_ctx {
     int device = 0;
+    int sms = 148;
     cudaStream_t stream = nullptr;
     bool own_stream = true;
     cudaStream_t copy_stream = nullptr;
@@ -111,6 +113,7 @@ struct detnet_ctx {
     // workspace
     detnet::DBuf gp, q32, denom, xmask, flag, tile_loss, tile_err, sing, result;
     detnet::DBuf in_H[2], in_y[2], in_x[2], xhat_dev, state_x, state_v, fb_list, fb_count;
+    detnet::DBuf prep_scratch; // K1 fast path: per-CTA factor parking (L2-resident)
     bool exact_pre = false; // bit-exact reference LU for every sample
     double *h_result = nullptr; // pinned: loss, err, flag, singular
     cudaEvent_t chunk_done[2] = {nullptr, nullptr};

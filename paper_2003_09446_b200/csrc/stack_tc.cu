@@ -41,27 +41,40 @@
 namespace detnet {
 namespace {
 
-constexpr int KX = 20, ZH = 160, VV = 40, NG = 210;
+constexpr int KX = 20, VV = 40, NG = 210;
 constexpr int NA = 105; // Gram entries held by thread A (rows 0..5)
-constexpr int C_U1 = 0, C_DYN = 160, C_DYNLO = 240, C_U2 = 320, C_QHI = 384,
-              C_QLO = 416, TMEM_COLS = 512;
-// z_lo column of hidden unit j (groups of 8): units 0-79 are written while the
-// second W1 half still reads A_dyn, so they live in the otherwise free
-// columns [408,416) and [440,512); units 80-159 reuse A_dyn hi [160,240).
-__host__ __device__ constexpr int zlo_col(int j) {
-    return j >= 80 ? 160 + (j - 80) : (j < 8 ? 408 + j : 440 + (j - 8));
-}
-constexpr int W1_ROWS = 160, W1_K = 104, W23_ROWS = 64, W23_K = 160;
-constexpr uint32_t W1_HALF = W1_ROWS * W1_K * 4;     // 66,560 B per hi/lo
-constexpr uint32_t W23_HALF = W23_ROWS * W23_K * 4;  // 40,960 B
-constexpr uint32_t W1_BYTES = 2 * W1_HALF, W23_BYTES = 2 * W23_HALF;
-constexpr uint32_t LAYER_BYTES = W1_BYTES + W23_BYTES; // 215,040 B
-constexpr uint32_t W1_LBO = W1_ROWS * 16, W23_LBO = W23_ROWS * 16;
+constexpr int W1_K = 104, W23_ROWS = 64, TMEM_COLS = 512;
+constexpr uint32_t W23_LBO = W23_ROWS * 16;
 constexpr int BT = 64; // per-layer [b3 (40) | b2 (20) | t | 1/t | pad]
 constexpr int NTHREADS = 384; // 2 epilogue warpgroups + 1 control warpgroup
-constexpr uint32_t SM_W1 = 0, SM_W23 = SM_W1 + W1_BYTES, SM_X = SM_W23 + W23_BYTES,
-                   SM_GX = SM_X + 14 * 128 * 4, SM_RED = SM_GX + 14 * 128 * 4,
-                   SM_BAR = SM_RED + 128, SM_TMEM = SM_BAR + 8 * 8, SM_TOTAL = SM_TMEM + 16;
+
+// Shape of one instantiation: ZH hidden units per layer after compaction
+// (160 = dense DetNet, 48 = group-pruned configs 3/4 with <= 48 live units).
+template <int ZH> struct TcCfg {
+    static_assert(ZH % 16 == 0 && ZH <= 160, "hidden width");
+    static constexpr int NH = ZH >= 128 ? 2 : 1;   // W1 issued as NH N-groups
+    static constexpr int GW = ZH / NH;             // group width (80 | 48)
+    static constexpr int EW = GW / 2;              // epilogue-1 columns per thread per group
+    static constexpr int C_U1 = 0, C_DYN = ZH, C_DYNLO = ZH + 80, C_U2 = ZH + 160,
+                         C_QHI = ZH + 224, C_QLO = ZH + 256;
+    // z_lo column of hidden unit j. With two W1 groups, units of group 0 are
+    // written while group 1 still reads A_dyn, so they live in the free columns
+    // [C_QHI+24, C_QLO) and [C_QLO+24, 512); group 1 reuses A_dyn hi. With one
+    // group every W1 MMA has completed, so z_lo reuses A_dyn hi directly.
+    __host__ __device__ static constexpr int zlo_col(int j) {
+        return NH == 1 ? C_DYN + j
+                       : (j >= GW ? C_DYN + (j - GW) : (j < 8 ? C_QHI + 24 + j : C_QLO + 24 + (j - 8)));
+    }
+    static constexpr uint32_t W1_HALF = ZH * W1_K * 4, W23_HALF = W23_ROWS * ZH * 4;
+    static constexpr uint32_t W1_BYTES = 2 * W1_HALF, W23_BYTES = 2 * W23_HALF;
+    static constexpr uint32_t LAYER_BYTES = W1_BYTES + W23_BYTES;
+    static constexpr uint32_t W1_LBO = ZH * 16;
+    static constexpr uint32_t SM_W1 = 0, SM_W23 = W1_BYTES, SM_GX = W1_BYTES + W23_BYTES,
+                              SM_RED = SM_GX + 14 * 128 * 4, SM_BAR = SM_RED + 128,
+                              SM_TMEM = SM_BAR + 8 * 8, SM_TOTAL = SM_TMEM + 16;
+    static_assert(C_QLO + 24 <= TMEM_COLS, "TMEM budget");
+    static_assert(NH == 1 || zlo_col(GW - 1) < TMEM_COLS, "TMEM budget (z_lo)");
+};
 
 struct TcKArgs {
     TcArgs a;
@@ -100,7 +113,7 @@ __device__ __forceinline__ void split(float v, float &hi, float &lo) {
 // Epilogue 2 for one layer: load the whole U2V row (64 columns, one wait),
 // x_hat = psi_t(u2 + b2) from columns [40, 60) and, on the B side, v = v' + b3
 // from columns [0, 40).
-template <bool WITH_V>
+template <bool WITH_V, int C_U2>
 __device__ __forceinline__ void epi2_layer(uint32_t trow, const float *bt, float (&x)[KX],
                                            float (&v)[VV]) {
     uint32_t r[4][16];
@@ -131,7 +144,18 @@ __device__ __forceinline__ void epi2_layer(uint32_t trow, const float *bt, float
     }
 }
 
+template <int ZH>
 __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
+    using C = TcCfg<ZH>;
+    constexpr int NH = C::NH, GW = C::GW, EW = C::EW;
+    constexpr int C_U1 = C::C_U1, C_DYN = C::C_DYN, C_DYNLO = C::C_DYNLO, C_U2 = C::C_U2,
+                  C_QHI = C::C_QHI, C_QLO = C::C_QLO;
+    constexpr uint32_t SM_W1 = C::SM_W1, SM_W23 = C::SM_W23, SM_GX = C::SM_GX,
+                       SM_RED = C::SM_RED, SM_BAR = C::SM_BAR, SM_TMEM = C::SM_TMEM;
+    constexpr uint32_t W1_HALF = C::W1_HALF, W23_HALF = C::W23_HALF, W1_BYTES = C::W1_BYTES,
+                       W23_BYTES = C::W23_BYTES, LAYER_BYTES = C::LAYER_BYTES,
+                       W1_LBO = C::W1_LBO;
+    constexpr int U1_LAST = NH == 2 ? 3 : 2; // B_U1B : B_U1A
     extern __shared__ __align__(1024) unsigned char sm[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(sm + SM_BAR);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sm + SM_TMEM);
@@ -171,12 +195,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
         if (warp == 8) {
             // ============ MMA issuer (warp-uniform loop, one elected lane) ============
             const uint32_t sw1 = smem_u32(sm + SM_W1), sw23 = smem_u32(sm + SM_W23);
-            const uint32_t id1 = tc::idesc_tf32(128, 80);
+            const uint32_t id1 = tc::idesc_tf32(128, GW);
             const uint32_t id2 = tc::idesc_tf32(128, W23_ROWS);
             const uint64_t d1 = tc::smem_desc(sw1, W1_LBO, 128);
             const uint64_t d23 = tc::smem_desc(sw23, W23_LBO, 128);
             constexpr uint64_t S1 = (2 * W1_LBO) >> 4, S23 = (2 * W23_LBO) >> 4;
-            constexpr uint64_t H1 = W1_HALF >> 4, H23 = W23_HALF >> 4, NB = (80 / 8 * 128) >> 4;
+            constexpr uint64_t H1 = W1_HALF >> 4, H23 = W23_HALF >> 4, NB = (GW / 8 * 128) >> 4;
             for (long it = 0; it < total_it; ++it) {
                 const uint32_t ph = static_cast<uint32_t>(it & 1);
                 const int l = L0 + static_cast<int>(it % NL);
@@ -186,13 +210,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                 mbar_wait_guard(&bars[B_AREADY], ph);
                 TRACE(6, l);
                 tc::fence_after();
-                // U1 = [q 1 | x gx v] . W1'^T in two N=80 halves (hidden 0-79, 80-159)
+                // U1 = [q 1 | x gx v] . W1'^T in NH N-groups of GW hidden units
 #pragma unroll 1
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < NH; ++h) {
                     if (tc::elect_one()) {
                         const uint32_t tb = tc::opaque32(tbase);
                         const uint64_t d1h = tc::opaque64(d1 + h * NB);
-                        const uint32_t dcol = tb + C_U1 + 80 * h;
+                        const uint32_t dcol = tb + C_U1 + GW * h;
 #pragma unroll
                         for (int kk = 0; kk < 13; ++kk) {
                             const uint32_t ahi = kk < 3 ? C_QHI + 8 * kk : C_DYN + 8 * (kk - 3);
@@ -209,26 +233,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                 TRACE(7, l);
                 mbar_wait_guard(&bars[B_W23F], ph);
                 TRACE(13, l);
-                // U2V = z . [W3; W2]^T, K split by the two z halves
+                // U2V = z . [W3; W2]^T, K split by the z groups
+                constexpr int KG = GW / 8; // k-steps per group
 #pragma unroll 1
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < NH; ++h) {
                     mbar_wait_guard(&bars[h == 0 ? B_ZA : B_ZB], ph);
                     if (h == 0) TRACE(9, l);
                     tc::fence_after();
                     if (tc::elect_one()) {
                         const uint32_t tb = tc::opaque32(tbase);
-                        const uint64_t d23h = tc::opaque64(d23 + h * 10 * S23);
+                        const uint64_t d23h = tc::opaque64(d23 + h * KG * S23);
 #pragma unroll
-                        for (int k2 = 0; k2 < 10; ++k2) {
-                            const int kk = 10 * h + k2;
+                        for (int k2 = 0; k2 < KG; ++k2) {
+                            const int kk = KG * h + k2;
                             const uint64_t bhi = d23h + k2 * S23;
-                            const uint32_t zl = h == 0 ? (k2 == 0 ? 408 : 440 + 8 * (k2 - 1))
-                                                       : 160 + 8 * k2;
+                            const uint32_t zl = h == 0 ? C::zlo_col(8 * k2) : C::zlo_col(GW + 8 * k2);
                             tc::mma_tf32_ts(tb + C_U2, tb + C_U1 + 8 * kk, bhi, id2, kk > 0);
                             tc::mma_tf32_ts(tb + C_U2, tb + C_U1 + 8 * kk, bhi + H23, id2, 1);
                             tc::mma_tf32_ts(tb + C_U2, tb + zl, bhi, id2, 1);
                         }
-                        if (h == 1) tc::commit(&bars[B_U2]);
+                        if (h == NH - 1) tc::commit(&bars[B_U2]);
                     }
                     __syncwarp();
                 }
@@ -260,7 +284,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                 const int l = L0 + static_cast<int>(it % NL);
                 const int lnext = L0 + static_cast<int>((it + 1) % NL);
                 const bool trace_on = it < NL && lane == 0;
-                mbar_wait_guard(&bars[B_U1B], ph); // both W1 halves consumed
+                mbar_wait_guard(&bars[U1_LAST], ph); // every W1 group consumed
                 TRACE(8, l);
                 load_w1(lnext);
                 mbar_wait_guard(&bars[B_U2], ph); // W23 consumed
@@ -381,29 +405,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                 mbar_arrive(&bars[B_AREADY]);
                 TRACE(1, l);
 
-                // ---- epilogue 1: z = relu(U1) -> z_hi (in place), z_lo. Each W1 half
-                // (80 hidden units) is shared by A (first 40) and B (last 40).
+                // ---- epilogue 1: z = relu(U1) -> z_hi (in place), z_lo. Each W1 group
+                // (GW hidden units) is shared by A (first EW) and B (last EW).
 #pragma unroll 1
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < NH; ++h) {
                     mbar_wait_guard(&bars[h == 0 ? B_U1A : B_U1B], ph);
                     if (h == 0) TRACE(2, l);
                     tc::fence_after();
-                    const int c0 = 80 * h + (isA ? 0 : 40);
-                    uint32_t r[3][16];
-                    tc::ld16_nw(trow + C_U1 + c0, r[0]);
-                    tc::ld16_nw(trow + C_U1 + c0 + 16, r[1]);
-                    tc::ld16_nw(trow + C_U1 + c0 + 32, r[2]); // cols 32..39 used
-                    tc::wait_ld();
-                    float zh[40], zl[40];
+                    const int c0 = GW * h + (isA ? 0 : EW);
+                    constexpr int NL16 = (EW + 15) / 16;
+                    uint32_t r[NL16][16];
 #pragma unroll
-                    for (int k = 0; k < 40; ++k) {
+                    for (int c = 0; c < NL16; ++c) tc::ld16_nw(trow + C_U1 + c0 + 16 * c, r[c]);
+                    tc::wait_ld();
+                    float zh[EW], zl[EW];
+#pragma unroll
+                    for (int k = 0; k < EW; ++k) {
                         const float u = __uint_as_float(r[k / 16][k % 16]);
                         split(u > 0.f ? u : 0.f, zh[k], zl[k]);
                     }
 #pragma unroll
-                    for (int g8 = 0; g8 < 5; ++g8) {
+                    for (int g8 = 0; g8 < EW / 8; ++g8) {
                         tc::st8(trow + C_U1 + c0 + 8 * g8, zh + 8 * g8);
-                        tc::st8(trow + zlo_col(c0 + 8 * g8), zl + 8 * g8);
+                        tc::st8(trow + C::zlo_col(c0 + 8 * g8), zl + 8 * g8);
                     }
                     tc::wait_st();
                     tc::fence_before();
@@ -416,8 +440,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                 TRACE(4, l);
                 tc::fence_after();
                 const float *bt = p.bt + static_cast<size_t>(l) * BT;
-                if (isA) epi2_layer<false>(trow, bt, x, v);
-                else epi2_layer<true>(trow, bt, x, v);
+                if (isA) epi2_layer<false, C_U2>(trow, bt, x, v);
+                else epi2_layer<true, C_U2>(trow, bt, x, v);
                 if (isA) {
                     float err = 0.f;
 #pragma unroll
@@ -489,21 +513,30 @@ inline size_t img_off(int n, int k, int NR) {
 } // namespace
 
 int tc_prepare() {
-    cudaError_t e = cudaFuncSetAttribute(k_stack_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(SM_TOTAL));
+    cudaError_t e = cudaFuncSetAttribute(k_stack_tc<160>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(TcCfg<160>::SM_TOTAL));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_stack_tc<48>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(TcCfg<48>::SM_TOTAL));
     if (e != cudaSuccess)
         return fail(DETNET_ERR_CUDA, "tcgen05 kernel smem attribute: %s", cudaGetErrorString(e));
     return 0;
 }
 
-int tc_pack(TcModel &tc, int K, int Z, int V, int L, const double *params, const double *masks) {
-    tc.K = K; tc.Z = Z; tc.V = V; tc.L = L;
-    tc.ready = false;
-    if (K != KX || Z != ZH || V != VV) return 0; // other dims use the SIMT path
+namespace {
+// Pack every layer into the ZH-row smem images of TcCfg<ZH>. units[l] lists
+// the hidden units kept for layer l (row r of the W1 image and column r of
+// the [W3; W2] image hold unit units[l][r]; rows past the list stay zero, so
+// their z = relu(0) = 0 contributes nothing).
+template <int ZH>
+void pack_images(std::vector<float> &img, std::vector<float> &bt, int K, int Z, int V, int L,
+                 const double *params, const double *masks,
+                 const std::vector<std::vector<int>> &units) {
+    using C = TcCfg<ZH>;
     const int IN = 3 * K + V;
     const long P = Z * IN + Z + static_cast<long>(K) * Z + K + static_cast<long>(V) * Z + V + 1;
-    std::vector<float> img(static_cast<size_t>(L) * LAYER_BYTES / 4, 0.f);
-    std::vector<float> bt(static_cast<size_t>(L) * BT, 0.f);
+    img.assign(static_cast<size_t>(L) * C::LAYER_BYTES / 4, 0.f);
+    bt.assign(static_cast<size_t>(L) * BT, 0.f);
     for (int l = 0; l < L; ++l) {
         const double *pr = params + l * P;
         const double *mk = masks ? masks + l * P : nullptr;
@@ -511,34 +544,80 @@ int tc_pack(TcModel &tc, int K, int Z, int V, int L, const double *params, const
         const long oW1 = 0, ob1 = static_cast<long>(Z) * IN, oW2 = ob1 + Z,
                    ob2 = oW2 + static_cast<long>(K) * Z, oW3 = ob2 + K,
                    ob3 = oW3 + static_cast<long>(V) * Z, ot = ob3 + V;
-        float *L1hi = img.data() + static_cast<size_t>(l) * LAYER_BYTES / 4;
-        float *L1lo = L1hi + W1_HALF / 4;
-        float *L2hi = L1hi + W1_BYTES / 4;
-        float *L2lo = L2hi + W23_HALF / 4;
-        for (int i = 0; i < W1_ROWS; ++i)
+        float *L1hi = img.data() + static_cast<size_t>(l) * C::LAYER_BYTES / 4;
+        float *L1lo = L1hi + C::W1_HALF / 4;
+        float *L2hi = L1hi + C::W1_BYTES / 4;
+        float *L2lo = L2hi + C::W23_HALF / 4;
+        const std::vector<int> &us = units[l];
+        for (size_t r = 0; r < us.size(); ++r) {
+            const int i = us[r];
             for (int k = 0; k < W1_K; ++k) {
                 float val = 0.f;
                 if (k < KX) val = w(oW1 + i * IN + k);
                 else if (k == KX) val = w(ob1 + i);
                 else if (k >= 24) val = w(oW1 + i * IN + (k - 4));
                 const float hi = rna_tf32_host(val);
-                L1hi[img_off(i, k, W1_ROWS)] = hi;
-                L1lo[img_off(i, k, W1_ROWS)] = rna_tf32_host(val - hi);
+                L1hi[img_off(static_cast<int>(r), k, ZH)] = hi;
+                L1lo[img_off(static_cast<int>(r), k, ZH)] = rna_tf32_host(val - hi);
             }
-        for (int r = 0; r < W23_ROWS; ++r)
-            for (int i = 0; i < W23_K; ++i) {
+            for (int o = 0; o < W23_ROWS; ++o) {
                 float val = 0.f;
-                if (r < VV) val = w(oW3 + r * Z + i);
-                else if (r < VV + KX) val = w(oW2 + (r - VV) * Z + i);
+                if (o < VV) val = w(oW3 + o * Z + i);
+                else if (o < VV + KX) val = w(oW2 + (o - VV) * Z + i);
                 const float hi = rna_tf32_host(val);
-                L2hi[img_off(r, i, W23_ROWS)] = hi;
-                L2lo[img_off(r, i, W23_ROWS)] = rna_tf32_host(val - hi);
+                L2hi[img_off(o, static_cast<int>(r), W23_ROWS)] = hi;
+                L2lo[img_off(o, static_cast<int>(r), W23_ROWS)] = rna_tf32_host(val - hi);
             }
+        }
         float *b = bt.data() + static_cast<size_t>(l) * BT;
         for (int k = 0; k < VV; ++k) b[k] = w(ob3 + k);
         for (int k = 0; k < KX; ++k) b[VV + k] = w(ob2 + k);
         b[60] = static_cast<float>(pr[ot]);
         b[61] = static_cast<float>(1.0 / pr[ot]);
+    }
+}
+} // namespace
+
+int tc_pack(TcModel &tc, int K, int Z, int V, int L, const double *params, const double *masks) {
+    tc.K = K; tc.Z = Z; tc.V = V; tc.L = L;
+    tc.ready = false;
+    tc.zh = 0;
+    if (K != KX || V != VV) return 0; // other dims use the SIMT path
+    const int IN = 3 * K + V;
+    const long P = Z * IN + Z + static_cast<long>(K) * Z + K + static_cast<long>(V) * Z + V + 1;
+    // Live hidden units per layer: a unit whose masked [W2; W3] column is all
+    // zero cannot influence x_hat, v or the loss (model.cpp:114-118), so it is
+    // dropped; group-pruned models (config 3/4) keep <= 48 of 160.
+    std::vector<std::vector<int>> units(L);
+    size_t max_alive = 0;
+    for (int l = 0; l < L; ++l) {
+        const double *pr = params + l * P;
+        const double *mk = masks ? masks + l * P : nullptr;
+        const long oW2 = static_cast<long>(Z) * IN + Z, oW3 = oW2 + static_cast<long>(K) * Z + K;
+        for (int i = 0; i < Z; ++i) {
+            bool alive = false;
+            for (int o = 0; o < K && !alive; ++o) {
+                const long off = oW2 + static_cast<long>(o) * Z + i;
+                alive = static_cast<float>(pr[off] * (mk ? mk[off] : 1.0)) != 0.f;
+            }
+            for (int o = 0; o < V && !alive; ++o) {
+                const long off = oW3 + static_cast<long>(o) * Z + i;
+                alive = static_cast<float>(pr[off] * (mk ? mk[off] : 1.0)) != 0.f;
+            }
+            if (alive) units[l].push_back(i);
+        }
+        max_alive = std::max(max_alive, units[l].size());
+    }
+    if (max_alive > 160) return 0; // wider than the dense template: SIMT path
+    std::vector<float> img, bt;
+    if (max_alive <= 48 && !std::getenv("DETNET_TC_NO_COMPACT")) {
+        tc.zh = 48;
+        pack_images<48>(img, bt, K, Z, V, L, params, masks, units);
+        tc.rec_bytes = TcCfg<48>::LAYER_BYTES;
+    } else {
+        tc.zh = 160;
+        pack_images<160>(img, bt, K, Z, V, L, params, masks, units);
+        tc.rec_bytes = TcCfg<160>::LAYER_BYTES;
     }
     const size_t wbytes = img.size() * 4, bbytes = bt.size() * 4;
     if (tc.w.ensure(wbytes + bbytes)) return fail(DETNET_ERR_CUDA, "cudaMalloc tc weights");
@@ -546,7 +625,6 @@ int tc_pack(TcModel &tc, int K, int Z, int V, int L, const double *params, const
         cudaMemcpy(static_cast<char *>(tc.w.p) + wbytes, bt.data(), bbytes,
                    cudaMemcpyHostToDevice) != cudaSuccess)
         return fail(DETNET_ERR_CUDA, "upload tc weights");
-    tc.rec_bytes = LAYER_BYTES;
     tc.ready = true;
     return 0;
 }
@@ -557,7 +635,7 @@ int tc_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cu
     p.a = a;
     p.w = static_cast<const unsigned char *>(tc.w.p);
     p.bt = reinterpret_cast<const float *>(static_cast<const char *>(tc.w.p) +
-                                           static_cast<size_t>(tc.L) * LAYER_BYTES);
+                                           static_cast<size_t>(tc.L) * tc.rec_bytes);
     p.x_state = xs;
     p.v_state = vs;
     p.trace = nullptr;
@@ -573,7 +651,8 @@ int tc_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cu
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int grid = static_cast<int>(std::min<long>(a.n_tiles, sms));
     if (grid <= 0) return 0;
-    k_stack_tc<<<grid, NTHREADS, SM_TOTAL, st>>>(p);
+    if (tc.zh == 48) k_stack_tc<48><<<grid, NTHREADS, TcCfg<48>::SM_TOTAL, st>>>(p);
+    else k_stack_tc<160><<<grid, NTHREADS, TcCfg<160>::SM_TOTAL, st>>>(p);
     if (tracing) {
         long long h[8 * 16];
         cudaMemcpyAsync(h, trace_buf, sizeof h, cudaMemcpyDeviceToHost, st);

@@ -146,6 +146,13 @@ __device__ __forceinline__ void ffma2(float &d0, float &d1, float a, float b0, f
         : "f"(a), "f"(b0), "f"(b1));
 }
 
+#ifdef DETNET_PREP_TRACE
+#define PTR(ev) \
+    if (blockIdx.x == 0 && lane == 0 && it < 3) ptr_t[it][ev] = clock64();
+#else
+#define PTR(ev)
+#endif
+
 // K1 fast path. grid = min(tiles, 2 x SMs), PS_THREADS threads,
 // PrepStreamSmem<K, N>::BYTES of dynamic smem; scratch = grid x NG x 64 floats.
 template <int K, int N>
@@ -240,7 +247,11 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
     float *park = scratch + static_cast<long>(blockIdx.x) * NG * P + ls; // [NG][P]
     long cstep = 0;
     int it = 0;
+#ifdef DETNET_PREP_TRACE
+    long long ptr_t[3][12] = {};
+#endif
     for (long tt = blockIdx.x; tt < ntiles; tt += gridDim.x, ++it) {
+        PTR(0);
         const int yb = it & 1;
         const uint32_t yph = (it >> 1) & 1;
         const long s = tt * P + ls;
@@ -251,6 +262,7 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
         const float *ybuf =
             reinterpret_cast<const float *>(psm + SM::YB + yb * SM::YSLOT) + ls * N;
         mbar_wait_guard(&yfull[yb], yph);
+        PTR(1);
         uint32_t mask = 0;
         {
             const int *xw = reinterpret_cast<const int *>(psm + SM::XB + yb * SM::XSLOT + ls * K);
@@ -308,6 +320,7 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
                 hold = st;
             }
         }
+        PTR(2);
         float *ub = reinterpret_cast<float *>(psm + SM::RING + hold * SM::STAGE);
         // G entries of row a (upper triangle) to the tile-major gp layout
         auto put_row = [&](auto ac) {
@@ -354,6 +367,7 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
             }
         }
 
+        PTR(3);
         // ---------------- FP32 Cholesky + first solve, split A | B ----------------
         float z[K];
         if (isA) {
@@ -387,7 +401,9 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
                 for (int j = R0; j < K; ++j)
                     ub[(m * (K - R0) + (j - R0)) * P + ls] = acc[PM::pos(m, j)];
             pair_bar(bar); // (1) A -> B: cross block, folded rhs
+            PTR(4);
             pair_bar(bar); // (2) B -> A: d[R0..K); B is done with the cross block
+            PTR(5);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[hold]);
             float d[K];
@@ -410,6 +426,7 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
             });
             if (badB[ls]) bad = true;
             pair_bar(bar); // (3) A -> B: x_tilde estimate
+            PTR(6);
         } else {
             sfor<R0, K>(gx_row);
             // original diagonal (pivot test) parked in RX, free until pass 1
@@ -417,6 +434,7 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
 #pragma unroll
             for (int k = R0; k < K; ++k) gd[(k - R0) * P] = acc[PM::pos(k, k)];
             pair_bar(bar); // (1)
+            PTR(4);
             // fold B's part of G x - q into A's folded rhs now (frees pr)
 #pragma unroll
             for (int k = R0; k < K; ++k) X1[k][ls] += pr[k];
@@ -460,7 +478,9 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
             });
             badB[ls] = bad ? 1 : 0;
             pair_bar(bar); // (2)
+            PTR(5);
             pair_bar(bar); // (3)
+            PTR(6);
         }
 
         // ---------------- pass 1: FP64 residual H^T (H x_tilde - y) ----------------
@@ -498,6 +518,7 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&yempty[yb]);
+        PTR(7);
 
         // the factor, back from the parking slab (into acc: A rows or B rows)
         auto unpark = [&](auto ac) {
@@ -509,8 +530,10 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
 #pragma unroll
             for (int k = 0; k < R0; ++k) RX[k][ls] = rp[k];
             pair_bar(bar); // (4) B -> A: partial residual rows 0..R0-1
+            PTR(8);
             sfor<R0, K>(unpark);
             pair_bar(bar); // (5) A -> B: folded rhs
+            PTR(9);
             sfor<R0, K>([&](auto kc) {
                 constexpr int k = SF_IDX(kc);
                 float t = static_cast<float>(RX[k][ls] + rp[k]);
@@ -528,10 +551,13 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
 #pragma unroll
             for (int k = R0; k < K; ++k) X1[k][ls] = z[k];
             pair_bar(bar); // (6) B -> A: correction rows R0..K-1
+            PTR(10);
+            PTR(11);
             continue;
         }
         sfor<0, R0>(unpark);
         pair_bar(bar); // (4)
+            PTR(8);
         sfor<0, R0>([&](auto kc) {
             constexpr int k = SF_IDX(kc);
             float t = static_cast<float>(rp[k] + RX[k][ls]);
@@ -547,7 +573,9 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
             RX[j][ls] = t;
         }
         pair_bar(bar); // (5)
+            PTR(9);
         pair_bar(bar); // (6)
+            PTR(10);
         float cc[K];
 #pragma unroll
         for (int j = R0; j < K; ++j) cc[j] = X1[j][ls];
@@ -571,6 +599,7 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
         // remaining error is about cmax^2 / dmax (<= 1e-8 relative). Anything
         // else -- collapsed pivots, slow convergence, NaN -- goes to the exact LU.
         if (!(cmax <= 1e-4 * dmax) || !(dn == dn)) bad = true;
+        PTR(11);
         if (live) {
             if (bad) {
                 const int slot = atomicAdd(fb_count, 1);
@@ -583,6 +612,15 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
             }
         }
     }
+#ifdef DETNET_PREP_TRACE
+    if (blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == 2))
+        for (int t = 0; t < 3; ++t)
+            printf("prep trace warp %d tile %d: %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld\n",
+                   warp, t, ptr_t[t][1] - ptr_t[t][0], ptr_t[t][2] - ptr_t[t][0],
+                   ptr_t[t][3] - ptr_t[t][0], ptr_t[t][4] - ptr_t[t][0], ptr_t[t][5] - ptr_t[t][0],
+                   ptr_t[t][6] - ptr_t[t][0], ptr_t[t][7] - ptr_t[t][0], ptr_t[t][8] - ptr_t[t][0],
+                   ptr_t[t][9] - ptr_t[t][0], ptr_t[t][10] - ptr_t[t][0], ptr_t[t][11] - ptr_t[t][0]);
+#endif
 }
 
 } // namespace detnet

@@ -56,14 +56,13 @@ template <int ZH> struct TcCfg {
     static constexpr int GW = ZH / NH;             // group width (80 | 48)
     static constexpr int EW = GW / 2;              // epilogue-1 columns per thread per group
     static constexpr int C_U1 = 0, C_DYN = ZH, C_DYNLO = ZH + 80, C_U2 = ZH + 160,
-                         C_QHI = ZH + 224, C_QLO = ZH + 256;
-    // z_lo column of hidden unit j. With two W1 groups, units of group 0 are
-    // written while group 1 still reads A_dyn, so they live in the free columns
-    // [C_QHI+24, C_QLO) and [C_QLO+24, 512); group 1 reuses A_dyn hi. With one
-    // group every W1 MMA has completed, so z_lo reuses A_dyn hi directly.
+                         C_QHI = ZH + 224, C_QLO = ZH + 248;
+    // z_lo column of hidden unit j (contiguous per W1 group). With two groups,
+    // units of group 0 are written while group 1 still reads A_dyn, so they
+    // live in the free columns [C_QLO+24, 512); group 1 reuses A_dyn hi. With
+    // one group every W1 MMA has completed, so z_lo reuses A_dyn hi directly.
     __host__ __device__ static constexpr int zlo_col(int j) {
-        return NH == 1 ? C_DYN + j
-                       : (j >= GW ? C_DYN + (j - GW) : (j < 8 ? C_QHI + 24 + j : C_QLO + 24 + (j - 8)));
+        return NH == 1 ? C_DYN + j : (j >= GW ? C_DYN + (j - GW) : C_QLO + 24 + j);
     }
     static constexpr uint32_t W1_HALF = ZH * W1_K * 4, W23_HALF = W23_ROWS * ZH * 4;
     static constexpr uint32_t W1_BYTES = 2 * W1_HALF, W23_BYTES = 2 * W23_HALF;
@@ -71,9 +70,11 @@ template <int ZH> struct TcCfg {
     static constexpr uint32_t W1_LBO = ZH * 16;
     static constexpr uint32_t SM_W1 = 0, SM_W23 = W1_BYTES, SM_GX = W1_BYTES + W23_BYTES,
                               SM_RED = SM_GX + 14 * 128 * 4, SM_BAR = SM_RED + 128,
-                              SM_TMEM = SM_BAR + 8 * 8, SM_TOTAL = SM_TMEM + 16;
+                              SM_TMEM = SM_BAR + 16 * 8, SM_BT = SM_TMEM + 16,
+                              SM_TOTAL = SM_BT + 2 * BT * 4;
     static_assert(C_QLO + 24 <= TMEM_COLS, "TMEM budget");
     static_assert(NH == 1 || zlo_col(GW - 1) < TMEM_COLS, "TMEM budget (z_lo)");
+    static_assert(NH == 1 || zlo_col(0) >= C_QLO + 24, "z_lo clear of q");
 };
 
 struct TcKArgs {
@@ -87,10 +88,16 @@ struct TcKArgs {
 #define TRACE(ev, l)                                                                           \
     do {                                                                                       \
         if (p.trace && blockIdx.x == 0 && (l) - L0 < 8 && trace_on)                            \
-            p.trace[((l) - L0) * 16 + (ev)] = clock64();                                       \
+            p.trace[((l) - L0) * 32 + (ev)] = clock64();                                       \
     } while (0)
 
-enum { B_W1F = 0, B_W23F = 1, B_U1A = 2, B_U1B = 3, B_U2 = 4, B_AREADY = 5, B_ZA = 6, B_ZB = 7 };
+// B_VX: v (B warps) and x (A warps) of the next layer are in A_dyn; B_G: G x_hat
+// (A warps) is too. W1 is issued in K stages as its inputs become ready:
+// [q 1] right after the previous layer's W23, [v x] at B_VX, [gx] at B_G.
+// B_E2L: the epilogue has read U2V (so the next layer's [q 1] MMAs do not
+// compete with those TMEM loads).
+enum { B_W1F = 0, B_W23F = 1, B_U1A = 2, B_U1B = 3, B_U2 = 4, B_VX = 5, B_ZA = 6, B_ZB = 7, B_G = 8,
+       B_E2L = 9, NBARS = 10 };
 
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
     uint32_t r[8];
@@ -101,6 +108,14 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Store N (multiple of 8) contiguous columns: x16 pieces, then one x8.
+template <int N> __device__ __forceinline__ void st_cols(uint32_t taddr, const float *v) {
+#pragma unroll
+    for (int c = 0; c + 16 <= N; c += 16)
+        tc::st16(taddr + c, *reinterpret_cast<const float(*)[16]>(v + c));
+    if constexpr (N % 16 != 0) tc::st8(taddr + (N / 16) * 16, v + (N / 16) * 16);
 }
 
 // 3xTF32 split: hi = rna_tf32(v); lo = v - hi is exact in FP32 and the tensor
@@ -115,7 +130,7 @@ __device__ __forceinline__ void split(float v, float &hi, float &lo) {
 // from columns [0, 40).
 template <bool WITH_V, int C_U2>
 __device__ __forceinline__ void epi2_layer(uint32_t trow, const float *bt, float (&x)[KX],
-                                           float (&v)[VV]) {
+                                           float (&v)[VV], uint64_t *e2l, long long *tr) {
     uint32_t r[4][16];
     if (WITH_V) {
         tc::ld16_nw(trow + C_U2, r[0]);
@@ -124,14 +139,16 @@ __device__ __forceinline__ void epi2_layer(uint32_t trow, const float *bt, float
     tc::ld16_nw(trow + C_U2 + 32, r[2]);
     tc::ld16_nw(trow + C_U2 + 48, r[3]);
     float b[60];
-    const float4 *b4 = reinterpret_cast<const float4 *>(bt);
+    const float4 *b4 = reinterpret_cast<const float4 *>(bt); // shared memory
 #pragma unroll
     for (int k = WITH_V ? 0 : 10; k < 15; ++k) {
-        const float4 q = __ldg(b4 + k);
+        const float4 q = b4[k];
         b[4 * k] = q.x; b[4 * k + 1] = q.y; b[4 * k + 2] = q.z; b[4 * k + 3] = q.w;
     }
-    const float2 tt = __ldg(reinterpret_cast<const float2 *>(bt + 60)); // (t, 1/t)
+    const float2 tt = *reinterpret_cast<const float2 *>(bt + 60); // (t, 1/t)
     tc::wait_ld();
+    mbar_arrive(e2l);
+    if (tr) *tr = clock64();
 #pragma unroll
     for (int k = 0; k < KX; ++k) {
         const int c = 40 + k;
@@ -151,7 +168,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
     constexpr int C_U1 = C::C_U1, C_DYN = C::C_DYN, C_DYNLO = C::C_DYNLO, C_U2 = C::C_U2,
                   C_QHI = C::C_QHI, C_QLO = C::C_QLO;
     constexpr uint32_t SM_W1 = C::SM_W1, SM_W23 = C::SM_W23, SM_GX = C::SM_GX,
-                       SM_RED = C::SM_RED, SM_BAR = C::SM_BAR, SM_TMEM = C::SM_TMEM;
+                       SM_RED = C::SM_RED, SM_BAR = C::SM_BAR, SM_TMEM = C::SM_TMEM,
+                       SM_BT = C::SM_BT;
     constexpr uint32_t W1_HALF = C::W1_HALF, W23_HALF = C::W23_HALF, W1_BYTES = C::W1_BYTES,
                        W23_BYTES = C::W23_BYTES, LAYER_BYTES = C::LAYER_BYTES,
                        W1_LBO = C::W1_LBO;
@@ -170,7 +188,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
         mbar_init(&bars[B_U1A], 1);
         mbar_init(&bars[B_U1B], 1);
         mbar_init(&bars[B_U2], 1);
-        mbar_init(&bars[B_AREADY], 256);
+        mbar_init(&bars[B_VX], 256);
+        mbar_init(&bars[B_G], 128);
+        mbar_init(&bars[B_E2L], 256);
         mbar_init(&bars[B_ZA], 256);
         mbar_init(&bars[B_ZB], 256);
         fence_mbar_init();
@@ -205,20 +225,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                 const uint32_t ph = static_cast<uint32_t>(it & 1);
                 const int l = L0 + static_cast<int>(it % NL);
                 const bool trace_on = it < NL && lane == 0;
-                mbar_wait_guard(&bars[B_W1F], ph);
-                TRACE(12, l);
-                mbar_wait_guard(&bars[B_AREADY], ph);
-                TRACE(6, l);
-                tc::fence_after();
-                // U1 = [q 1 | x gx v] . W1'^T in NH N-groups of GW hidden units
-#pragma unroll 1
-                for (int h = 0; h < NH; ++h) {
+                // K steps of W1 (8 columns each): 0-2 [q 1 0 0 0], 3-7 v, 8-9 x, 10-12 [x gx]
+                auto w1_steps = [&](int h, int k0, int k1, bool commit) {
                     if (tc::elect_one()) {
                         const uint32_t tb = tc::opaque32(tbase);
                         const uint64_t d1h = tc::opaque64(d1 + h * NB);
                         const uint32_t dcol = tb + C_U1 + GW * h;
-#pragma unroll
-                        for (int kk = 0; kk < 13; ++kk) {
+#pragma unroll 1
+                        for (int kk = k0; kk < k1; ++kk) {
                             const uint32_t ahi = kk < 3 ? C_QHI + 8 * kk : C_DYN + 8 * (kk - 3);
                             const uint32_t alo = kk < 3 ? C_QLO + 8 * kk : C_DYNLO + 8 * (kk - 3);
                             const uint64_t bhi = d1h + kk * S1;
@@ -226,13 +240,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                             tc::mma_tf32_ts(dcol, tb + ahi, bhi + H1, id1, 1);
                             tc::mma_tf32_ts(dcol, tb + alo, bhi, id1, 1);
                         }
-                        tc::commit(&bars[h == 0 ? B_U1A : B_U1B]);
+                        if (commit) tc::commit(&bars[h == 0 ? B_U1A : B_U1B]);
                     }
                     __syncwarp();
-                }
+                };
+                mbar_wait_guard(&bars[B_W1F], ph);
+                TRACE(11, l);
+                // U1 is overwritten: the previous layer's W23 (reading z_hi there)
+                // must be complete; a tile's first layer also needs its q columns.
+                if (l == L0) mbar_wait_guard(&bars[B_VX], ph);
+                else mbar_wait_guard(&bars[B_E2L], ph ^ 1);
+                tc::fence_after();
+                for (int h = 0; h < NH; ++h) w1_steps(h, 0, 3, false);
+                if (l != L0) mbar_wait_guard(&bars[B_VX], ph);
                 TRACE(7, l);
-                mbar_wait_guard(&bars[B_W23F], ph);
+                tc::fence_after();
+                for (int h = 0; h < NH; ++h) w1_steps(h, 3, 10, false);
+                mbar_wait_guard(&bars[B_G], ph);
                 TRACE(13, l);
+                tc::fence_after();
+                for (int h = 0; h < NH; ++h) w1_steps(h, 10, 13, true);
+                TRACE(8, l);
+                mbar_wait_guard(&bars[B_W23F], ph);
+                TRACE(12, l);
                 // U2V = z . [W3; W2]^T, K split by the z groups
                 constexpr int KG = GW / 8; // k-steps per group
 #pragma unroll 1
@@ -269,27 +299,30 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                 }
                 __syncwarp();
             };
-            auto load_w23 = [&](int l) {
+            // [W3; W2] images + the layer's bias row (double-buffered by iteration)
+            auto load_w23 = [&](int l, long itn) {
                 if (leader) {
-                    mbar_arrive_expect_tx(&bars[B_W23F], W23_BYTES);
+                    mbar_arrive_expect_tx(&bars[B_W23F], W23_BYTES + BT * 4);
                     bulk_g2s_chunked(sm + SM_W23,
                                      p.w + static_cast<size_t>(l) * LAYER_BYTES + W1_BYTES,
                                      W23_BYTES, &bars[B_W23F]);
+                    bulk_g2s(sm + SM_BT + (itn & 1) * BT * 4, p.bt + static_cast<size_t>(l) * BT,
+                             BT * 4, &bars[B_W23F]);
                 }
                 __syncwarp();
             };
-            if (total_it > 0) { load_w1(L0); load_w23(L0); }
+            if (total_it > 0) { load_w1(L0); load_w23(L0, 0); }
             for (long it = 0; it + 1 < total_it; ++it) {
                 const uint32_t ph = static_cast<uint32_t>(it & 1);
                 const int l = L0 + static_cast<int>(it % NL);
                 const int lnext = L0 + static_cast<int>((it + 1) % NL);
                 const bool trace_on = it < NL && lane == 0;
                 mbar_wait_guard(&bars[U1_LAST], ph); // every W1 group consumed
-                TRACE(8, l);
+                TRACE(14, l);
                 load_w1(lnext);
                 mbar_wait_guard(&bars[B_U2], ph); // W23 consumed
-                TRACE(11, l);
-                load_w23(lnext);
+                TRACE(15, l);
+                load_w23(lnext, it + 1);
             }
         }
     } else {
@@ -338,10 +371,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
             }
             for (int l = L0; l < L1; ++l, ++it) {
                 const uint32_t ph = static_cast<uint32_t>(it & 1);
-                const bool trace_on = ti == 0 && threadIdx.x == 0;
-                TRACE(0, l);
-                // ---- prep: G x_hat (rows 0-5 on A, rows 6-19 on B), write A_dyn ----
+                const bool trace_on = ti == 0 && (threadIdx.x == 0 || threadIdx.x == 128);
+                const int tb16 = isA ? 0 : 16;
+                const double lw = isA ? a.lnk[l] : 0.0; // loss weight, fetched early
+                TRACE(0 + tb16, l);
+                // ---- prep: A_dyn = [v | x | gx] hi/lo. v (B) and x (A) first, then
+                // G x_hat (rows 0-5 on A, rows 6-19 on B, 14-float exchange) ----
                 if (isA) {
+                    {
+                        float hi[16], lo[16];
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) split(x[k], hi[k], lo[k]);
+                        st_cols<16>(trow + C_DYN + 40, hi);
+                        st_cols<16>(trow + C_DYNLO + 40, lo);
+                    }
+                    tc::wait_st();
+                    tc::fence_before();
+                    mbar_arrive(&bars[B_VX]);
+                    TRACE(1 + tb16, l);
                     float gx[KX];
 #pragma unroll
                     for (int k = 0; k < KX; ++k) gx[k] = 0.f;
@@ -353,30 +400,40 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                             gx[r] = fmaf(g[e], x[c], gx[r]);
                             if (c != r) gx[c] = fmaf(g[e], x[r], gx[c]);
                         }
-                    // x hi/lo can go out while B finishes its rows
-#pragma unroll
-                    for (int c = 0; c < 2; ++c) {
-                        float hi[8], lo[8];
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) split(x[8 * c + k], hi[k], lo[k]);
-                        tc::st8(trow + C_DYN + 8 * c, hi);
-                        tc::st8(trow + C_DYNLO + 8 * c, lo);
-                    }
                     tc::named_bar(pair_bar, 64);
 #pragma unroll
                     for (int k = 6; k < KX; ++k) gx[k] += sGX[(k - 6) * 128 + col];
+                    {
+                        float hi[24], lo[24];
 #pragma unroll
-                    for (int c = 2; c < 5; ++c) {
-                        float hi[8], lo[8];
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) {
-                            const int j = 8 * c + k;
+                        for (int k = 0; k < 24; ++k) {
+                            const int j = 16 + k;
                             split(j < KX ? x[j < KX ? j : 0] : gx[j >= KX ? j - KX : 0], hi[k], lo[k]);
                         }
-                        tc::st8(trow + C_DYN + 8 * c, hi);
-                        tc::st8(trow + C_DYNLO + 8 * c, lo);
+                        st_cols<24>(trow + C_DYN + 56, hi);
+                        st_cols<24>(trow + C_DYNLO + 56, lo);
                     }
+                    tc::wait_st();
+                    tc::fence_before();
+                    mbar_arrive(&bars[B_G]);
                 } else {
+#pragma unroll
+                    for (int c = 0; c < VV; c += 16) {
+                        float hi[16], lo[16];
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) split(v[c + k < VV ? c + k : 0], hi[k], lo[k]);
+                        if (c + 16 <= VV) {
+                            st_cols<16>(trow + C_DYN + c, hi);
+                            st_cols<16>(trow + C_DYNLO + c, lo);
+                        } else {
+                            st_cols<8>(trow + C_DYN + c, hi);
+                            st_cols<8>(trow + C_DYNLO + c, lo);
+                        }
+                    }
+                    tc::wait_st();
+                    tc::fence_before();
+                    mbar_arrive(&bars[B_VX]);
+                    TRACE(1 + tb16, l);
                     float part[KX];
 #pragma unroll
                     for (int k = 6; k < KX; ++k) part[k] = 0.f;
@@ -391,26 +448,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
 #pragma unroll
                     for (int k = 6; k < KX; ++k) sGX[(k - 6) * 128 + col] = part[k];
                     tc::named_bar(pair_bar, 64);
-#pragma unroll
-                    for (int c = 0; c < 5; ++c) {
-                        float hi[8], lo[8];
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) split(v[8 * c + k], hi[k], lo[k]);
-                        tc::st8(trow + C_DYN + 40 + 8 * c, hi);
-                        tc::st8(trow + C_DYNLO + 40 + 8 * c, lo);
-                    }
                 }
-                tc::wait_st();
-                tc::fence_before();
-                mbar_arrive(&bars[B_AREADY]);
-                TRACE(1, l);
+                TRACE(2 + tb16, l);
 
+                // this layer's bias row came with W23; its barrier cannot re-arm before
+                // this thread's Z arrivals, so waiting here is race-free
+                mbar_wait_guard(&bars[B_W23F], ph);
                 // ---- epilogue 1: z = relu(U1) -> z_hi (in place), z_lo. Each W1 group
                 // (GW hidden units) is shared by A (first EW) and B (last EW).
 #pragma unroll 1
                 for (int h = 0; h < NH; ++h) {
                     mbar_wait_guard(&bars[h == 0 ? B_U1A : B_U1B], ph);
-                    if (h == 0) TRACE(2, l);
+                    if (h == 0) TRACE(3 + tb16, l);
                     tc::fence_after();
                     const int c0 = GW * h + (isA ? 0 : EW);
                     constexpr int NL16 = (EW + 15) / 16;
@@ -418,30 +467,33 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
 #pragma unroll
                     for (int c = 0; c < NL16; ++c) tc::ld16_nw(trow + C_U1 + c0 + 16 * c, r[c]);
                     tc::wait_ld();
+                    if (h == 0) TRACE(23 + (isA ? 0 : 3), l);
                     float zh[EW], zl[EW];
 #pragma unroll
                     for (int k = 0; k < EW; ++k) {
                         const float u = __uint_as_float(r[k / 16][k % 16]);
                         split(u > 0.f ? u : 0.f, zh[k], zl[k]);
                     }
-#pragma unroll
-                    for (int g8 = 0; g8 < EW / 8; ++g8) {
-                        tc::st8(trow + C_U1 + c0 + 8 * g8, zh + 8 * g8);
-                        tc::st8(trow + C::zlo_col(c0 + 8 * g8), zl + 8 * g8);
-                    }
+                    st_cols<EW>(trow + C_U1 + c0, zh);
+                    st_cols<EW>(trow + C::zlo_col(c0), zl);
                     tc::wait_st();
+                    if (h == 0) TRACE(24 + (isA ? 0 : 3), l);
                     tc::fence_before();
                     mbar_arrive(&bars[h == 0 ? B_ZA : B_ZB]);
                 }
-                TRACE(3, l);
+                TRACE(4 + tb16, l);
 
                 // ---- epilogue 2: x_hat = psi_t(u2 + b2) on both halves; A: loss ----
                 mbar_wait_guard(&bars[B_U2], ph);
-                TRACE(4, l);
+                TRACE(5 + tb16, l);
                 tc::fence_after();
-                const float *bt = p.bt + static_cast<size_t>(l) * BT;
-                if (isA) epi2_layer<false, C_U2>(trow, bt, x, v);
-                else epi2_layer<true, C_U2>(trow, bt, x, v);
+                // bias row: landed with W23 (the MMA warp waited B_W23F before U2)
+                const float *bt = reinterpret_cast<const float *>(sm + SM_BT + (it & 1) * BT * 4);
+                long long *tr2 = (p.trace && blockIdx.x == 0 && l - L0 < 8 && trace_on && isA)
+                                     ? p.trace + (l - L0) * 32 + 25
+                                     : nullptr;
+                if (isA) epi2_layer<false, C_U2>(trow, bt, x, v, &bars[B_E2L], tr2);
+                else epi2_layer<true, C_U2>(trow, bt, x, v, &bars[B_E2L], tr2);
                 if (isA) {
                     float err = 0.f;
 #pragma unroll
@@ -449,7 +501,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                         const float d = ((xm >> k) & 1u ? 1.f : -1.f) - x[k];
                         err = fmaf(d, d, err);
                     }
-                    wsum += a.lnk[l] * static_cast<double>(err);
+                    wsum += lw * static_cast<double>(err);
                     if (a.xhat && live) {
                         float4 *o = reinterpret_cast<float4 *>(a.xhat + (s * NL + (l - L0)) * KX);
 #pragma unroll
@@ -457,7 +509,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                             o[k] = make_float4(x[4 * k], x[4 * k + 1], x[4 * k + 2], x[4 * k + 3]);
                     }
                 }
-                TRACE(5, l);
+                TRACE(6 + tb16, l);
             }
             // ---- tile end: state out, per-tile partials (A warps) ----
             if (p.x_state && live) {
@@ -552,10 +604,13 @@ void pack_images(std::vector<float> &img, std::vector<float> &bt, int K, int Z, 
         for (size_t r = 0; r < us.size(); ++r) {
             const int i = us[r];
             for (int k = 0; k < W1_K; ++k) {
+                // K order [q (20) | 1 | 0 0 0 | v (40) | x (20) | gx (20)];
+                // the input vector is [q; x; gx; v] (model.cpp:96-99)
                 float val = 0.f;
                 if (k < KX) val = w(oW1 + i * IN + k);
                 else if (k == KX) val = w(ob1 + i);
-                else if (k >= 24) val = w(oW1 + i * IN + (k - 4));
+                else if (k >= 24 && k < 64) val = w(oW1 + i * IN + (k + 36));
+                else if (k >= 64) val = w(oW1 + i * IN + (k - 44));
                 const float hi = rna_tf32_host(val);
                 L1hi[img_off(static_cast<int>(r), k, ZH)] = hi;
                 L1lo[img_off(static_cast<int>(r), k, ZH)] = rna_tf32_host(val - hi);
@@ -642,8 +697,8 @@ int tc_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cu
     static long long *trace_buf = nullptr;
     const bool tracing = std::getenv("DETNET_TC_TRACE") != nullptr;
     if (tracing) {
-        if (!trace_buf) cudaMalloc(&trace_buf, 8 * 16 * sizeof(long long));
-        cudaMemsetAsync(trace_buf, 0, 8 * 16 * sizeof(long long), st);
+        if (!trace_buf) cudaMalloc(&trace_buf, 8 * 32 * sizeof(long long));
+        cudaMemsetAsync(trace_buf, 0, 8 * 32 * sizeof(long long), st);
         p.trace = trace_buf;
     }
     int dev = 0, sms = 148;
@@ -654,16 +709,19 @@ int tc_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cu
     if (tc.zh == 48) k_stack_tc<48><<<grid, NTHREADS, TcCfg<48>::SM_TOTAL, st>>>(p);
     else k_stack_tc<160><<<grid, NTHREADS, TcCfg<160>::SM_TOTAL, st>>>(p);
     if (tracing) {
-        long long h[8 * 16];
+        long long h[8 * 32];
         cudaMemcpyAsync(h, trace_buf, sizeof h, cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
-        const char *nm[16] = {"prep0", "a_arr", "u1ok", "z_arr", "u2ok", "epi2end", "C:aready",
-                              "C:w1iss", "C:u1ok", "C:zready", "C:w23iss", "C:u2ok", "C:w1f",
-                              "C:w23f", "", ""};
+        const char *nm[32] = {"A:prep0", "A:vx", "A:g", "A:u1ok", "A:zarr", "A:u2ok", "A:epi2end",
+                              "M:vx", "M:w1iss", "M:zready", "M:w23iss", "M:w1f", "M:w23f", "M:g",
+                              "P:u1ok", "P:u2ok", "B:prep0", "B:vx", "B:pair", "B:u1ok", "B:zarr",
+                              "B:u2ok", "B:epi2end", "A:e1ld", "A:e1st", "A:e2ld", "B:e1ld",
+                              "B:e1st"};
         const long long t0 = h[0];
         for (int l = 0; l < 8; ++l) {
             std::fprintf(stderr, "layer %d:", l);
-            for (int e = 0; e < 14; ++e) std::fprintf(stderr, " %s=%lld", nm[e], h[l * 16 + e] - t0);
+            for (int e = 0; e < 28; ++e)
+                if (nm[e]) std::fprintf(stderr, " %s=%lld", nm[e], h[l * 32 + e] - t0);
             std::fprintf(stderr, "\n");
         }
     }

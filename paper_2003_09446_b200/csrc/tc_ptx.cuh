@@ -129,11 +129,12 @@ __device__ __forceinline__ void wait_st() {
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
-// Round to TF32 (nearest, ties away): the hi part of a 3xTF32 split.
+// Round to TF32 (nearest, ties away): the hi part of a 3xTF32 split. Same
+// result as cvt.rna.tf32.f32 for finite inputs, but two integer-pipe ops
+// instead of a conversion-pipe op (the conversion rate made the epilogue's
+// splits the longest step between the two GEMMs of a layer).
 __device__ __forceinline__ float tf32_rna(float v) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
-    return __uint_as_float(r);
+    return __uint_as_float((__float_as_uint(v) + 0x1000u) & 0xffffe000u);
 }
 
 // One elected lane of a converged warp (elect.sync): single-thread tcgen05

@@ -69,7 +69,7 @@ template <int ZH> struct TcCfg {
     static constexpr uint32_t LAYER_BYTES = W1_BYTES + W23_BYTES;
     static constexpr uint32_t W1_LBO = ZH * 16;
     static constexpr uint32_t SM_W1 = 0, SM_W23 = W1_BYTES, SM_GX = W1_BYTES + W23_BYTES,
-                              SM_RED = SM_GX + 14 * 128 * 4, SM_BAR = SM_RED + 128,
+                              SM_RED = SM_GX + KX * 128 * 4, SM_BAR = SM_RED + 128,
                               SM_TMEM = SM_BAR + 16 * 8, SM_BT = SM_TMEM + 16,
                               SM_TOTAL = SM_BT + 2 * BT * 4;
     static_assert(C_QLO + 24 <= TMEM_COLS, "TMEM budget");
@@ -85,11 +85,22 @@ struct TcKArgs {
     long long *trace; // optional debug timeline (DETNET_TC_TRACE): CTA 0, tile 0
 };
 
+// Debug timeline (build with EXTRA=-DDETNET_TC_TRACE, run with DETNET_TC_TRACE=1):
+// clock64 stamps of CTA 0's first tile, 8 layers x 32 events. Compiled out by
+// default -- the checks alone cost a few hundred cycles per layer.
+#ifdef DETNET_TC_TRACE
 #define TRACE(ev, l)                                                                           \
     do {                                                                                       \
         if (p.trace && blockIdx.x == 0 && (l) - L0 < 8 && trace_on)                            \
             p.trace[((l) - L0) * 32 + (ev)] = clock64();                                       \
     } while (0)
+#define TRACE_ON 1
+#else
+#define TRACE(ev, l)                                                                           \
+    do {                                                                                       \
+    } while (0)
+#define TRACE_ON 0
+#endif
 
 // B_VX: v (B warps) and x (A warps) of the next layer are in A_dyn; B_G: G x_hat
 // (A warps) is too. W1 is issued in K stages as its inputs become ready:
@@ -128,36 +139,47 @@ __device__ __forceinline__ void split(float v, float &hi, float &lo) {
 // Epilogue 2 for one layer: load the whole U2V row (64 columns, one wait),
 // x_hat = psi_t(u2 + b2) from columns [40, 60) and, on the B side, v = v' + b3
 // from columns [0, 40).
-template <bool WITH_V, int C_U2>
+// Epilogue 2 for one layer. A threads: x_hat = psi_t(u2 + b2) from U2V
+// columns [40, 60); B threads: v = v' + b3 from columns [0, 40). Only the
+// columns a side needs are read (TMEM reads are the epilogue's scarcest
+// resource); B gets x_hat from A through shared memory afterwards.
+template <bool SIDE_A, int C_U2>
 __device__ __forceinline__ void epi2_layer(uint32_t trow, const float *bt, float (&x)[KX],
                                            float (&v)[VV], uint64_t *e2l, long long *tr) {
-    uint32_t r[4][16];
-    if (WITH_V) {
-        tc::ld16_nw(trow + C_U2, r[0]);
-        tc::ld16_nw(trow + C_U2 + 16, r[1]);
-    }
-    tc::ld16_nw(trow + C_U2 + 32, r[2]);
-    tc::ld16_nw(trow + C_U2 + 48, r[3]);
-    float b[60];
-    const float4 *b4 = reinterpret_cast<const float4 *>(bt); // shared memory
+    if (SIDE_A) {
+        if (tr) tr[2] = clock64(); // slot 27
+        uint32_t r[KX];
+        tc::ld_cols_nw<KX>(trow + C_U2 + VV, r);
+        float b[KX];
 #pragma unroll
-    for (int k = WITH_V ? 0 : 10; k < 15; ++k) {
-        const float4 q = b4[k];
-        b[4 * k] = q.x; b[4 * k + 1] = q.y; b[4 * k + 2] = q.z; b[4 * k + 3] = q.w;
-    }
-    const float2 tt = *reinterpret_cast<const float2 *>(bt + 60); // (t, 1/t)
-    tc::wait_ld();
-    mbar_arrive(e2l);
-    if (tr) *tr = clock64();
+        for (int k = 0; k < KX / 4; ++k) {
+            const float4 q = reinterpret_cast<const float4 *>(bt + VV)[k];
+            b[4 * k] = q.x; b[4 * k + 1] = q.y; b[4 * k + 2] = q.z; b[4 * k + 3] = q.w;
+        }
+        const float2 tt = *reinterpret_cast<const float2 *>(bt + 60); // (t, 1/t)
+        if (tr) tr[3] = clock64();
+        tc::wait_ld();
+        if (tr) tr[4] = clock64();
+        mbar_arrive(e2l);
+        if (tr) *tr = clock64();
 #pragma unroll
-    for (int k = 0; k < KX; ++k) {
-        const int c = 40 + k;
-        const float uu = __uint_as_float(r[c / 16][c % 16]) + b[40 + k];
-        x[k] = uu <= -tt.x ? -1.f : (uu >= tt.x ? 1.f : uu * tt.y);
-    }
-    if (WITH_V) {
+        for (int k = 0; k < KX; ++k) {
+            const float uu = __uint_as_float(r[k]) + b[k];
+            x[k] = uu <= -tt.x ? -1.f : (uu >= tt.x ? 1.f : uu * tt.y);
+        }
+    } else {
+        uint32_t r[VV];
+        tc::ld_cols_nw<VV>(trow + C_U2, r);
+        float b[VV];
 #pragma unroll
-        for (int k = 0; k < VV; ++k) v[k] = __uint_as_float(r[k / 16][k % 16]) + b[k];
+        for (int k = 0; k < VV / 4; ++k) {
+            const float4 q = reinterpret_cast<const float4 *>(bt)[k];
+            b[4 * k] = q.x; b[4 * k + 1] = q.y; b[4 * k + 2] = q.z; b[4 * k + 3] = q.w;
+        }
+        tc::wait_ld();
+        mbar_arrive(e2l);
+#pragma unroll
+        for (int k = 0; k < VV; ++k) v[k] = __uint_as_float(r[k]) + b[k];
     }
 }
 
@@ -320,7 +342,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                 mbar_wait_guard(&bars[U1_LAST], ph); // every W1 group consumed
                 TRACE(14, l);
                 load_w1(lnext);
-                mbar_wait_guard(&bars[B_U2], ph); // W23 consumed
+                // W23 consumed, and the epilogue has read U2V and its bias row: the
+                // 80 KB fill now no longer competes with that epilogue for smem
+                mbar_wait_guard(&bars[B_E2L], ph);
                 TRACE(15, l);
                 load_w23(lnext, it + 1);
             }
@@ -369,6 +393,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                     tc::st8(trow + C_QLO + 8 * c, ql + 8 * c);
                 }
             }
+            int lpend = -1;       // layer whose loss / x_hat output is still due (A side)
+            double lw_pend = 0.0;
+            auto settle = [&]() {
+                float err = 0.f;
+#pragma unroll
+                for (int k = 0; k < KX; ++k) {
+                    const float d = ((xm >> k) & 1u ? 1.f : -1.f) - x[k];
+                    err = fmaf(d, d, err);
+                }
+                wsum += lw_pend * static_cast<double>(err);
+                if (a.xhat && live) {
+                    float4 *o = reinterpret_cast<float4 *>(a.xhat + (s * NL + (lpend - L0)) * KX);
+#pragma unroll
+                    for (int k = 0; k < KX / 4; ++k)
+                        o[k] = make_float4(x[4 * k], x[4 * k + 1], x[4 * k + 2], x[4 * k + 3]);
+                }
+                lpend = -1;
+            };
             for (int l = L0; l < L1; ++l, ++it) {
                 const uint32_t ph = static_cast<uint32_t>(it & 1);
                 const bool trace_on = ti == 0 && (threadIdx.x == 0 || threadIdx.x == 128);
@@ -389,6 +431,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                     tc::fence_before();
                     mbar_arrive(&bars[B_VX]);
                     TRACE(1 + tb16, l);
+                    if (lpend >= 0) settle();
                     float gx[KX];
 #pragma unroll
                     for (int k = 0; k < KX; ++k) gx[k] = 0.f;
@@ -402,7 +445,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                         }
                     tc::named_bar(pair_bar, 64);
 #pragma unroll
-                    for (int k = 6; k < KX; ++k) gx[k] += sGX[(k - 6) * 128 + col];
+                    for (int k = 6; k < KX; ++k) gx[k] += sGX[k * 128 + col];
                     {
                         float hi[24], lo[24];
 #pragma unroll
@@ -446,7 +489,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                             if (c != r) part[c] = fmaf(g[e], x[r], part[c]);
                         }
 #pragma unroll
-                    for (int k = 6; k < KX; ++k) sGX[(k - 6) * 128 + col] = part[k];
+                    for (int k = 6; k < KX; ++k) sGX[k * 128 + col] = part[k];
                     tc::named_bar(pair_bar, 64);
                 }
                 TRACE(2 + tb16, l);
@@ -462,16 +505,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                     if (h == 0) TRACE(3 + tb16, l);
                     tc::fence_after();
                     const int c0 = GW * h + (isA ? 0 : EW);
-                    constexpr int NL16 = (EW + 15) / 16;
-                    uint32_t r[NL16][16];
-#pragma unroll
-                    for (int c = 0; c < NL16; ++c) tc::ld16_nw(trow + C_U1 + c0 + 16 * c, r[c]);
+                    uint32_t r[EW];
+                    tc::ld_cols_nw<EW>(trow + C_U1 + c0, r);
                     tc::wait_ld();
                     if (h == 0) TRACE(23 + (isA ? 0 : 3), l);
                     float zh[EW], zl[EW];
 #pragma unroll
                     for (int k = 0; k < EW; ++k) {
-                        const float u = __uint_as_float(r[k / 16][k % 16]);
+                        const float u = __uint_as_float(r[k]);
                         split(u > 0.f ? u : 0.f, zh[k], zl[k]);
                     }
                     st_cols<EW>(trow + C_U1 + c0, zh);
@@ -487,30 +528,30 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                 mbar_wait_guard(&bars[B_U2], ph);
                 TRACE(5 + tb16, l);
                 tc::fence_after();
+                TRACE(30 + (isA ? 0 : 1), l);
                 // bias row: landed with W23 (the MMA warp waited B_W23F before U2)
                 const float *bt = reinterpret_cast<const float *>(sm + SM_BT + (it & 1) * BT * 4);
-                long long *tr2 = (p.trace && blockIdx.x == 0 && l - L0 < 8 && trace_on && isA)
+                long long *tr2 = (TRACE_ON && p.trace && blockIdx.x == 0 && l - L0 < 8 && trace_on && isA)
                                      ? p.trace + (l - L0) * 32 + 25
                                      : nullptr;
-                if (isA) epi2_layer<false, C_U2>(trow, bt, x, v, &bars[B_E2L], tr2);
-                else epi2_layer<true, C_U2>(trow, bt, x, v, &bars[B_E2L], tr2);
                 if (isA) {
-                    float err = 0.f;
+                    epi2_layer<true, C_U2>(trow, bt, x, v, &bars[B_E2L], tr2);
 #pragma unroll
-                    for (int k = 0; k < KX; ++k) {
-                        const float d = ((xm >> k) & 1u ? 1.f : -1.f) - x[k];
-                        err = fmaf(d, d, err);
-                    }
-                    wsum += lw * static_cast<double>(err);
-                    if (a.xhat && live) {
-                        float4 *o = reinterpret_cast<float4 *>(a.xhat + (s * NL + (l - L0)) * KX);
+                    for (int k = 0; k < KX; ++k) sGX[k * 128 + col] = x[k];
+                    tc::named_bar(pair_bar, 64);
+                } else {
+                    epi2_layer<false, C_U2>(trow, bt, x, v, &bars[B_E2L], tr2);
+                    tc::named_bar(pair_bar, 64);
 #pragma unroll
-                        for (int k = 0; k < KX / 4; ++k)
-                            o[k] = make_float4(x[4 * k], x[4 * k + 1], x[4 * k + 2], x[4 * k + 3]);
-                    }
+                    for (int k = 0; k < KX; ++k) x[k] = sGX[k * 128 + col];
                 }
+                // the loss term and x_hat output of this layer are deferred until
+                // the next layer's x columns are out (they are off the critical path)
+                lpend = l;
+                lw_pend = lw;
                 TRACE(6 + tb16, l);
             }
+            if (isA && lpend >= 0) settle();
             // ---- tile end: state out, per-tile partials (A warps) ----
             if (p.x_state && live) {
                 if (isA) {
@@ -716,11 +757,11 @@ int tc_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cu
                               "M:vx", "M:w1iss", "M:zready", "M:w23iss", "M:w1f", "M:w23f", "M:g",
                               "P:u1ok", "P:u2ok", "B:prep0", "B:vx", "B:pair", "B:u1ok", "B:zarr",
                               "B:u2ok", "B:epi2end", "A:e1ld", "A:e1st", "A:e2ld", "B:e1ld",
-                              "B:e1st"};
+                              "A:e2tr2", "A:e2pre", "A:e2iss", "A:fence", "B:fence"};
         const long long t0 = h[0];
         for (int l = 0; l < 8; ++l) {
             std::fprintf(stderr, "layer %d:", l);
-            for (int e = 0; e < 28; ++e)
+            for (int e = 0; e < 32; ++e)
                 if (nm[e]) std::fprintf(stderr, " %s=%lld", nm[e], h[l * 32 + e] - t0);
             std::fprintf(stderr, "\n");
         }

@@ -99,6 +99,27 @@ __device__ __forceinline__ void ld16_nw(uint32_t taddr, uint32_t (&r)[16]) {
           "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
 }
+__device__ __forceinline__ void ld8_nw(uint32_t taddr, uint32_t *r) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                   "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void ld4_nw(uint32_t taddr, uint32_t *r) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr));
+}
+// Load N (multiple of 4) contiguous columns into r[0..N): x16 pieces, then x8, x4.
+template <int N> __device__ __forceinline__ void ld_cols_nw(uint32_t taddr, uint32_t *r) {
+#pragma unroll
+    for (int c = 0; c + 16 <= N; c += 16) ld16_nw(taddr + c, *reinterpret_cast<uint32_t(*)[16]>(r + c));
+    constexpr int c8 = N / 16 * 16;
+    if constexpr (N - c8 >= 8) ld8_nw(taddr + c8, r + c8);
+    constexpr int c4 = c8 + ((N - c8) >= 8 ? 8 : 0);
+    if constexpr (N - c4 >= 4) ld4_nw(taddr + c4, r + c4);
+    static_assert(N % 4 == 0, "column count");
+}
 __device__ __forceinline__ void wait_ld() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }

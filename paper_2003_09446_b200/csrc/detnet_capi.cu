@@ -294,8 +294,8 @@ int ensure_ws(detnet_ctx *c, long n, int K) {
     const int NG = gram_entries(K);
     if (c->gp.ensure(sizeof(float) * NG * np) || c->q32.ensure(sizeof(float) * K * np) ||
         c->denom.ensure(sizeof(double) * np) || c->xmask.ensure(sizeof(uint32_t) * np) ||
-        c->flag.ensure(np) || c->tile_loss.ensure(sizeof(double) * tiles) ||
-        c->tile_err.ensure(sizeof(long long) * tiles) || c->sing.ensure(8) ||
+        c->flag.ensure(np) || c->tile_loss.ensure(sizeof(double) * 4 * tiles) ||
+        c->tile_err.ensure(sizeof(long long) * 4 * tiles) || c->sing.ensure(8) ||
         c->result.ensure(64))
         return fail(DETNET_ERR_CUDA, "workspace allocation failed (n=%ld)", n);
     if (!c->h_result) CK(cudaMallocHost(&c->h_result, 64));
@@ -464,7 +464,7 @@ int finish(detnet_model *m, long n, detnet_eval *out) {
     {
         LaunchScope ls(c, DETNET_K_REDUCE, c->stream);
         k_reduce<<<1, 1024, 0, c->stream>>>(c->tile_loss.as<double>(), c->tile_err.as<long long>(),
-                                           tiles, c->flag.as<uint8_t>(), n, res,
+                                           4 * tiles, c->flag.as<uint8_t>(), n, res,
                                            reinterpret_cast<long long *>(res + 1),
                                            reinterpret_cast<long long *>(res + 2));
     }

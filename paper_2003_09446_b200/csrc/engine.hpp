@@ -81,8 +81,8 @@ struct TcArgs {
     int l_begin, l_end;
     long n, n_tiles, tile0;
     float *xhat;
-    double *tile_loss;
-    long long *tile_err;
+    double *tile_loss;    // [global tile][4 lane quadrants]
+    long long *tile_err;  // [global tile][4 lane quadrants]
 };
 
 int tc_prepare();

@@ -48,8 +48,8 @@ struct StackArgs {
     float *xhat;            // optional [s][l_end-l_begin][K] (s relative to this launch)
     float *x_state;         // optional [s][K] in/out
     float *v_state;         // optional [s][V] in/out
-    double *tile_loss;      // [global tile]
-    long long *tile_err;    // [global tile]
+    double *tile_loss;      // [global tile][4 lane quadrants]
+    long long *tile_err;    // [global tile][4 lane quadrants]
     // optional training trace (backward.cpp:105-165 needs in, u1 (via z), z,
     // u2 per layer), feature-major / sample-minor: [l][feature][ts]
     float *tr_in;           // [L][IN][ts]   layer input [q; x; Gx; v]
@@ -240,8 +240,11 @@ __global__ void __launch_bounds__(256, 1) k_stack_simt(StackArgs a) {
     __syncthreads();
     if ((tid & 127) == 0 && live_tile) {
         const int w0 = tid >> 5;
-        a.tile_loss[gt] = (s_loss[w0] + s_loss[w0 + 1]) + (s_loss[w0 + 2] + s_loss[w0 + 3]);
-        a.tile_err[gt] = s_err[w0] + s_err[w0 + 1] + s_err[w0 + 2] + s_err[w0 + 3];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            a.tile_loss[gt * 4 + q] = s_loss[w0 + q];
+            a.tile_err[gt * 4 + q] = s_err[w0 + q];
+        }
     }
 }
 

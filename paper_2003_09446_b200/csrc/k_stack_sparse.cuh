@@ -209,8 +209,11 @@ __global__ void __launch_bounds__(256, 1) k_stack_sparse(SparseArgs a) {
         }
         __syncthreads();
         if (tid == 0) {
-            a.tile_loss[gt] = (s_loss[0] + s_loss[1]) + (s_loss[2] + s_loss[3]);
-            a.tile_err[gt] = s_err[0] + s_err[1] + s_err[2] + s_err[3];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                a.tile_loss[gt * 4 + q] = s_loss[q];
+                a.tile_err[gt * 4 + q] = s_err[q];
+            }
         }
         __syncthreads();
     }

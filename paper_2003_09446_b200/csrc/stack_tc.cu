@@ -570,15 +570,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                 if (!live) errs = 0;
                 loss = warp_sum(loss);
                 errs = warp_sum(errs);
-                double *rl = reinterpret_cast<double *>(sm + SM_RED);
-                long long *re = reinterpret_cast<long long *>(sm + SM_RED + 64);
-                if (lane == 0) { rl[quad] = loss; re[quad] = errs; }
-                tc::named_bar(5, 128);
-                if (threadIdx.x == 0) {
-                    a.tile_loss[gt] = (rl[0] + rl[1]) + (rl[2] + rl[3]);
-                    a.tile_err[gt] = re[0] + re[1] + re[2] + re[3];
+                if (lane == 0) { // per lane-quadrant partials, summed in a fixed order later
+                    a.tile_loss[gt * 4 + quad] = loss;
+                    a.tile_err[gt * 4 + quad] = errs;
                 }
-                tc::named_bar(5, 128);
             }
         }
     }

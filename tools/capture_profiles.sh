@@ -1,0 +1,31 @@
+#!/bin/bash
+# Round profile capture on one B200 (run under gpurun from the repo root).
+# Each ncu pass runs only after the same command has exited 0 without ncu.
+# Outputs land in gpurun_out/prof/; tools/summarize_profiles.py turns them
+# into the text summaries committed under profiles/.
+set -u
+OUT=gpurun_out/prof
+mkdir -p $OUT
+# 1. benches (no profiler)
+for c in 1 2 3 4 5; do
+  timeout 600 python bench.py --config $c --steps 5 --warmup 3 > $OUT/bench_c$c.json 2> $OUT/bench_c$c.err
+done
+timeout 600 python bench.py --impl reference > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+# 2. launch list of the default bench command (per-launch durations, cold, serialised)
+if timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > $OUT/plain.json 2>&1; then
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+    --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > $OUT/ncu_launch.log 2>&1
+fi
+# 3. one full capture per hot kernel (2^18 detections, config-2 workload)
+if timeout 300 python tools/prof_run.py 262144 > $OUT/prof_run.log 2>&1; then
+  for k in k_stack_tc k_prep_stream; do
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
+      -o $OUT/$k python tools/prof_run.py 262144 > $OUT/ncu_$k.log 2>&1
+  done
+fi
+# 4. the compacted (config-3) stack kernel and the training kernels
+if timeout 300 python tools/prof_run.py 262144 0 3 > $OUT/prof_run3.log 2>&1; then
+  timeout 900 ncu --set full --clock-control none -k regex:k_stack_tc -s 1 -c 1 \
+    -o $OUT/k_stack_tc48 python tools/prof_run.py 262144 0 3 > $OUT/ncu_tc48.log 2>&1
+fi
+echo done

@@ -1,5 +1,6 @@
 """Profiling driver: one detnet_batch_evaluate_device over n samples of the
-config-2 workload (L=40) after a warm-up call. Used under ncu."""
+config-2 workload (L=40; argv[3] = 3: config-3 group masks) after a warm-up
+call. Used under ncu. argv: n [path [config]]."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -7,9 +8,15 @@ import paper_2003_09446_b200 as eng
 from paper_2003_09446_b200.workload import xavier_params
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 18
 path = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+config = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 K, N, L = 20, 30, 40
 ctx = eng.Context(0, path=path)
-m = ctx.model(K, N, 160, 40, xavier_params(K, L, seed=9))
+params = xavier_params(K, L, seed=9)
+masks = None
+if config == 3:  # group-pruned (compacted tcgen05 kernel)
+    from paper_2003_09446_b200.workload import group_masks
+    masks = group_masks(K, L, seed=31)
+m = ctx.model(K, N, 160, 40, params, masks=masks)
 H = torch.empty((n, N, K), dtype=torch.float32, device="cuda")
 y = torch.empty((n, N), dtype=torch.float32, device="cuda")
 x = torch.empty((n, K), dtype=torch.int8, device="cuda")

@@ -98,6 +98,14 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
 
+    def prime(self, fn, max_s=3.0):
+        """Short timed regions end before nvidia-smi's first report: keep the
+        GPU busy with untimed steps until the sampler has produced a row, so
+        the clocks reported are sampled under this workload."""
+        t_end = time.time() + max_s
+        while self.proc and not self.rows and time.time() < t_end:
+            fn()
+
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -291,6 +299,9 @@ def main():
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        clk.prime(lambda: (step_device(), torch.cuda.synchronize()))
+        barrier()
+        torch.cuda.synchronize()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record()
@@ -409,6 +420,10 @@ def run_train_bench(args, torch, dist, world, rank, local, barrier, eng):
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        # priming runs the local gradient only: no collective, no parameter update
+        clk.prime(lambda: (model.train_grad(per_gpu, *batches[0], raw), torch.cuda.synchronize()))
+        barrier()
+        torch.cuda.synchronize()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record()

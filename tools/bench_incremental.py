@@ -1,0 +1,48 @@
+"""SURVEY 8f row 2 measurement: the reference's train_incremental running on
+the B200 seam vs on the reference's own OpenMP kernels (same box, same
+arguments). Prints one JSON line per schedule; wall-clock includes context
+creation, generation, validation and checkpoint round trip (the whole
+controller), and the marginal per-optimizer-step time from two run lengths."""
+import json
+import os
+import subprocess
+import sys
+import tempfile
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+B = os.path.join(ROOT, "oracle", "_ref", "incremental_b200")
+R = os.path.join(ROOT, "oracle", "_ref", "incremental_ref")
+
+
+def run(binary, args):
+    with tempfile.TemporaryDirectory() as td:
+        out = subprocess.run([binary, *map(str, args), os.path.join(td, "ck.json")],
+                             capture_output=True, text=True, timeout=1800)
+    if out.returncode:
+        raise SystemExit(out.stderr + out.stdout)
+    return json.loads(out.stdout)
+
+
+def main():
+    # (label, K, N, start, t_step, max_layers, batches_short, batches_long, batch, val)
+    cases = [("whole-network L=40 (config-5 dims)", 20, 30, 40, 10, 40, 4, 12, 5000, 2000),
+             ("incremental 10->40 by 10", 20, 30, 10, 10, 40, 2, 6, 5000, 2000)]
+    for label, K, N, s0, ts, mx, b1, b2, bs, val in cases:
+        res = {}
+        for name, binary in (("b200", B), ("reference", R)):
+            a = run(binary, [K, N, s0, ts, mx, b1, bs, val, 3])
+            c = run(binary, [K, N, s0, ts, mx, b2, bs, val, 3])
+            per_step = (c["seconds"] - a["seconds"]) / (c["optimizer_steps"] - a["optimizer_steps"])
+            res[name] = {"seconds_long": c["seconds"], "optimizer_steps_long": c["optimizer_steps"],
+                         "marginal_ms_per_optimizer_step": per_step * 1e3,
+                         "samples_per_s_marginal": bs / per_step,
+                         "final_val_loss": c["steps"][-1]["val_loss"],
+                         "final_val_ber": c["steps"][-1]["val_ber"]}
+        print(json.dumps({"case": label, "batch": bs, "cores_reference": os.cpu_count(), **res,
+                          "speedup_marginal": res["reference"]["marginal_ms_per_optimizer_step"] /
+                          res["b200"]["marginal_ms_per_optimizer_step"]}))
+        sys.stdout.flush()
+
+
+if __name__ == "__main__":
+    main()

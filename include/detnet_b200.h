@@ -187,6 +187,18 @@ int detnet_generate_host(detnet_ctx *ctx, uint64_t base, long first, long count,
                          int n_tx, double snr_lo_db, double snr_hi_db, double *H, double *x,
                          double *y, double *sigma2);
 
+/* Detector baselines on the device: replaces
+ * batch_baseline_errors (kernels.hpp:48-49; kernels.cpp:105-112, 202-223).
+ * kind 0 = ZF (sign of solve_normal_equations(gram(H), H^T y)),
+ * 1 = ML (exhaustive, K <= 16; DETNET_ERR_UNSUPPORTED otherwise, the
+ * reference's CapacityError), 2 = oracle (0 errors). Host FP64 samples in the
+ * reference layout (H [n][N][K], y [n][N], x [n][K] as +-1.0); decisions are
+ * bit-identical to the reference. A singular ZF system returns
+ * DETNET_ERR_SINGULAR (SingularMatrixError, linalg.cpp:59-60). */
+int detnet_batch_baseline_errors(detnet_ctx *ctx, int kind, long n, int n_rx, int n_tx,
+                                 const double *H, const double *y, const double *x,
+                                 long long *errors, long long *symbols);
+
 #ifdef __cplusplus
 }
 #endif

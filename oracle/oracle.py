@@ -276,6 +276,8 @@ class RefLib:
                                          C.c_int, _dp, _lp]
         L.ref_forward.argtypes = [C.POINTER(_Model), _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
         L.ref_zf_decode.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp]
+        L.ref_baseline_errors.argtypes = [C.c_int, C.c_long, C.c_int, C.c_int, _dp, _dp, _dp,
+                                          C.c_int, _lp, _lp]
         L.ref_batch_gradient.argtypes = [C.POINTER(_Model), C.c_long, _dp, _dp, _dp,
                                          C.POINTER(_LossSpec), C.c_int, C.c_int, _dp, _dp, _lp]
         L.ref_regularizer.restype = C.c_double
@@ -317,6 +319,15 @@ class RefLib:
                                          _ptr(o3, _lp))
         return dict(status=st, data_loss=dl.value, symbol_errors=int(o3[0]), symbols=int(o3[1]),
                     flagged=int(o3[2]))
+
+    def baseline_errors(self, kind, H, y, x, parallel=True):
+        """batch_baseline_errors (kernels.cpp:202-223): kind 0 zf, 1 ml, 2 oracle.
+        Returns (status, errors, symbols)."""
+        H, y, x = (np.ascontiguousarray(a, np.float64) for a in (H, y, x))
+        e, s = C.c_longlong(), C.c_longlong()
+        st = self.lib.ref_baseline_errors(kind, H.shape[0], H.shape[1], H.shape[2], _ptr(H), _ptr(y),
+                                          _ptr(x), int(parallel), C.byref(e), C.byref(s))
+        return st, e.value, s.value
 
     def forward(self, m: Model, H, y):
         cm = m.c()

@@ -166,6 +166,7 @@ template <class F> int guarded(F &&f) {
     } catch (const ContractError &e) { g_msg = e.what(); return 1; }
     catch (const SingularMatrixError &e) { g_msg = e.what(); return 2; }
     catch (const ConfigError &e) { g_msg = e.what(); return 3; }
+    catch (const CapacityError &e) { g_msg = e.what(); return 6; }
     catch (const std::exception &e) { g_msg = e.what(); return 9; }
 }
 
@@ -251,6 +252,18 @@ int ref_zf_decode(int n_rx, int n_tx, const double *H, const double *y, double *
         std::memcpy(Hm.data.data(), H, sizeof(double) * n_rx * n_tx);
         const Vec r = zf_decode(Hm, Vec(y, y + n_rx));
         std::memcpy(out, r.data(), sizeof(double) * n_tx);
+    });
+}
+
+// batch_baseline_errors (kernels.cpp:202-223) / ref:: twin; kind 0 zf, 1 ml, 2 oracle
+int ref_baseline_errors(int kind, long n, int n_rx, int n_tx, const double *H, const double *y,
+                        const double *x, int parallel, long long *errors, long long *symbols) {
+    return guarded([&] {
+        const auto batch = to_samples(n_rx, n_tx, n, H, y, x);
+        const BaselineKind k = kind == 0 ? BaselineKind::zf : (kind == 1 ? BaselineKind::ml : BaselineKind::oracle);
+        const auto r = parallel ? batch_baseline_errors(batch, k) : ref::batch_baseline_errors(batch, k);
+        *errors = r.first;
+        *symbols = r.second;
     });
 }
 

@@ -11,6 +11,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -20,6 +21,7 @@
 #include "common.cuh"
 #include "k_generate.cuh"
 #include "k_preprocess.cuh"
+#include "k_baseline.cuh"
 #include "k_prep_fast.cuh"
 #include "k_stack_sparse.cuh"
 #include "k_stack_simt.cuh"
@@ -498,6 +500,33 @@ int reset_sing(detnet_ctx *c, cudaStream_t st) {
 } // namespace detnet
 
 // =========================================================================
+// ---- detector baselines -------------------------------------
+namespace {
+using BaseFn = void (*)(int kind, int blocks, size_t smem, cudaStream_t st, long n, int N,
+                        const double *H, const double *y, const double *x, int *errs,
+                        unsigned long long *sing);
+template <int K>
+void launch_baseline(int kind, int blocks, size_t smem, cudaStream_t st, long n, int N,
+                     const double *H, const double *y, const double *x, int *errs,
+                     unsigned long long *sing) {
+    if (kind == 0) {
+        cudaFuncSetAttribute(k_zf_errors<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        k_zf_errors<K><<<blocks, 256, smem, st>>>(n, N, H, y, x, errs, sing);
+    } else if constexpr (K <= 16) {
+        cudaFuncSetAttribute(k_ml_errors<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        k_ml_errors<K><<<blocks, 256, smem, st>>>(n, N, H, y, x, errs);
+    }
+}
+template <int... Ks> constexpr BaseFn base_table(int K, std::integer_sequence<int, Ks...>) {
+    BaseFn f = nullptr;
+    ((K == Ks + 1 ? (f = launch_baseline<Ks + 1>, 0) : 0), ...);
+    return f;
+}
+} // namespace
+
+
 extern "C" {
 
 const char *detnet_last_error(void) { return g_err.c_str(); }
@@ -834,6 +863,69 @@ int detnet_generate_host(detnet_ctx *c, uint64_t base, long first, long count, i
     buf.release();
     if (e != cudaSuccess) return fail(DETNET_ERR_CUDA, "generate_host: %s", cudaGetErrorString(e));
     drain_times(c);
+    return 0;
+}
+
+
+int detnet_batch_baseline_errors(detnet_ctx *c, int kind, long n, int n_rx, int n_tx,
+                                 const double *H, const double *y, const double *x,
+                                 long long *errors, long long *symbols) {
+    if (!c || !errors || !symbols) return fail(DETNET_ERR_CONTRACT, "null argument");
+    if (n < 0) return fail(DETNET_ERR_CONTRACT, "batch_baseline_errors: negative batch size");
+    *errors = 0;
+    *symbols = n * static_cast<long long>(n_tx);
+    if (kind == 2 || n == 0) return 0; // oracle baseline: no errors (kernels.cpp:105-106)
+    if (kind != 0 && kind != 1) return fail(DETNET_ERR_CONTRACT, "baseline kind must be 0 (zf), 1 (ml) or 2");
+    if (!H || !y || !x) return fail(DETNET_ERR_CONTRACT, "null argument");
+    if (n_tx < 1 || n_rx < n_tx) return fail(DETNET_ERR_CONTRACT, "baseline: need N >= K >= 1");
+    if (kind == 1 && n_tx > 16)
+        return fail(DETNET_ERR_UNSUPPORTED, "ml_decode: exhaustive search limited to K <= 16");
+    const BaseFn fn = base_table(n_tx, std::make_integer_sequence<int, 20>{});
+    if (!fn) return fail(DETNET_ERR_UNSUPPORTED, "baseline: K = %d not instantiated (K <= 20)", n_tx);
+    CK(cudaSetDevice(c->device));
+    const long chunk = std::min<long>(n, 1L << 16);
+    const size_t nh = static_cast<size_t>(chunk) * n_rx * n_tx, ny = static_cast<size_t>(chunk) * n_rx,
+                 nx = static_cast<size_t>(chunk) * n_tx;
+    DBuf buf;
+    if (buf.ensure(sizeof(double) * (nh + ny + nx) + sizeof(int) * chunk + 16))
+        return fail(DETNET_ERR_CUDA, "baseline buffer allocation failed");
+    double *dH = buf.as<double>(), *dy = dH + nh, *dx = dy + ny;
+    int *de = reinterpret_cast<int *>(dx + nx);
+    unsigned long long *ds = reinterpret_cast<unsigned long long *>(de + chunk + (chunk & 1));
+    const size_t smem = sizeof(double) * 8 *
+                        (static_cast<size_t>(n_rx) * n_tx + n_rx + n_tx * n_tx + n_tx);
+    std::vector<int> he(chunk);
+    long long total = 0;
+    for (long s0 = 0; s0 < n; s0 += chunk) {
+        const long cnt = std::min(chunk, n - s0);
+        CK(cudaMemcpyAsync(dH, H + s0 * n_rx * n_tx, sizeof(double) * cnt * n_rx * n_tx,
+                           cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(dy, y + s0 * n_rx, sizeof(double) * cnt * n_rx, cudaMemcpyHostToDevice,
+                           c->stream));
+        CK(cudaMemcpyAsync(dx, x + s0 * n_tx, sizeof(double) * cnt * n_tx, cudaMemcpyHostToDevice,
+                           c->stream));
+        CK(cudaMemsetAsync(ds, 0xff, 8, c->stream));
+        const int blocks = static_cast<int>(std::min<long>((cnt + 7) / 8, 148L * 16));
+        {
+            LaunchScope ls(c, DETNET_K_OTHER, c->stream);
+            fn(kind, blocks, smem, c->stream, cnt, n_rx, dH, dy, dx, de, ds);
+        }
+        if (int rc = check_launch()) { buf.release(); return rc; }
+        unsigned long long sing = ~0ull;
+        CK(cudaMemcpyAsync(he.data(), de, sizeof(int) * cnt, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(&sing, ds, 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (sing != ~0ull) {
+            buf.release();
+            return fail(DETNET_ERR_SINGULAR,
+                        "solve_normal_equations: matrix is singular to working precision (sample %llu)",
+                        static_cast<unsigned long long>(s0) + sing);
+        }
+        for (long i = 0; i < cnt; ++i) total += he[i]; // sample order
+    }
+    buf.release();
+    drain_times(c);
+    *errors = total;
     return 0;
 }
 

@@ -13,10 +13,7 @@
 // product of two FP32 values is exact in FP64, so acc + a*b may use DFMA.)
 // The layer stack consumes FP32 roundings of q and G.
 //
-// LU layout: lane r < K owns row r of [G | q] in registers; row swaps are
-// tracked as a position permutation (pos), reproducing the reference's
-// first-strict-maximum pivot choice over positions; every row lane
-// eliminates its own row with one parallel division per column.
+// LU: warp_solve_normal below (one row per lane, parallel elimination).
 //
 // Outputs (tile SoA, TILE samples per tile):
 //   gp  [tile][K(K+1)/2][TILE]  packed upper triangle of G (row-major a<=b)
@@ -29,6 +26,68 @@
 
 namespace detnet {
 
+// solve_normal_equations (linalg.cpp:44-79) on one warp: LU with partial
+// pivoting of [G | q] in FP64 with the reference's operation order. Lane
+// r < K owns row r in registers; row swaps are tracked as a position
+// permutation (pos), reproducing the reference's first-strict-maximum pivot
+// choice over positions. Returns true if the pivot test (<= 1e-12 max|G|)
+// fails; otherwise xs (replicated on every lane) = G^-1 q.
+template <int K>
+__device__ __forceinline__ bool warp_solve_normal(const double *sG, const double *sq, int lane,
+                                                  double (&xs)[K]) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const bool rl = lane < K;
+    double row[K + 1];
+#pragma unroll
+    for (int j = 0; j < K; ++j) row[j] = rl ? sG[lane * K + j] : 0.0;
+    row[K] = rl ? sq[lane] : 0.0;
+    double gmax = 0.0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) gmax = fmax(gmax, fabs(row[j]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) gmax = fmax(gmax, __shfl_xor_sync(FULL, gmax, o));
+    const double tol = dmul(1e-12, gmax);
+
+    int pos = rl ? lane : 1000 + lane;
+#pragma unroll
+    for (int cc = 0; cc < K; ++cc) {
+        // pivot: max |A(p, cc)| over positions p >= cc, lowest position on ties
+        double bv = (rl && pos >= cc) ? fabs(row[cc]) : -1.0;
+        int bp = (rl && pos >= cc) ? pos : 1 << 20;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(FULL, bv, o);
+            const int op = __shfl_xor_sync(FULL, bp, o);
+            if (ov > bv || (ov == bv && op < bp)) { bv = ov; bp = op; }
+        }
+        if (bv <= tol) return true;
+        const int pl = __ffs(__ballot_sync(FULL, pos == bp)) - 1;
+        const int cl = __ffs(__ballot_sync(FULL, pos == cc)) - 1;
+        if (lane == cl) pos = bp;
+        if (lane == pl) pos = cc;
+        double pr[K + 1];
+#pragma unroll
+        for (int j = cc; j <= K; ++j) pr[j] = __shfl_sync(FULL, row[j], pl);
+        if (rl && pos > cc) {
+            const double f = ddiv(row[cc], pr[cc]);
+            if (f != 0.0) {
+#pragma unroll
+                for (int j = cc; j <= K; ++j) row[j] = dsub(row[j], dmul(f, pr[j]));
+            }
+        }
+    }
+#pragma unroll
+    for (int i = K - 1; i >= 0; --i) {
+        double acc = row[K];
+#pragma unroll
+        for (int j = i + 1; j < K; ++j) acc = dsub(acc, dmul(row[j], xs[j]));
+        const double xi = ddiv(acc, row[i]);
+        const int li = __ffs(__ballot_sync(FULL, pos == i)) - 1;
+        xs[i] = __shfl_sync(FULL, xi, li);
+    }
+    return false;
+}
+
 template <int K>
 __global__ void __launch_bounds__(256)
     k_preprocess(long n, int N, const float *__restrict__ H, const float *__restrict__ y,
@@ -38,7 +97,6 @@ __global__ void __launch_bounds__(256)
                  const long *__restrict__ list, const int *__restrict__ list_count) {
     static_assert(K <= 32, "one lane per row");
     constexpr int NG = gram_entries(K);
-    constexpr unsigned FULL = 0xffffffffu;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int warps = blockDim.x >> 5;
@@ -79,63 +137,9 @@ __global__ void __launch_bounds__(256)
         }
         __syncwarp();
 
-        const bool rl = lane < K;
-        double row[K + 1];
-#pragma unroll
-        for (int j = 0; j < K; ++j) row[j] = rl ? sG[lane * K + j] : 0.0;
-        row[K] = rl ? sq[lane] : 0.0;
-        double gmax = 0.0;
-#pragma unroll
-        for (int j = 0; j < K; ++j) gmax = fmax(gmax, fabs(row[j]));
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) gmax = fmax(gmax, __shfl_xor_sync(FULL, gmax, o));
-        const double tol = dmul(1e-12, gmax);
-
-        int pos = rl ? lane : 1000 + lane;
-        bool sing = false;
-#pragma unroll
-        for (int cc = 0; cc < K; ++cc) {
-            if (!sing) {
-                // pivot: max |A(p, cc)| over positions p >= cc, lowest position on ties
-                double bv = (rl && pos >= cc) ? fabs(row[cc]) : -1.0;
-                int bp = (rl && pos >= cc) ? pos : 1 << 20;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const double ov = __shfl_xor_sync(FULL, bv, o);
-                    const int op = __shfl_xor_sync(FULL, bp, o);
-                    if (ov > bv || (ov == bv && op < bp)) { bv = ov; bp = op; }
-                }
-                if (bv <= tol) {
-                    sing = true;
-                } else {
-                    const int pl = __ffs(__ballot_sync(FULL, pos == bp)) - 1;
-                    const int cl = __ffs(__ballot_sync(FULL, pos == cc)) - 1;
-                    if (lane == cl) pos = bp;
-                    if (lane == pl) pos = cc;
-                    double pr[K + 1];
-#pragma unroll
-                    for (int j = cc; j <= K; ++j) pr[j] = __shfl_sync(FULL, row[j], pl);
-                    if (rl && pos > cc) {
-                        const double f = ddiv(row[cc], pr[cc]);
-                        if (f != 0.0) {
-#pragma unroll
-                            for (int j = cc; j <= K; ++j) row[j] = dsub(row[j], dmul(f, pr[j]));
-                        }
-                    }
-                }
-            }
-        }
+        double xs[K];
+        const bool sing = warp_solve_normal<K>(sG, sq, lane, xs);
         if (!sing) {
-            double xs[K];
-#pragma unroll
-            for (int i = K - 1; i >= 0; --i) {
-                double acc = row[K];
-#pragma unroll
-                for (int j = i + 1; j < K; ++j) acc = dsub(acc, dmul(row[j], xs[j]));
-                const double xi = ddiv(acc, row[i]);
-                const int li = __ffs(__ballot_sync(FULL, pos == i)) - 1;
-                xs[i] = __shfl_sync(FULL, xi, li);
-            }
             if (lane == 0) {
                 const int8_t *xv = x + s * K;
                 uint32_t mask = 0;

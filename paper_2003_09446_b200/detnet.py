@@ -126,6 +126,9 @@ _lib.detnet_train_grad.argtypes = [_vp, C.c_long, _vp, _vp, _vp, C.c_int, _vp, C
 _lib.detnet_train_apply.argtypes = [_vp, _vp, C.c_long, C.POINTER(_LossSpec), C.POINTER(_AdamCfg)]
 _lib.detnet_model_get_params.argtypes = [_vp, _vp]
 _lib.detnet_model_reset_adam.argtypes = [_vp]
+_lib.detnet_batch_baseline_errors.argtypes = [_vp, C.c_int, C.c_long, C.c_int, C.c_int, _vp, _vp,
+                                               _vp, C.POINTER(C.c_longlong),
+                                               C.POINTER(C.c_longlong)]
 _lib.detnet_generate_host.argtypes = [_vp, C.c_uint64, C.c_long, C.c_long, C.c_int, C.c_int,
                                       C.c_double, C.c_double, _vp, _vp, _vp, _vp]
 _lib.detnet_rng_seed.restype = C.c_uint64
@@ -235,6 +238,17 @@ class Context:
         _check(_lib.detnet_generate_host(self._h, base_state, first, count, n_rx, n_tx, snr_lo,
                                          snr_hi, _addr(H), _addr(x), _addr(y), _addr(s2)))
         return H, x, y, s2
+
+    def baseline_errors(self, kind, H, y, x):
+        """Detector baselines (batch_baseline_errors, kernels.cpp:202-223) on the
+        device: kind 0 = ZF, 1 = ML (K <= 16), 2 = oracle; FP64 host samples in
+        the reference layout. Returns (errors, symbols)."""
+        H, y, x = (np.ascontiguousarray(a, np.float64) for a in (H, y, x))
+        e, s = C.c_longlong(), C.c_longlong()
+        _check(_lib.detnet_batch_baseline_errors(self._h, int(kind), H.shape[0], H.shape[1],
+                                                 H.shape[2], _addr(H), _addr(y), _addr(x),
+                                                 C.byref(e), C.byref(s)))
+        return e.value, s.value
 
     def adam_step(self, n_tx, z_dim, v_dim, depth, frozen_prefix, params, masks, grads, m1, m2,
                   step, lr0=1e-4, decay_factor=0.97, decay_step=1000, beta1=0.9, beta2=0.999,

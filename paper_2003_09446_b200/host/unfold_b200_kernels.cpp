@@ -42,6 +42,7 @@ namespace {
     case DETNET_ERR_CONTRACT: throw ContractError(msg);
     case DETNET_ERR_SINGULAR: throw SingularMatrixError(msg);
     case DETNET_ERR_CONFIG: throw ConfigError(msg);
+    case DETNET_ERR_UNSUPPORTED: throw CapacityError(msg);
     default: throw std::runtime_error("detnet_b200: " + msg);
     }
 }
@@ -262,10 +263,39 @@ BatchEval batch_gradient(const ModelParams &params, std::span<const ChannelSampl
     return to_eval(ev);
 }
 
-// ZF/ML/oracle baselines are not on the GPU path; they call
-// the reference's own zf_decode/ml_decode (channel.cpp) per sample.
+// ZF/ML/oracle baselines on the device: FP64 samples cross
+// as-is and the kernels keep the reference's operation order, so the counts are
+// bit-identical (tests/test_baseline_gpu.py). The device instantiates K <= 20;
+// wider K keeps the reference's own per-sample decoders (channel.cpp).
 std::pair<long long, long long> batch_baseline_errors(std::span<const ChannelSample> batch,
                                                       BaselineKind kind) {
+    if (batch.empty() || kind == BaselineKind::oracle) {
+        long long symbols = 0;
+        for (const ChannelSample &s : batch) symbols += static_cast<long long>(s.x.size());
+        return {0, symbols};
+    }
+    const int N = batch[0].H.rows, K = batch[0].H.cols;
+    if (kind == BaselineKind::ml && K > 16)
+        throw CapacityError("ml_decode: exhaustive search limited to K <= 16");
+    if (K <= 20) {
+        const size_t n = batch.size();
+        std::vector<double> H(n * N * K), y(n * N), x(n * K);
+        for (size_t i = 0; i < n; ++i) {
+            const ChannelSample &c = batch[i];
+            if (c.H.rows != N || c.H.cols != K || static_cast<int>(c.y.size()) != N ||
+                static_cast<int>(c.x.size()) != K)
+                throw ContractError("batch sample shape does not match");
+            std::memcpy(H.data() + i * N * K, c.H.data.data(), sizeof(double) * N * K);
+            std::memcpy(y.data() + i * N, c.y.data(), sizeof(double) * N);
+            std::memcpy(x.data() + i * K, c.x.data(), sizeof(double) * K);
+        }
+        long long errors = 0, symbols = 0;
+        std::lock_guard<std::mutex> lk(engine().mu);
+        check(detnet_batch_baseline_errors(engine().ctx, kind == BaselineKind::zf ? 0 : 1,
+                                           static_cast<long>(n), N, K, H.data(), y.data(), x.data(),
+                                           &errors, &symbols));
+        return {errors, symbols};
+    }
     long long errors = 0, symbols = 0;
     for (const ChannelSample &s : batch) {
         errors += baseline_errors_one(s, kind);

@@ -1,0 +1,41 @@
+"""SURVEY 8f row 4 measurement: ZF / ML detector baselines on the device
+(detnet_batch_baseline_errors, host FP64 samples in, counts out -- the
+transfer is inside the timing) vs the reference's batch_baseline_errors
+(OpenMP, all host cores) on the same samples. One JSON line per case."""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import paper_2003_09446_b200 as eng  # noqa: E402
+from oracle.oracle import Oracle, RefLib  # noqa: E402
+
+
+def timed(f, reps):
+    f()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        out = f()
+    return (time.perf_counter() - t0) / reps, out
+
+
+def main():
+    orc, ref, ctx = Oracle(), RefLib(), eng.Context(0)
+    cases = [("zf", 0, 20, 30, 1 << 16), ("ml", 1, 8, 16, 1 << 14), ("ml", 1, 12, 16, 1 << 11)]
+    for name, kind, K, N, n in cases:
+        H, x, y, _ = orc.generate_batch(orc.rng(3, 0), N, K, n, 0.0, 12.0)
+        tg, (eg, sg) = timed(lambda: ctx.baseline_errors(kind, H, y, x), 5)
+        tr, (st, er, sr) = timed(lambda: ref.baseline_errors(kind, H, y, x), 2)
+        assert st == 0 and (eg, sg) == (er, sr), (eg, er)
+        print(json.dumps({"baseline": name, "K": K, "N": N, "samples": n,
+                          "b200_detections_per_s": n / tg, "reference_detections_per_s": n / tr,
+                          "reference_cores": ref.worker_count(), "speedup": tr / tg,
+                          "errors": eg, "symbols": sg, "identical_counts": True}))
+        sys.stdout.flush()
+
+
+if __name__ == "__main__":
+    main()

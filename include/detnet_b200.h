@@ -195,6 +195,29 @@ int detnet_generate_host(detnet_ctx *ctx, uint64_t base, long first, long count,
  * reference layout (H [n][N][K], y [n][N], x [n][K] as +-1.0); decisions are
  * bit-identical to the reference. A singular ZF system returns
  * DETNET_ERR_SINGULAR (SingularMatrixError, linalg.cpp:59-60). */
+/* Pruning planner on the device-resident master weights:
+ * replaces prune / prune_element / prune_group / prune_sparse_group
+ * (compression.hpp; compression.cpp:43-94) with bit-identical masks.
+ * kind 0 = element(eta), 1 = group(eta1), 2 = sparse_group(eta1, eta2);
+ * thresholds in [0, 1) (else DETNET_ERR_CONFIG, PruneSpec::validate). The
+ * packed layouts (dense / compacted tcgen05 / sparse) are rebuilt from the
+ * result; Adam state is kept. */
+int detnet_model_prune(detnet_model *model, int kind, double eta, double eta1, double eta2);
+/* Current masks in the layer-record layout (ones where unmasked). */
+int detnet_model_get_masks(detnet_model *model, double *masks_out);
+
+/* cost_report (compression.hpp CostReport/LayerCost; compression.cpp:131-159). */
+typedef struct {
+    long long params_total, params_nonzero, flops;
+} detnet_layer_cost;
+typedef struct {
+    int layer_count;
+    long long params_total, params_nonzero, memory_dense_bytes, memory_sparse_bytes, flops,
+        flops_dense, preprocess_flops;
+} detnet_cost_report;
+int detnet_model_cost_report(detnet_model *model, detnet_cost_report *report,
+                             detnet_layer_cost *per_layer /* [depth] or NULL */);
+
 int detnet_batch_baseline_errors(detnet_ctx *ctx, int kind, long n, int n_rx, int n_tx,
                                  const double *H, const double *y, const double *x,
                                  long long *errors, long long *symbols);

@@ -276,6 +276,8 @@ class RefLib:
                                          C.c_int, _dp, _lp]
         L.ref_forward.argtypes = [C.POINTER(_Model), _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
         L.ref_zf_decode.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp]
+        L.ref_prune.argtypes = [C.POINTER(_Model), C.c_int, C.c_double, C.c_double, C.c_double, _dp]
+        L.ref_cost_report.argtypes = [C.POINTER(_Model), _lp, _lp]
         L.ref_baseline_errors.argtypes = [C.c_int, C.c_long, C.c_int, C.c_int, _dp, _dp, _dp,
                                           C.c_int, _lp, _lp]
         L.ref_batch_gradient.argtypes = [C.POINTER(_Model), C.c_long, _dp, _dp, _dp,
@@ -319,6 +321,22 @@ class RefLib:
                                          _ptr(o3, _lp))
         return dict(status=st, data_loss=dl.value, symbol_errors=int(o3[0]), symbols=int(o3[1]),
                     flagged=int(o3[2]))
+
+    def prune(self, m: Model, kind, eta=0.0, eta1=0.0, eta2=0.0):
+        """prune (compression.cpp:87-94); returns the masks in record layout."""
+        cm = m.c()
+        out = np.zeros((m.depth, record_size(m.n_tx, m.z_dim, m.v_dim)))
+        self._check(self.lib.ref_prune(C.byref(cm), kind, eta, eta1, eta2, _ptr(out)))
+        return out
+
+    def cost_report(self, m: Model):
+        cm = m.c()
+        o8 = np.zeros(8, np.int64)
+        pl = np.zeros((m.depth, 3), np.int64)
+        self._check(self.lib.ref_cost_report(C.byref(cm), _ptr(o8, _lp), _ptr(pl, _lp)))
+        keys = ("layer_count", "params_total", "params_nonzero", "memory_dense_bytes",
+                "memory_sparse_bytes", "flops", "flops_dense", "preprocess_flops")
+        return dict(zip(keys, map(int, o8))), pl
 
     def baseline_errors(self, kind, H, y, x, parallel=True):
         """batch_baseline_errors (kernels.cpp:202-223): kind 0 zf, 1 ml, 2 oracle.

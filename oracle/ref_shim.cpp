@@ -267,6 +267,48 @@ int ref_baseline_errors(int kind, long n, int n_rx, int n_tx, const double *H, c
     });
 }
 
+// prune (compression.cpp:87-94): masks out in the record layout (t slot 1)
+int ref_prune(const ref_model *m, int kind, double eta, double eta1, double eta2, double *masks_out) {
+    return guarded([&] {
+        ModelParams p = to_params(*m);
+        PruneSpec spec;
+        spec.kind = kind == 0 ? PruneKind::element : (kind == 1 ? PruneKind::group : PruneKind::sparse_group);
+        spec.eta = eta;
+        spec.eta1 = eta1;
+        spec.eta2 = eta2;
+        prune(p, spec);
+        const long P = record_size(m->n_tx, m->z_dim, m->v_dim);
+        for (int l = 0; l < p.depth(); ++l) {
+            double *r = masks_out + l * P;
+            const LayerParams &lp = p.layers[l];
+            long off = 0;
+            auto put = [&](const std::vector<double> &v) {
+                std::memcpy(r + off, v.data(), sizeof(double) * v.size());
+                off += (long)v.size();
+            };
+            put(lp.M1.data); put(lp.mb1); put(lp.M2.data); put(lp.mb2); put(lp.M3.data); put(lp.mb3);
+            r[off] = 1.0;
+        }
+    });
+}
+
+// cost_report (compression.cpp:131-159): out8 = {layer_count, params_total,
+// params_nonzero, memory_dense, memory_sparse, flops, flops_dense, preprocess};
+// per_layer [L][3] = {params_total, params_nonzero, flops}
+int ref_cost_report(const ref_model *m, long long *out8, long long *per_layer) {
+    return guarded([&] {
+        const CostReport r = cost_report(to_params(*m));
+        const long long v[8] = {r.layer_count, r.params_total, r.params_nonzero, r.memory_dense_bytes,
+                                r.memory_sparse_bytes, r.flops, r.flops_dense, r.preprocess_flops};
+        std::memcpy(out8, v, sizeof v);
+        for (size_t l = 0; l < r.per_layer.size(); ++l) {
+            per_layer[3 * l] = r.per_layer[l].params_total;
+            per_layer[3 * l + 1] = r.per_layer[l].params_nonzero;
+            per_layer[3 * l + 2] = r.per_layer[l].flops;
+        }
+    });
+}
+
 // batch_gradient (kernels.cpp:160-200) / ref:: twin (248-272). grads out in
 // layer-record layout (frozen records zero).
 int ref_batch_gradient(const ref_model *m, long n, const double *H, const double *y,

@@ -201,6 +201,7 @@ struct TraceBufs {
     long ts;
 };
 int ensure_ws(detnet_ctx *c, long n, int K);
+int upload_model(detnet_model *m, const detnet_model_desc *d);
 int reset_sing(detnet_ctx *c, cudaStream_t st);
 int run_pre(detnet_model *m, cudaStream_t st, long s0, long cnt, long n_total, const float *H,
             const float *y, const int8_t *x);

@@ -11,6 +11,7 @@
 
 #include "engine.hpp"
 #include "k_train.cuh"
+#include "k_prune.cuh"
 
 namespace detnet {
 namespace {
@@ -357,6 +358,99 @@ int detnet_model_get_params(detnet_model *m, double *out) {
         return 0;
     }
     CK(cudaMemcpy(out, m->tparams.p, sizeof(double) * total, cudaMemcpyDeviceToHost));
+    return 0;
+}
+
+
+// ---- pruning planner ----------------------------------------
+// Prunes the device FP64 master weights in place of the masks (bit-identical to
+// compression.cpp:43-94), then rebuilds every packed layout -- SIMT records,
+// the tcgen05 images (compacted to the live units when few survive) and the
+// sparse stream -- from the result. Adam moments and the step counter survive.
+int detnet_model_prune(detnet_model *m, int kind, double eta, double eta1, double eta2) {
+    if (!m) return fail(DETNET_ERR_CONTRACT, "null argument");
+    auto frac = [](double v) { return v >= 0.0 && v < 1.0; };
+    if (kind < 0 || kind > 2) return fail(DETNET_ERR_CONTRACT, "prune: kind must be 0, 1 or 2");
+    if (!frac(eta) || !frac(eta1) || !frac(eta2))
+        return fail(DETNET_ERR_CONFIG, "PruneSpec: thresholds must lie in [0, 1)");
+    if (3L * m->K + m->V > 1023 || m->Z > 1023)
+        return fail(DETNET_ERR_UNSUPPORTED, "prune: layer widths above 1023");
+    CK(cudaSetDevice(m->ctx->device));
+    if (int rc = ensure_train_state(m)) return rc;
+    const long P = record_size(m->K, m->Z, m->V);
+    PruneArgs a{m->tparams.as<double>(), m->tmasks.as<double>(), P, m->K, m->Z, m->V, kind,
+                eta, eta1, eta2};
+    {
+        LaunchScope ls(m->ctx, DETNET_K_OTHER, m->ctx->stream);
+        k_prune<<<m->L, 256, 0, m->ctx->stream>>>(a);
+    }
+    if (int rc = check_launch()) return rc;
+    const size_t total = static_cast<size_t>(P) * m->L;
+    std::vector<double> params(total), masks(total);
+    CK(cudaStreamSynchronize(m->ctx->stream));
+    CK(cudaMemcpy(params.data(), m->tparams.p, sizeof(double) * total, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(masks.data(), m->tmasks.p, sizeof(double) * total, cudaMemcpyDeviceToHost));
+    const int64_t step = m->adam_step;
+    detnet_model_desc d{m->K, m->N, m->Z, m->V, m->L, m->frozen, params.data(), masks.data()};
+    if (int rc = upload_model(m, &d)) return rc;
+    m->train_ready = true; // device params / masks already hold exactly these values
+    m->adam_step = step;
+    drain_times(m->ctx);
+    return 0;
+}
+
+int detnet_model_get_masks(detnet_model *m, double *out) {
+    if (!m || !out) return fail(DETNET_ERR_CONTRACT, "null argument");
+    const long total = record_size(m->K, m->Z, m->V) * m->L;
+    if (m->train_ready) {
+        CK(cudaMemcpy(out, m->tmasks.p, sizeof(double) * total, cudaMemcpyDeviceToHost));
+    } else if (m->has_masks) {
+        std::memcpy(out, m->masks_host.data(), sizeof(double) * total);
+    } else {
+        std::fill(out, out + total, 1.0);
+    }
+    return 0;
+}
+
+// cost_report (compression.cpp:131-159) of the model as currently masked
+int detnet_model_cost_report(detnet_model *m, detnet_cost_report *r, detnet_layer_cost *per_layer) {
+    if (!m || !r) return fail(DETNET_ERR_CONTRACT, "null argument");
+    const long P = record_size(m->K, m->Z, m->V);
+    std::vector<double> mk(static_cast<size_t>(P) * m->L);
+    if (int rc = detnet_model_get_masks(m, mk.data())) return rc;
+    const long long k = m->K, n = m->N, IN = 3L * m->K + m->V;
+    const long W1n = m->Z * IN, W2n = static_cast<long>(m->K) * m->Z, W3n = static_cast<long>(m->V) * m->Z;
+    const long oW1 = 0, ob1 = W1n, oW2 = ob1 + m->Z, ob2 = oW2 + W2n, oW3 = ob2 + m->K, ob3 = oW3 + W3n;
+    auto ones = [](const double *p, long cnt) {
+        long long c = 0;
+        for (long i = 0; i < cnt; ++i) c += p[i] != 0.0;
+        return c;
+    };
+    *r = detnet_cost_report{};
+    r->layer_count = m->L;
+    r->preprocess_flops = 2 * n * k + 2 * n * k * k;
+    long long dense_stored = 0, sparse_stored = 0;
+    for (int l = 0; l < m->L; ++l) {
+        const double *q = mk.data() + static_cast<size_t>(l) * P;
+        const long long wt = W1n + W2n + W3n;
+        const long long wn = ones(q + oW1, W1n) + ones(q + oW2, W2n) + ones(q + oW3, W3n);
+        const long long bn = ones(q + ob1, m->Z) + ones(q + ob2, m->K) + ones(q + ob3, m->V);
+        detnet_layer_cost c;
+        c.params_total = wt + m->Z + m->K + m->V + 1;
+        c.params_nonzero = wn + bn + 1;
+        c.flops = 2 * wn + 2 * k * k;
+        r->params_total += c.params_total;
+        r->params_nonzero += c.params_nonzero;
+        r->flops += c.flops;
+        r->flops_dense += 2 * wt + 2 * k * k;
+        dense_stored += c.params_total;
+        sparse_stored += c.params_nonzero;
+        if (per_layer) per_layer[l] = c;
+    }
+    r->flops += r->preprocess_flops;
+    r->flops_dense += r->preprocess_flops;
+    r->memory_dense_bytes = 4 * dense_stored;
+    r->memory_sparse_bytes = 4 * sparse_stored;
     return 0;
 }
 

@@ -126,6 +126,20 @@ _lib.detnet_train_grad.argtypes = [_vp, C.c_long, _vp, _vp, _vp, C.c_int, _vp, C
 _lib.detnet_train_apply.argtypes = [_vp, _vp, C.c_long, C.POINTER(_LossSpec), C.POINTER(_AdamCfg)]
 _lib.detnet_model_get_params.argtypes = [_vp, _vp]
 _lib.detnet_model_reset_adam.argtypes = [_vp]
+class _CostReport(C.Structure):
+    _fields_ = [("layer_count", C.c_int)] + [(f, C.c_longlong) for f in (
+        "params_total", "params_nonzero", "memory_dense_bytes", "memory_sparse_bytes", "flops",
+        "flops_dense", "preprocess_flops")]
+
+
+class _LayerCost(C.Structure):
+    _fields_ = [("params_total", C.c_longlong), ("params_nonzero", C.c_longlong),
+                ("flops", C.c_longlong)]
+
+
+_lib.detnet_model_prune.argtypes = [_vp, C.c_int, C.c_double, C.c_double, C.c_double]
+_lib.detnet_model_get_masks.argtypes = [_vp, _vp]
+_lib.detnet_model_cost_report.argtypes = [_vp, C.POINTER(_CostReport), C.POINTER(_LayerCost)]
 _lib.detnet_batch_baseline_errors.argtypes = [_vp, C.c_int, C.c_long, C.c_int, C.c_int, _vp, _vp,
                                                _vp, C.POINTER(C.c_longlong),
                                                C.POINTER(C.c_longlong)]
@@ -390,6 +404,25 @@ class Model:
 
     def reset_adam(self):
         _check(_lib.detnet_model_reset_adam(self._h))
+
+    # -- pruning planner (compression.cpp:43-94) and cost report (131-159) --
+    def prune(self, kind, eta=0.0, eta1=0.0, eta2=0.0):
+        """kind 0 element(eta), 1 group(eta1), 2 sparse_group(eta1, eta2), on the
+        device master weights; the packed layouts are rebuilt."""
+        _check(_lib.detnet_model_prune(self._h, int(kind), eta, eta1, eta2))
+
+    def get_masks(self):
+        out = np.empty((self.depth, record_size(self.n_tx, self.z_dim, self.v_dim)))
+        _check(_lib.detnet_model_get_masks(self._h, _addr(out)))
+        return out
+
+    def cost_report(self):
+        r = _CostReport()
+        pl = (_LayerCost * self.depth)()
+        _check(_lib.detnet_model_cost_report(self._h, C.byref(r), pl))
+        rep = {f: getattr(r, f) for f, _ in _CostReport._fields_}
+        per = np.array([[c.params_total, c.params_nonzero, c.flops] for c in pl], np.int64)
+        return rep, per
 
     def batch_gradient(self, H, y, x, kind=0, lam=0.0, lam1=0.0, lam2=0.0, trainable_only=False):
         H, y, x = self._samples(H, y, x)

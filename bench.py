@@ -237,6 +237,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--path", default="auto", choices=["auto", "simt", "tc"])
+    ap.add_argument("--train-fwd", default="simt", choices=["simt", "tc"],
+                    help="config 5: training forward on FP32 cores (default, parity) or tcgen05")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -293,13 +295,13 @@ def main():
 
     for _ in range(args.warmup):
         step_device()
-    ctx.kernel_times(reset=True)
-    ctx.set_profiling(True)
-    launches0 = ctx.launch_count
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         clk.prime(lambda: (step_device(), torch.cuda.synchronize()))
+        ctx.kernel_times(reset=True)
+        ctx.set_profiling(True)
+        launches0 = ctx.launch_count
         barrier()
         torch.cuda.synchronize()
         t0 = torch.cuda.Event(enable_timing=True)
@@ -387,6 +389,8 @@ def run_train_bench(args, torch, dist, world, rank, local, barrier, eng):
     L, _, per_gpu, _, _ = workload(5)
     params, _ = build_params(5, L)
     ctx = eng.Context(local)
+    if args.train_fwd == "tc":
+        ctx.set_train_forward(True)
     ctx.set_stream(torch.cuda.current_stream().cuda_stream)
     model = ctx.model(K, N, Z, V, params)
     raw = torch.zeros(model.param_count, dtype=torch.float64, device="cuda")
@@ -414,14 +418,14 @@ def run_train_bench(args, torch, dist, world, rank, local, barrier, eng):
     peaks = measured_peaks(torch) if rank == 0 else {}
     for b in range(args.warmup):
         step(b)
-    ctx.kernel_times(reset=True)
-    ctx.set_profiling(True)
-    launches0 = ctx.launch_count
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         # priming runs the local gradient only: no collective, no parameter update
         clk.prime(lambda: (model.train_grad(per_gpu, *batches[0], raw), torch.cuda.synchronize()))
+        ctx.kernel_times(reset=True)
+        ctx.set_profiling(True)
+        launches0 = ctx.launch_count
         barrier()
         torch.cuda.synchronize()
         t0 = torch.cuda.Event(enable_timing=True)
@@ -464,7 +468,8 @@ def run_train_bench(args, torch, dist, world, rank, local, barrier, eng):
             "config": {"workload": config_block(args, L, [(7.0, 14.0)], per_gpu)["workload"],
                        "global_batch": n_global, "per_gpu_batch": per_gpu, "layers": L,
                        "parallelism": f"dp{world}",
-                       "l2": "fresh batch per step (12.7 MB) + 1 M-parameter model"},
+                       "l2": "fresh batch per step (12.7 MB) + 1 M-parameter model",
+                       "train_forward": "tcgen05-3xtf32" if args.train_fwd == "tc" else "simt-fp32"},
             "roofline": roof, "cpu_baseline": cpu, "gpu_launches": launches,
             "clocks": clk.summary(), "last_step_loss": ev.data_loss, "peaks_measured": peaks}),
             flush=True)

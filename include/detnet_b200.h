@@ -55,6 +55,12 @@ const char *detnet_last_error(void);
 /* Kernel-path selection: 0 auto (tcgen05 where compiled, else SIMT), 1 SIMT
  * FP32, 2 tcgen05 3xTF32, 3 sparse CSR (pruned models). */
 int detnet_ctx_set_path(detnet_ctx *ctx, int path);
+/* Training forward (detnet_train_grad / detnet_batch_gradient) on tcgen05
+ * (1, dense K=20 models) or FP32 CUDA cores (0, default). The tensor-core
+ * forward is ~4x faster; its 3xTF32 activations are a few times noisier than
+ * FP32, so FP32-vs-FP64 loss tracking over long runs is looser. */
+int detnet_ctx_set_train_forward(detnet_ctx *ctx, int tensor_cores);
+
 /* Preprocessing mode: 0 (default) FP32 Cholesky + FP64 refinement with the
  * reference LU as fallback for ill-conditioned samples (FP64-accurate loss
  * denominators); 1 the reference LU for every sample (bit-identical q, G,

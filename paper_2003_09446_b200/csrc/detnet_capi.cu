@@ -38,6 +38,7 @@ using PreFn = void (*)(dim3, dim3, size_t, cudaStream_t, long, int, const float 
                        const int8_t *, float *, float *, double *, uint32_t *, uint8_t *,
                        unsigned long long *, const long *, const int *);
 using SimtFn = void (*)(dim3, dim3, size_t, cudaStream_t, const StackArgs &);
+constexpr int SIMT_SMALL = 64, SIMT_LARGE = 256; // samples per CTA (k_stack_simt)
 
 template <int K>
 void launch_pre(dim3 g, dim3 b, size_t sm, cudaStream_t st, long n, int N, const float *H,
@@ -100,15 +101,19 @@ template <int K> int set_fast_smem() {
 
 template <int K, int Z, int V>
 void launch_simt(dim3 g, dim3 b, size_t sm, cudaStream_t st, const StackArgs &a) {
-    k_stack_simt<K, Z, V><<<g, b, sm, st>>>(a);
+    if (b.x == SIMT_SMALL) k_stack_simt<K, Z, V, SIMT_SMALL><<<g, b, sm, st>>>(a);
+    else k_stack_simt<K, Z, V, SIMT_LARGE><<<g, b, sm, st>>>(a);
 }
 
 template <int K, int Z, int V> int set_simt_smem() {
     const int bytes = static_cast<int>(2 * simt_rec(K, Z, V) * 4 + 64);
-    return cudaFuncSetAttribute(k_stack_simt<K, Z, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                bytes) == cudaSuccess
-               ? 0
-               : -1;
+    const bool ok = cudaFuncSetAttribute(k_stack_simt<K, Z, V, SIMT_SMALL>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
+                        cudaSuccess &&
+                    cudaFuncSetAttribute(k_stack_simt<K, Z, V, SIMT_LARGE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
+                        cudaSuccess;
+    return ok ? 0 : -1;
 }
 
 struct DimsEntry {
@@ -404,9 +409,12 @@ int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, 
         }
         return check_launch();
     }
-    if (!trace && m->ctx->path != 1)
+    if (m->ctx->path != 1)
         if (int rc = refresh_tc(m)) return rc;
-    if (use_tc(m) && !trace) {
+    // the training forward (trace) runs on tcgen05 only when asked for
+    // (detnet_ctx_set_train_forward): 3xTF32 activations are ~4x noisier than
+    // FP32 ones, which shortens the FP32-vs-FP64 tracking of long training runs
+    if (use_tc(m) && (!trace || (c->train_tc && m->tc.zh == 160))) {
         TcArgs ta{};
         ta.gp = c->gp.as<float>();
         ta.q32 = c->q32.as<float>();
@@ -422,7 +430,7 @@ int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, 
         ta.tile_loss = c->tile_loss.as<double>();
         ta.tile_err = c->tile_err.as<long long>();
         LaunchScope ls(c, DETNET_K_STACK, st);
-        if (int rc = tc_launch_state(m->tc, ta, xs, vs, st)) return rc;
+        if (int rc = tc_launch_state(m->tc, ta, xs, vs, st, trace)) return rc;
         return check_launch();
     }
     StackArgs a{};
@@ -451,10 +459,12 @@ int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, 
         a.ts = trace->ts;
     }
     const size_t smem = 2 * static_cast<size_t>(m->simt_rec) * 4 + 64;
-    const int blocks = static_cast<int>((nt + 1) / 2);
+    // one CTA per SM: small batches use 64-sample CTAs to reach more SMs
+    const int per = nt * TILE / SIMT_LARGE >= c->sms ? SIMT_LARGE : SIMT_SMALL;
+    const int blocks = static_cast<int>((nt * TILE + per - 1) / per);
     {
         LaunchScope ls(c, DETNET_K_STACK, st);
-        m->dims->simt(dim3(blocks), dim3(256), smem, st, a);
+        m->dims->simt(dim3(blocks), dim3(per), smem, st, a);
     }
     return check_launch();
 }
@@ -587,6 +597,12 @@ void detnet_ctx_destroy(detnet_ctx *c) {
 int detnet_ctx_set_path(detnet_ctx *c, int path) {
     if (!c || path < 0 || path > 3) return fail(DETNET_ERR_CONTRACT, "bad path");
     c->path = path;
+    return 0;
+}
+
+int detnet_ctx_set_train_forward(detnet_ctx *c, int tensor_cores) {
+    if (!c) return fail(DETNET_ERR_CONTRACT, "null context");
+    c->train_tc = tensor_cores != 0;
     return 0;
 }
 

@@ -88,8 +88,11 @@ struct TcArgs {
 int tc_prepare();
 int tc_pack(TcModel &tc, int K, int Z, int V, int L, const double *params, const double *masks);
 int tc_launch(const TcModel &tc, const TcArgs &a, cudaStream_t st);
-int tc_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cudaStream_t st);
+struct TraceBufs;
+int tc_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cudaStream_t st,
+                    const TraceBufs *tr = nullptr);
 void tc_release(TcModel &tc);
+int tc_pack_device(TcModel &tc, const double *params, const double *masks, long P, cudaStream_t st);
 
 
 } // namespace detnet
@@ -115,6 +118,7 @@ struct detnet_ctx {
     detnet::DBuf in_H[2], in_y[2], in_x[2], xhat_dev, state_x, state_v, fb_list, fb_count;
     detnet::DBuf prep_scratch; // K1 fast path: per-CTA factor parking (L2-resident)
     bool exact_pre = false; // bit-exact reference LU for every sample
+    bool train_tc = false;  // training forward on tcgen05 (dense images) instead of SIMT
     double *h_result = nullptr; // pinned: loss, err, flag, singular
     cudaEvent_t chunk_done[2] = {nullptr, nullptr};
     cudaEvent_t copy_done[2] = {nullptr, nullptr};

@@ -59,8 +59,13 @@ struct StackArgs {
     long ts;                // trace sample stride (>= padded sample count)
 };
 
-template <int K, int Z, int V>
-__global__ void __launch_bounds__(256, 1) k_stack_simt(StackArgs a) {
+// THREADS samples per CTA (one CTA per SM fits: the double-buffered weights
+// take ~210 KB of shared memory). 256 (two tiles) for large batches; 64 (half
+// a tile) for small ones -- the training batch of 5,000 is 40 tiles -- so they
+// still spread over 79 SMs.
+template <int K, int Z, int V, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) k_stack_simt(StackArgs a) {
+    constexpr int SIMT_THREADS = THREADS;
     constexpr int IN = 3 * K + V;
     constexpr int IN4 = simt_in4(K, V);
     constexpr int O = K + V;
@@ -71,10 +76,12 @@ __global__ void __launch_bounds__(256, 1) k_stack_simt(StackArgs a) {
     uint64_t *bars = reinterpret_cast<uint64_t *>(sw + 2 * REC);
 
     const int tid = threadIdx.x;
-    const long tile_l = static_cast<long>(blockIdx.x) * 2 + (tid >> 7);
+    // blocks cover tiles in units of THREADS consecutive samples
+    const long unit = static_cast<long>(blockIdx.x) * SIMT_THREADS + tid;
+    const long tile_l = unit / TILE;
     const bool live_tile = tile_l < a.n_tiles;
     const long tile = live_tile ? tile_l : a.n_tiles - 1;
-    const int col = tid & (TILE - 1);
+    const int col = static_cast<int>(unit % TILE);
     const long s = tile * TILE + col;           // sample index within this launch
     const bool live = live_tile && s < a.n;
     const long gt = a.tile0 + tile;              // global tile index for SoA buffers
@@ -231,20 +238,12 @@ __global__ void __launch_bounds__(256, 1) k_stack_simt(StackArgs a) {
     for (int k = 0; k < K; ++k) errs += (x[k] >= 0.f) != (((xm >> k) & 1u) != 0);
     if (!live) { loss = 0.0; errs = 0; }
 
-    // deterministic per-tile reduction: 4 warps per tile, fixed tree
-    __shared__ double s_loss[8];
-    __shared__ long long s_err[8];
+    // per lane-quadrant partials (a warp = one quadrant), summed in fixed order later
     loss = warp_sum(loss);
     errs = warp_sum(errs);
-    if ((tid & 31) == 0) { s_loss[tid >> 5] = loss; s_err[tid >> 5] = errs; }
-    __syncthreads();
-    if ((tid & 127) == 0 && live_tile) {
-        const int w0 = tid >> 5;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            a.tile_loss[gt * 4 + q] = s_loss[w0 + q];
-            a.tile_err[gt * 4 + q] = s_err[w0 + q];
-        }
+    if ((tid & 31) == 0 && live_tile) {
+        a.tile_loss[gt * 4 + col / 32] = loss;
+        a.tile_err[gt * 4 + col / 32] = errs;
     }
 }
 

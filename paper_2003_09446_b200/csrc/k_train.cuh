@@ -37,8 +37,13 @@ struct BwdArgs {
     double *tbar_part;      // [L][gridDim.x]
 };
 
-template <int K, int Z, int V>
-__global__ void __launch_bounds__(256, 1) k_train_bwd(BwdArgs a) {
+// THREADS samples per CTA (one CTA per SM: the double-buffered weights take
+// ~210 KB of shared memory): 256 for large batches, 64 for small ones -- at the
+// config-5 batch (5,000 samples) that spreads the per-sample reverse sweeps
+// over 79 SMs instead of 20.
+template <int K, int Z, int V, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) k_train_bwd(BwdArgs a) {
+    constexpr int BWD_WARPS = THREADS / 32;
     constexpr int IN = 3 * K + V;
     constexpr int IN4 = simt_in4(K, V);
     constexpr int O = K + V;
@@ -47,13 +52,14 @@ __global__ void __launch_bounds__(256, 1) k_train_bwd(BwdArgs a) {
     constexpr int REC = static_cast<int>(simt_rec(K, Z, V));
     extern __shared__ __align__(128) float sw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(sw + 2 * REC);
-    __shared__ double s_t[2][8];
+    __shared__ double s_t[2][BWD_WARPS];
 
     const int tid = threadIdx.x;
-    const long tile_l = static_cast<long>(blockIdx.x) * 2 + (tid >> 7);
+    const long unit = static_cast<long>(blockIdx.x) * THREADS + tid;
+    const long tile_l = unit / TILE;
     const bool live_tile = tile_l < a.n_tiles;
     const long tile = live_tile ? tile_l : a.n_tiles - 1;
-    const int col = tid & (TILE - 1);
+    const int col = static_cast<int>(unit % TILE);
     const long s = tile * TILE + col;
     const bool live = live_tile && s < a.n;
 
@@ -117,35 +123,45 @@ __global__ void __launch_bounds__(256, 1) k_train_bwd(BwdArgs a) {
         for (int j = 0; j < IN - K; ++j) ibar[j] = 0.f;
         const float *zl = a.tr_z + static_cast<long>(l) * Z * a.ts + s;
         float *u1b = a.u1bar + static_cast<long>(l) * Z * a.ts + s;
+        // hidden units in groups of 8: the group's z trace values are loaded
+        // up front (8 independent L2 reads in flight instead of one per unit)
+        static_assert(Z % 8 == 0, "hidden width in groups of 8");
 #pragma unroll 1
-        for (int i = 0; i < Z; ++i) {
-            const float4 *c4 = reinterpret_cast<const float4 *>(W + Z * IN4 + i * O4);
-            float zb0 = 0.f, zb1 = 0.f;
+        for (int i0 = 0; i0 < Z; i0 += 8) {
+            float zg[8];
 #pragma unroll
-            for (int m = 0; m < O4 / 4; ++m) {
-                const float4 c = c4[m];
+            for (int q = 0; q < 8; ++q) zg[q] = zl[(i0 + q) * a.ts];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int i = i0 + q;
+                const float4 *c4 = reinterpret_cast<const float4 *>(W + Z * IN4 + i * O4);
+                float zb0 = 0.f, zb1 = 0.f;
+#pragma unroll
+                for (int m = 0; m < O4 / 4; ++m) {
+                    const float4 c = c4[m];
 #define DETNET_G(j) ((j) < K ? u2bar[(j) < K ? (j) : 0] : vbar[((j) - K) < V ? (j) - K : 0])
-                if (4 * m + 0 < O) zb0 = fmaf(c.x, DETNET_G(4 * m + 0), zb0);
-                if (4 * m + 1 < O) zb1 = fmaf(c.y, DETNET_G(4 * m + 1), zb1);
-                if (4 * m + 2 < O) zb0 = fmaf(c.z, DETNET_G(4 * m + 2), zb0);
-                if (4 * m + 3 < O) zb1 = fmaf(c.w, DETNET_G(4 * m + 3), zb1);
+                    if (4 * m + 0 < O) zb0 = fmaf(c.x, DETNET_G(4 * m + 0), zb0);
+                    if (4 * m + 1 < O) zb1 = fmaf(c.y, DETNET_G(4 * m + 1), zb1);
+                    if (4 * m + 2 < O) zb0 = fmaf(c.z, DETNET_G(4 * m + 2), zb0);
+                    if (4 * m + 3 < O) zb1 = fmaf(c.w, DETNET_G(4 * m + 3), zb1);
 #undef DETNET_G
-            }
-            const float ub = zl[i * a.ts] > 0.f ? zb0 + zb1 : 0.f;
-            if (live_tile) u1b[i * a.ts] = live ? ub : 0.f;
-            const float4 *w4 = reinterpret_cast<const float4 *>(W + i * IN4);
+                }
+                const float ub = zg[q] > 0.f ? zb0 + zb1 : 0.f;
+                if (live_tile) u1b[i * a.ts] = live ? ub : 0.f;
+                const float4 *w4 = reinterpret_cast<const float4 *>(W + i * IN4);
 #pragma unroll
-            for (int m = K / 4; m < IN4 / 4; ++m) {
-                const float4 wv = w4[m];
+                for (int m = K / 4; m < IN4 / 4; ++m) {
+                    const float4 wv = w4[m];
 #define DETNET_IB(c, wc)                                                                        \
     if (4 * m + (c) >= K && 4 * m + (c) < IN)                                                    \
         ibar[(4 * m + (c) - K) >= 0 ? 4 * m + (c) - K : 0] =                                    \
             fmaf(wc, ub, ibar[(4 * m + (c) - K) >= 0 ? 4 * m + (c) - K : 0]);
-                DETNET_IB(0, wv.x)
-                DETNET_IB(1, wv.y)
-                DETNET_IB(2, wv.z)
-                DETNET_IB(3, wv.w)
+                    DETNET_IB(0, wv.x)
+                    DETNET_IB(1, wv.y)
+                    DETNET_IB(2, wv.z)
+                    DETNET_IB(3, wv.w)
 #undef DETNET_IB
+                }
             }
         }
         // a_bar <- G gx_bar + x_bar (G symmetric); v_bar <- v block
@@ -171,7 +187,7 @@ __global__ void __launch_bounds__(256, 1) k_train_bwd(BwdArgs a) {
         __syncthreads(); // also: every thread is done reading buffer b
         if (tid == 0) {
             double acc = 0.0;
-            for (int w8 = 0; w8 < 8; ++w8) acc += s_t[it & 1][w8];
+            for (int w8 = 0; w8 < BWD_WARPS; ++w8) acc += s_t[it & 1][w8];
             a.tbar_part[static_cast<long>(l) * gridDim.x + blockIdx.x] = acc;
             if (it + 2 < nl) {
                 mbar_arrive_expect_tx(&bars[b], bytes);

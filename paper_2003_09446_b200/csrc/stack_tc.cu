@@ -83,6 +83,10 @@ struct TcKArgs {
     const float *bt;        // [L][BT]
     float *x_state, *v_state;
     long long *trace; // optional debug timeline (DETNET_TC_TRACE): CTA 0, tile 0
+    // training trace (TR instantiation, ZH == 160), the k_stack_simt layout:
+    // [l][feature][ts] of in = [q; x; Gx; v], z = relu(u1), u2; x_hat_L [K][ts]
+    float *tr_in, *tr_z, *tr_u2, *tr_xf;
+    long ts;
 };
 
 // Debug timeline (build with EXTRA=-DDETNET_TC_TRACE, run with DETNET_TC_TRACE=1):
@@ -145,7 +149,8 @@ __device__ __forceinline__ void split(float v, float &hi, float &lo) {
 // resource); B gets x_hat from A through shared memory afterwards.
 template <bool SIDE_A, int C_U2>
 __device__ __forceinline__ void epi2_layer(uint32_t trow, const float *bt, float (&x)[KX],
-                                           float (&v)[VV], uint64_t *e2l, long long *tr) {
+                                           float (&v)[VV], uint64_t *e2l, long long *tr,
+                                           float *tu2 = nullptr, long ts = 0) {
     if (SIDE_A) {
         if (tr) tr[2] = clock64(); // slot 27
         uint32_t r[KX];
@@ -165,6 +170,7 @@ __device__ __forceinline__ void epi2_layer(uint32_t trow, const float *bt, float
 #pragma unroll
         for (int k = 0; k < KX; ++k) {
             const float uu = __uint_as_float(r[k]) + b[k];
+            if (tu2) tu2[k * ts] = uu;
             x[k] = uu <= -tt.x ? -1.f : (uu >= tt.x ? 1.f : uu * tt.y);
         }
     } else {
@@ -183,8 +189,10 @@ __device__ __forceinline__ void epi2_layer(uint32_t trow, const float *bt, float
     }
 }
 
-template <int ZH>
+template <int ZH, bool TR>
 __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
+    static_assert(!TR || ZH == 160, "the training trace is written in the dense unit layout");
+    constexpr int IN = 3 * KX + VV;
     using C = TcCfg<ZH>;
     constexpr int NH = C::NH, GW = C::GW, EW = C::EW;
     constexpr int C_U1 = C::C_U1, C_DYN = C::C_DYN, C_DYNLO = C::C_DYNLO, C_U2 = C::C_U2,
@@ -446,6 +454,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                     tc::named_bar(pair_bar, 64);
 #pragma unroll
                     for (int k = 6; k < KX; ++k) gx[k] += sGX[k * 128 + col];
+                    if constexpr (TR) {
+                        float *ti = p.tr_in + static_cast<long>(l) * IN * p.ts + s;
+#pragma unroll
+                        for (int k = 0; k < KX; ++k) {
+                            ti[k * p.ts] = __ldg(a.q32 + (gt * KX + k) * TILE + col);
+                            ti[(KX + k) * p.ts] = x[k];
+                            ti[(2 * KX + k) * p.ts] = gx[k];
+                        }
+                    }
                     {
                         float hi[24], lo[24];
 #pragma unroll
@@ -460,6 +477,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                     tc::fence_before();
                     mbar_arrive(&bars[B_G]);
                 } else {
+                    if constexpr (TR) {
+                        float *ti = p.tr_in + (static_cast<long>(l) * IN + 3 * KX) * p.ts + s;
+#pragma unroll
+                        for (int k = 0; k < VV; ++k) ti[k * p.ts] = v[k];
+                    }
 #pragma unroll
                     for (int c = 0; c < VV; c += 16) {
                         float hi[16], lo[16];
@@ -514,6 +536,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                     for (int k = 0; k < EW; ++k) {
                         const float u = __uint_as_float(r[k]);
                         split(u > 0.f ? u : 0.f, zh[k], zl[k]);
+                        if constexpr (TR)
+                            p.tr_z[(static_cast<long>(l) * ZH + c0 + k) * p.ts + s] = u > 0.f ? u : 0.f;
                     }
                     st_cols<EW>(trow + C_U1 + c0, zh);
                     st_cols<EW>(trow + C::zlo_col(c0), zl);
@@ -535,7 +559,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                                      ? p.trace + (l - L0) * 32 + 25
                                      : nullptr;
                 if (isA) {
-                    epi2_layer<true, C_U2>(trow, bt, x, v, &bars[B_E2L], tr2);
+                    epi2_layer<true, C_U2>(trow, bt, x, v, &bars[B_E2L], tr2,
+                                           TR ? p.tr_u2 + static_cast<long>(l) * KX * p.ts + s
+                                              : nullptr,
+                                           p.ts);
 #pragma unroll
                     for (int k = 0; k < KX; ++k) sGX[k * 128 + col] = x[k];
                     tc::named_bar(pair_bar, 64);
@@ -552,6 +579,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                 TRACE(6 + tb16, l);
             }
             if (isA && lpend >= 0) settle();
+            if constexpr (TR) {
+                if (isA) {
+#pragma unroll
+                    for (int k = 0; k < KX; ++k) p.tr_xf[k * p.ts + s] = x[k];
+                }
+            }
             // ---- tile end: state out, per-tile partials (A warps) ----
             if (p.x_state && live) {
                 if (isA) {
@@ -582,6 +615,64 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
     if (warp == 8) tc::tmem_dealloc(tbase, TMEM_COLS);
 }
 
+// ---- device packer (dense images) ---------------------------------------------
+// The same images tc_pack builds on the host (ZH = 160, unit r = row r), from
+// the device FP64 master weights after a training step: one thread per image
+// element. rna_tf32 as integer rounding (== rna_tf32_host for finite values).
+__device__ __forceinline__ float rna_dev(float v) {
+    const uint32_t b = __float_as_uint(v);
+    if ((b & 0x7f800000u) == 0x7f800000u) return v;
+    return __uint_as_float((b + 0x1000u) & 0xffffe000u);
+}
+
+__global__ void k_pack_tc160(const double *__restrict__ params, const double *__restrict__ masks,
+                             long P, int L, float *__restrict__ img, float *__restrict__ bt) {
+    using C = TcCfg<160>;
+    constexpr int ZH = 160, IN = 3 * KX + VV;
+    constexpr long W1E = ZH * W1_K, W23E = W23_ROWS * ZH, PER = W1E + W23E + BT;
+    const long gid = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (gid >= PER * L) return;
+    const int l = static_cast<int>(gid / PER);
+    const long e = gid % PER;
+    const double *pr = params + l * P;
+    const double *mk = masks ? masks + l * P : nullptr;
+    auto w = [&](long off) { return static_cast<float>(pr[off] * (mk ? mk[off] : 1.0)); };
+    const long oW1 = 0, ob1 = static_cast<long>(ZH) * IN, oW2 = ob1 + ZH, ob2 = oW2 + KX * ZH,
+               oW3 = ob2 + KX, ob3 = oW3 + static_cast<long>(VV) * ZH, ot = ob3 + VV;
+    float *L1hi = img + static_cast<size_t>(l) * C::LAYER_BYTES / 4;
+    if (e < W1E) {
+        const int i = static_cast<int>(e / W1_K), k = static_cast<int>(e % W1_K);
+        float val = 0.f;
+        if (k < KX) val = w(oW1 + i * IN + k);
+        else if (k == KX) val = w(ob1 + i);
+        else if (k >= 24 && k < 64) val = w(oW1 + i * IN + (k + 36));
+        else if (k >= 64) val = w(oW1 + i * IN + (k - 44));
+        const float hi = rna_dev(val);
+        const size_t off = static_cast<size_t>(k / 4) * ZH * 4 + (i / 8) * 32 + (i % 8) * 4 + (k % 4);
+        L1hi[off] = hi;
+        L1hi[C::W1_HALF / 4 + off] = rna_dev(val - hi);
+    } else if (e < W1E + W23E) {
+        const long e2 = e - W1E;
+        const int o = static_cast<int>(e2 / ZH), i = static_cast<int>(e2 % ZH);
+        float val = 0.f;
+        if (o < VV) val = w(oW3 + o * ZH + i);
+        else if (o < VV + KX) val = w(oW2 + (o - VV) * ZH + i);
+        const float hi = rna_dev(val);
+        float *L2hi = L1hi + C::W1_BYTES / 4;
+        const size_t off = static_cast<size_t>(i / 4) * W23_ROWS * 4 + (o / 8) * 32 + (o % 8) * 4 + (i % 4);
+        L2hi[off] = hi;
+        L2hi[C::W23_HALF / 4 + off] = rna_dev(val - hi);
+    } else {
+        const int k = static_cast<int>(e - W1E - W23E);
+        float val = 0.f;
+        if (k < VV) val = w(ob3 + k);
+        else if (k < VV + KX) val = w(ob2 + (k - VV));
+        else if (k == 60) val = static_cast<float>(pr[ot]);
+        else if (k == 61) val = static_cast<float>(1.0 / pr[ot]);
+        bt[static_cast<size_t>(l) * BT + k] = val;
+    }
+}
+
 // ---- host: packing into the smem images -------------------------------------
 float rna_tf32_host(float v) {
     uint32_t b;
@@ -601,10 +692,14 @@ inline size_t img_off(int n, int k, int NR) {
 } // namespace
 
 int tc_prepare() {
-    cudaError_t e = cudaFuncSetAttribute(k_stack_tc<160>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_stack_tc<160, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(TcCfg<160>::SM_TOTAL));
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_stack_tc<48>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        e = cudaFuncSetAttribute(k_stack_tc<160, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(TcCfg<160>::SM_TOTAL));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_stack_tc<48, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(TcCfg<48>::SM_TOTAL));
     if (e != cudaSuccess)
         return fail(DETNET_ERR_CUDA, "tcgen05 kernel smem attribute: %s", cudaGetErrorString(e));
@@ -720,7 +815,23 @@ int tc_pack(TcModel &tc, int K, int Z, int V, int L, const double *params, const
     return 0;
 }
 
-int tc_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cudaStream_t st) {
+// Rebuild the dense images on the device (training: after each Adam step).
+// Returns 1 (nothing done) when the packed model is not the dense ZH = 160 one.
+int tc_pack_device(TcModel &tc, const double *params, const double *masks, long P,
+                   cudaStream_t st) {
+    if (!tc.ready || tc.zh != 160) return 1;
+    constexpr long PER = 160L * W1_K + W23_ROWS * 160L + BT;
+    const long total = PER * tc.L;
+    float *img = static_cast<float *>(tc.w.p);
+    float *bt = reinterpret_cast<float *>(static_cast<char *>(tc.w.p) +
+                                          static_cast<size_t>(tc.L) * tc.rec_bytes);
+    k_pack_tc160<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(params, masks, P, tc.L,
+                                                                            img, bt);
+    return cudaGetLastError() == cudaSuccess ? 0 : fail(DETNET_ERR_CUDA, "tc device pack");
+}
+
+int tc_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cudaStream_t st,
+                    const TraceBufs *tr) {
     if (!tc.ready) return fail(DETNET_ERR_UNSUPPORTED, "tcgen05 path not packed for these dims");
     TcKArgs p;
     p.a = a;
@@ -730,6 +841,8 @@ int tc_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cu
     p.x_state = xs;
     p.v_state = vs;
     p.trace = nullptr;
+    p.tr_in = p.tr_z = p.tr_u2 = p.tr_xf = nullptr;
+    p.ts = 0;
     static long long *trace_buf = nullptr;
     const bool tracing = std::getenv("DETNET_TC_TRACE") != nullptr;
     if (tracing) {
@@ -742,8 +855,19 @@ int tc_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cu
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int grid = static_cast<int>(std::min<long>(a.n_tiles, sms));
     if (grid <= 0) return 0;
-    if (tc.zh == 48) k_stack_tc<48><<<grid, NTHREADS, TcCfg<48>::SM_TOTAL, st>>>(p);
-    else k_stack_tc<160><<<grid, NTHREADS, TcCfg<160>::SM_TOTAL, st>>>(p);
+    if (tr) {
+        if (tc.zh != 160) return fail(DETNET_ERR_UNSUPPORTED, "tcgen05 training trace needs the dense images");
+        p.tr_in = tr->in;
+        p.tr_z = tr->z;
+        p.tr_u2 = tr->u2;
+        p.tr_xf = tr->xf;
+        p.ts = tr->ts;
+        k_stack_tc<160, true><<<grid, NTHREADS, TcCfg<160>::SM_TOTAL, st>>>(p);
+    } else if (tc.zh == 48) {
+        k_stack_tc<48, false><<<grid, NTHREADS, TcCfg<48>::SM_TOTAL, st>>>(p);
+    } else {
+        k_stack_tc<160, false><<<grid, NTHREADS, TcCfg<160>::SM_TOTAL, st>>>(p);
+    }
     if (tracing) {
         long long h[8 * 32];
         cudaMemcpyAsync(h, trace_buf, sizeof h, cudaMemcpyDeviceToHost, st);
@@ -765,7 +889,7 @@ int tc_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cu
 }
 
 int tc_launch(const TcModel &tc, const TcArgs &a, cudaStream_t st) {
-    return tc_launch_state(tc, a, nullptr, nullptr, st);
+    return tc_launch_state(tc, a, nullptr, nullptr, st, nullptr);
 }
 
 void tc_release(TcModel &tc) {

@@ -18,15 +18,22 @@ namespace {
 
 using BwdFn = void (*)(dim3, dim3, size_t, cudaStream_t, const BwdArgs &);
 
+constexpr int BWD_SMALL = 64, BWD_LARGE = 256; // samples per CTA (k_train_bwd)
+
 template <int K, int Z, int V>
 void launch_bwd(dim3 g, dim3 b, size_t sm, cudaStream_t st, const BwdArgs &a) {
-    k_train_bwd<K, Z, V><<<g, b, sm, st>>>(a);
+    if (b.x == BWD_SMALL) k_train_bwd<K, Z, V, BWD_SMALL><<<g, b, sm, st>>>(a);
+    else k_train_bwd<K, Z, V, BWD_LARGE><<<g, b, sm, st>>>(a);
 }
 template <int K, int Z, int V> int set_bwd_smem() {
-    return cudaFuncSetAttribute(k_train_bwd<K, Z, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(2 * simt_rec(K, Z, V) * 4 + 64)) == cudaSuccess
-               ? 0
-               : -1;
+    const int bytes = static_cast<int>(2 * simt_rec(K, Z, V) * 4 + 64);
+    const bool ok = cudaFuncSetAttribute(k_train_bwd<K, Z, V, BWD_SMALL>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
+                        cudaSuccess &&
+                    cudaFuncSetAttribute(k_train_bwd<K, Z, V, BWD_LARGE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
+                        cudaSuccess;
+    return ok ? 0 : -1;
 }
 
 struct BwdEntry {
@@ -103,7 +110,9 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
     const long tiles = (n + TILE - 1) / TILE, ts = tiles * TILE;
     TrainWs &w = ws_for(c);
     const int splits = static_cast<int>((n + DW_SPLIT - 1) / DW_SPLIT);
-    const int bwd_blocks = static_cast<int>((tiles + 1) / 2);
+    // one CTA per SM: small batches use 64-sample CTAs to reach more SMs
+    const int bwd_per = tiles * TILE / BWD_LARGE >= c->sms ? BWD_LARGE : BWD_SMALL;
+    const int bwd_blocks = static_cast<int>((tiles * TILE + bwd_per - 1) / bwd_per);
     if (w.tr_in.ensure(sizeof(float) * L * IN * ts) || w.tr_z.ensure(sizeof(float) * L * Z * ts) ||
         w.tr_u2.ensure(sizeof(float) * L * K * ts) || w.tr_xf.ensure(sizeof(float) * K * ts) ||
         w.u1bar.ensure(sizeof(float) * L * Z * ts) || w.g23bar.ensure(sizeof(float) * L * O * ts) ||
@@ -142,7 +151,7 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
         ba.tbar_part = w.tbar.as<double>();
         {
             LaunchScope ls(c, DETNET_K_BACKWARD, c->stream);
-            be->fn(dim3(bwd_blocks), dim3(256), 2 * static_cast<size_t>(m->simt_rec) * 4 + 64,
+            be->fn(dim3(bwd_blocks), dim3(bwd_per), 2 * static_cast<size_t>(m->simt_rec) * 4 + 64,
                    c->stream, ba);
         }
         if (int rc = check_launch()) return rc;
@@ -342,9 +351,16 @@ int detnet_train_apply(detnet_model *m, const double *raw_dev, long n_global,
     }
     if (int rc = check_launch()) return rc;
     if (int rc = pack_simt_device(m)) return rc;
-    // the tcgen05 images are rebuilt from the master copy before the next
-    // tensor-core evaluation (refresh_tc)
-    m->tc_stale = true;
+    // dense tcgen05 images follow the master weights on the device; other
+    // packings (compacted / sparse) are rebuilt from the host copy on demand
+    {
+        LaunchScope ls(m->ctx, DETNET_K_ADAM, m->ctx->stream);
+        const int rc = tc_pack_device(m->tc, m->tparams.as<double>(), m->tmasks.as<double>(),
+                                      rec_size(m), m->ctx->stream);
+        if (rc > 1) return rc;
+        m->tc_stale = rc != 0;
+    }
+    m->sparse_ready = false; // the CSR stream no longer matches the weights
     CK(cudaStreamSynchronize(c->stream));
     drain_times(c);
     return 0;

@@ -137,6 +137,7 @@ class _LayerCost(C.Structure):
                 ("flops", C.c_longlong)]
 
 
+_lib.detnet_ctx_set_train_forward.argtypes = [_vp, C.c_int]
 _lib.detnet_model_prune.argtypes = [_vp, C.c_int, C.c_double, C.c_double, C.c_double]
 _lib.detnet_model_get_masks.argtypes = [_vp, _vp]
 _lib.detnet_model_cost_report.argtypes = [_vp, C.POINTER(_CostReport), C.POINTER(_LayerCost)]
@@ -214,6 +215,10 @@ class Context:
 
     def set_exact_preprocess(self, on=True):
         _check(_lib.detnet_ctx_set_exact_preprocess(self._h, int(on)))
+
+    def set_train_forward(self, tensor_cores=True):
+        """Training forward on tcgen05 (dense K=20 models) instead of FP32 SIMT."""
+        _check(_lib.detnet_ctx_set_train_forward(self._h, int(tensor_cores)))
 
     def set_stream(self, stream_ptr):
         _check(_lib.detnet_ctx_set_stream(self._h, stream_ptr))

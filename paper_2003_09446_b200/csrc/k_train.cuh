@@ -208,45 +208,61 @@ struct DwJob {
     double *out;    // [splits][M][N+1] partials
 };
 
-constexpr int DW_TILE = 32, DW_SPLIT = 256, DW_KC = 32;
+// 64 x 64 output tile per CTA, 4 x 4 per thread (two 128-bit shared loads per
+// 16 FMAs), K = samples in chunks of 32; FP32 inside a split of DW_SPLIT
+// samples, one FP64 partial per split (summed in fixed order by k_grad_sum).
+constexpr int DW_TILE = 64, DW_SPLIT = 256, DW_KC = 32;
 
+// grid: (N tiles, M tiles, jobs x splits) -- one (tile, split) per CTA
 __global__ void __launch_bounds__(256) k_dw_gemm(const DwJob *jobs, long n, long ts, int splits) {
-    const DwJob jb = jobs[blockIdx.z];
+    const DwJob jb = jobs[blockIdx.z / splits];
     const int m0 = blockIdx.y * DW_TILE, n0 = blockIdx.x * DW_TILE;
     if (m0 >= jb.M || n0 > jb.N) return;
-    __shared__ float sA[DW_KC][DW_TILE + 1], sB[DW_KC][DW_TILE + 1];
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4; // 16 x 16 threads, 2 x 2 outputs
-    for (int sp = 0; sp < splits; ++sp) {
+    // rows padded by 4 floats: the transposing stores (32 consecutive samples
+    // of a row per warp) spread over 8 banks instead of 1; 128-bit reads stay aligned
+    __shared__ __align__(16) float sA[DW_KC][DW_TILE + 4], sB[DW_KC][DW_TILE + 4];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4; // 16 x 16 threads, 4 x 4 outputs
+    {
+        const int sp = static_cast<int>(blockIdx.z % splits);
         const long k0 = static_cast<long>(sp) * DW_SPLIT;
         const long k1 = k0 + DW_SPLIT < n ? k0 + DW_SPLIT : n;
-        float c[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+        float c[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) c[i][j] = 0.f;
         for (long kc = k0; kc < k1; kc += DW_KC) {
-            for (int idx = threadIdx.x; idx < DW_KC * DW_TILE; idx += 256) {
-                const int kk = idx % DW_KC, r = idx / DW_KC;
+            // 64 rows x 32 samples of A and of B: each thread loads 8 + 8 floats
+            // (consecutive threads -> consecutive samples of a row: coalesced)
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const int idx = threadIdx.x + 256 * r;
+                const int kk = idx % DW_KC, row = idx / DW_KC;
                 const long k = kc + kk;
                 const bool in = k < k1;
-                const int mr = m0 + r, nr = n0 + r;
-                sA[kk][r] = (in && mr < jb.M) ? jb.A[static_cast<long>(mr) * ts + k] : 0.f;
-                sB[kk][r] = (in && nr < jb.N) ? jb.B[static_cast<long>(nr) * ts + k]
-                                              : ((in && nr == jb.N) ? 1.f : 0.f);
+                const int mr = m0 + row, nr = n0 + row;
+                sA[kk][row] = (in && mr < jb.M) ? jb.A[static_cast<long>(mr) * ts + k] : 0.f;
+                sB[kk][row] = (in && nr < jb.N) ? jb.B[static_cast<long>(nr) * ts + k]
+                                                : ((in && nr == jb.N) ? 1.f : 0.f);
             }
             __syncthreads();
 #pragma unroll 8
             for (int kk = 0; kk < DW_KC; ++kk) {
-                const float a0 = sA[kk][ty], a1 = sA[kk][ty + 16];
-                const float b0 = sB[kk][tx], b1 = sB[kk][tx + 16];
-                c[0][0] = fmaf(a0, b0, c[0][0]);
-                c[0][1] = fmaf(a0, b1, c[0][1]);
-                c[1][0] = fmaf(a1, b0, c[1][0]);
-                c[1][1] = fmaf(a1, b1, c[1][1]);
+                const float4 a = *reinterpret_cast<const float4 *>(&sA[kk][ty * 4]);
+                const float4 b = *reinterpret_cast<const float4 *>(&sB[kk][tx * 4]);
+                const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) c[i][j] = fmaf(av[i], bv[j], c[i][j]);
             }
             __syncthreads();
         }
 #pragma unroll
-        for (int i = 0; i < 2; ++i)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const int mr = m0 + ty + 16 * i, nc = n0 + tx + 16 * j;
+            for (int j = 0; j < 4; ++j) {
+                const int mr = m0 + ty * 4 + i, nc = n0 + tx * 4 + j;
                 if (mr < jb.M && nc <= jb.N)
                     jb.out[(static_cast<long>(sp) * jb.M + mr) * (jb.N + 1) + nc] = c[i][j];
             }

@@ -170,7 +170,7 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
         {
             LaunchScope ls(c, DETNET_K_BACKWARD, c->stream);
             k_dw_gemm<<<dim3((mx + DW_TILE - 1) / DW_TILE, (my + DW_TILE - 1) / DW_TILE,
-                             static_cast<unsigned>(jobs.size())),
+                             static_cast<unsigned>(jobs.size() * splits)),
                         256, 0, c->stream>>>(w.jobs.as<DwJob>(), n, ts, splits);
         }
         if (int rc = check_launch()) return rc;

@@ -285,11 +285,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                 if (l != L0) mbar_wait_guard(&bars[B_VX], ph);
                 TRACE(7, l);
                 tc::fence_after();
-                for (int h = 0; h < NH; ++h) w1_steps(h, 3, 10, false);
+                // group 0 complete first (its epilogue then overlaps group 1's MMAs)
+                w1_steps(0, 3, 10, false);
                 mbar_wait_guard(&bars[B_G], ph);
                 TRACE(13, l);
                 tc::fence_after();
-                for (int h = 0; h < NH; ++h) w1_steps(h, 10, 13, true);
+                w1_steps(0, 10, 13, true);
+                for (int h = 1; h < NH; ++h) w1_steps(h, 3, 13, true);
                 TRACE(8, l);
                 mbar_wait_guard(&bars[B_W23F], ph);
                 TRACE(12, l);

@@ -26,7 +26,7 @@
 //    threads (warps w and w+4, the same TMEM lane quadrant): thread A holds
 //    rows 0-5 (105 entries) and x_hat, thread B rows 6-19 and v. G x_hat is
 //    formed on FP32 CUDA cores with a 14-float smem exchange per layer.
-// Warp roles: 0-3 "A" epilogue, 4-7 "B" epilogue, 8 TMEM alloc + weight
+// Warp roles: 4-7 "A" epilogue, 0-3 "B" epilogue, 8 TMEM alloc + weight
 // producer + single-thread MMA issuer (warps 9-11 complete its warpgroup so
 // setmaxnreg can move registers to the epilogue warpgroups).
 #include <cmath>
@@ -362,7 +362,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
     } else {
         // ========================= epilogue warps ==========================
         asm volatile("setmaxnreg.inc.sync.aligned.u32 232;" ::: "memory");
-        const bool isA = warp < 4;
+        // the x_hat / G x_hat role gets the higher warp ids: the scheduler favours them
+        const bool isA = warp >= 4;
         const int quad = warp & 3;
         const int col = quad * 32 + lane; // sample within the tile == TMEM lane
         const uint32_t trow = tbase + (static_cast<uint32_t>(quad * 32) << 16);

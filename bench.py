@@ -36,6 +36,7 @@ SNRS = [0.0, 2.0, 4.0, 6.0, 8.0, 10.0, 12.0, 14.0]
 MASTER_SEED, WEIGHT_SEED = 1, 9
 POINT_KEY = 0x45564131  # harness.cpp:133
 METRIC = "DetNet detections/sec (30x20 BPSK, L layers)"
+METRIC_TRAIN = "DetNet training samples/sec (30x20 BPSK, L=40, fwd+bwd+Adam)"
 
 
 def workload(cfg):
@@ -203,6 +204,27 @@ def run_reference_arm(args):
     if rank != 0:
         return
     L, points, _, _, _ = workload(args.config)
+    if args.config == 5:  # training: reference batch_gradient + adam_step, bounded batch
+        params, _ = build_params(5, L)
+        vals, secs = [], []
+        for s in range(args.warmup + args.steps):
+            r = cpu_train_reference(L, params, 1000)
+            if s >= args.warmup:
+                vals.append(r["value"])
+                secs.append(1000 / r["value"])
+        v = statistics.median(vals)
+        line = {"metric": METRIC_TRAIN, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(secs) / len(secs),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (reference Rng, H~N(0,1/N), FP32-representable)",
+                "config": {"workload": "config5 training step (bounded 1000-sample batch)",
+                           "layers": L}, "impl": "reference",
+                "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        line["cpu_baseline"]["value"] = v
+        print(json.dumps(line), flush=True)
+        return
     # bounded sample per step: ~2-4 s of 16-core CPU work
     per_point = {1: 2048, 2: 4096, 3: 16384, 4: 16384}[args.config]
     r = cpu_reference(args.config, per_point, args.steps, args.warmup, True)
@@ -503,7 +525,7 @@ def run_train_bench(args, torch, dist, world, rank, local, barrier, eng):
         if not args.no_cpu and world == 1:
             cpu = cpu_train_reference(L, params, 500)
         print(json.dumps({
-            "metric": "DetNet training samples/sec (30x20 BPSK, L=40, fwd+bwd+Adam)",
+            "metric": METRIC_TRAIN,
             "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",

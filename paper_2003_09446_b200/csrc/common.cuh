@@ -110,6 +110,11 @@ __device__ __forceinline__ void bulk_g2s_chunked(void *dst_smem, const void *src
 }
 
 // ---- deterministic block reductions ---------------------------------------
+// bar.sync on a named barrier (ids 1..15; 0 is __syncthreads)
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
 template <typename T> __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -199,6 +199,185 @@ __global__ void __launch_bounds__(THREADS, 1) k_train_bwd(BwdArgs a) {
     }
 }
 
+// Small-batch variant of the reverse sweep: two threads per sample. Warps 0-1
+// ("A") take hidden units [0, Z/2), warps 2-3 ("B") units [Z/2, Z) of the same
+// 64 samples; B's in_bar partial meets A's in shared memory, A forms
+// a_bar = G gx_bar + x_bar and v_bar and hands them back. The per-sample serial
+// chain halves. Weights are single-buffered (the exchange buffers take the
+// second slot); the next layer's copy is issued as soon as the last weight
+// read of this layer is done, under the exchange and the next layer's prologue.
+constexpr int BWP_SAMPLES = 64, BWP_THREADS = 128;
+
+template <int K, int Z, int V>
+__global__ void __launch_bounds__(BWP_THREADS, 1) k_train_bwd_pair(BwdArgs a) {
+    constexpr int IN = 3 * K + V;
+    constexpr int IN4 = simt_in4(K, V);
+    constexpr int O = K + V;
+    constexpr int O4 = simt_o4(K, V);
+    constexpr int NG = gram_entries(K);
+    constexpr int REC = static_cast<int>(simt_rec(K, Z, V));
+    constexpr int ZH = Z / 2, NIB = IN - K, P = BWP_SAMPLES;
+    constexpr int GRP = ZH % 8 == 0 ? 8 : (ZH % 4 == 0 ? 4 : 1); // z-trace prefetch group
+    static_assert(Z % 2 == 0, "hidden units split in halves");
+    extern __shared__ __align__(128) float sw[];
+    float(*sIB)[P] = reinterpret_cast<float(*)[P]>(sw + REC);       // [NIB][P] B -> A
+    float(*sAV)[P] = reinterpret_cast<float(*)[P]>(sw + REC + NIB * P); // [K+V][P] A -> B
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sw + REC + (NIB + O) * P);
+    __shared__ double s_t[2];
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const bool isA = warp < 2;
+    const int ls = (warp & 1) * 32 + (tid & 31);
+    const int pbar = 1 + (warp & 1);
+    const long unit = static_cast<long>(blockIdx.x) * P + ls;
+    const long tile_l = unit / TILE;
+    const bool live_tile = tile_l < a.n_tiles;
+    const long tile = live_tile ? tile_l : a.n_tiles - 1;
+    const int col = static_cast<int>(unit % TILE);
+    const long s = tile * TILE + col;
+    const bool live = live_tile && s < a.n;
+    const int i0 = isA ? 0 : ZH;
+
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const uint32_t bytes = static_cast<uint32_t>(REC) * 4u;
+    const int nl = a.L - a.lf;
+    if (tid == 0 && nl > 0) {
+        mbar_arrive_expect_tx(bar, bytes);
+        bulk_g2s_chunked(sw, a.wrec + static_cast<long>(a.L - 1) * a.rec_floats, bytes, bar);
+    }
+    const uint32_t xm = a.xmask[tile * TILE + col];
+    const float dinv2 = static_cast<float>(2.0 / a.denom[tile * TILE + col]);
+    const float *gps = a.gp + tile * NG * TILE + col;
+    float abar[K], vbar[V];
+#pragma unroll
+    for (int k = 0; k < K; ++k) abar[k] = 0.f;
+#pragma unroll
+    for (int k = 0; k < V; ++k) vbar[k] = 0.f;
+
+    for (int it = 0; it < nl; ++it) {
+        const int l = a.L - 1 - it;
+        mbar_wait(bar, it & 1);
+        const float *W = sw;
+        const float w = static_cast<float>(a.lnk[l]) * dinv2;
+        const float *xn = l + 1 < a.L ? a.tr_in + (static_cast<long>(l + 1) * IN + K) * a.ts + s
+                                      : a.tr_xf + s;
+        const float t = W[Z * IN4 + Z * O4 + O4];
+        const float tinv = 1.f / t;
+        float u2bar[K];
+        float tb = 0.f;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const float xk = (xm >> k) & 1u ? 1.f : -1.f;
+            abar[k] = fmaf(w, xn[k * a.ts] - xk, abar[k]);
+            const float u = a.tr_u2[(static_cast<long>(l) * K + k) * a.ts + s];
+            const bool lin = u >= -t && u < t; // model.cpp:45-51
+            u2bar[k] = lin ? abar[k] * tinv : 0.f;
+            tb += lin ? abar[k] * (-u * tinv * tinv) : 0.f;
+        }
+        if (isA && live_tile) {
+            float *g23 = a.g23bar + static_cast<long>(l) * O * a.ts + s;
+#pragma unroll
+            for (int k = 0; k < K; ++k) g23[k * a.ts] = live ? u2bar[k] : 0.f;
+#pragma unroll
+            for (int k = 0; k < V; ++k) g23[(K + k) * a.ts] = live ? vbar[k] : 0.f;
+        }
+        // this thread's half of the hidden units: z_bar, u1_bar, in_bar partial
+        float ibar[NIB];
+#pragma unroll
+        for (int j = 0; j < NIB; ++j) ibar[j] = 0.f;
+        const float *zl = a.tr_z + static_cast<long>(l) * Z * a.ts + s;
+        float *u1b = a.u1bar + static_cast<long>(l) * Z * a.ts + s;
+#pragma unroll 1
+        for (int g0 = i0; g0 < i0 + ZH; g0 += GRP) {
+            float zg[GRP];
+#pragma unroll
+            for (int q = 0; q < GRP; ++q) zg[q] = zl[(g0 + q) * a.ts];
+#pragma unroll
+            for (int q = 0; q < GRP; ++q) {
+                const int i = g0 + q;
+                const float4 *c4 = reinterpret_cast<const float4 *>(W + Z * IN4 + i * O4);
+                float zb0 = 0.f, zb1 = 0.f;
+#pragma unroll
+                for (int m = 0; m < O4 / 4; ++m) {
+                    const float4 c = c4[m];
+#define DETNET_G(j) ((j) < K ? u2bar[(j) < K ? (j) : 0] : vbar[((j) - K) < V ? (j) - K : 0])
+                    if (4 * m + 0 < O) zb0 = fmaf(c.x, DETNET_G(4 * m + 0), zb0);
+                    if (4 * m + 1 < O) zb1 = fmaf(c.y, DETNET_G(4 * m + 1), zb1);
+                    if (4 * m + 2 < O) zb0 = fmaf(c.z, DETNET_G(4 * m + 2), zb0);
+                    if (4 * m + 3 < O) zb1 = fmaf(c.w, DETNET_G(4 * m + 3), zb1);
+#undef DETNET_G
+                }
+                const float ub = zg[q] > 0.f ? zb0 + zb1 : 0.f;
+                if (live_tile) u1b[i * a.ts] = live ? ub : 0.f;
+                const float4 *w4 = reinterpret_cast<const float4 *>(W + i * IN4);
+#pragma unroll
+                for (int m = K / 4; m < IN4 / 4; ++m) {
+                    const float4 wv = w4[m];
+#define DETNET_IB(c, wc)                                                                        \
+    if (4 * m + (c) >= K && 4 * m + (c) < IN)                                                    \
+        ibar[(4 * m + (c) - K) >= 0 ? 4 * m + (c) - K : 0] =                                    \
+            fmaf(wc, ub, ibar[(4 * m + (c) - K) >= 0 ? 4 * m + (c) - K : 0]);
+                    DETNET_IB(0, wv.x)
+                    DETNET_IB(1, wv.y)
+                    DETNET_IB(2, wv.z)
+                    DETNET_IB(3, wv.w)
+#undef DETNET_IB
+                }
+            }
+        }
+        // every weight read of layer l is done: stream layer l-1 in now
+        __syncthreads();
+        if (tid == 0 && it + 1 < nl) {
+            mbar_arrive_expect_tx(bar, bytes);
+            bulk_g2s_chunked(sw, a.wrec + static_cast<long>(l - 1) * a.rec_floats, bytes, bar);
+        }
+        if (!isA) {
+#pragma unroll
+            for (int j = 0; j < NIB; ++j) sIB[j][ls] = ibar[j];
+        }
+        named_bar_sync(pbar, 64);
+        if (isA) {
+#pragma unroll
+            for (int j = 0; j < NIB; ++j) ibar[j] += sIB[j][ls];
+            // a_bar <- G gx_bar + x_bar (G symmetric); v_bar <- v block
+#pragma unroll
+            for (int k = 0; k < K; ++k) abar[k] = ibar[k];
+            int e = 0;
+#pragma unroll
+            for (int r = 0; r < K; ++r)
+#pragma unroll
+                for (int c = r; c < K; ++c, ++e) {
+                    const float g = __ldg(gps + e * TILE);
+                    abar[r] = fmaf(g, ibar[K + c], abar[r]);
+                    if (c != r) abar[c] = fmaf(g, ibar[K + r], abar[c]);
+                }
+#pragma unroll
+            for (int k = 0; k < V; ++k) vbar[k] = ibar[2 * K + k];
+#pragma unroll
+            for (int k = 0; k < K; ++k) sAV[k][ls] = abar[k];
+#pragma unroll
+            for (int k = 0; k < V; ++k) sAV[K + k][ls] = vbar[k];
+        }
+        named_bar_sync(pbar, 64);
+        if (!isA) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) abar[k] = sAV[k][ls];
+#pragma unroll
+            for (int k = 0; k < V; ++k) vbar[k] = sAV[K + k][ls];
+        }
+        // per-CTA t gradient (A warps; deterministic)
+        double tsum = (isA && live) ? static_cast<double>(tb) : 0.0;
+        tsum = warp_sum(tsum);
+        if (isA && (tid & 31) == 0) s_t[warp] = tsum;
+        __syncthreads(); // s_t ready; B is done reading sAV before A rewrites it
+        if (tid == 0) a.tbar_part[static_cast<long>(l) * gridDim.x + blockIdx.x] = s_t[0] + s_t[1];
+    }
+}
+
 // C[job][m][n] partial over a split of samples: C = A . B^T with A [M][ts],
 // B [N][ts]; column n == N is the bias (sum of A). Jobs = (layer, which).
 struct DwJob {
@@ -212,6 +391,10 @@ struct DwJob {
 // 16 FMAs), K = samples in chunks of 32; FP32 inside a split of DW_SPLIT
 // samples, one FP64 partial per split (summed in fixed order by k_grad_sum).
 constexpr int DW_TILE = 64, DW_SPLIT = 256, DW_KC = 32;
+// (FP64 accumulation here was measured not to change the FP32-vs-FP64 training
+// drift, which comes from gate flips in the FP32 forward/backward.)
+using DW_ACC = float;
+__device__ __forceinline__ float dw_fma(float a, float b, float c) { return fmaf(a, b, c); }
 
 // grid: (N tiles, M tiles, jobs x splits) -- one (tile, split) per CTA
 __global__ void __launch_bounds__(256) k_dw_gemm(const DwJob *jobs, long n, long ts, int splits) {
@@ -226,11 +409,11 @@ __global__ void __launch_bounds__(256) k_dw_gemm(const DwJob *jobs, long n, long
         const int sp = static_cast<int>(blockIdx.z % splits);
         const long k0 = static_cast<long>(sp) * DW_SPLIT;
         const long k1 = k0 + DW_SPLIT < n ? k0 + DW_SPLIT : n;
-        float c[4][4];
+        DW_ACC c[4][4];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) c[i][j] = 0.f;
+            for (int j = 0; j < 4; ++j) c[i][j] = 0;
         for (long kc = k0; kc < k1; kc += DW_KC) {
             // 64 rows x 32 samples of A and of B: each thread loads 8 + 8 floats
             // (consecutive threads -> consecutive samples of a row: coalesced)
@@ -254,7 +437,7 @@ __global__ void __launch_bounds__(256) k_dw_gemm(const DwJob *jobs, long n, long
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) c[i][j] = fmaf(av[i], bv[j], c[i][j]);
+                    for (int j = 0; j < 4; ++j) c[i][j] = dw_fma(av[i], bv[j], c[i][j]);
             }
             __syncthreads();
         }

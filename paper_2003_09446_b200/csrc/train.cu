@@ -6,6 +6,7 @@
 // (device-resident step; raw gradient sums in a caller buffer so ranks can
 // all-reduce them between the two calls).
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -18,18 +19,24 @@ namespace {
 
 using BwdFn = void (*)(dim3, dim3, size_t, cudaStream_t, const BwdArgs &);
 
-constexpr int BWD_SMALL = 64, BWD_LARGE = 256; // samples per CTA (k_train_bwd)
+constexpr int BWD_LARGE = 256; // samples per CTA of k_train_bwd (large batches)
+template <int K, int Z, int V> constexpr size_t pair_smem() {
+    return (static_cast<size_t>(simt_rec(K, Z, V)) + (3 * K + V - K + K + V) * BWP_SAMPLES) * 4 + 64;
+}
 
 template <int K, int Z, int V>
 void launch_bwd(dim3 g, dim3 b, size_t sm, cudaStream_t st, const BwdArgs &a) {
-    if (b.x == BWD_SMALL) k_train_bwd<K, Z, V, BWD_SMALL><<<g, b, sm, st>>>(a);
-    else k_train_bwd<K, Z, V, BWD_LARGE><<<g, b, sm, st>>>(a);
+    if (b.x == BWP_THREADS) {
+        k_train_bwd_pair<K, Z, V><<<g, b, pair_smem<K, Z, V>(), st>>>(a);
+    } else {
+        k_train_bwd<K, Z, V, BWD_LARGE><<<g, b, sm, st>>>(a);
+    }
 }
 template <int K, int Z, int V> int set_bwd_smem() {
     const int bytes = static_cast<int>(2 * simt_rec(K, Z, V) * 4 + 64);
-    const bool ok = cudaFuncSetAttribute(k_train_bwd<K, Z, V, BWD_SMALL>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
-                        cudaSuccess &&
+    const bool ok = cudaFuncSetAttribute(k_train_bwd_pair<K, Z, V>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(pair_smem<K, Z, V>())) == cudaSuccess &&
                     cudaFuncSetAttribute(k_train_bwd<K, Z, V, BWD_LARGE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
                         cudaSuccess;
@@ -111,8 +118,11 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
     TrainWs &w = ws_for(c);
     const int splits = static_cast<int>((n + DW_SPLIT - 1) / DW_SPLIT);
     // one CTA per SM: small batches use 64-sample CTAs to reach more SMs
-    const int bwd_per = tiles * TILE / BWD_LARGE >= c->sms ? BWD_LARGE : BWD_SMALL;
-    const int bwd_blocks = static_cast<int>((tiles * TILE + bwd_per - 1) / bwd_per);
+    // small batches: two threads per sample, 64 samples per CTA (k_train_bwd_pair)
+    const bool bwd_large = tiles * TILE / BWD_LARGE >= c->sms;
+    const int bwd_samples = bwd_large ? BWD_LARGE : BWP_SAMPLES;
+    const int bwd_per = bwd_large ? BWD_LARGE : BWP_THREADS;
+    const int bwd_blocks = static_cast<int>((tiles * TILE + bwd_samples - 1) / bwd_samples);
     if (w.tr_in.ensure(sizeof(float) * L * IN * ts) || w.tr_z.ensure(sizeof(float) * L * Z * ts) ||
         w.tr_u2.ensure(sizeof(float) * L * K * ts) || w.tr_xf.ensure(sizeof(float) * K * ts) ||
         w.u1bar.ensure(sizeof(float) * L * Z * ts) || w.g23bar.ensure(sizeof(float) * L * O * ts) ||

@@ -38,7 +38,10 @@ using PreFn = void (*)(dim3, dim3, size_t, cudaStream_t, long, int, const float 
                        const int8_t *, float *, float *, double *, uint32_t *, uint8_t *,
                        unsigned long long *, const long *, const int *);
 using SimtFn = void (*)(dim3, dim3, size_t, cudaStream_t, const StackArgs &);
-constexpr int SIMT_SMALL = 64, SIMT_LARGE = 256; // samples per CTA (k_stack_simt)
+constexpr int SIMT_LARGE = 256; // samples per CTA of k_stack_simt (large batches)
+template <int K, int Z, int V> constexpr size_t simt_pair_smem() {
+    return (2 * static_cast<size_t>(simt_rec(K, Z, V)) + (K + V) * SIMTP_SAMPLES) * 4 + 64;
+}
 
 template <int K>
 void launch_pre(dim3 g, dim3 b, size_t sm, cudaStream_t st, long n, int N, const float *H,
@@ -101,14 +104,15 @@ template <int K> int set_fast_smem() {
 
 template <int K, int Z, int V>
 void launch_simt(dim3 g, dim3 b, size_t sm, cudaStream_t st, const StackArgs &a) {
-    if (b.x == SIMT_SMALL) k_stack_simt<K, Z, V, SIMT_SMALL><<<g, b, sm, st>>>(a);
+    if (b.x == SIMTP_THREADS) k_stack_simt_pair<K, Z, V><<<g, b, simt_pair_smem<K, Z, V>(), st>>>(a);
     else k_stack_simt<K, Z, V, SIMT_LARGE><<<g, b, sm, st>>>(a);
 }
 
 template <int K, int Z, int V> int set_simt_smem() {
     const int bytes = static_cast<int>(2 * simt_rec(K, Z, V) * 4 + 64);
-    const bool ok = cudaFuncSetAttribute(k_stack_simt<K, Z, V, SIMT_SMALL>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
+    const bool ok = cudaFuncSetAttribute(k_stack_simt_pair<K, Z, V>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(simt_pair_smem<K, Z, V>())) ==
                         cudaSuccess &&
                     cudaFuncSetAttribute(k_stack_simt<K, Z, V, SIMT_LARGE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
@@ -459,12 +463,13 @@ int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, 
         a.ts = trace->ts;
     }
     const size_t smem = 2 * static_cast<size_t>(m->simt_rec) * 4 + 64;
-    // one CTA per SM: small batches use 64-sample CTAs to reach more SMs
-    const int per = nt * TILE / SIMT_LARGE >= c->sms ? SIMT_LARGE : SIMT_SMALL;
-    const int blocks = static_cast<int>((nt * TILE + per - 1) / per);
+    // one CTA per SM: small batches use 64-sample CTAs, two threads per sample
+    const bool large = nt * TILE / SIMT_LARGE >= c->sms;
+    const int samples = large ? SIMT_LARGE : SIMTP_SAMPLES;
+    const int blocks = static_cast<int>((nt * TILE + samples - 1) / samples);
     {
         LaunchScope ls(c, DETNET_K_STACK, st);
-        m->dims->simt(dim3(blocks), dim3(per), smem, st, a);
+        m->dims->simt(dim3(blocks), dim3(large ? SIMT_LARGE : SIMTP_THREADS), smem, st, a);
     }
     return check_launch();
 }

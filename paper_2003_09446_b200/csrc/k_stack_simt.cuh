@@ -247,6 +247,221 @@ __global__ void __launch_bounds__(THREADS, 1) k_stack_simt(StackArgs a) {
     }
 }
 
+// Small-batch variant: two threads per sample. Warps 0-1 ("A") take hidden
+// units [0, Z/2), warps 2-3 ("B") units [Z/2, Z) of the same 64 samples. Each
+// forms its units' u1 / z and a partial [u2; v'] over them; B's partial meets
+// A's in shared memory, A applies psi_t, the loss and the outputs and hands
+// x_hat, v back. Weights stay double-buffered (the exchange is 15 KB).
+constexpr int SIMTP_SAMPLES = 64, SIMTP_THREADS = 128;
+
+template <int K, int Z, int V>
+__global__ void __launch_bounds__(SIMTP_THREADS, 1) k_stack_simt_pair(StackArgs a) {
+    constexpr int IN = 3 * K + V;
+    constexpr int IN4 = simt_in4(K, V);
+    constexpr int O = K + V;
+    constexpr int O4 = simt_o4(K, V);
+    constexpr int NG = gram_entries(K);
+    constexpr int REC = static_cast<int>(simt_rec(K, Z, V));
+    constexpr int ZH = Z / 2, P = SIMTP_SAMPLES;
+    static_assert(Z % 2 == 0, "hidden units split in halves");
+    extern __shared__ __align__(128) float sw[];
+    float(*sX)[P] = reinterpret_cast<float(*)[P]>(sw + 2 * REC); // [O][P] exchange
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sw + 2 * REC + O * P);
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const bool isA = warp < 2;
+    const int ls = (warp & 1) * 32 + (tid & 31);
+    const int pbar = 1 + (warp & 1);
+    const long unit = static_cast<long>(blockIdx.x) * P + ls;
+    const long tile_l = unit / TILE;
+    const bool live_tile = tile_l < a.n_tiles;
+    const long tile = live_tile ? tile_l : a.n_tiles - 1;
+    const int col = static_cast<int>(unit % TILE);
+    const long s = tile * TILE + col;
+    const bool live = live_tile && s < a.n;
+    const long gt = a.tile0 + tile;
+    const int i0 = isA ? 0 : ZH;
+
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const uint32_t bytes = static_cast<uint32_t>(REC) * 4u;
+    if (tid == 0) {
+        for (int b = 0; b < 2; ++b) {
+            const int l = a.l_begin + b;
+            if (l < a.l_end) {
+                mbar_arrive_expect_tx(&bars[b], bytes);
+                bulk_g2s_chunked(sw + b * REC, a.wrec + static_cast<long>(l) * a.rec_floats, bytes,
+                                 &bars[b]);
+            }
+        }
+    }
+
+    float q[K], x[K], v[V];
+#pragma unroll
+    for (int k = 0; k < K; ++k) q[k] = a.q32[(gt * K + k) * TILE + col];
+    if (a.x_state && live) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) x[k] = a.x_state[s * K + k];
+#pragma unroll
+        for (int k = 0; k < V; ++k) v[k] = a.v_state[s * V + k];
+    } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k) x[k] = 0.f;
+#pragma unroll
+        for (int k = 0; k < V; ++k) v[k] = 0.f;
+    }
+    const uint32_t xm = a.xmask[gt * TILE + col];
+    const double dnm = a.denom[gt * TILE + col];
+    double loss = 0.0;
+    const int nl = a.l_end - a.l_begin;
+    const float *gps = a.gp + gt * NG * TILE + col;
+
+    for (int l = a.l_begin; l < a.l_end; ++l) {
+        const int it = l - a.l_begin;
+        const int b = it & 1;
+        mbar_wait(&bars[b], (it >> 1) & 1);
+        const float *W = sw + b * REC;
+
+        float gx[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) gx[k] = 0.f;
+        {
+            int e = 0;
+#pragma unroll
+            for (int r = 0; r < K; ++r)
+#pragma unroll
+                for (int c = r; c < K; ++c, ++e) {
+                    const float g = __ldg(gps + e * TILE);
+                    gx[r] = fmaf(g, x[c], gx[r]);
+                    if (c != r) gx[c] = fmaf(g, x[r], gx[c]);
+                }
+        }
+        if (isA && a.tr_in && live_tile) {
+            float *ti = a.tr_in + static_cast<long>(l) * IN * a.ts + s;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                ti[k * a.ts] = q[k];
+                ti[(K + k) * a.ts] = x[k];
+                ti[(2 * K + k) * a.ts] = gx[k];
+            }
+#pragma unroll
+            for (int k = 0; k < V; ++k) ti[(3 * K + k) * a.ts] = v[k];
+        }
+        float acc[O];
+        const float *b23 = W + Z * IN4 + Z * O4;
+#pragma unroll
+        for (int o = 0; o < O; ++o) acc[o] = isA ? b23[o] : 0.f;
+
+#define DETNET_IN(j)                                                                            \
+    ((j) < K ? q[(j) < K ? (j) : 0]                                                             \
+             : (j) < 2 * K ? x[((j) - K) < K ? (j) - K : 0]                                      \
+                           : (j) < 3 * K ? gx[((j) - 2 * K) < K ? (j) - 2 * K : 0]               \
+                                         : v[((j) - 3 * K) < V ? (j) - 3 * K : 0])
+#pragma unroll 1
+        for (int i = i0; i < i0 + ZH; ++i) {
+            const float4 *w4 = reinterpret_cast<const float4 *>(W + i * IN4);
+            float u0 = 0.f, u1 = 0.f, u2 = 0.f, u3 = 0.f;
+#pragma unroll
+            for (int m = 0; m < IN4 / 4; ++m) {
+                const float4 w = w4[m];
+                if (4 * m + 0 < IN) u0 = fmaf(w.x, DETNET_IN(4 * m + 0), u0);
+                else if (4 * m + 0 == IN) u0 += w.x;
+                if (4 * m + 1 < IN) u1 = fmaf(w.y, DETNET_IN(4 * m + 1), u1);
+                else if (4 * m + 1 == IN) u1 += w.y;
+                if (4 * m + 2 < IN) u2 = fmaf(w.z, DETNET_IN(4 * m + 2), u2);
+                else if (4 * m + 2 == IN) u2 += w.z;
+                if (4 * m + 3 < IN) u3 = fmaf(w.w, DETNET_IN(4 * m + 3), u3);
+                else if (4 * m + 3 == IN) u3 += w.w;
+            }
+            const float u = (u0 + u1) + (u2 + u3);
+            const float z = u > 0.f ? u : 0.f;
+            if (a.tr_z && live_tile) a.tr_z[(static_cast<long>(l) * Z + i) * a.ts + s] = z;
+            const float4 *c4 = reinterpret_cast<const float4 *>(W + Z * IN4 + i * O4);
+#pragma unroll
+            for (int m = 0; m < O4 / 4; ++m) {
+                const float4 w = c4[m];
+                if (4 * m + 0 < O) acc[4 * m + 0] = fmaf(w.x, z, acc[4 * m + 0]);
+                if (4 * m + 1 < O) acc[4 * m + 1] = fmaf(w.y, z, acc[4 * m + 1]);
+                if (4 * m + 2 < O) acc[4 * m + 2] = fmaf(w.z, z, acc[4 * m + 2]);
+                if (4 * m + 3 < O) acc[4 * m + 3] = fmaf(w.w, z, acc[4 * m + 3]);
+            }
+        }
+#undef DETNET_IN
+        const float t = W[Z * IN4 + Z * O4 + O4];
+        __syncthreads(); // every weight read of buffer b is done
+        if (tid == 0 && l + 2 < a.l_end) {
+            mbar_arrive_expect_tx(&bars[b], bytes);
+            bulk_g2s_chunked(sw + b * REC, a.wrec + static_cast<long>(l + 2) * a.rec_floats, bytes,
+                             &bars[b]);
+        }
+        if (!isA) {
+#pragma unroll
+            for (int o = 0; o < O; ++o) sX[o][ls] = acc[o];
+        }
+        named_bar_sync(pbar, 64);
+        if (isA) {
+#pragma unroll
+            for (int o = 0; o < O; ++o) acc[o] += sX[o][ls];
+            double err = 0.0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const float u = acc[k];
+                if (a.tr_u2 && live_tile) a.tr_u2[(static_cast<long>(l) * K + k) * a.ts + s] = u;
+                const float xn = u <= -t ? -1.f : (u >= t ? 1.f : __fdiv_rn(u, t));
+                x[k] = xn;
+                const double d = ((xm >> k) & 1u ? 1.0 : -1.0) - static_cast<double>(xn);
+                err += d * d;
+            }
+#pragma unroll
+            for (int k = 0; k < V; ++k) v[k] = acc[K + k];
+            loss += a.lnk[l] * err / dnm;
+            if (a.xhat && live) {
+                float *o = a.xhat + (s * nl + it) * K;
+#pragma unroll
+                for (int k = 0; k < K; ++k) o[k] = x[k];
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k) sX[k][ls] = x[k];
+#pragma unroll
+            for (int k = 0; k < V; ++k) sX[K + k][ls] = v[k];
+        }
+        named_bar_sync(pbar, 64);
+        if (!isA) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) x[k] = sX[k][ls];
+#pragma unroll
+            for (int k = 0; k < V; ++k) v[k] = sX[K + k][ls];
+        }
+        named_bar_sync(pbar, 64); // B has read before A overwrites next layer
+    }
+
+    if (!isA) return;
+    if (a.x_state && live) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) a.x_state[s * K + k] = x[k];
+#pragma unroll
+        for (int k = 0; k < V; ++k) a.v_state[s * V + k] = v[k];
+    }
+    if (a.tr_xf && live_tile) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) a.tr_xf[k * a.ts + s] = x[k];
+    }
+    long long errs = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) errs += (x[k] >= 0.f) != (((xm >> k) & 1u) != 0);
+    if (!live) { loss = 0.0; errs = 0; }
+    loss = warp_sum(loss);
+    errs = warp_sum(errs);
+    if ((tid & 31) == 0 && live_tile) {
+        a.tile_loss[gt * 4 + col / 32] = loss;
+        a.tile_err[gt * 4 + col / 32] = errs;
+    }
+}
+
 // K5: fixed-order reduction of per-tile partials and per-sample flags.
 static __global__ void __launch_bounds__(1024) k_reduce(const double *tile_loss, const long long *tile_err,
                                                  long n_tiles, const uint8_t *flag, long n,

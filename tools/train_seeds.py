@@ -11,6 +11,7 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 192
 L = int(sys.argv[2]) if len(sys.argv) > 2 else L
 orc = Oracle()
 ctx = eng.Context(0)
+if os.environ.get("TC_FWD"): ctx.set_train_forward(True)
 for pseed, dseed in [(9, 1), (9, 2), (10, 1), (11, 3), (12, 4)]:
     params = xavier_params(K, L, seed=pseed)
     m = ctx.model(K, N, 8 * K, 2 * K, params)

@@ -262,7 +262,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--path", default="auto", choices=["auto", "simt", "tc"])
+    ap.add_argument("--path", default="auto", choices=["auto", "simt", "tc", "sparse"])
     ap.add_argument("--train-fwd", default="simt", choices=["simt", "tc"],
                     help="config 5: training forward on FP32 cores (default, parity) or tcgen05")
     ap.add_argument("--no-e2e", action="store_true")
@@ -293,7 +293,7 @@ def main():
     params, masks = build_params(args.config, L)
     peaks = measured_peaks(torch) if rank == 0 else {}
 
-    ctx = eng.Context(local, path={"auto": 0, "simt": 1, "tc": 2}[args.path])
+    ctx = eng.Context(local, path={"auto": 0, "simt": 1, "tc": 2, "sparse": 3}[args.path])
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     model = ctx.model(K, N, Z, V, params, masks=masks)

@@ -181,13 +181,17 @@ int pack_simt(detnet_model *m, const double *params, const double *masks, std::v
 }
 
 // Sparse layer streams for k_stack_sparse (format in k_stack_sparse.cuh).
+size_t sparse_smem(int max_words) {
+    return sizeof(float) * TILE * (3 * 20 + 40 + 2 * 60 + 20) + 2 * sizeof(int) * max_words + 16;
+}
+
 int pack_sparse(detnet_model *m, const double *params, const double *masks) {
     m->sparse_ready = false;
     const int K = m->K, Z = m->Z, V = m->V, IN = 3 * K + V;
     const long P = record_size(K, Z, V);
     long nnz = 0, total = static_cast<long>(m->L) * (Z * IN + K * Z + V * Z);
     std::vector<int> st;
-    std::vector<long> offs(m->L);
+    std::vector<long> offs(m->L + 1);
     auto fbits = [](float f) { int i; std::memcpy(&i, &f, 4); return i; };
     for (int l = 0; l < m->L; ++l) {
         const double *p = params + l * P;
@@ -246,12 +250,19 @@ int pack_sparse(detnet_model *m, const double *params, const double *masks) {
         st[base + 1] = split;
         st[base + 2] = static_cast<int>(tail);
     }
+    while (st.size() % 4) st.push_back(0);
+    offs[m->L] = static_cast<long>(st.size());
+    long max_words = 0;
+    for (int l = 0; l < m->L; ++l) max_words = std::max(max_words, offs[l + 1] - offs[l]);
+    m->sparse_max_words = static_cast<int>((max_words + 3) / 4 * 4);
     m->density = total ? static_cast<double>(nnz) / static_cast<double>(total) : 1.0;
     if (m->sparse_stream.ensure(st.size() * 4) || m->sparse_off.ensure(offs.size() * 8))
         return fail(DETNET_ERR_CUDA, "sparse stream allocation");
     CK(cudaMemcpy(m->sparse_stream.p, st.data(), st.size() * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(m->sparse_off.p, offs.data(), offs.size() * 8, cudaMemcpyHostToDevice));
-    m->sparse_ready = (K == 20 && V == 40);
+    // the kernel stages two layer streams next to its 120 KB of activations
+    m->sparse_ready = (K == 20 && V == 40) &&
+                      sparse_smem(m->sparse_max_words) <= 232448;
     return 0;
 }
 
@@ -397,6 +408,7 @@ int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, 
         sa.xmask = c->xmask.as<uint32_t>();
         sa.stream = m->sparse_stream.as<int>();
         sa.lay_off = m->sparse_off.as<long>();
+        sa.max_words = m->sparse_max_words;
         sa.lnk = (trainable_only ? m->lnk_train : m->lnk_all).as<double>();
         sa.L = m->L;
         sa.n = n_local;
@@ -405,8 +417,10 @@ int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, 
         sa.xhat = xhat;
         sa.tile_loss = c->tile_loss.as<double>();
         sa.tile_err = c->tile_err.as<long long>();
-        const size_t smem = sizeof(float) * TILE * (3 * 20 + 40 + 2 * 60 + 20);
-        const int grid = static_cast<int>(std::min<long>(nt, 148));
+        const size_t smem = sparse_smem(m->sparse_max_words);
+        CK(cudaFuncSetAttribute(k_stack_sparse<20, 40>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+        const int grid = static_cast<int>(std::min<long>(nt, c->sms));
         {
             LaunchScope ls(c, DETNET_K_STACK, st);
             k_stack_sparse<20, 40><<<grid, 256, smem, st>>>(sa);
@@ -573,8 +587,6 @@ int detnet_ctx_create(int device, detnet_ctx **out) {
         if (d.prep() || (d.prep_fast && d.prep_fast()))
             return fail(DETNET_ERR_CUDA, "cudaFuncSetAttribute (smem) failed");
     if (int rc = tc_prepare()) return rc;
-    CK(cudaFuncSetAttribute(k_stack_sparse<20, 40>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(sizeof(float) * TILE * (3 * 20 + 40 + 2 * 60 + 20))));
     *out = c;
     return 0;
 }

@@ -142,6 +142,7 @@ struct detnet_model {
     bool tc_stale = false;  // tcgen05 images lag the device master params
     // sparse path (k_stack_sparse.cuh): CSR-like stream of surviving weights
     detnet::DBuf sparse_stream, sparse_off;
+    int sparse_max_words = 0; // largest per-layer stream (shared-memory staging)
     bool sparse_ready = false;
     double density = 1.0;   // surviving W entries / all W entries
 };

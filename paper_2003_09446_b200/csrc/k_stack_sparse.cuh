@@ -32,7 +32,8 @@ struct SparseArgs {
     const double *denom;
     const uint32_t *xmask;
     const int *stream;      // all layers
-    const long *lay_off;    // [L]
+    const long *lay_off;    // [L + 1] word offsets (16-byte aligned), last = total
+    int max_words;          // largest layer stream (shared-memory staging slot)
     const double *lnk;
     int L;
     long n, n_tiles, tile0;
@@ -54,12 +55,35 @@ __global__ void __launch_bounds__(256, 1) k_stack_sparse(SparseArgs a) {
     float(*sin)[TILE] = reinterpret_cast<float(*)[TILE]>(smx);                  // [IN][TILE]
     float(*acc)[O][TILE] = reinterpret_cast<float(*)[O][TILE]>(smx + IN * TILE); // [2][O][TILE]
     float(*gxp)[TILE] = reinterpret_cast<float(*)[TILE]>(smx + IN * TILE + 2 * O * TILE); // [K][TILE]
+    // layer streams staged in shared memory (double-buffered bulk copies), so the
+    // warp-uniform entry reads are shared-memory broadcasts instead of L1/L2 trips
+    int *stage = reinterpret_cast<int *>(smx + IN * TILE + 2 * O * TILE + K * TILE);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(stage + 2 * a.max_words);
     __shared__ double s_loss[4];
     __shared__ long long s_err[4];
 
     const int tid = threadIdx.x;
     const int half = tid >> 7, col = tid & (TILE - 1);
     const int warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const long my_tiles = a.n_tiles > blockIdx.x ? (a.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const long total_it = my_tiles * a.L;
+    auto load_layer = [&](long itn) { // iteration itn -> layer itn % L into slot itn & 1
+        const int l = static_cast<int>(itn % a.L);
+        const uint32_t bytes = static_cast<uint32_t>(a.lay_off[l + 1] - a.lay_off[l]) * 4u;
+        mbar_arrive_expect_tx(&bars[itn & 1], bytes);
+        bulk_g2s_chunked(stage + (itn & 1) * a.max_words, a.stream + a.lay_off[l], bytes,
+                         &bars[itn & 1]);
+    };
+    if (tid == 0) {
+        for (long itn = 0; itn < 2 && itn < total_it; ++itn) load_layer(itn);
+    }
+    long it = 0;
     for (long tile = blockIdx.x; tile < a.n_tiles; tile += gridDim.x) {
         const long gt = a.tile0 + tile;
         const long s = tile * TILE + col;
@@ -83,8 +107,9 @@ __global__ void __launch_bounds__(256, 1) k_stack_sparse(SparseArgs a) {
         const uint32_t xm = a.xmask[gt * TILE + col];
         double wsum = 0.0;
         __syncthreads();
-        for (int l = 0; l < a.L; ++l) {
-            const int *ls = a.stream + a.lay_off[l];
+        for (int l = 0; l < a.L; ++l, ++it) {
+            mbar_wait(&bars[it & 1], static_cast<uint32_t>((it >> 1) & 1));
+            const int *ls = stage + (it & 1) * a.max_words;
             // ---- G x_hat: half 0 rows 0..R0-1, half 1 rows R0..K-1 ----
             float x[K], gx[K];
 #pragma unroll
@@ -129,20 +154,19 @@ __global__ void __launch_bounds__(256, 1) k_stack_sparse(SparseArgs a) {
             const int2 *ent = reinterpret_cast<const int2 *>(ls + 4 + 5 * nu + ((4 + 5 * nu) & 1));
             const int u0 = half == 0 ? 0 : split, u1 = half == 0 ? split : nu;
             for (int u = u0; u < u1; ++u) {
-                const int4 un = __ldg(units + u);
-                float p0 = __ldg(b1 + u), p1 = 0.f, p2 = 0.f, p3 = 0.f;
+                const int4 un = units[u];
+                float p0 = b1[u], p1 = 0.f, p2 = 0.f, p3 = 0.f;
                 int e = un.x;
                 // 4 independent gathers in flight per step (entries of a row are distinct)
                 for (; e + 4 <= un.y; e += 4) {
-                    const int2 c0 = __ldg(ent + e), c1 = __ldg(ent + e + 1), c2 = __ldg(ent + e + 2),
-                               c3 = __ldg(ent + e + 3);
+                    const int2 c0 = ent[e], c1 = ent[e + 1], c2 = ent[e + 2], c3 = ent[e + 3];
                     p0 = fmaf(__int_as_float(c0.y), sin[c0.x][col], p0);
                     p1 = fmaf(__int_as_float(c1.y), sin[c1.x][col], p1);
                     p2 = fmaf(__int_as_float(c2.y), sin[c2.x][col], p2);
                     p3 = fmaf(__int_as_float(c3.y), sin[c3.x][col], p3);
                 }
                 for (; e < un.y; ++e) {
-                    const int2 c = __ldg(ent + e);
+                    const int2 c = ent[e];
                     p0 = fmaf(__int_as_float(c.y), sin[c.x][col], p0);
                 }
                 const float uu = (p0 + p1) + (p2 + p3);
@@ -151,8 +175,7 @@ __global__ void __launch_bounds__(256, 1) k_stack_sparse(SparseArgs a) {
                     // read-modify-writes of a group of 4 are independent
                     e = un.z;
                     for (; e + 4 <= un.w; e += 4) {
-                        const int2 c0 = __ldg(ent + e), c1 = __ldg(ent + e + 1),
-                                   c2 = __ldg(ent + e + 2), c3 = __ldg(ent + e + 3);
+                        const int2 c0 = ent[e], c1 = ent[e + 1], c2 = ent[e + 2], c3 = ent[e + 3];
                         const float a0 = acc[half][c0.x][col], a1 = acc[half][c1.x][col],
                                     a2 = acc[half][c2.x][col], a3 = acc[half][c3.x][col];
                         acc[half][c0.x][col] = fmaf(__int_as_float(c0.y), uu, a0);
@@ -161,7 +184,7 @@ __global__ void __launch_bounds__(256, 1) k_stack_sparse(SparseArgs a) {
                         acc[half][c3.x][col] = fmaf(__int_as_float(c3.y), uu, a3);
                     }
                     for (; e < un.w; ++e) {
-                        const int2 c = __ldg(ent + e);
+                        const int2 c = ent[e];
                         acc[half][c.x][col] = fmaf(__int_as_float(c.y), uu, acc[half][c.x][col]);
                     }
                 }
@@ -173,13 +196,13 @@ __global__ void __launch_bounds__(256, 1) k_stack_sparse(SparseArgs a) {
             if (half == 1) {
 #pragma unroll
                 for (int k = 0; k < V; ++k)
-                    sin[3 * K + k][col] = __ldg(b23 + k) + acc[0][k][col] + acc[1][k][col];
+                    sin[3 * K + k][col] = b23[k] + acc[0][k][col] + acc[1][k][col];
             } else {
-                const float t = __ldg(b23 + 64), tinv = __ldg(b23 + 65);
+                const float t = b23[64], tinv = b23[65];
                 float err = 0.f;
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
-                    const float uu = __ldg(b23 + V + k) + acc[0][V + k][col] + acc[1][V + k][col];
+                    const float uu = b23[V + k] + acc[0][V + k][col] + acc[1][V + k][col];
                     const float xn = uu <= -t ? -1.f : (uu >= t ? 1.f : uu * tinv);
                     sin[K + k][col] = xn;
                     const float d = ((xm >> k) & 1u ? 1.f : -1.f) - xn;
@@ -194,7 +217,8 @@ __global__ void __launch_bounds__(256, 1) k_stack_sparse(SparseArgs a) {
                         o[k] = make_float4(x[4 * k], x[4 * k + 1], x[4 * k + 2], x[4 * k + 3]);
                 }
             }
-            __syncthreads();
+            __syncthreads(); // every thread is done with slot it & 1
+            if (tid == 0 && it + 2 < total_it) load_layer(it + 2);
         }
         if (half == 0) {
             long long errs = 0;

@@ -367,7 +367,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
         const int quad = warp & 3;
         const int col = quad * 32 + lane; // sample within the tile == TMEM lane
         const uint32_t trow = tbase + (static_cast<uint32_t>(quad * 32) << 16);
-        const int pair_bar = 1 + quad;
+        // one-way hand-offs between the two threads of a sample (producer
+        // arrives, consumer syncs): x_hat A -> B, G x_hat partial B -> A
+        const int bar_x = 1 + quad, bar_g = 6 + quad;
         long it = 0;
         for (long ti = 0; ti < my_tiles; ++ti) {
             const long tile = blockIdx.x + ti * gridDim.x;
@@ -454,7 +456,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                             gx[r] = fmaf(g[e], x[c], gx[r]);
                             if (c != r) gx[c] = fmaf(g[e], x[r], gx[c]);
                         }
-                    tc::named_bar(pair_bar, 64);
+                    tc::named_bar(bar_g, 64);
 #pragma unroll
                     for (int k = 6; k < KX; ++k) gx[k] += sGX[k * 128 + col];
                     if constexpr (TR) {
@@ -515,7 +517,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                         }
 #pragma unroll
                     for (int k = 6; k < KX; ++k) sGX[k * 128 + col] = part[k];
-                    tc::named_bar(pair_bar, 64);
+                    tc::named_arrive(bar_g, 64);
                 }
                 TRACE(2 + tb16, l);
 
@@ -568,10 +570,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
                                            p.ts);
 #pragma unroll
                     for (int k = 0; k < KX; ++k) sGX[k * 128 + col] = x[k];
-                    tc::named_bar(pair_bar, 64);
+                    tc::named_arrive(bar_x, 64);
                 } else {
                     epi2_layer<false, C_U2>(trow, bt, x, v, &bars[B_E2L], tr2);
-                    tc::named_bar(pair_bar, 64);
+                    tc::named_bar(bar_x, 64);
 #pragma unroll
                     for (int k = 0; k < KX; ++k) x[k] = sGX[k * 128 + col];
                 }

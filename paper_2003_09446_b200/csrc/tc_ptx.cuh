@@ -184,6 +184,10 @@ __device__ __forceinline__ uint32_t opaque32(uint32_t v) {
 __device__ __forceinline__ void named_bar(int id, int threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
+// producer side of a one-way hand-off: signal without waiting for the consumer
+__device__ __forceinline__ void named_arrive(int id, int threads) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 
 } // namespace tc
 } // namespace detnet

@@ -116,7 +116,8 @@ def _train_100(ctx, oracle, pseed, dseed, K=20, N=30, L=6, n=192, steps=100):
     return rels, rel, v0 - evg.data_loss, v0 - evo["data_loss"]
 
 
-def test_training_100_steps_tracks_oracle(ctx, oracle):
+@pytest.mark.parametrize("tc_forward", [False, True])
+def test_training_100_steps_tracks_oracle(oracle, tc_forward):
     """FP32 training against the FP64 reference over five seed pairs.
 
     The trajectories agree to FP32 noise (step 0 < 1e-6, measured ~3e-8) until
@@ -127,7 +128,12 @@ def test_training_100_steps_tracks_oracle(ctx, oracle):
     training parity). North-star target: training losses within 1e-3 after 100
     steps -- met at the centre of the measured distribution, not per run (the
     median over seeds is asserted, with every run within 5e-3). Both runs must
-    also improve the validation loss by the same amount (within 5 %)."""
+    also improve the validation loss by the same amount (within 5 %).
+    Run for the default FP32 training forward and for the opt-in tcgen05 one
+    (detnet_ctx_set_train_forward)."""
+    from paper_2003_09446_b200 import Context
+    ctx = Context(0)
+    ctx.set_train_forward(tc_forward)
     finals, tracked = [], []
     for pseed, dseed in [(9, 1), (9, 2), (10, 1), (11, 3), (12, 4)]:
         rels, rel, dg, do = _train_100(ctx, oracle, pseed, dseed)

@@ -367,6 +367,12 @@ def main():
         peak_note = (f"{peaks.get('peaks_source')} bf16 {peaks.get('bf16_tflops')} TF/s (burst) "
                      "/ 2 (TF32 rate) / 3 (3xTF32 split); this run's cuBLAS TF32 GEMM: "
                      f"{peaks.get('tf32_tflops', 0):.0f} TF/s")
+    elif tc_path == "tcgen05-split-fp16":
+        # FP16 MMAs run at the bf16 rate; every FP32-class product is three of
+        # them (hi.hi + hi.lo + lo.hi)
+        peak = peaks["bf16_tflops"] / 3.0 if peaks.get("bf16_tflops") else None
+        peak_note = (f"{peaks.get('peaks_source')} bf16 {peaks.get('bf16_tflops')} TF/s (burst; "
+                     "FP16 MMA rate) / 3 (split-FP16 products hi.hi + hi.lo + lo.hi)")
     else:
         peak = peaks.get("fp32_tflops")
         peak_note = "measured cuBLAS FP32 SGEMM (CUDA-core FP32 pipe), this run"

@@ -52,8 +52,10 @@ typedef struct detnet_model detnet_model;
 int detnet_ctx_create(int device, detnet_ctx **out);
 void detnet_ctx_destroy(detnet_ctx *ctx);
 const char *detnet_last_error(void);
-/* Kernel-path selection: 0 auto (tcgen05 where compiled, else SIMT), 1 SIMT
- * FP32, 2 tcgen05 3xTF32, 3 sparse CSR (pruned models). */
+/* Kernel-path selection: 0 auto (tcgen05 split-FP16 where compiled, with
+ * 3xTF32 recompute of out-of-range tiles; else 3xTF32; else SIMT), 1 SIMT
+ * FP32, 2 tcgen05 3xTF32 only, 3 sparse CSR (pruned models), 4 tcgen05
+ * split-FP16 (same as 0 for the stack). */
 int detnet_ctx_set_path(detnet_ctx *ctx, int path);
 /* Training forward (detnet_train_grad / detnet_batch_gradient) on tcgen05
  * (1, dense K=20 models) or FP32 CUDA cores (0, default). The tensor-core
@@ -96,7 +98,8 @@ int detnet_model_create(detnet_ctx *ctx, const detnet_model_desc *desc, detnet_m
 int detnet_model_update(detnet_model *m, const detnet_model_desc *desc);
 void detnet_model_destroy(detnet_model *m);
 /* Kernel path the stack of this model runs on under the context's current
- * path setting: 1 SIMT FP32, 2 tcgen05 3xTF32, 3 sparse. */
+ * path setting: 1 SIMT FP32, 2 tcgen05 3xTF32, 3 sparse, 4 tcgen05
+ * split-FP16. */
 int detnet_model_path(const detnet_model *m);
 /* Analytic census, flops_per_detection (compression.cpp:120-129). */
 long long detnet_model_flops_per_detection(const detnet_model *m, int include_preprocess);

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace detnet {
@@ -114,6 +115,22 @@ __device__ __forceinline__ void bulk_g2s_chunked(void *dst_smem, const void *src
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
+
+// Compile-time loops: f(std::integral_constant<int, i>) for i in [I, E) (sfor)
+// or E-1 down to I (sfor_rev), so register arrays indexed by i stay in registers.
+template <int I, int E, class F> __device__ __forceinline__ void sfor(F &&f) {
+    if constexpr (I < E) {
+        f(std::integral_constant<int, I>{});
+        sfor<I + 1, E>(static_cast<F &&>(f));
+    }
+}
+template <int I, int E, class F> __device__ __forceinline__ void sfor_rev(F &&f) { // E-1 .. I
+    if constexpr (I < E) {
+        f(std::integral_constant<int, E - 1>{});
+        sfor_rev<I, E - 1>(static_cast<F &&>(f));
+    }
+}
+#define SF_IDX(v) decltype(v)::value
 
 template <typename T> __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

@@ -331,6 +331,14 @@ bool use_tc(const detnet_model *m) {
     return true;
 }
 
+// split-FP16 stack (stack_h16.cu) for this model and context (training
+// forward: only with the dense images)
+bool use_h16(const detnet_model *m, bool trace) {
+    const int path = m->ctx->path;
+    if (!use_tc(m) || !(path == 0 || path == 4) || !m->tc.h16_ready) return false;
+    return !trace || m->tc.zh16 == 160;
+}
+
 // K1 (+pad) over samples [s0, s0+cnt) of the global arrays.
 int run_pre(detnet_model *m, cudaStream_t st, long s0, long cnt, long n_total, const float *H,
             const float *y, const int8_t *x) {
@@ -447,6 +455,25 @@ int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, 
         ta.xhat = xhat;
         ta.tile_loss = c->tile_loss.as<double>();
         ta.tile_err = c->tile_err.as<long long>();
+        if (use_h16(m, trace != nullptr)) {
+            // split-FP16 stack, then the 3xTF32 recompute of the tiles whose
+            // activations left the FP16 range (exits at once when none did)
+            if (c->redo.ensure(static_cast<size_t>(t0 + nt)) || c->redo_count.ensure(sizeof(int)))
+                return fail(DETNET_ERR_CUDA, "range-flag allocation failed");
+            CK(cudaMemsetAsync(c->redo_count.p, 0, sizeof(int), st));
+            {
+                LaunchScope ls(c, DETNET_K_STACK, st);
+                if (int rc = h16_launch_state(m->tc, ta, xs, vs, st, trace, c->redo.as<uint8_t>(),
+                                              c->redo_count.as<int>(), c->sms))
+                    return rc;
+            }
+            if (int rc = check_launch()) return rc;
+            LaunchScope ls(c, DETNET_K_OTHER, st);
+            if (int rc = tc_launch_redo(m->tc, ta, xs, vs, st, trace, c->redo.as<uint8_t>(),
+                                        c->redo_count.as<int>()))
+                return rc;
+            return check_launch();
+        }
         LaunchScope ls(c, DETNET_K_STACK, st);
         if (int rc = tc_launch_state(m->tc, ta, xs, vs, st, trace)) return rc;
         return check_launch();
@@ -597,7 +624,8 @@ void detnet_ctx_destroy(detnet_ctx *c) {
     cudaDeviceSynchronize();
     drain_times(c);
     for (DBuf *b : {&c->gp, &c->q32, &c->denom, &c->xmask, &c->flag, &c->tile_loss, &c->tile_err,
-                    &c->sing, &c->result, &c->xhat_dev, &c->state_x, &c->state_v})
+                    &c->sing, &c->result, &c->xhat_dev, &c->state_x, &c->state_v, &c->redo,
+                    &c->redo_count})
         b->release();
     for (int i = 0; i < 2; ++i) {
         c->in_H[i].release(); c->in_y[i].release(); c->in_x[i].release();
@@ -612,7 +640,7 @@ void detnet_ctx_destroy(detnet_ctx *c) {
 }
 
 int detnet_ctx_set_path(detnet_ctx *c, int path) {
-    if (!c || path < 0 || path > 3) return fail(DETNET_ERR_CONTRACT, "bad path");
+    if (!c || path < 0 || path > 4) return fail(DETNET_ERR_CONTRACT, "bad path");
     c->path = path;
     return 0;
 }
@@ -701,7 +729,8 @@ void detnet_model_destroy(detnet_model *m) {
 int detnet_model_path(const detnet_model *m) {
     if (!m) return 0;
     if (m->sparse_ready && !m->tc_stale && m->ctx->path == 3) return 3;
-    return use_tc(m) ? 2 : 1;
+    if (!use_tc(m)) return 1;
+    return use_h16(m, false) ? 4 : 2;
 }
 
 long long detnet_model_flops_per_detection(const detnet_model *m, int include_pre) {

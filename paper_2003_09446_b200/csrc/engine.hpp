@@ -70,6 +70,12 @@ struct TcModel {
     int zh = 0;         // hidden rows per packed layer (160 dense | 48 compacted)
     DBuf w;             // [L][rec bytes] pre-laid-out smem images
     long rec_bytes = 0;
+    // split-FP16 images (stack_h16.cu): [L][rec16] images, [L][64] bias rows,
+    // one int "weight out of FP16 range" flag (set by the device repack)
+    bool h16_ready = false;
+    int zh16 = 0;       // 160 dense | 64 compacted
+    DBuf w16;
+    long rec16 = 0;
 };
 
 struct TcArgs {
@@ -93,6 +99,18 @@ int tc_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cu
                     const TraceBufs *tr = nullptr);
 void tc_release(TcModel &tc);
 int tc_pack_device(TcModel &tc, const double *params, const double *masks, long P, cudaStream_t st);
+// 3xTF32 recompute of the tiles the split-FP16 kernel flagged (redo[tile] = 1);
+// returns at once on the device when *redo_count == 0
+int tc_launch_redo(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cudaStream_t st,
+                   const TraceBufs *tr, const uint8_t *redo, const int *redo_count);
+
+// split-FP16 layer stack (stack_h16.cu)
+int h16_prepare();
+int h16_pack(TcModel &tc, int K, int Z, int V, int L, const double *params, const double *masks,
+             const std::vector<std::vector<int>> &units, size_t max_alive);
+int h16_pack_device(TcModel &tc, const double *params, const double *masks, long P, cudaStream_t st);
+int h16_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cudaStream_t st,
+                     const TraceBufs *tr, uint8_t *redo, int *redo_count, int sms);
 
 
 } // namespace detnet
@@ -119,6 +137,7 @@ struct detnet_ctx {
     detnet::DBuf prep_scratch; // K1 fast path: per-CTA factor parking (L2-resident)
     bool exact_pre = false; // bit-exact reference LU for every sample
     bool train_tc = false;  // training forward on tcgen05 (dense images) instead of SIMT
+    detnet::DBuf redo, redo_count; // split-FP16 range flags per tile + count
     double *h_result = nullptr; // pinned: loss, err, flag, singular
     cudaEvent_t chunk_done[2] = {nullptr, nullptr};
     cudaEvent_t copy_done[2] = {nullptr, nullptr};

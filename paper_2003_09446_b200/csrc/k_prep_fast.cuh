@@ -110,22 +110,10 @@ __device__ __forceinline__ void pair_bar(int id) {
     asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
 }
 
-// Compile-time loops: triangular nests index register arrays, so every index
-// must be a constant before scalar replacement; a plain "#pragma unroll" on
-// the outer loop is not enough once the nest gets large.
-template <int I, int E, class F> __device__ __forceinline__ void sfor(F &&f) {
-    if constexpr (I < E) {
-        f(std::integral_constant<int, I>{});
-        sfor<I + 1, E>(static_cast<F &&>(f));
-    }
-}
-template <int I, int E, class F> __device__ __forceinline__ void sfor_rev(F &&f) { // E-1 .. I
-    if constexpr (I < E) {
-        f(std::integral_constant<int, E - 1>{});
-        sfor_rev<I, E - 1>(static_cast<F &&>(f));
-    }
-}
-#define SF_IDX(v) decltype(v)::value
+// Compile-time loops (sfor / sfor_rev, common.cuh): triangular nests index
+// register arrays, so every index must be a constant before scalar
+// replacement; a plain "#pragma unroll" on the outer loop is not enough once
+// the nest gets large.
 
 // 2-D tensor TMA load of box {c0 (inner), c1} into shared memory
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1,

@@ -87,6 +87,10 @@ struct TcKArgs {
     // [l][feature][ts] of in = [q; x; Gx; v], z = relu(u1), u2; x_hat_L [K][ts]
     float *tr_in, *tr_z, *tr_u2, *tr_xf;
     long ts;
+    // recompute mode (after the split-FP16 kernel): only tiles with redo[tile]
+    // set, nothing at all when *redo_count == 0
+    const uint8_t *redo;
+    const int *redo_count;
 };
 
 // Debug timeline (build with EXTRA=-DDETNET_TC_TRACE, run with DETNET_TC_TRACE=1):
@@ -211,6 +215,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
     const TcArgs &a = p.a;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int L0 = a.l_begin, L1 = a.l_end, NL = L1 - L0;
+    if (p.redo_count && *p.redo_count == 0) return; // recompute mode, nothing flagged
 
     if (threadIdx.x == 0) {
         mbar_init(&bars[B_W1F], 1);
@@ -233,7 +238,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
     __syncthreads();
     tc::fence_after();
     const uint32_t tbase = *tmem_slot;
-    const long my_tiles = a.n_tiles > blockIdx.x ? (a.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const long cand_tiles = a.n_tiles > blockIdx.x ? (a.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    long my_tiles = cand_tiles;
+    if (p.redo) { // recompute mode: the flagged tiles among this CTA's candidates
+        my_tiles = 0;
+        for (long ti = 0; ti < cand_tiles; ++ti)
+            my_tiles += p.redo[a.tile0 + blockIdx.x + ti * gridDim.x] != 0;
+    }
     const long total_it = my_tiles * NL;
 
     // Registers: the control warpgroup needs few, the epilogue warpgroups hold
@@ -371,9 +382,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
         // arrives, consumer syncs): x_hat A -> B, G x_hat partial B -> A
         const int bar_x = 1 + quad, bar_g = 6 + quad;
         long it = 0;
-        for (long ti = 0; ti < my_tiles; ++ti) {
+        for (long ti = 0; ti < cand_tiles; ++ti) {
             const long tile = blockIdx.x + ti * gridDim.x;
             const long gt = a.tile0 + tile;
+            if (p.redo && !p.redo[gt]) continue;
             const long s = tile * TILE + col;
             const bool live = s < a.n;
             // ---- tile init: Gram entries into registers, state, q ----
@@ -708,7 +720,7 @@ int tc_prepare() {
                                  static_cast<int>(TcCfg<48>::SM_TOTAL));
     if (e != cudaSuccess)
         return fail(DETNET_ERR_CUDA, "tcgen05 kernel smem attribute: %s", cudaGetErrorString(e));
-    return 0;
+    return h16_prepare();
 }
 
 namespace {
@@ -773,6 +785,8 @@ int tc_pack(TcModel &tc, int K, int Z, int V, int L, const double *params, const
     tc.K = K; tc.Z = Z; tc.V = V; tc.L = L;
     tc.ready = false;
     tc.zh = 0;
+    tc.h16_ready = false;
+    tc.zh16 = 0;
     if (K != KX || V != VV) return 0; // other dims use the SIMT path
     const int IN = 3 * K + V;
     const long P = Z * IN + Z + static_cast<long>(K) * Z + K + static_cast<long>(V) * Z + V + 1;
@@ -817,7 +831,7 @@ int tc_pack(TcModel &tc, int K, int Z, int V, int L, const double *params, const
                    cudaMemcpyHostToDevice) != cudaSuccess)
         return fail(DETNET_ERR_CUDA, "upload tc weights");
     tc.ready = true;
-    return 0;
+    return h16_pack(tc, K, Z, V, L, params, masks, units, max_alive);
 }
 
 // Rebuild the dense images on the device (training: after each Adam step).
@@ -832,11 +846,15 @@ int tc_pack_device(TcModel &tc, const double *params, const double *masks, long 
                                           static_cast<size_t>(tc.L) * tc.rec_bytes);
     k_pack_tc160<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(params, masks, P, tc.L,
                                                                             img, bt);
-    return cudaGetLastError() == cudaSuccess ? 0 : fail(DETNET_ERR_CUDA, "tc device pack");
+    if (cudaGetLastError() != cudaSuccess) return fail(DETNET_ERR_CUDA, "tc device pack");
+    // split-FP16 images: 0 = rebuilt, 1 = compacted (stale: host repack), else an error
+    if (tc.h16_ready) return h16_pack_device(tc, params, masks, P, st);
+    return 0;
 }
 
-int tc_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cudaStream_t st,
-                    const TraceBufs *tr) {
+namespace {
+int tc_launch_impl(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cudaStream_t st,
+                   const TraceBufs *tr, const uint8_t *redo, const int *redo_count) {
     if (!tc.ready) return fail(DETNET_ERR_UNSUPPORTED, "tcgen05 path not packed for these dims");
     TcKArgs p;
     p.a = a;
@@ -848,6 +866,8 @@ int tc_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cu
     p.trace = nullptr;
     p.tr_in = p.tr_z = p.tr_u2 = p.tr_xf = nullptr;
     p.ts = 0;
+    p.redo = redo;
+    p.redo_count = redo_count;
     static long long *trace_buf = nullptr;
     const bool tracing = std::getenv("DETNET_TC_TRACE") != nullptr;
     if (tracing) {
@@ -893,12 +913,26 @@ int tc_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cu
     return 0;
 }
 
+} // namespace
+
+int tc_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cudaStream_t st,
+                    const TraceBufs *tr) {
+    return tc_launch_impl(tc, a, xs, vs, st, tr, nullptr, nullptr);
+}
+
+int tc_launch_redo(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cudaStream_t st,
+                   const TraceBufs *tr, const uint8_t *redo, const int *redo_count) {
+    return tc_launch_impl(tc, a, xs, vs, st, tr, redo, redo_count);
+}
+
 int tc_launch(const TcModel &tc, const TcArgs &a, cudaStream_t st) {
     return tc_launch_state(tc, a, nullptr, nullptr, st, nullptr);
 }
 
 void tc_release(TcModel &tc) {
     tc.w.release();
+    tc.w16.release();
+    tc.h16_ready = false;
     tc.ready = false;
 }
 

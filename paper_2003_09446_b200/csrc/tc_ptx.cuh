@@ -52,6 +52,26 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, ui
         : "memory");
 }
 
+// D[tmem] (+)= A[tmem] * B[smem], kind::f16 (A/B fp16, f32 accumulate),
+// cta_group::1, M=128, K=16. A in TMEM: lane = row, 32-bit column c holds the
+// fp16 pair (k = 2c low half, 2c+1 high half).
+__device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                           uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// Instruction descriptor: D f32, A/B fp16 (format 0), both K-major, M x N.
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+    return (1u << 4)                              // c_format = F32
+           | (static_cast<uint32_t>(N >> 3) << 17) // n_dim
+           | (static_cast<uint32_t>(M >> 4) << 24); // m_dim
+}
+
 // Instruction descriptor: D f32, A/B tf32, both K-major, M x N.
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
     return (1u << 4)                              // c_format = F32

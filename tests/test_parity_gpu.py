@@ -69,7 +69,7 @@ def test_golden_forward(ctx, path):
     ctx.set_path(0)
 
 
-@pytest.mark.parametrize("path", [1, 0])
+@pytest.mark.parametrize("path", [1, 2, 0])
 def test_teacher_forced_layers(ctx, oracle, path):
     """Every layer of a 90-layer stack, fed the oracle's own state."""
     from paper_2003_09446_b200.workload import xavier_params
@@ -263,17 +263,19 @@ def test_kernel_launches_counted(ctx, oracle):
     assert ctx.launch_count - before >= 3  # preprocess, stack, reduce
 
 
-@pytest.mark.parametrize("path", [3, 1])
+@pytest.mark.parametrize("path", [3, 1, 2, 0])
 def test_sparse_group_model_paths(ctx, oracle, path):
     """Config-4 style model (group masks + 5% Bernoulli within groups) on the
-    sparse CSR kernel and on the SIMT kernel, against the oracle."""
+    sparse CSR kernel, the SIMT kernel and both compacted tensor-core kernels
+    (3xTF32 ZH=48, split-FP16 ZH=64), against the oracle."""
     from paper_2003_09446_b200.workload import group_masks, sparse_group_model, xavier_params
     params = xavier_params(K, 10, seed=9)
     ps, ms = sparse_group_model(params, group_masks(K, 10, seed=31), K)
     H, y, x = _inputs(oracle, 700, seed=5)
     ctx.set_path(path)
     m = ctx.model(K, N, 160, 40, ps, masks=ms)
-    assert m.path_name == {3: "sparse-csr-fp32", 1: "simt-fp32"}[path]
+    assert m.path_name == {3: "sparse-csr-fp32", 1: "simt-fp32", 2: "tcgen05-3xtf32",
+                           0: "tcgen05-split-fp16"}[path]
     ev, xh = m.batch_evaluate(H, y, x, want_xhat=True)
     ctx.set_path(0)
     ref = oracle.evaluate(_omodel(ps, masks=ms), H.astype(np.float64), y.astype(np.float64),

@@ -54,6 +54,31 @@ def test_batch_gradient(ctx, oracle, K, N, L, n, kind, lam, lam1, lam2, masked, 
     assert ev.flagged == ref["flagged"]
 
 
+@pytest.mark.parametrize("tc_path", [0, 2])
+@pytest.mark.parametrize("kind,lam,lam1,lam2", [(0, 0, 0, 0), (2, 0, 0.04, 0.04)])
+def test_batch_gradient_tensor_core_forward(oracle, tc_path, kind, lam, lam1, lam2):
+    """Gradients with the training forward on tensor cores: split FP16 (path
+    0) and 3xTF32 (path 2), same bound as the FP32 forward."""
+    from paper_2003_09446_b200 import Context
+    from paper_2003_09446_b200.workload import xavier_params
+    K, N, L, n = 20, 30, 4, 700
+    c = Context(0)
+    c.set_train_forward(True)
+    c.set_path(tc_path)
+    params = xavier_params(K, L, seed=5)
+    masks = _masks(params, K, 3)
+    H, y, x = _inputs(oracle, n, K, N)
+    m = c.model(K, N, 8 * K, 2 * K, params, masks=masks, frozen_prefix=1)
+    ev, g = m.batch_gradient(H, y, x, kind, lam, lam1, lam2)
+    om = OModel(K, N, 8 * K, 2 * K, L, params, masks=masks, frozen_prefix=1)
+    ref = oracle.batch_gradient(om, H.astype(np.float64), y.astype(np.float64),
+                                x.astype(np.float64), kind, lam, lam1, lam2)
+    scale = np.max(np.abs(ref["grads"]))
+    assert np.max(np.abs(g - ref["grads"])) <= 2e-4 * scale
+    assert np.all(g[:1] == 0.0) and np.all(g[masks == 0.0] == 0.0)
+    assert abs(ev.data_loss - ref["data_loss"]) <= 1e-4 * abs(ref["data_loss"])
+
+
 def test_adam_bit_exact(ctx, oracle):
     from paper_2003_09446_b200.workload import xavier_params
     K, L = 4, 3
@@ -130,10 +155,15 @@ def test_training_100_steps_tracks_oracle(oracle, tc_forward):
     median over seeds is asserted, with every run within 5e-3). Both runs must
     also improve the validation loss by the same amount (within 5 %).
     Run for the default FP32 training forward and for the opt-in tcgen05 one
-    (detnet_ctx_set_train_forward)."""
+    (detnet_ctx_set_train_forward; split FP16). The tensor-core forward is
+    noisier per operation (~2^-22 vs 2^-24), so its runs separate from FP64
+    sooner and drift further: over 20 seed pairs (tools/train_seeds.py) the
+    final median is 2.65e-3 (max 6.0e-3) against 0.96e-3 (max 2.6e-3) for
+    FP32, so its bounds are 4e-3 (median) and 1e-2 (each run)."""
     from paper_2003_09446_b200 import Context
     ctx = Context(0)
     ctx.set_train_forward(tc_forward)
+    med_max, run_max = (4e-3, 1e-2) if tc_forward else (1.5e-3, 5e-3)
     finals, tracked = [], []
     for pseed, dseed in [(9, 1), (9, 2), (10, 1), (11, 3), (12, 4)]:
         rels, rel, dg, do = _train_100(ctx, oracle, pseed, dseed)
@@ -141,11 +171,11 @@ def test_training_100_steps_tracks_oracle(oracle, tc_forward):
         assert rels[0] <= 1e-6, (pseed, dseed, rels[0])
         # steps before the first visible separation (a gate flip)
         tracked.append(next((i for i, r in enumerate(rels) if r > 1e-5), len(rels)))
-        assert rel <= 5e-3, (pseed, dseed, rel)
+        assert rel <= run_max, (pseed, dseed, rel)
         assert abs(dg - do) <= 0.05 * abs(do), (pseed, dseed, dg, do)
         finals.append(rel)
     med = float(np.median(finals))
     print(f"100-step training: steps tracked to 1e-5 per seed {tracked}; final validation "
           f"loss rel per seed {finals}; median {med:.2e}")
     assert np.median(tracked) >= 5, tracked
-    assert med <= 1.5e-3, finals
+    assert med <= med_max, finals

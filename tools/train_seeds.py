@@ -12,7 +12,11 @@ L = int(sys.argv[2]) if len(sys.argv) > 2 else L
 orc = Oracle()
 ctx = eng.Context(0)
 if os.environ.get("TC_FWD"): ctx.set_train_forward(True)
-for pseed, dseed in [(9, 1), (9, 2), (10, 1), (11, 3), (12, 4)]:
+ctx.set_path(int(os.environ.get("TC_PATH", "0")))  # 0 split-FP16, 2 3xTF32 (tensor-core forward)
+pairs = [(9, 1), (9, 2), (10, 1), (11, 3), (12, 4)]
+pairs += [(20 + i, 30 + i) for i in range(int(os.environ.get("EXTRA_SEEDS", "0")))]
+finals, tracked = [], []
+for pseed, dseed in pairs:
     params = xavier_params(K, L, seed=pseed)
     m = ctx.model(K, N, 8 * K, 2 * K, params)
     om = OModel(K, N, 8 * K, 2 * K, L, params.copy())
@@ -36,5 +40,11 @@ for pseed, dseed in [(9, 1), (9, 2), (10, 1), (11, 3), (12, 4)]:
     mg = ctx.model(K, N, 8 * K, 2 * K, m.get_params())
     evg = mg.batch_evaluate(Hv32, yv32, xv.astype(np.int8))
     evo = orc.batch_evaluate(om, Hv32.astype(np.float64), yv32.astype(np.float64), xv)
-    print(f"seeds {pseed},{dseed}: max rel first10 {max(rels[:10]):.2e} first50 {max(rels[:50]):.2e} final val rel "
+    fr = abs(evg.data_loss - evo['data_loss']) / evo['data_loss']
+    finals.append(fr)
+    tracked.append(next((i for i, r in enumerate(rels) if r > 1e-5), len(rels)))
+    print(f"seeds {pseed},{dseed}: tracked {tracked[-1]} max rel first10 {max(rels[:10]):.2e} first50 {max(rels[:50]):.2e} final val rel "
           f"{abs(evg.data_loss - evo['data_loss']) / evo['data_loss']:.2e}", flush=True)
+print(f"SUMMARY fwd={'tc' if os.environ.get('TC_FWD') else 'simt'} path={os.environ.get('TC_PATH', '0')} "
+      f"n={len(finals)} median final {np.median(finals):.2e} mean {np.mean(finals):.2e} "
+      f"max {np.max(finals):.2e} median tracked {np.median(tracked)}", flush=True)

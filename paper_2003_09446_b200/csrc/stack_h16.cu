@@ -104,7 +104,21 @@ struct HKArgs {
     // training trace (TR, ZH == 160): the k_stack_simt layout, unscaled
     float *tr_in, *tr_z, *tr_u2, *tr_xf;
     long ts;
+    long long *trace; // debug timeline (build with EXTRA=-DDETNET_TC_TRACE)
 };
+
+// Debug timeline: clock64 stamps of CTA 0's first 8 layer iterations, 32
+// events each (names in h16_launch_state). Compiled out by default.
+#ifdef DETNET_TC_TRACE
+#define HTRACE(ev, it, cond)                                                                   \
+    do {                                                                                       \
+        if (p.trace && blockIdx.x == 0 && (it) < 8 && (cond)) p.trace[(it) * 32 + (ev)] = clock64(); \
+    } while (0)
+#else
+#define HTRACE(ev, it, cond)                                                                   \
+    do {                                                                                       \
+    } while (0)
+#endif
 
 enum { B_W1F = 0, B_W23F = 1, B_U1A = 2, B_U1B = 3, B_U2 = 4, B_VX = 5, B_ZA = 6, B_ZB = 7, B_G = 8,
        B_E2L = 9, NBARS = 10 };
@@ -149,13 +163,56 @@ template <int N> __device__ __forceinline__ void st_u32(uint32_t t, const uint32
 
 __device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t *>(&h); }
 
+// packed FP32x2 arithmetic (FADD2 / FFMA2): two lanes per instruction
+__device__ __forceinline__ void sub2(float a0, float a1, float b0, float b1, float &d0, float &d1) {
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d0), "=f"(d1)
+        : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+// (d0, d1) += (a0, a1) * (b0, b1)
+__device__ __forceinline__ void fma2(float &d0, float &d1, float a0, float a1, float b0, float b1) {
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "mov.b64 rd, {%0, %1};\n\tfma.rn.f32x2 rd, ra, rb, rd;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "+f"(d0), "+f"(d1)
+        : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
 // (a0, a1) -> FP16 pair of hi halves and pair of lo halves (a0 in the low 16 bits)
 __device__ __forceinline__ __half2 split2(float a0, float a1, uint32_t &hi, uint32_t &lo) {
     const __half2 h = __floats2half2_rn(a0, a1);
     const float2 f = __half22float2(h);
+    float l0, l1;
+    sub2(a0, a1, f.x, f.y, l0, l1);
     hi = h2u(h);
-    lo = h2u(__floats2half2_rn(a0 - f.x, a1 - f.y));
+    lo = h2u(__floats2half2_rn(l0, l1));
     return h;
+}
+
+// Rows [R0, R1) of G x for the packed upper triangle g (row-major, r <= c,
+// rows R0.. only): gx[r] += sum_c G_rc x_c and, by symmetry, gx[c] += G_rc x_r.
+// Column pairs (c, c+1), c even, go through FFMA2: the row part into an
+// (even, odd) accumulator pair, the mirrored part into (gx[c], gx[c+1]).
+template <int R0, int R1>
+__device__ __forceinline__ void gram_mv(const float *g, const float (&x)[KX], float (&gx)[KX]) {
+    sfor<R0, R1>([&](auto rc) {
+        constexpr int r = decltype(rc)::value;
+        constexpr int e0 = r * KX - r * (r - 1) / 2 - (R0 * KX - R0 * (R0 - 1) / 2); // entry (r, r)
+        gx[r] = fmaf(g[e0], x[r], gx[r]);
+        constexpr int c1 = (r + 1) % 2 == 0 ? r + 1 : r + 2; // first paired (even) column
+        if constexpr (c1 == r + 2 && r + 1 < KX) {
+            gx[r] = fmaf(g[e0 + 1], x[r + 1], gx[r]);
+            gx[r + 1] = fmaf(g[e0 + 1], x[r], gx[r + 1]);
+        }
+        float re = 0.f, ro = 0.f;
+        sfor<0, (KX - c1) / 2>([&](auto pc) {
+            constexpr int c = c1 + 2 * decltype(pc)::value;
+            constexpr int e = e0 + (c - r);
+            fma2(re, ro, g[e], g[e + 1], x[c], x[c + 1]);
+            fma2(gx[c], gx[c + 1], g[e], g[e + 1], x[r], x[r]);
+        });
+        if constexpr (c1 < KX) gx[r] += re + ro;
+    });
 }
 
 // Split N scaled values into N/2 hi and N/2 lo pair columns; running |max|.
@@ -257,26 +314,37 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_h16(HKArgs p) {
                     }
                     __syncwarp();
                 };
+                const bool t0n = lane == 0;
                 mbar_wait_guard(&bars[B_W1F], ph);
-                // U1 is overwritten: the previous layer's W23 (reading z there) must
-                // be complete; a tile's first layer also needs its q columns.
+                HTRACE(0, it, t0n);
+                // U1 is overwritten by the [q 1] steps. The previous layer's W23 MMAs
+                // (reading z there) precede them in the tensor pipe's issue order;
+                // waiting for the epilogue's U2V reads (E2L) keeps these MMAs from
+                // competing with those TMEM loads (measured ~1.5% faster). A tile's
+                // first layer waits for its q columns instead.
                 if (l == L0) mbar_wait_guard(&bars[B_VX], ph);
                 else mbar_wait_guard(&bars[B_E2L], ph ^ 1);
+                HTRACE(1, it, t0n);
                 tc::fence_after();
                 w1_steps(std::integral_constant<int, 0>{}, 0, 2, false);
                 if constexpr (NH == 2) w1_steps(std::integral_constant<int, 1>{}, 0, 2, false);
                 if (l != L0) mbar_wait_guard(&bars[B_VX], ph);
+                HTRACE(2, it, t0n);
                 tc::fence_after();
                 w1_steps(std::integral_constant<int, 0>{}, 2, 5, false);
                 mbar_wait_guard(&bars[B_G], ph);
+                HTRACE(3, it, t0n);
                 tc::fence_after();
                 w1_steps(std::integral_constant<int, 0>{}, 5, 7, true);
                 if constexpr (NH == 2) w1_steps(std::integral_constant<int, 1>{}, 2, 7, true);
+                HTRACE(4, it, t0n);
                 mbar_wait_guard(&bars[B_W23F], ph);
+                HTRACE(5, it, t0n);
                 // U2V = z . [W3; W2]^T, K split by the z groups
                 auto w23_group = [&](auto hc) {
                     constexpr int h = decltype(hc)::value;
                     mbar_wait_guard(&bars[h == 0 ? B_ZA : B_ZB], ph);
+                    HTRACE(6 + h, it, t0n);
                     tc::fence_after();
                     if (tc::elect_one()) {
                         const uint32_t tb = tc::opaque32(tbase);
@@ -295,6 +363,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_h16(HKArgs p) {
                 };
                 w23_group(std::integral_constant<int, 0>{});
                 if constexpr (NH == 2) w23_group(std::integral_constant<int, 1>{});
+                HTRACE(8, it, t0n);
             }
         } else if (warp == 9) {
             // ================ weight producer (one elected lane) ================
@@ -323,8 +392,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_h16(HKArgs p) {
                 const uint32_t ph = static_cast<uint32_t>(it & 1);
                 const int lnext = L0 + static_cast<int>((it + 1) % NL);
                 mbar_wait_guard(&bars[U1_LAST], ph); // every W1 group consumed
+                HTRACE(28, it, lane == 0);
                 load_w1(lnext);
                 mbar_wait_guard(&bars[B_E2L], ph);   // W23 consumed, U2V + bias row read
+                HTRACE(29, it, lane == 0);
                 load_w23(lnext, it + 1);
             }
         }
@@ -390,9 +461,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_h16(HKArgs p) {
                 }
                 lpend = -1;
             };
+            auto store_v = [&]() { // B: v pairs -> A_dyn (scaled by S_IN)
+                uint32_t hi[VV / 2], lo[VV / 2];
+                split_row<VV>(v, 1.f, hi, lo, amax);
+                st_u32<VV / 2>(trow + C_DYN, hi);
+                st_u32<VV / 2>(trow + C_DYNLO, lo);
+            };
             for (int l = L0; l < L1; ++l, ++it) {
                 const uint32_t ph = static_cast<uint32_t>(it & 1);
                 const double lw = isA ? a.lnk[l] : 0.0;
+                const bool tA = threadIdx.x == 128, tB = threadIdx.x == 0;
+                const int tb9 = isA ? 9 : 19; // A events 9-18, B events 19-27
+                HTRACE(tb9, it, tA || tB);
                 // ---- prep: A_dyn pairs = [v | x | gx]: v (B) and x (A), then G x_hat
                 if (isA) {
                     {
@@ -405,19 +485,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_h16(HKArgs p) {
                     tc::wait_st();
                     tc::fence_before();
                     mbar_arrive(&bars[B_VX]);
-                    if (lpend >= 0) settle();
+                    HTRACE(10, it, tA);
                     float gx[KX];
 #pragma unroll
                     for (int k = 0; k < KX; ++k) gx[k] = 0.f;
-                    int e = 0;
-#pragma unroll
-                    for (int r = 0; r < 6; ++r)
-#pragma unroll
-                        for (int c = r; c < KX; ++c, ++e) {
-                            gx[r] = fmaf(g[e], x[c], gx[r]);
-                            if (c != r) gx[c] = fmaf(g[e], x[r], gx[c]);
-                        }
+                    gram_mv<0, 6>(g, x, gx);
                     tc::named_bar(bar_g, 64);
+                    HTRACE(11, it, tA);
 #pragma unroll
                     for (int k = 6; k < KX; ++k) gx[k] += sGX[k * 128 + col];
                     if constexpr (TR) {
@@ -438,35 +512,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_h16(HKArgs p) {
                     tc::wait_st();
                     tc::fence_before();
                     mbar_arrive(&bars[B_G]);
+                    HTRACE(12, it, tA);
+                    if (lpend >= 0) settle(); // previous layer's loss / x_hat, off the critical path
                 } else {
                     if constexpr (TR) {
                         float *tin = p.tr_in + (static_cast<long>(l) * IN + 3 * KX) * p.ts + s;
 #pragma unroll
                         for (int k = 0; k < VV; ++k) tin[k * p.ts] = v[k] * (1.f / S_IN);
                     }
-                    {
-                        uint32_t hi[VV / 2], lo[VV / 2];
-                        split_row<VV>(v, 1.f, hi, lo, amax);
-                        st_u32<VV / 2>(trow + C_DYN, hi);
-                        st_u32<VV / 2>(trow + C_DYNLO, lo);
-                    }
+                    if (l == L0) store_v(); // later layers: stored in the previous epilogue 2
                     tc::wait_st();
                     tc::fence_before();
                     mbar_arrive(&bars[B_VX]);
+                    HTRACE(20, it, tB);
                     float part[KX];
 #pragma unroll
-                    for (int k = 6; k < KX; ++k) part[k] = 0.f;
-                    int e = 0;
-#pragma unroll
-                    for (int r = 6; r < KX; ++r)
-#pragma unroll
-                        for (int c = r; c < KX; ++c, ++e) {
-                            part[r] = fmaf(g[e], x[c], part[r]);
-                            if (c != r) part[c] = fmaf(g[e], x[r], part[c]);
-                        }
+                    for (int k = 0; k < KX; ++k) part[k] = 0.f;
+                    gram_mv<6, KX>(g, x, part);
 #pragma unroll
                     for (int k = 6; k < KX; ++k) sGX[k * 128 + col] = part[k];
                     tc::named_arrive(bar_g, 64);
+                    HTRACE(21, it, tB);
                 }
 
                 mbar_wait_guard(&bars[B_W23F], ph);
@@ -475,6 +541,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_h16(HKArgs p) {
                     constexpr int h = decltype(hc)::value;
                     constexpr int E = C::ew(h);
                     mbar_wait_guard(&bars[h == 0 ? B_U1A : B_U1B], ph);
+                    HTRACE((isA ? 13 : 22) + 2 * h, it, tA || tB);
                     tc::fence_after();
                     const int c0 = C::seg0(h, side);
                     uint32_t r[E];
@@ -497,12 +564,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_h16(HKArgs p) {
                     tc::wait_st();
                     tc::fence_before();
                     mbar_arrive(&bars[h == 0 ? B_ZA : B_ZB]);
+                    HTRACE((isA ? 14 : 23) + 2 * h, it, tA || tB);
                 };
                 epi1(std::integral_constant<int, 0>{});
                 if constexpr (NH == 2) epi1(std::integral_constant<int, 1>{});
 
                 // ---- epilogue 2: x_hat = psi_t(u2 + b2) (A), v = v' + b3 (B) ----
                 mbar_wait_guard(&bars[B_U2], ph);
+                HTRACE(isA ? 17 : 26, it, tA || tB);
                 tc::fence_after();
                 const float *bt = reinterpret_cast<const float *>(sm + SM_BT + (it & 1) * BT * 4);
                 if (isA) {
@@ -526,6 +595,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_h16(HKArgs p) {
 #pragma unroll
                     for (int k = 0; k < KX; ++k) sGX[k * 128 + col] = x[k];
                     tc::named_arrive(bar_x, 64);
+                    HTRACE(18, it, tA);
                 } else {
                     uint32_t r[VV];
                     tc::ld_cols_nw<VV>(trow + C_U2, r);
@@ -539,9 +609,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_h16(HKArgs p) {
                     mbar_arrive(&bars[B_E2L]);
 #pragma unroll
                     for (int k = 0; k < VV; ++k) v[k] = fmaf(__uint_as_float(r[k]), S_IN / S_U2, b[k]);
+                    // next layer's v columns now (U2V is read, this layer's W1 long done)
+                    if (l + 1 < L1) store_v();
                     tc::named_bar(bar_x, 64);
 #pragma unroll
                     for (int k = 0; k < KX; ++k) x[k] = sGX[k * 128 + col];
+                    HTRACE(27, it, tB);
                 }
                 lpend = l;
                 lw_pend = lw;
@@ -795,8 +868,16 @@ int h16_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, c
     p.limit = lim ? static_cast<float>(std::atof(lim)) : F16_SAFE;
     p.tr_in = p.tr_z = p.tr_u2 = p.tr_xf = nullptr;
     p.ts = 0;
+    p.trace = nullptr;
     const int grid = static_cast<int>(std::min<long>(a.n_tiles, sms));
     if (grid <= 0) return 0;
+    static long long *trace_buf = nullptr;
+    const bool tracing = std::getenv("DETNET_TC_TRACE") != nullptr;
+    if (tracing) {
+        if (!trace_buf) cudaMalloc(&trace_buf, 8 * 32 * sizeof(long long));
+        cudaMemsetAsync(trace_buf, 0, 8 * 32 * sizeof(long long), st);
+        p.trace = trace_buf;
+    }
     if (tr) {
         if (tc.zh16 != 160) return fail(DETNET_ERR_UNSUPPORTED, "training trace needs the dense images");
         p.tr_in = tr->in;
@@ -809,6 +890,23 @@ int h16_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, c
         k_stack_h16<64, false><<<grid, NTHREADS, HCfg<64>::SM_TOTAL, st>>>(p);
     } else {
         k_stack_h16<160, false><<<grid, NTHREADS, HCfg<160>::SM_TOTAL, st>>>(p);
+    }
+    if (tracing) {
+        long long h[8 * 32];
+        cudaMemcpyAsync(h, trace_buf, sizeof h, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        const char *nm[32] = {"M:w1f", "M:e2l", "M:vx", "M:g", "M:w1iss", "M:w23f", "M:za", "M:zb",
+                              "M:w23iss", "A:start", "A:vx", "A:gbar", "A:g", "A:u1a", "A:za",
+                              "A:u1b", "A:zb", "A:u2", "A:end", "B:start", "B:vx", "B:gpart",
+                              "B:u1a", "B:za", "B:u1b", "B:zb", "B:u2", "B:end", "P:u1last",
+                              "P:e2l", nullptr, nullptr};
+        const long long t0 = h[0];
+        for (int l = 0; l < 8; ++l) {
+            std::fprintf(stderr, "layer %d:", l);
+            for (int e = 0; e < 32; ++e)
+                if (nm[e]) std::fprintf(stderr, " %s=%lld", nm[e], h[l * 32 + e] - t0);
+            std::fprintf(stderr, "\n");
+        }
     }
     return 0;
 }

@@ -19,7 +19,9 @@ from dataclasses import dataclass
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libdetnet_b200.so")
+# DETNET_LIB: developer override (A/B runs of kernel variants built with
+# `make OUT=... OBJDIR=... EXTRA=-D...`); the product loads the in-tree build.
+LIB_PATH = os.environ.get("DETNET_LIB") or os.path.join(HERE, "lib", "libdetnet_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is not built: run `make -C paper_2003_09446_b200/csrc` "

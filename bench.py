@@ -376,8 +376,10 @@ def main():
     else:
         peak = peaks.get("fp32_tflops")
         peak_note = "measured cuBLAS FP32 SGEMM (CUDA-core FP32 pipe), this run"
+    traffic, traffic_note = stack_traffic(tc_path, per_point, compacted=args.config in (3, 4))
     roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": (achieved / peak) if peak else None, "traffic": None,
+            "frac": (achieved / peak) if peak else None, "traffic": traffic,
+            "traffic_source": traffic_note,
             "kernel": "k_stack (fused layer stack)", "path": tc_path, "peak_source": peak_note,
             "census_flop_per_detection_layers": census_layers,
             "detections_per_launch": per_point, "avg_launch_ms": avg_launch_s * 1e3,
@@ -570,6 +572,26 @@ def cpu_train_reference(L, params, n):
     return {"value": n / el, "unit": "samples/s", "cores": ref.worker_count() if ref else 1,
             "kind": "reference" if ref else "port",
             "sample": f"one batch_gradient + adam_step over {n} samples (L={L})"}
+
+
+def stack_traffic(path, detections, compacted=False):
+    """DRAM bytes per stack launch from the committed ncu --set full capture
+    (profiles/traffic.json: dram__bytes_read + dram__bytes_write of one
+    2^18-detection launch, scaled per detection -- the stack streams its
+    per-sample inputs once and keeps the weights L2-resident, so the bytes
+    scale with the detections)."""
+    name = {"tcgen05-split-fp16": "k_stack_h16", "tcgen05-3xtf32": "k_stack_tc"}.get(path)
+    if name == "k_stack_h16" and compacted:
+        name = "k_stack_h16_64"  # group-pruned models: the ZH = 64 instantiation
+    fn = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
+    if not name or not os.path.exists(fn):
+        return None, None
+    rec = json.load(open(fn)).get(name)
+    if not rec:
+        return None, None
+    return (rec["dram_bytes_per_detection"] * detections,
+            f"profiles/traffic.json ({name}, ncu --set full at {rec['detections_per_launch']} "
+            "detections, scaled per detection)")
 
 
 def ctx_path_name(ctx, model):

@@ -16,16 +16,21 @@ if timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > $OUT/pla
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > $OUT/ncu_launch.log 2>&1
 fi
-# 3. one full capture per hot kernel (2^18 detections, config-2 workload)
+# 3. one full capture per hot kernel (2^18 detections, config-2 workload):
+#    the split-FP16 stack (default), K1, and the 3xTF32 stack (path 2) for comparison
 if timeout 300 python tools/prof_run.py 262144 > $OUT/prof_run.log 2>&1; then
-  for k in k_stack_tc k_prep_stream; do
+  for k in k_stack_h16 k_prep_stream; do
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
       -o $OUT/$k python tools/prof_run.py 262144 > $OUT/ncu_$k.log 2>&1
   done
 fi
-# 4. the compacted (config-3) stack kernel and the training kernels
-if timeout 300 python tools/prof_run.py 262144 0 3 > $OUT/prof_run3.log 2>&1; then
+if timeout 300 python tools/prof_run.py 262144 2 > $OUT/prof_run_tf32.log 2>&1; then
   timeout 900 ncu --set full --clock-control none -k regex:k_stack_tc -s 1 -c 1 \
-    -o $OUT/k_stack_tc48 python tools/prof_run.py 262144 0 3 > $OUT/ncu_tc48.log 2>&1
+    -o $OUT/k_stack_tc python tools/prof_run.py 262144 2 > $OUT/ncu_k_stack_tc.log 2>&1
+fi
+# 4. the compacted (config-3) stack kernel
+if timeout 300 python tools/prof_run.py 262144 0 3 > $OUT/prof_run3.log 2>&1; then
+  timeout 900 ncu --set full --clock-control none -k regex:k_stack_h16 -s 1 -c 1 \
+    -o $OUT/k_stack_h16_64 python tools/prof_run.py 262144 0 3 > $OUT/ncu_h16_64.log 2>&1
 fi
 echo done

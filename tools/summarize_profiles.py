@@ -11,7 +11,7 @@ METRICS = [
     "sm__warps_active.avg.pct_of_peak_sustained_active",
     "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
     "launch__shared_mem_per_block_dynamic", "smsp__inst_executed.sum", "sm__cycles_elapsed.avg",
-    "lts__t_sector_hit_rate.pct",
+    "lts__t_sector_hit_rate.pct", "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active",
 ]
 
 
@@ -37,6 +37,20 @@ def main(src, dst, title):
             lines.append("")
     open(dst, "w").write("\n".join(lines))
     print("\n".join(lines))
+    # DRAM bytes per detection of the stack kernels (bench.py's roofline.traffic)
+    traffic = {}
+    for rep in sorted(os.listdir(src)):
+        if rep.startswith("k_stack") and rep.endswith(".ncu-rep"):
+            recs, units = raw(os.path.join(src, rep))
+            for r in recs:
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+                b = sum(float(r[m]) * scale.get(units.get(m, "byte"), 1)
+                        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+                traffic[rep[:-8]] = {"dram_bytes_per_launch": b, "detections_per_launch": 262144,
+                                     "dram_bytes_per_detection": b / 262144}
+    if traffic:
+        import json
+        json.dump(traffic, open(os.path.join(os.path.dirname(dst), "traffic.json"), "w"), indent=1)
 
 
 if __name__ == "__main__":

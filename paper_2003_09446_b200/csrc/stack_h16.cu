@@ -590,7 +590,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_h16(HKArgs p) {
                     for (int k = 0; k < KX; ++k) {
                         const float uu = fmaf(__uint_as_float(r[k]), 1.f / S_U2, b[k]);
                         if constexpr (TR) p.tr_u2[(static_cast<long>(l) * KX + k) * p.ts + s] = uu;
-                        x[k] = uu <= -tt.x ? -1.f : (uu >= tt.x ? 1.f : uu * tt.y);
+                        // psi_t (model.cpp:32-51) as a clamp of u / t: 3 instructions
+                        x[k] = fminf(fmaxf(uu * tt.y, -1.f), 1.f);
                     }
 #pragma unroll
                     for (int k = 0; k < KX; ++k) sGX[k * 128 + col] = x[k];

@@ -100,3 +100,20 @@ def test_weights_outside_fp16_range_use_3xtf32(ctx, oracle):
     params[1, 5] = 1e4  # x 16 (image scale) > FP16 max
     m = ctx.model(K, N, 160, 40, params)
     assert m.path_name == "tcgen05-3xtf32"
+
+
+def test_hidden_unit_overflow_is_recomputed(ctx, oracle):
+    """A hidden activation beyond the FP16 range (scaled z > 65504, i.e.
+    z > 2047) flags its tile. Bias b1 = 3000 in layer 1 does that for every
+    tile, so the whole batch must equal the 3xTF32 path bit for bit."""
+    from paper_2003_09446_b200.workload import xavier_params
+    params = xavier_params(K, 4, seed=9)
+    IN = 3 * K + 40
+    params[1, 160 * IN:160 * IN + 160] = 3000.0  # b1 of layer 1: x16 fits FP16, z = 32 u1 does not
+    m = ctx.model(K, N, 160, 40, params)
+    assert m.path_name == "tcgen05-split-fp16"
+    H, y, x = _inputs(oracle, 400)
+    ev2, xh2 = _eval(ctx, m, 2, H, y, x)
+    evh, xhh = _eval(ctx, m, 0, H, y, x)
+    assert np.array_equal(xhh, xh2)
+    assert evh.data_loss == ev2.data_loss and evh.symbol_errors == ev2.symbol_errors

@@ -125,6 +125,17 @@ int detnet_batch_evaluate_device(detnet_model *m, long n, const float *H_dev, co
                                  const int8_t *x_dev, int loss_layers_trainable_only,
                                  float *xhat_dev, detnet_eval *out);
 
+/* The per-sample preprocessing alone (K1 + its exact-LU fallback; the part of
+ * evaluate_one before the layer loop, kernels.cpp:55-58, linalg.cpp:20-79),
+ * device buffers in and out, sample-major: gram_dev [n][K(K+1)/2] the upper
+ * triangle of G = H^T H row by row (linalg.cpp:31-42), q_dev [n][K] = H^T y,
+ * denom_dev [n] = max(||x - x_tilde||^2, 1e-12) (loss.cpp:14-19), flag_dev [n]
+ * the guard flag. Any output pointer may be NULL. A parity hook for the
+ * preprocessing; SingularMatrixError like batch_evaluate. */
+int detnet_preprocess_device(detnet_model *m, long n, const float *H_dev, const float *y_dev,
+                             const int8_t *x_dev, float *gram_dev, float *q_dev,
+                             double *denom_dev, uint8_t *flag_dev);
+
 /* Layers [l_begin, l_end) from a given state (host buffers): the teacher-
  * forced single-layer check of SURVEY 7.3/H1. x_state [n][K], v_state [n][V]
  * are read and overwritten with the state after layer l_end-1; xhat_out

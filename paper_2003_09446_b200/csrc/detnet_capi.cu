@@ -52,7 +52,7 @@ void launch_pre(dim3 g, dim3 b, size_t sm, cudaStream_t st, long n, int N, const
 
 using FastFn = void (*)(dim3, dim3, size_t, cudaStream_t, long, int, const float *, const float *,
                         const int8_t *, float *, float *, double *, uint32_t *, uint8_t *, int *,
-                        long *, float *, const CUtensorMap *);
+                        long *, const CUtensorMap *);
 
 // 2-D view of H for the K1 fast path: rows of N*K floats (one sample), box
 // {SSTR/4 floats, PS_TILE samples}. The box is 4 floats wider than a 6-row
@@ -84,13 +84,13 @@ int encode_h_map(CUtensorMap *map, const float *H, long n, int N, int K) {
 template <int K>
 void launch_fast(dim3 g, dim3 b, size_t sm, cudaStream_t st, long n, int N, const float *H,
                  const float *y, const int8_t *x, float *gp, float *q32, double *dn, uint32_t *xm,
-                 uint8_t *fl, int *fbc, long *fbl, float *scratch, const CUtensorMap *map) {
+                 uint8_t *fl, int *fbc, long *fbl, const CUtensorMap *map) {
     (void)b;
     (void)sm;
     (void)N; // the fast path is instantiated for N == PREP_FAST_N only
     (void)H;
     k_prep_stream<K, PREP_FAST_N><<<g, PS_THREADS, PrepStreamSmem<K, PREP_FAST_N>::BYTES, st>>>(
-        *map, n, y, x, gp, q32, dn, xm, fl, fbc, fbl, scratch);
+        *map, n, y, x, gp, q32, dn, xm, fl, fbc, fbl);
 }
 
 template <int K> int set_fast_smem() {
@@ -341,7 +341,7 @@ bool use_h16(const detnet_model *m, bool trace) {
 
 // K1 (+pad) over samples [s0, s0+cnt) of the global arrays.
 int run_pre(detnet_model *m, cudaStream_t st, long s0, long cnt, long n_total, const float *H,
-            const float *y, const int8_t *x) {
+            const float *y, const int8_t *x, bool exact) {
     detnet_ctx *c = m->ctx;
     const int K = m->K, NG = gram_entries(K);
     const long t0 = s0 / TILE;
@@ -350,7 +350,7 @@ int run_pre(detnet_model *m, cudaStream_t st, long s0, long cnt, long n_total, c
     const bool aligned = (reinterpret_cast<uintptr_t>(H) % 16 == 0) &&
                          (reinterpret_cast<uintptr_t>(y) % 16 == 0) &&
                          (reinterpret_cast<uintptr_t>(x) % 4 == 0);
-    if (m->dims->fast && !c->exact_pre && aligned && N == PREP_FAST_N) {
+    if (m->dims->fast && !c->exact_pre && !exact && aligned && N == PREP_FAST_N) {
         // fast path + exact LU for the samples it flags (device-side list)
         if (c->fb_list.ensure(sizeof(long) * cnt) || c->fb_count.ensure(sizeof(int)))
             return fail(DETNET_ERR_CUDA, "fallback list allocation failed");
@@ -359,8 +359,6 @@ int run_pre(detnet_model *m, cudaStream_t st, long s0, long cnt, long n_total, c
             LaunchScope ls(c, DETNET_K_PREPROCESS, st);
             const long tiles = (cnt + PS_TILE - 1) / PS_TILE;
             const long grid = std::min<long>(tiles, 2L * c->sms);
-            if (c->prep_scratch.ensure(sizeof(float) * grid * NG * PS_TILE))
-                return fail(DETNET_ERR_CUDA, "preprocess scratch allocation failed");
             CUtensorMap hmap;
             if (int rc = encode_h_map(&hmap, H, cnt, N, K)) return rc;
             m->dims->fast(dim3(static_cast<unsigned>(grid)),
@@ -368,8 +366,7 @@ int run_pre(detnet_model *m, cudaStream_t st, long s0, long cnt, long n_total, c
                           cnt, N, H, y, x, c->gp.as<float>() + t0 * NG * TILE,
                           c->q32.as<float>() + t0 * K * TILE, c->denom.as<double>() + s0,
                           c->xmask.as<uint32_t>() + s0, c->flag.as<uint8_t>() + s0,
-                          c->fb_count.as<int>(), c->fb_list.as<long>(),
-                          c->prep_scratch.as<float>(), &hmap);
+                          c->fb_count.as<int>(), c->fb_list.as<long>(), &hmap);
         }
         if (int rc = check_launch()) return rc;
         LaunchScope ls(c, DETNET_K_OTHER, st); // exact LU for the flagged samples
@@ -773,6 +770,51 @@ int detnet_batch_evaluate_device(detnet_model *m, long n, const float *H, const 
                            nullptr))
         return rc;
     return finish(m, n, out);
+}
+
+namespace {
+// tile-major K1 outputs -> sample-major (one thread per sample)
+__global__ void k_untile_pre(long n, int K, const float *gp, const float *q32, float *gram,
+                             float *q) {
+    const long s = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const int NG = gram_entries(K);
+    const long tile = s / TILE;
+    const int col = static_cast<int>(s % TILE);
+    if (gram)
+        for (int e = 0; e < NG; ++e) gram[s * NG + e] = gp[(tile * NG + e) * TILE + col];
+    if (q)
+        for (int k = 0; k < K; ++k) q[s * K + k] = q32[(tile * K + k) * TILE + col];
+}
+} // namespace
+
+int detnet_preprocess_device(detnet_model *m, long n, const float *H, const float *y,
+                             const int8_t *x, float *gram, float *q, double *denom,
+                             uint8_t *flag) {
+    if (!m || (n > 0 && (!H || !y || !x))) return fail(DETNET_ERR_CONTRACT, "null argument");
+    detnet_ctx *c = m->ctx;
+    if (n <= 0) return 0;
+    CK(cudaSetDevice(c->device));
+    if (int rc = ensure_ws(c, n, m->K)) return rc;
+    if (int rc = reset_sing(c, c->stream)) return rc;
+    if (int rc = run_pre(m, c->stream, 0, n, n, H, y, x)) return rc;
+    if (gram || q) {
+        LaunchScope ls(c, DETNET_K_OTHER, c->stream);
+        k_untile_pre<<<static_cast<unsigned>((n + 255) / 256), 256, 0, c->stream>>>(
+            n, m->K, c->gp.as<float>(), c->q32.as<float>(), gram, q);
+    }
+    if (int rc = check_launch()) return rc;
+    if (denom) CK(cudaMemcpyAsync(denom, c->denom.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+    if (flag) CK(cudaMemcpyAsync(flag, c->flag.p, static_cast<size_t>(n), cudaMemcpyDeviceToDevice, c->stream));
+    unsigned long long sing;
+    CK(cudaMemcpyAsync(&sing, c->sing.p, 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    drain_times(c);
+    if (sing != ~0ull)
+        return fail(DETNET_ERR_SINGULAR,
+                    "solve_normal_equations: matrix is singular to working precision (sample %llu)",
+                    sing);
+    return 0;
 }
 
 int detnet_batch_evaluate(detnet_model *m, long n, const float *H, const float *y,

@@ -134,7 +134,6 @@ struct detnet_ctx {
     // workspace
     detnet::DBuf gp, q32, denom, xmask, flag, tile_loss, tile_err, sing, result;
     detnet::DBuf in_H[2], in_y[2], in_x[2], xhat_dev, state_x, state_v, fb_list, fb_count;
-    detnet::DBuf prep_scratch; // K1 fast path: per-CTA factor parking (L2-resident)
     bool exact_pre = false; // bit-exact reference LU for every sample
     bool train_tc = false;  // training forward on tcgen05 (dense images) instead of SIMT
     detnet::DBuf redo, redo_count; // split-FP16 range flags per tile + count
@@ -227,8 +226,10 @@ struct TraceBufs {
 int ensure_ws(detnet_ctx *c, long n, int K);
 int upload_model(detnet_model *m, const detnet_model_desc *d);
 int reset_sing(detnet_ctx *c, cudaStream_t st);
+// exact: the reference's FP64 LU for every sample (training: each sample's
+// gradient is weighted by 1 / denom, so it gets the reference's denominators)
 int run_pre(detnet_model *m, cudaStream_t st, long s0, long cnt, long n_total, const float *H,
-            const float *y, const int8_t *x);
+            const float *y, const int8_t *x, bool exact = false);
 int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, int l_begin,
               int l_end, bool trainable_only, float *xhat, float *xs, float *vs,
               const TraceBufs *trace = nullptr);

@@ -5,22 +5,27 @@
 //   q = H^T y, G = H^T H                      -> FP32 outputs for the layer stack
 //   d = x - x_tilde = G^-1 H^T (H x - y)      -> denom = max(||d||^2, 1e-12)
 // Instead of the reference's FP64 LU (linalg.cpp:44-79, kept bit-exact in
-// k_preprocess.cuh), d starts from an FP32 Cholesky solve of G d0 = G x - q
-// and is refined with the residual H^T (H (x - d) - y) formed in FP64 straight
-// from the FP32 inputs, so d (hence the loss denominator) is FP64-accurate
-// (~1e-10 relative) for well-conditioned samples. Samples whose Cholesky
-// pivots collapse or whose refinement does not converge are queued for the
-// exact reference LU (k_preprocess on an index list), which also owns
+// k_preprocess.cuh), d is one FP32 Cholesky solve G d = p with the right-hand
+// side p = H^T (H x - y) accumulated in the same pass over H as the Gram
+// matrix. H x - y is the channel noise itself (x_j = +-1, x_j h_ij exact), so
+// p carries none of the cancellation of the algebraically equal G x - q, and
+// d is FP32-accurate (~cond(G) x 2^-24, measured <= 1e-5 relative in ||d||^2).
+// Samples whose Cholesky pivots collapse, whose noise is small enough for the
+// rounding of H x - y to matter (||H x - y||^2 < 1e-3 ||y||^2, i.e. SNR above
+// ~30 dB, which includes the reference's 1e-12 guard, loss.cpp:16-19), or that
+// produce NaN are queued for the exact
+// reference LU (k_preprocess on an index list), which also owns
 // SingularMatrixError.
 //
 // Work split: warps 0-1 ("A") and 2-3 ("B") hold the same 64 samples, so
 // every branch below is warp-uniform. A owns Gram rows 0..R0-1 (upper-triangle
-// entries [0, NA)) and q, B rows R0..K-1. The Cholesky factor is computed in
-// registers where the Gram halves already live: A factors its rows, hands the
-// cross block to B through shared memory (one 64-thread named barrier per
-// hand-off), B applies the Schur update and factors the trailing block. The
-// triangular solves run split the same way; the FP64 residual is split by
-// rows of H. The factor is parked in shared memory for the solves.
+// entries [0, NA)) and q, B rows R0..K-1 and p. The Cholesky factor is
+// computed in registers where the Gram halves already live: A factors its
+// rows, takes p from B, solves its rows and hands the cross block and the
+// folded right-hand side to B through shared memory (one 64-thread named
+// barrier per hand-off); B applies the Schur update, factors the trailing
+// block and solves it forwards and backwards; A finishes the back
+// substitution and forms ||d||^2.
 #pragma once
 
 #include <cuda.h>
@@ -30,9 +35,10 @@
 
 namespace detnet {
 
+// Rows [0, R0) of the Gram matrix (and q) belong to thread A, rows [R0, K) (and
+// p) to thread B; R0 splits the upper triangle about in half (6 of 20).
 template <int K> struct PrepSplit {
     static constexpr int NG = K * (K + 1) / 2;
-    // first row index whose entries belong to half 1 (about half the entries)
     static constexpr int r0() {
         int acc = 0;
         for (int r = 0; r < K; ++r) {
@@ -42,12 +48,6 @@ template <int K> struct PrepSplit {
         return K;
     }
     static constexpr int R0 = r0();
-    static constexpr int NA = [] {
-        int a = 0;
-        for (int r = 0; r < R0; ++r) a += K - r;
-        return a;
-    }();
-    static constexpr int NB = NG - NA;
 };
 
 __host__ __device__ constexpr int tri_idx(int K, int a, int b) { // a <= b
@@ -57,12 +57,9 @@ __host__ __device__ constexpr int tri_idx(int K, int a, int b) { // a <= b
 // ---- streaming layout ------------------------------------------------------
 // Persistent CTAs, 2 per SM: 4 consumer warps + 1 producer warp. A tile is 64
 // consecutive samples; its H block (64 x N x K floats, contiguous) is streamed
-// twice through a 2-stage ring of 6-row chunks by 1-D bulk copies (one per
-// sample; the per-sample stride is padded to 496 B so the 8-lane phases of a
-// 128-bit shared load hit distinct banks): pass 0 feeds the Gram, pass 1
-// (normally an L2 hit) the FP64 residual. Between the passes the Cholesky
-// factor is parked in a per-CTA scratch slab that stays L2-resident (it is
-// rewritten every tile), which keeps pass 1 within the register budget.
+// once through a 2-stage ring of 6-row chunks by a 2-D tensor TMA (box 124
+// floats x 64 samples: the per-sample stride in a stage is padded to 496 B so
+// the 8-lane phases of a 128-bit shared load hit distinct banks).
 constexpr int PS_TILE = 64, PS_ROWS = 6, PS_THREADS = 160;
 constexpr int PREP_FAST_N = 30; // n_rx the fast path is instantiated for (K = 20 configs)
 template <int K, int N> struct PrepStreamSmem {
@@ -78,9 +75,8 @@ template <int K, int N> struct PrepStreamSmem {
     static constexpr uint32_t XB = YB + 2 * YSLOT;                    // int8 [2][64][K]
     static constexpr uint32_t XSLOT = (PS_TILE * K + 127) / 128 * 128;
     static constexpr uint32_t X1 = XB + 2 * XSLOT;                    // float [K][64]
-    static constexpr uint32_t XT = X1 + K * PS_TILE * 4;              // double [K][64]
-    static constexpr uint32_t RX = XT + K * PS_TILE * 8;              // double [K][64]
-    static constexpr uint32_t BAD = RX + K * PS_TILE * 8;             // int [64]
+    static constexpr uint32_t XF = X1 + K * PS_TILE * 4;              // float [64][K] (x = +-1)
+    static constexpr uint32_t BAD = XF + K * PS_TILE * 4;             // int [64]
     static constexpr uint32_t BARS = BAD + PS_TILE * 4;               // 8 mbarriers
     static constexpr uint32_t BYTES = BARS + 8 * 8;
     static_assert(PS_ROWS * ROWB <= SSTR && SSTR % 16 == 0 && (SSTR / 16) % 2 == 1,
@@ -134,6 +130,15 @@ __device__ __forceinline__ void ffma2(float &d0, float &d1, float a, float b0, f
         : "f"(a), "f"(b0), "f"(b1));
 }
 
+// (d0, d1) += (a0, a1) * (b0, b1)
+__device__ __forceinline__ void fma2p(float &d0, float &d1, float a0, float a1, float b0, float b1) {
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rd, {%0, %1};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rd;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "+f"(d0), "+f"(d1)
+        : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
 #ifdef DETNET_PREP_TRACE
 #define PTR(ev) \
     if (blockIdx.x == 0 && lane == 0 && it < 3) ptr_t[it][ev] = clock64();
@@ -142,26 +147,24 @@ __device__ __forceinline__ void ffma2(float &d0, float &d1, float a, float b0, f
 #endif
 
 // K1 fast path. grid = min(tiles, 2 x SMs), PS_THREADS threads,
-// PrepStreamSmem<K, N>::BYTES of dynamic smem; scratch = grid x NG x 64 floats.
+// PrepStreamSmem<K, N>::BYTES of dynamic smem.
 template <int K, int N>
 __global__ void __launch_bounds__(PS_THREADS, 2)
     k_prep_stream(const __grid_constant__ CUtensorMap tmH, long n, const float *__restrict__ y,
                   const int8_t *__restrict__ x, float *__restrict__ gp, float *__restrict__ q32,
                   double *__restrict__ denom, uint32_t *__restrict__ xmask,
                   uint8_t *__restrict__ flag, int *__restrict__ fb_count,
-                  long *__restrict__ fb_list, float *__restrict__ scratch) {
+                  long *__restrict__ fb_list) {
     using S = PrepSplit<K>;
     using SM = PrepStreamSmem<K, N>;
-    constexpr int NG = S::NG, R0 = S::R0, P = PS_TILE;
+    constexpr int R0 = S::R0, P = PS_TILE;
     using PM = PairMap<K, R0>;
     constexpr int NMAX = PM::NA2 > PM::NB2 ? PM::NA2 : PM::NB2;
-    constexpr int NCH = N / PS_ROWS, RH = PS_ROWS / 2;
+    constexpr int NCH = N / PS_ROWS;
     static_assert(K % 4 == 0 && K <= 32 && R0 % 2 == 0, "row pairs / float4 rows / 32-bit mask");
-    static_assert(R0 * (K - R0) * P * 4 <= SM::STAGE, "cross block must fit one ring stage");
+    static_assert(R0 * (K - R0) * 32 * 4 <= 32 * SM::SSTR, "cross block must fit a pair's rows");
     extern __shared__ __align__(128) unsigned char psm[];
     float(*X1)[P] = reinterpret_cast<float(*)[P]>(psm + SM::X1);
-    double(*XT)[P] = reinterpret_cast<double(*)[P]>(psm + SM::XT);
-    double(*RX)[P] = reinterpret_cast<double(*)[P]>(psm + SM::RX);
     int *badB = reinterpret_cast<int *>(psm + SM::BAD);
     uint64_t *bars = reinterpret_cast<uint64_t *>(psm + SM::BARS);
     uint64_t *full = bars, *empty = bars + 2, *yfull = bars + 4, *yempty = bars + 6;
@@ -181,6 +184,8 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
 
     if (warp == 4) {
         // ===================== producer =====================
+        uint64_t pol; // H is read exactly once
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
         long cstep = 0;
         int it = 0;
         for (long tt = blockIdx.x; tt < ntiles; tt += gridDim.x, ++it) {
@@ -205,24 +210,16 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&yfull[yb]);
             }
-            for (int pass = 0; pass < 2; ++pass) {
-                // keep H in L2 between the passes; drop it after the second
-                uint64_t pol;
-                if (pass == 0)
-                    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-                else
-                    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-                for (int c = 0; c < NCH; ++c, ++cstep) {
-                    const int st = static_cast<int>(cstep & 1);
-                    const uint32_t ph = static_cast<uint32_t>((cstep >> 1) & 1);
-                    mbar_wait_guard(&empty[st], ph ^ 1);
-                    if (lane == 0) {
-                        mbar_arrive_expect_tx(&full[st], SM::STAGE);
-                        tma_load_2d(psm + SM::RING + st * SM::STAGE, &tmH, c * PS_ROWS * K,
-                                    static_cast<int>(s0), &full[st], pol);
-                    }
-                    __syncwarp();
+            for (int c = 0; c < NCH; ++c, ++cstep) {
+                const int st = static_cast<int>(cstep & 1);
+                const uint32_t ph = static_cast<uint32_t>((cstep >> 1) & 1);
+                mbar_wait_guard(&empty[st], ph ^ 1);
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(&full[st], SM::STAGE);
+                    tma_load_2d(psm + SM::RING + st * SM::STAGE, &tmH, c * PS_ROWS * K,
+                                static_cast<int>(s0), &full[st], pol);
                 }
+                __syncwarp();
             }
         }
         return;
@@ -232,7 +229,6 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
     const bool isA = warp < 2;
     const int ls = (warp & 1) * 32 + lane;
     const int bar = 1 + (warp & 1);
-    float *park = scratch + static_cast<long>(blockIdx.x) * NG * P + ls; // [NG][P]
     long cstep = 0;
     int it = 0;
 #ifdef DETNET_PREP_TRACE
@@ -264,13 +260,22 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
         }
         auto xs = [&](int j) { return (mask >> j) & 1u ? 1.f : -1.f; };
 
-        // ---------------- pass 0: Gram halves (+ q on A), FP32 pairs ----------------
+        // ---- the one pass over H: Gram halves; q = H^T y (A); p = H^T (H x - y) (B) ----
         float acc[NMAX];
 #pragma unroll
         for (int e = 0; e < NMAX; ++e) acc[e] = 0.f;
-        float pr[K];
+        float pr[K]; // A: q, B: p
 #pragma unroll
         for (int j = 0; j < K; ++j) pr[j] = 0.f;
+        // B: x as +-1 floats in shared memory (this thread's row only), read
+        // back four at a time per H row: keeps 20 registers free for p
+        float4 *xf = reinterpret_cast<float4 *>(psm + SM::XF) + ls * (K / 4);
+        if (!isA) {
+#pragma unroll
+            for (int q4 = 0; q4 < K / 4; ++q4)
+                xf[q4] = make_float4(xs(4 * q4), xs(4 * q4 + 1), xs(4 * q4 + 2), xs(4 * q4 + 3));
+        }
+        float rr = 0.f, yy = 0.f; // B: ||H x - y||^2, ||y||^2
         int hold = 0; // stage of the last Gram chunk: released after the Schur hand-off
 #pragma unroll 1
         for (int c = 0; c < NCH; ++c, ++cstep) {
@@ -292,13 +297,28 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
                     for (int b = a & ~1; b < K; b += 2)
                         ffma2(acc[PM::pos(a, b)], acc[PM::pos(a, b) + 1], h[a], h[b], h[b + 1]);
                 };
+                const float yi = ybuf[c * PS_ROWS + r];
                 if (isA) {
                     sfor<0, R0>(row);
-                    const float yi = ybuf[c * PS_ROWS + r];
 #pragma unroll
                     for (int j = 0; j < K; j += 2) ffma2(pr[j], pr[j + 1], yi, h[j], h[j + 1]);
                 } else {
                     sfor<R0, K>(row);
+                    // residual of the transmitted x on this receive row: (H x - y)_i.
+                    // x_j h_j is exact; it is the noise itself (y = H x + n), so no
+                    // G-sized cancellation enters p, unlike G x - q.
+                    float re = -yi, ro = 0.f;
+#pragma unroll
+                    for (int q4 = 0; q4 < K / 4; ++q4) {
+                        const float4 xq = xf[q4];
+                        fma2p(re, ro, h[4 * q4], h[4 * q4 + 1], xq.x, xq.y);
+                        fma2p(re, ro, h[4 * q4 + 2], h[4 * q4 + 3], xq.z, xq.w);
+                    }
+                    const float ri = re + ro;
+#pragma unroll
+                    for (int j = 0; j < K; j += 2) ffma2(pr[j], pr[j + 1], ri, h[j], h[j + 1]);
+                    rr = fmaf(ri, ri, rr); // noise energy
+                    yy = fmaf(yi, yi, yy); // received energy
                 }
             }
             __syncwarp();
@@ -308,24 +328,20 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
                 hold = st;
             }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&yempty[yb]); // y / x of this tile consumed
         PTR(2);
-        float *ub = reinterpret_cast<float *>(psm + SM::RING + hold * SM::STAGE);
+        // The cross block of a warp pair goes into the pair's OWN sample rows of
+        // the held stage: the other pair's B may still be reading its rows of
+        // that chunk (B has more work per H row than A).
+        float *ub = reinterpret_cast<float *>(psm + SM::RING + hold * SM::STAGE +
+                                              (warp & 1) * 32 * SM::SSTR) + lane;
         // G entries of row a (upper triangle) to the tile-major gp layout
         auto put_row = [&](auto ac) {
             constexpr int a = SF_IDX(ac);
 #pragma unroll
             for (int b = a; b < K; ++b)
-                gp[(tile * NG + tri_idx(K, a, b)) * TILE + col] = acc[PM::pos(a, b)];
-        };
-        // partial G x over row a's entries (symmetric contributions)
-        auto gx_row = [&](auto ac) {
-            constexpr int a = SF_IDX(ac);
-#pragma unroll
-            for (int b = a; b < K; ++b) {
-                const float g = acc[PM::pos(a, b)];
-                pr[a] = fmaf(g, xs(b), pr[a]);
-                if (b != a) pr[b] = fmaf(g, xs(a), pr[b]);
-            }
+                gp[(tile * S::NG + tri_idx(K, a, b)) * TILE + col] = acc[PM::pos(a, b)];
         };
         // right-looking Cholesky step k on rows (k, LAST): diag slot <- 1/L_kk
         bool bad = false;
@@ -354,31 +370,30 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
                 sfor<R0, K>(put_row);
             }
         }
-
         PTR(3);
-        // ---------------- FP32 Cholesky + first solve, split A | B ----------------
+
+        // ---- d = x - x_tilde = G^-1 p: FP32 Cholesky G = R^T R, split A | B ----
         float z[K];
         if (isA) {
-            // r0 = G x - q over A's entries (B's entries only touch indices >= R0)
-#pragma unroll
-            for (int j = 0; j < K; ++j) pr[j] = -pr[j];
-            sfor<0, R0>(gx_row);
             float gd[R0];
 #pragma unroll
             for (int k = 0; k < R0; ++k) gd[k] = acc[PM::pos(k, k)];
             sfor<0, R0>([&](auto kc) {
                 chol_step(kc, std::integral_constant<int, R0>{}, [&](int k) { return gd[k]; });
             });
+            pair_bar(bar); // (0) B -> A: p
+            PTR(4);
+            // forward solve R^T z = p on rows [0, R0), fold them into rows [R0, K)
             sfor<0, R0>([&](auto kc) {
                 constexpr int k = SF_IDX(kc);
-                float t = pr[k];
+                float t = X1[k][ls];
 #pragma unroll
                 for (int m = 0; m < k; ++m) t = fmaf(-acc[PM::pos(m, k)], z[m], t);
                 z[k] = t * acc[PM::pos(k, k)];
             });
 #pragma unroll
             for (int j = R0; j < K; ++j) {
-                float t = pr[j];
+                float t = X1[j][ls];
 #pragma unroll
                 for (int m = 0; m < R0; ++m) t = fmaf(-acc[PM::pos(m, j)], z[m], t);
                 X1[j][ls] = t;
@@ -387,11 +402,14 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
             for (int m = 0; m < R0; ++m)
 #pragma unroll
                 for (int j = R0; j < K; ++j)
-                    ub[(m * (K - R0) + (j - R0)) * P + ls] = acc[PM::pos(m, j)];
+                    ub[(m * (K - R0) + (j - R0)) * 32] = acc[PM::pos(m, j)];
             pair_bar(bar); // (1) A -> B: cross block, folded rhs
-            PTR(4);
-            pair_bar(bar); // (2) B -> A: d[R0..K); B is done with the cross block
             PTR(5);
+            pair_bar(bar); // (2) B -> A: d[R0..K); B is done with the cross block
+            PTR(6);
+            // the cross block was written through the generic proxy into a ring
+            // stage the TMA (async proxy) refills next: order the two
+            fence_proxy_async();
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[hold]);
             float d[K];
@@ -404,33 +422,40 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
                 for (int j = k + 1; j < K; ++j) t = fmaf(-acc[PM::pos(k, j)], d[j], t);
                 d[k] = t * acc[PM::pos(k, k)];
             });
-#pragma unroll
-            for (int j = 0; j < K; ++j)
-                XT[j][ls] = static_cast<double>(xs(j)) - static_cast<double>(d[j]);
-            sfor<0, R0>([&](auto ac) {
-                constexpr int a = SF_IDX(ac);
-#pragma unroll
-                for (int b = a; b < K; ++b) park[tri_idx(K, a, b) * P] = acc[PM::pos(a, b)];
-            });
             if (badB[ls]) bad = true;
-            pair_bar(bar); // (3) A -> B: x_tilde estimate
-            PTR(6);
+            double dn = 0.0;
+#pragma unroll
+            for (int j = 0; j < K; ++j) dn = fma(static_cast<double>(d[j]), static_cast<double>(d[j]), dn);
+            // near-noise-free samples (the reference's 1e-12 guard,
+            // loss.cpp:16-19; also caught by B's energy test) and NaN take the exact LU
+            if (!(dn >= 1e-6)) bad = true;
+            PTR(7);
+            if (live) {
+                if (bad) {
+                    const int slot = atomicAdd(fb_count, 1);
+                    fb_list[slot] = s;
+                    flag[s] = 0;
+                    denom[s] = 1.0;
+                } else {
+                    flag[s] = 0;
+                    denom[s] = dn;
+                }
+            }
         } else {
-            sfor<R0, K>(gx_row);
-            // original diagonal (pivot test) parked in RX, free until pass 1
-            float *gd = reinterpret_cast<float *>(&RX[0][0]) + ls;
+            float gd[K - R0];
 #pragma unroll
-            for (int k = R0; k < K; ++k) gd[(k - R0) * P] = acc[PM::pos(k, k)];
-            pair_bar(bar); // (1)
+            for (int k = R0; k < K; ++k) gd[k - R0] = acc[PM::pos(k, k)];
+#pragma unroll
+            for (int j = 0; j < K; ++j) X1[j][ls] = pr[j];
+            pair_bar(bar); // (0)
             PTR(4);
-            // fold B's part of G x - q into A's folded rhs now (frees pr)
-#pragma unroll
-            for (int k = R0; k < K; ++k) X1[k][ls] += pr[k];
+            pair_bar(bar); // (1)
+            PTR(5);
             sfor<0, R0>([&](auto mc) {
                 constexpr int m = SF_IDX(mc);
                 float u[K];
 #pragma unroll
-                for (int j = R0; j < K; ++j) u[j] = ub[(m * (K - R0) + (j - R0)) * P + ls];
+                for (int j = R0; j < K; ++j) u[j] = ub[(m * (K - R0) + (j - R0)) * 32];
                 sfor<R0, K>([&](auto ic) {
                     constexpr int i = SF_IDX(ic);
 #pragma unroll
@@ -440,8 +465,7 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[hold]);
             sfor<R0, K>([&](auto kc) {
-                chol_step(kc, std::integral_constant<int, K>{},
-                          [&](int k) { return gd[(k - R0) * P]; });
+                chol_step(kc, std::integral_constant<int, K>{}, [&](int k) { return gd[k - R0]; });
             });
             sfor<R0, K>([&](auto kc) {
                 constexpr int k = SF_IDX(kc);
@@ -459,155 +483,23 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
             });
 #pragma unroll
             for (int k = R0; k < K; ++k) X1[k][ls] = z[k];
-            sfor<R0, K>([&](auto ac) {
-                constexpr int a = SF_IDX(ac);
-#pragma unroll
-                for (int b = a; b < K; ++b) park[tri_idx(K, a, b) * P] = acc[PM::pos(a, b)];
-            });
+            // H x - y is formed in FP32 from y ~ H x: once the noise is below
+            // ~1e-3 of the signal (SNR above ~30 dB) its rounding error reaches
+            // 1e-5 of ||d||^2 -- such samples take the exact LU.
+            if (!(rr >= 1e-3f * yy)) bad = true;
             badB[ls] = bad ? 1 : 0;
             pair_bar(bar); // (2)
-            PTR(5);
-            pair_bar(bar); // (3)
             PTR(6);
-        }
-
-        // ---------------- pass 1: FP64 residual H^T (H x_tilde - y) ----------------
-        // rows [0, 3) of every chunk on A, [3, 6) on B
-        double xt[K], rp[K];
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-            xt[j] = XT[j][ls];
-            rp[j] = 0.0;
-        }
-        const int rbeg = isA ? 0 : RH;
-#pragma unroll 1
-        for (int c = 0; c < NCH; ++c, ++cstep) {
-            const int st = static_cast<int>(cstep & 1);
-            mbar_wait_guard(&full[st], static_cast<uint32_t>((cstep >> 1) & 1));
-            const float4 *hrow = reinterpret_cast<const float4 *>(psm + SM::RING + st * SM::STAGE +
-                                                                  ls * SM::SSTR) +
-                                 rbeg * (K / 4);
-#pragma unroll 1
-            for (int r = 0; r < RH; ++r) {
-                double hd[K];
-#pragma unroll
-                for (int q4 = 0; q4 < K / 4; ++q4) {
-                    const float4 v = hrow[r * (K / 4) + q4];
-                    hd[4 * q4] = v.x; hd[4 * q4 + 1] = v.y; hd[4 * q4 + 2] = v.z; hd[4 * q4 + 3] = v.w;
-                }
-                double e = -static_cast<double>(ybuf[c * PS_ROWS + rbeg + r]);
-#pragma unroll
-                for (int k = 0; k < K; ++k) e = fma(hd[k], xt[k], e);
-#pragma unroll
-                for (int k = 0; k < K; ++k) rp[k] = fma(hd[k], e, rp[k]);
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&yempty[yb]);
-        PTR(7);
-
-        // the factor, back from the parking slab (into acc: A rows or B rows)
-        auto unpark = [&](auto ac) {
-            constexpr int a = SF_IDX(ac);
-#pragma unroll
-            for (int b = a; b < K; ++b) acc[PM::pos(a, b)] = park[tri_idx(K, a, b) * P];
-        };
-        if (!isA) {
-#pragma unroll
-            for (int k = 0; k < R0; ++k) RX[k][ls] = rp[k];
-            pair_bar(bar); // (4) B -> A: partial residual rows 0..R0-1
-            PTR(8);
-            sfor<R0, K>(unpark);
-            pair_bar(bar); // (5) A -> B: folded rhs
-            PTR(9);
-            sfor<R0, K>([&](auto kc) {
-                constexpr int k = SF_IDX(kc);
-                float t = static_cast<float>(RX[k][ls] + rp[k]);
-#pragma unroll
-                for (int m = R0; m < k; ++m) t = fmaf(-acc[PM::pos(m, k)], z[m], t);
-                z[k] = t * acc[PM::pos(k, k)];
-            });
-            sfor_rev<R0, K>([&](auto kc) {
-                constexpr int k = SF_IDX(kc);
-                float t = z[k];
-#pragma unroll
-                for (int j = k + 1; j < K; ++j) t = fmaf(-acc[PM::pos(k, j)], z[j], t);
-                z[k] = t * acc[PM::pos(k, k)];
-            });
-#pragma unroll
-            for (int k = R0; k < K; ++k) X1[k][ls] = z[k];
-            pair_bar(bar); // (6) B -> A: correction rows R0..K-1
-            PTR(10);
-            PTR(11);
-            continue;
-        }
-        sfor<0, R0>(unpark);
-        pair_bar(bar); // (4)
-            PTR(8);
-        sfor<0, R0>([&](auto kc) {
-            constexpr int k = SF_IDX(kc);
-            float t = static_cast<float>(rp[k] + RX[k][ls]);
-#pragma unroll
-            for (int m = 0; m < k; ++m) t = fmaf(-acc[PM::pos(m, k)], z[m], t);
-            z[k] = t * acc[PM::pos(k, k)];
-        });
-#pragma unroll
-        for (int j = R0; j < K; ++j) {
-            double t = rp[j];
-#pragma unroll
-            for (int m = 0; m < R0; ++m) t -= static_cast<double>(acc[PM::pos(m, j)] * z[m]);
-            RX[j][ls] = t;
-        }
-        pair_bar(bar); // (5)
-            PTR(9);
-        pair_bar(bar); // (6)
-            PTR(10);
-        float cc[K];
-#pragma unroll
-        for (int j = R0; j < K; ++j) cc[j] = X1[j][ls];
-        sfor_rev<0, R0>([&](auto kc) {
-            constexpr int k = SF_IDX(kc);
-            float t = z[k];
-#pragma unroll
-            for (int j = k + 1; j < K; ++j) t = fmaf(-acc[PM::pos(k, j)], cc[j], t);
-            cc[k] = t * acc[PM::pos(k, k)];
-        });
-        double dn = 0.0, cmax = 0.0, dmax = 0.0;
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-            const double xtj = xt[j] - static_cast<double>(cc[j]);
-            const double dj = static_cast<double>(xs(j)) - xtj;
-            dn = fma(dj, dj, dn);
-            cmax = fmax(cmax, fabs(static_cast<double>(cc[j])));
-            dmax = fmax(dmax, fabs(dj));
-        }
-        // One refinement step suffices when its correction is small: the
-        // remaining error is about cmax^2 / dmax (<= 1e-8 relative). Anything
-        // else -- collapsed pivots, slow convergence, NaN -- goes to the exact LU.
-        if (!(cmax <= 1e-4 * dmax) || !(dn == dn)) bad = true;
-        PTR(11);
-        if (live) {
-            if (bad) {
-                const int slot = atomicAdd(fb_count, 1);
-                fb_list[slot] = s;
-                flag[s] = 0;
-                denom[s] = 1.0;
-            } else {
-                flag[s] = dn < 1e-12 ? 1 : 0;
-                denom[s] = dn < 1e-12 ? 1e-12 : dn;
-            }
+            PTR(7);
         }
     }
 #ifdef DETNET_PREP_TRACE
     if (blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == 2))
         for (int t = 0; t < 3; ++t)
-            printf("prep trace warp %d tile %d: %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld\n",
-                   warp, t, ptr_t[t][1] - ptr_t[t][0], ptr_t[t][2] - ptr_t[t][0],
-                   ptr_t[t][3] - ptr_t[t][0], ptr_t[t][4] - ptr_t[t][0], ptr_t[t][5] - ptr_t[t][0],
-                   ptr_t[t][6] - ptr_t[t][0], ptr_t[t][7] - ptr_t[t][0], ptr_t[t][8] - ptr_t[t][0],
-                   ptr_t[t][9] - ptr_t[t][0], ptr_t[t][10] - ptr_t[t][0], ptr_t[t][11] - ptr_t[t][0]);
+            printf("prep trace warp %d tile %d: %lld %lld %lld %lld %lld %lld %lld\n", warp, t,
+                   ptr_t[t][1] - ptr_t[t][0], ptr_t[t][2] - ptr_t[t][0], ptr_t[t][3] - ptr_t[t][0],
+                   ptr_t[t][4] - ptr_t[t][0], ptr_t[t][5] - ptr_t[t][0], ptr_t[t][6] - ptr_t[t][0],
+                   ptr_t[t][7] - ptr_t[t][0]);
 #endif
 }
 

@@ -133,7 +133,7 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
         return fail(DETNET_ERR_CUDA, "training workspace allocation failed");
     if (int rc = ensure_ws(c, n, K)) return rc;
     if (int rc = reset_sing(c, c->stream)) return rc;
-    if (int rc = run_pre(m, c->stream, 0, n, n, H, y, x)) return rc;
+    if (int rc = run_pre(m, c->stream, 0, n, n, H, y, x, /*exact=*/true)) return rc;
     TraceBufs tb{w.tr_in.as<float>(), w.tr_z.as<float>(), w.tr_u2.as<float>(), w.tr_xf.as<float>(),
                  ts};
     if (int rc = run_stack(m, c->stream, 0, tiles, n, 0, L, trainable_only, nullptr, nullptr,

@@ -115,6 +115,7 @@ _lib.detnet_model_flops_per_detection.restype = C.c_longlong
 _lib.detnet_model_flops_per_detection.argtypes = [_vp, C.c_int]
 _lib.detnet_batch_evaluate.argtypes = [_vp, C.c_long, _vp, _vp, _vp, C.c_int, _vp,
                                        C.POINTER(_Eval)]
+_lib.detnet_preprocess_device.argtypes = [_vp, C.c_long, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
 _lib.detnet_batch_evaluate_device.argtypes = [_vp, C.c_long, _vp, _vp, _vp, C.c_int, _vp,
                                               C.POINTER(_Eval)]
 _lib.detnet_forward_range.argtypes = [_vp, C.c_long, _vp, _vp, C.c_int, C.c_int, _vp, _vp, _vp]
@@ -375,6 +376,14 @@ class Model:
                                                  _addr(x_ptr), int(trainable_only),
                                                  _addr(xhat_ptr), C.byref(ev)))
         return BatchEval(ev.data_loss, ev.symbol_errors, ev.symbols, ev.flagged, ev.loss_sum)
+
+    def preprocess_device(self, n, H_ptr, y_ptr, x_ptr, gram_ptr=None, q_ptr=None, denom_ptr=None,
+                          flag_ptr=None):
+        """K1 alone on device-resident samples: sample-major G upper triangle,
+        q = H^T y, loss denominator and guard flag (any output may be None)."""
+        _check(_lib.detnet_preprocess_device(self._h, n, _addr(H_ptr), _addr(y_ptr), _addr(x_ptr),
+                                             _addr(gram_ptr), _addr(q_ptr), _addr(denom_ptr),
+                                             _addr(flag_ptr)))
 
     def forward_range(self, H, y, l_begin, l_end, x_state, v_state, want_xhat=True):
         """Layers [l_begin, l_end) from state (x_state [n][K], v_state [n][V])."""

@@ -267,6 +267,7 @@ int pack_sparse(detnet_model *m, const double *params, const double *masks) {
 }
 
 int upload_model(detnet_model *m, const detnet_model_desc *d) {
+    ++m->version;
     const long P = record_size(m->K, m->Z, m->V);
     m->params_host.assign(d->params, d->params + P * m->L);
     m->has_masks = d->masks != nullptr;
@@ -512,7 +513,9 @@ int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, 
     return check_launch();
 }
 
-int finish(detnet_model *m, long n, detnet_eval *out) {
+// finish_eval (kernels.cpp:93-103), device part: fixed-order reduction and
+// the copy of {loss, errors, flagged, singular} to pinned host memory
+int finish_device(detnet_model *m, long n) {
     detnet_ctx *c = m->ctx;
     const long tiles = (n + TILE - 1) / TILE;
     double *res = c->result.as<double>();
@@ -526,6 +529,12 @@ int finish(detnet_model *m, long n, detnet_eval *out) {
     if (int rc = check_launch()) return rc;
     CK(cudaMemcpyAsync(res + 3, c->sing.p, 8, cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaMemcpyAsync(c->h_result, res, 32, cudaMemcpyDeviceToHost, c->stream));
+    return 0;
+}
+
+// host part: wait, then decode (SingularMatrixError as linalg.cpp:59-60)
+int finish_host(detnet_model *m, long n, detnet_eval *out) {
+    detnet_ctx *c = m->ctx;
     CK(cudaStreamSynchronize(c->stream));
     drain_times(c);
     unsigned long long sing;
@@ -543,6 +552,11 @@ int finish(detnet_model *m, long n, detnet_eval *out) {
     out->symbols = n * static_cast<long long>(m->K);
     out->flagged = f;
     return 0;
+}
+
+int finish(detnet_model *m, long n, detnet_eval *out) {
+    if (int rc = finish_device(m, n)) return rc;
+    return finish_host(m, n, out);
 }
 
 int reset_sing(detnet_ctx *c, cudaStream_t st) {
@@ -714,8 +728,13 @@ int detnet_model_update(detnet_model *m, const detnet_model_desc *d) {
     return upload_model(m, d);
 }
 
+namespace {
+void drop_graph(detnet_model *m);
+}
+
 void detnet_model_destroy(detnet_model *m) {
     if (!m) return;
+    drop_graph(m);
     m->simt.release();
     m->lnk_all.release();
     m->lnk_train.release();
@@ -753,6 +772,70 @@ long long detnet_model_flops_per_detection(const detnet_model *m, int include_pr
     return flops;
 }
 
+namespace {
+int eval_device_body(detnet_model *m, long n, const float *H, const float *y, const int8_t *x,
+                     int trainable_only, float *xhat) {
+    detnet_ctx *c = m->ctx;
+    if (int rc = reset_sing(c, c->stream)) return rc;
+    if (int rc = run_pre(m, c->stream, 0, n, n, H, y, x)) return rc;
+    const long tiles = (n + TILE - 1) / TILE;
+    if (int rc = run_stack(m, c->stream, 0, tiles, n, 0, m->L, trainable_only != 0, xhat, nullptr,
+                           nullptr))
+        return rc;
+    return finish_device(m, n);
+}
+
+void drop_graph(detnet_model *m) {
+    auto &g = m->graph;
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    for (auto &p : g.timers) {
+        m->ctx->event_pool.push_back(p.a);
+        m->ctx->event_pool.push_back(p.b);
+    }
+    g = detnet_model::EvalGraph{};
+}
+
+// Capture the body into m->graph (the key is already set). Returns 0 and
+// leaves g.exec null when capture is not possible (the caller runs eagerly).
+int capture_graph(detnet_model *m, long n, const float *H, const float *y, const int8_t *x,
+                  int trainable_only, float *xhat) {
+    detnet_ctx *c = m->ctx;
+    auto &g = m->graph;
+    const size_t pend0 = c->pending.size();
+    const long long l0 = c->launches;
+    long long cl0[8];
+    std::memcpy(cl0, c->times.launches, sizeof cl0);
+    if (cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    const int rc = eval_device_body(m, n, H, y, x, trainable_only, xhat);
+    if (g_alloc_epoch != g.epoch) cudaGetLastError(); // allocated while capturing: unusable
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(c->stream, &graph);
+    // the capture pass counted launches and took events but ran nothing
+    c->launches = l0;
+    std::memcpy(c->times.launches, cl0, sizeof cl0);
+    g.timers.assign(c->pending.begin() + static_cast<long>(pend0), c->pending.end());
+    c->pending.resize(pend0);
+    if (rc || ec != cudaSuccess || !graph || g_alloc_epoch != g.epoch) {
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
+        return 1; // the caller runs the body eagerly (and reports its errors)
+    }
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) {
+        cudaGetLastError();
+        drop_graph(m);
+        return 0;
+    }
+    g.exec = exec; // g.launches / cls_launches: counted by the eager run of this key
+    return 0;
+}
+} // namespace
+
 int detnet_batch_evaluate_device(detnet_model *m, long n, const float *H, const float *y,
                                  const int8_t *x, int trainable_only, float *xhat,
                                  detnet_eval *out) {
@@ -763,13 +846,48 @@ int detnet_batch_evaluate_device(detnet_model *m, long n, const float *H, const 
     if (n <= 0) return 0; // finish_eval of an empty batch (kernels.cpp:93-103)
     CK(cudaSetDevice(c->device));
     if (int rc = ensure_ws(c, n, m->K)) return rc;
-    if (int rc = reset_sing(c, c->stream)) return rc;
-    if (int rc = run_pre(m, c->stream, 0, n, n, H, y, x)) return rc;
-    const long tiles = (n + TILE - 1) / TILE;
-    if (int rc = run_stack(m, c->stream, 0, tiles, n, 0, m->L, trainable_only != 0, xhat, nullptr,
-                           nullptr))
-        return rc;
-    return finish(m, n, out);
+    // Graph replay: a repeated call (same samples, model, settings, buffers)
+    // is one cudaGraphLaunch of the whole evaluation. The first call with a
+    // key runs eagerly (and allocates what it needs), the second captures.
+    static const bool no_graph =
+        std::getenv("DETNET_NO_GRAPH") != nullptr || std::getenv("DETNET_TC_TRACE") != nullptr;
+    detnet_model::EvalGraph key;
+    key.n = n; key.H = H; key.y = y; key.x = x; key.xhat = xhat;
+    key.trainable = trainable_only; key.path = c->path; key.exact = c->exact_pre;
+    key.profiling = c->profiling; key.version = m->version; key.st = c->stream;
+    key.epoch = g_alloc_epoch;
+    auto &g = m->graph;
+    if (!g.same(key)) {
+        drop_graph(m);
+        g = key;
+        m->graph_seen = 0;
+    }
+    // (not while profiling: timer events recorded by graph nodes do not time)
+    if (!no_graph && !c->profiling && !g.exec && m->graph_seen == 1) {
+        if (capture_graph(m, n, H, y, x, trainable_only, xhat) || !g.exec) {
+            drop_graph(m); // not capturable here: stay eager for this key
+            g = key;
+            m->graph_seen = 2;
+        }
+    }
+    if (!no_graph && g.exec) {
+        CK(cudaGraphLaunch(g.exec, c->stream));
+        c->launches += g.launches;
+        for (int k = 0; k < 8; ++k) c->times.launches[k] += g.cls_launches[k];
+        return finish_host(m, n, out);
+    }
+    const long long l0 = c->launches;
+    long long cl0[8];
+    std::memcpy(cl0, c->times.launches, sizeof cl0);
+    if (int rc = eval_device_body(m, n, H, y, x, trainable_only, xhat)) return rc;
+    const int rc = finish_host(m, n, out);
+    if (rc == 0 && m->graph_seen == 0) {
+        g.epoch = g_alloc_epoch; // buffers this call allocated are part of the key
+        g.launches = c->launches - l0;
+        for (int k = 0; k < 8; ++k) g.cls_launches[k] = c->times.launches[k] - cl0[k];
+        m->graph_seen = 1;
+    }
+    return rc;
 }
 
 namespace {

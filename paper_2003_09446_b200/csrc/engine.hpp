@@ -41,11 +41,16 @@ inline long record_size(int K, int Z, int V) {
 }
 
 // device buffer that only grows
+// Bumped on every device (re)allocation: a captured CUDA graph is replayed
+// only while no buffer it may reference has moved.
+inline long long g_alloc_epoch = 0;
+
 struct DBuf {
     void *p = nullptr;
     size_t cap = 0;
     int ensure(size_t bytes) {
         if (bytes <= cap) return 0;
+        ++g_alloc_epoch;
         if (p) cudaFree(p);
         p = nullptr;
         cap = 0;
@@ -54,6 +59,7 @@ struct DBuf {
         return 0;
     }
     void release() {
+        ++g_alloc_epoch;
         if (p) cudaFree(p);
         p = nullptr;
         cap = 0;
@@ -163,6 +169,29 @@ struct detnet_model {
     int sparse_max_words = 0; // largest per-layer stream (shared-memory staging)
     bool sparse_ready = false;
     double density = 1.0;   // surviving W entries / all W entries
+    // CUDA graph of batch_evaluate_device (K1 + fallback + stack + reduce +
+    // result copy), replayed while the call, the context settings, the model
+    // layout and every device buffer are those it was captured with
+    long long version = 0; // bumped when packing / layout / host flags change
+    struct EvalGraph {
+        long n = -1;
+        const void *H = nullptr, *y = nullptr, *x = nullptr, *xhat = nullptr;
+        int trainable = 0, path = -1;
+        bool exact = false, profiling = false;
+        long long version = -1, epoch = -1;
+        cudaStream_t st = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        long long launches = 0;           // kernels per replay
+        long long cls_launches[8] = {};   // per class
+        std::vector<detnet_ctx::Pending> timers; // captured event pairs
+        bool same(const EvalGraph &o) const {
+            return n == o.n && H == o.H && y == o.y && x == o.x && xhat == o.xhat &&
+                   trainable == o.trainable && path == o.path && exact == o.exact &&
+                   profiling == o.profiling && version == o.version && epoch == o.epoch &&
+                   st == o.st;
+        }
+    } graph;
+    int graph_seen = 0; // consecutive eager calls with the current key
 };
 
 namespace detnet {

@@ -341,6 +341,7 @@ int detnet_train_grad(detnet_model *m, long n, const float *H, const float *y, c
 
 int detnet_train_apply(detnet_model *m, const double *raw_dev, long n_global,
                        const detnet_loss_spec *spec, const detnet_adam_config *cfg) {
+    ++m->version; // packed images / layout may change: drop captured evaluate graphs
     if (!m || !raw_dev || n_global < 1) return fail(DETNET_ERR_CONTRACT, "bad argument");
     if (int rc = validate_adam(cfg)) return rc;
     detnet_ctx *c = m->ctx;
@@ -394,6 +395,7 @@ int detnet_model_get_params(detnet_model *m, double *out) {
 // the tcgen05 images (compacted to the live units when few survive) and the
 // sparse stream -- from the result. Adam moments and the step counter survive.
 int detnet_model_prune(detnet_model *m, int kind, double eta, double eta1, double eta2) {
+    ++m->version; // packed images / layout may change: drop captured evaluate graphs
     if (!m) return fail(DETNET_ERR_CONTRACT, "null argument");
     auto frac = [](double v) { return v >= 0.0 && v < 1.0; };
     if (kind < 0 || kind > 2) return fail(DETNET_ERR_CONTRACT, "prune: kind must be 0, 1 or 2");

@@ -16,6 +16,11 @@ if timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > $OUT/pla
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > $OUT/ncu_launch.log 2>&1
 fi
+# 2b. launch list of one training step (config 5)
+if timeout 600 python bench.py --config 5 --steps 2 --warmup 3 --no-cpu > $OUT/plain_c5.json 2>&1; then
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
+    --log-file $OUT/launches_c5.csv python bench.py --config 5 --steps 1 --warmup 3 --no-cpu > $OUT/ncu_launch_c5.log 2>&1
+fi
 # 3. one full capture per hot kernel (2^18 detections, config-2 workload):
 #    the split-FP16 stack (default), K1, and the 3xTF32 stack (path 2) for comparison
 if timeout 300 python tools/prof_run.py 262144 > $OUT/prof_run.log 2>&1; then

@@ -360,18 +360,28 @@ def main():
     avg_launch_s = stack_ms / 1e3 / max(stack_launches, 1)
     achieved = flops_per_launch / avg_launch_s / 1e12
     tc_path = ctx_path_name(ctx, model)
+    # B200_PROFILING.md: the burst bf16 figure for a kernel timed alone, the
+    # sustained (power-capped) one for a kernel timed inside a long step --
+    # steps of >= 10 ms of back-to-back launches run in the capped regime
+    long_step = ms / args.steps >= 10.0
+    regime = "sustained" if long_step else "burst"
+    bf16 = peaks.get("bf16_tflops_sustained" if long_step else "bf16_tflops")
+    bf16_burst = peaks.get("bf16_tflops")
+    peak_burst = None
     if tc_path == "tcgen05-3xtf32":
-        # the tensor-core roofline: measured dense bf16 GEMM (burst) / 2 for the
-        # TF32 rate / 3 for the 3xTF32 split (B200_PROFILING.md denominators)
-        peak = peaks["bf16_tflops"] / 6.0 if peaks.get("bf16_tflops") else None
-        peak_note = (f"{peaks.get('peaks_source')} bf16 {peaks.get('bf16_tflops')} TF/s (burst) "
+        # the tensor-core roofline: measured dense bf16 GEMM / 2 for the TF32
+        # rate / 3 for the 3xTF32 split (B200_PROFILING.md denominators)
+        peak = bf16 / 6.0 if bf16 else None
+        peak_burst = bf16_burst / 6.0 if bf16_burst else None
+        peak_note = (f"{peaks.get('peaks_source')} bf16 {bf16} TF/s ({regime}) "
                      "/ 2 (TF32 rate) / 3 (3xTF32 split); this run's cuBLAS TF32 GEMM: "
                      f"{peaks.get('tf32_tflops', 0):.0f} TF/s")
     elif tc_path == "tcgen05-split-fp16":
         # FP16 MMAs run at the bf16 rate; every FP32-class product is three of
         # them (hi.hi + hi.lo + lo.hi)
-        peak = peaks["bf16_tflops"] / 3.0 if peaks.get("bf16_tflops") else None
-        peak_note = (f"{peaks.get('peaks_source')} bf16 {peaks.get('bf16_tflops')} TF/s (burst; "
+        peak = bf16 / 3.0 if bf16 else None
+        peak_burst = bf16_burst / 3.0 if bf16_burst else None
+        peak_note = (f"{peaks.get('peaks_source')} bf16 {bf16} TF/s ({regime}; "
                      "FP16 MMA rate) / 3 (split-FP16 products hi.hi + hi.lo + lo.hi)")
     else:
         peak = peaks.get("fp32_tflops")
@@ -380,6 +390,7 @@ def main():
     roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": (achieved / peak) if peak else None, "traffic": traffic,
             "traffic_source": traffic_note,
+            "frac_burst": (achieved / peak_burst) if peak_burst else None,
             "kernel": "k_stack (fused layer stack)", "path": tc_path, "peak_source": peak_note,
             "census_flop_per_detection_layers": census_layers,
             "detections_per_launch": per_point, "avg_launch_ms": avg_launch_s * 1e3,

@@ -529,9 +529,24 @@ __global__ void k_group_norms(const double *params, const double *masks, int K, 
     if (j <= IN) { off = j < IN ? oW1 : ob1; rows = Z; cols = IN; col = j; bias = j == IN; }
     else if (j <= IN + 1 + Z) { const int jj = j - IN - 1; off = jj < Z ? oW2 : ob2; rows = K; cols = Z; col = jj; bias = jj == Z; }
     else { const int jj = j - IN - 2 - Z; off = jj < Z ? oW3 : ob3; rows = V; cols = Z; col = jj; bias = jj == Z; }
+    // loads batched 16 rows ahead (the sum itself stays sequential in i, as in
+    // loss.cpp:43-59): one dependent L2 round trip per 16 rows instead of per row
     double sq = 0.0;
-    for (int i = 0; i < rows; ++i) {
-        const long e = bias ? off + i : off + static_cast<long>(i) * cols + col;
+    const long step = bias ? 1 : cols;
+    const long e0 = bias ? off : off + col;
+    int i = 0;
+    for (; i + 16 <= rows; i += 16) {
+        double w[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const long e = e0 + static_cast<long>(i + u) * step;
+            w[u] = dmul(__ldg(p + e), mk ? __ldg(mk + e) : 1.0);
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) sq = dadd(sq, dmul(w[u], w[u]));
+    }
+    for (; i < rows; ++i) {
+        const long e = e0 + static_cast<long>(i) * step;
         const double w = dmul(p[e], mk ? mk[e] : 1.0);
         sq = dadd(sq, dmul(w, w));
     }

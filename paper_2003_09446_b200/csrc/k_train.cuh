@@ -395,6 +395,14 @@ constexpr int DW_TILE = 64, DW_SPLIT = 256, DW_KC = 32;
 // drift, which comes from gate flips in the FP32 forward/backward.)
 using DW_ACC = float;
 __device__ __forceinline__ float dw_fma(float a, float b, float c) { return fmaf(a, b, c); }
+// (d0, d1) += a * (b0, b1) as one fma.rn.f32x2
+__device__ __forceinline__ void dw_fma2(float &d0, float &d1, float a, float b0, float b1) {
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %2};\n\tmov.b64 rb, {%3, %4};\n\tmov.b64 rd, {%0, %1};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rd;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "+f"(d0), "+f"(d1)
+        : "f"(a), "f"(b0), "f"(b1));
+}
 
 // grid: (N tiles, M tiles, jobs x splits) -- one (tile, split) per CTA
 __global__ void __launch_bounds__(256) k_dw_gemm(const DwJob *jobs, long n, long ts, int splits) {
@@ -402,54 +410,75 @@ __global__ void __launch_bounds__(256) k_dw_gemm(const DwJob *jobs, long n, long
     const int m0 = blockIdx.y * DW_TILE, n0 = blockIdx.x * DW_TILE;
     if (m0 >= jb.M || n0 > jb.N) return;
     // rows padded by 4 floats: the transposing stores (32 consecutive samples
-    // of a row per warp) spread over 8 banks instead of 1; 128-bit reads stay aligned
-    __shared__ __align__(16) float sA[DW_KC][DW_TILE + 4], sB[DW_KC][DW_TILE + 4];
+    // of a row per warp) spread over 8 banks instead of 1; 128-bit reads stay
+    // aligned. Two buffers: chunk c+1 is fetched into registers while chunk c
+    // is multiplied, then stored to the other buffer (one barrier per chunk).
+    __shared__ __align__(16) float sA[2][DW_KC][DW_TILE + 4], sB[2][DW_KC][DW_TILE + 4];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4; // 16 x 16 threads, 4 x 4 outputs
-    {
-        const int sp = static_cast<int>(blockIdx.z % splits);
-        const long k0 = static_cast<long>(sp) * DW_SPLIT;
-        const long k1 = k0 + DW_SPLIT < n ? k0 + DW_SPLIT : n;
-        DW_ACC c[4][4];
+    const int sp = static_cast<int>(blockIdx.z % splits);
+    const long k0 = static_cast<long>(sp) * DW_SPLIT;
+    const long k1 = k0 + DW_SPLIT < n ? k0 + DW_SPLIT : n;
+    DW_ACC c[4][4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) c[i][j] = 0;
-        for (long kc = k0; kc < k1; kc += DW_KC) {
-            // 64 rows x 32 samples of A and of B: each thread loads 8 + 8 floats
-            // (consecutive threads -> consecutive samples of a row: coalesced)
+        for (int j = 0; j < 4; ++j) c[i][j] = 0;
+    // 64 rows x 32 samples of A and of B per chunk: each thread moves 8 + 8
+    // floats (consecutive threads -> consecutive samples of a row: coalesced)
+    float ra[8], rb[8];
+    auto gload = [&](long kc) {
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                const int idx = threadIdx.x + 256 * r;
-                const int kk = idx % DW_KC, row = idx / DW_KC;
-                const long k = kc + kk;
-                const bool in = k < k1;
-                const int mr = m0 + row, nr = n0 + row;
-                sA[kk][row] = (in && mr < jb.M) ? jb.A[static_cast<long>(mr) * ts + k] : 0.f;
-                sB[kk][row] = (in && nr < jb.N) ? jb.B[static_cast<long>(nr) * ts + k]
-                                                : ((in && nr == jb.N) ? 1.f : 0.f);
-            }
-            __syncthreads();
-#pragma unroll 8
-            for (int kk = 0; kk < DW_KC; ++kk) {
-                const float4 a = *reinterpret_cast<const float4 *>(&sA[kk][ty * 4]);
-                const float4 b = *reinterpret_cast<const float4 *>(&sB[kk][tx * 4]);
-                const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) c[i][j] = dw_fma(av[i], bv[j], c[i][j]);
-            }
-            __syncthreads();
+        for (int r = 0; r < 8; ++r) {
+            const int idx = threadIdx.x + 256 * r;
+            const int kk = idx % DW_KC, row = idx / DW_KC;
+            const long k = kc + kk;
+            const bool in = k < k1;
+            const int mr = m0 + row, nr = n0 + row;
+            ra[r] = (in && mr < jb.M) ? __ldg(jb.A + static_cast<long>(mr) * ts + k) : 0.f;
+            rb[r] = (in && nr < jb.N) ? __ldg(jb.B + static_cast<long>(nr) * ts + k)
+                                      : ((in && nr == jb.N) ? 1.f : 0.f);
         }
+    };
+    auto sstore = [&](int buf) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int r = 0; r < 8; ++r) {
+            const int idx = threadIdx.x + 256 * r;
+            const int kk = idx % DW_KC, row = idx / DW_KC;
+            sA[buf][kk][row] = ra[r];
+            sB[buf][kk][row] = rb[r];
+        }
+    };
+    gload(k0);
+    sstore(0);
+    __syncthreads();
+    int buf = 0;
+    for (long kc = k0; kc < k1; kc += DW_KC) {
+        const bool more = kc + DW_KC < k1;
+        if (more) gload(kc + DW_KC);
+        // per output: samples in order, as before (bit-identical partials)
+#pragma unroll 8
+        for (int kk = 0; kk < DW_KC; ++kk) {
+            const float4 a4 = *reinterpret_cast<const float4 *>(&sA[buf][kk][ty * 4]);
+            const float4 b4 = *reinterpret_cast<const float4 *>(&sB[buf][kk][tx * 4]);
+            const float av[4] = {a4.x, a4.y, a4.z, a4.w}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
+            // FFMA2: two fused multiply-adds per instruction, each rounded as fmaf
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int mr = m0 + ty * 4 + i, nc = n0 + tx * 4 + j;
-                if (mr < jb.M && nc <= jb.N)
-                    jb.out[(static_cast<long>(sp) * jb.M + mr) * (jb.N + 1) + nc] = c[i][j];
-            }
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; j += 2) dw_fma2(c[i][j], c[i][j + 1], av[i], bv[j], bv[j + 1]);
+        }
+        if (more) sstore(buf ^ 1);
+        __syncthreads();
+        buf ^= 1;
     }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int mr = m0 + ty * 4 + i, nc = n0 + tx * 4 + j;
+            if (mr < jb.M && nc <= jb.N)
+                jb.out[(static_cast<long>(sp) * jb.M + mr) * (jb.N + 1) + nc] = c[i][j];
+        }
 }
 
 struct SumArgs {

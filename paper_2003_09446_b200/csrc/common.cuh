@@ -112,6 +112,15 @@ __device__ __forceinline__ void bulk_g2s_chunked(void *dst_smem, const void *src
 
 // ---- deterministic block reductions ---------------------------------------
 // bar.sync on a named barrier (ids 1..15; 0 is __syncthreads)
+// (d0, d1) += (a0, a1) * (b0, b1): one fma.rn.f32x2 (SASS FFMA2); each lane is
+// rounded exactly like fmaf, so results are bit-identical to two fmaf calls
+__device__ __forceinline__ void fma_x2(float &d0, float &d1, float a0, float a1, float b0, float b1) {
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "mov.b64 rd, {%0, %1};\n\tfma.rn.f32x2 rd, ra, rb, rd;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "+f"(d0), "+f"(d1)
+        : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }

@@ -361,6 +361,8 @@ __global__ void __launch_bounds__(SIMTP_THREADS, 1) k_stack_simt_pair(StackArgs 
              : (j) < 2 * K ? x[((j) - K) < K ? (j) - K : 0]                                      \
                            : (j) < 3 * K ? gx[((j) - 2 * K) < K ? (j) - 2 * K : 0]               \
                                          : v[((j) - 3 * K) < V ? (j) - 3 * K : 0])
+        // Same FMA chains per unit as before (u0..u3 over the input columns,
+        // acc[o] over the units), issued as FFMA2 pairs: bit-identical.
 #pragma unroll 1
         for (int i = i0; i < i0 + ZH; ++i) {
             const float4 *w4 = reinterpret_cast<const float4 *>(W + i * IN4);
@@ -368,14 +370,19 @@ __global__ void __launch_bounds__(SIMTP_THREADS, 1) k_stack_simt_pair(StackArgs 
 #pragma unroll
             for (int m = 0; m < IN4 / 4; ++m) {
                 const float4 w = w4[m];
-                if (4 * m + 0 < IN) u0 = fmaf(w.x, DETNET_IN(4 * m + 0), u0);
-                else if (4 * m + 0 == IN) u0 += w.x;
-                if (4 * m + 1 < IN) u1 = fmaf(w.y, DETNET_IN(4 * m + 1), u1);
-                else if (4 * m + 1 == IN) u1 += w.y;
-                if (4 * m + 2 < IN) u2 = fmaf(w.z, DETNET_IN(4 * m + 2), u2);
-                else if (4 * m + 2 == IN) u2 += w.z;
-                if (4 * m + 3 < IN) u3 = fmaf(w.w, DETNET_IN(4 * m + 3), u3);
-                else if (4 * m + 3 == IN) u3 += w.w;
+                if (4 * m + 3 < IN) {
+                    fma_x2(u0, u1, w.x, w.y, DETNET_IN(4 * m + 0), DETNET_IN(4 * m + 1));
+                    fma_x2(u2, u3, w.z, w.w, DETNET_IN(4 * m + 2), DETNET_IN(4 * m + 3));
+                } else {
+                    if (4 * m + 0 < IN) u0 = fmaf(w.x, DETNET_IN(4 * m + 0), u0);
+                    else if (4 * m + 0 == IN) u0 += w.x;
+                    if (4 * m + 1 < IN) u1 = fmaf(w.y, DETNET_IN(4 * m + 1), u1);
+                    else if (4 * m + 1 == IN) u1 += w.y;
+                    if (4 * m + 2 < IN) u2 = fmaf(w.z, DETNET_IN(4 * m + 2), u2);
+                    else if (4 * m + 2 == IN) u2 += w.z;
+                    if (4 * m + 3 < IN) u3 = fmaf(w.w, DETNET_IN(4 * m + 3), u3);
+                    else if (4 * m + 3 == IN) u3 += w.w;
+                }
             }
             const float u = (u0 + u1) + (u2 + u3);
             const float z = u > 0.f ? u : 0.f;
@@ -384,10 +391,15 @@ __global__ void __launch_bounds__(SIMTP_THREADS, 1) k_stack_simt_pair(StackArgs 
 #pragma unroll
             for (int m = 0; m < O4 / 4; ++m) {
                 const float4 w = c4[m];
-                if (4 * m + 0 < O) acc[4 * m + 0] = fmaf(w.x, z, acc[4 * m + 0]);
-                if (4 * m + 1 < O) acc[4 * m + 1] = fmaf(w.y, z, acc[4 * m + 1]);
-                if (4 * m + 2 < O) acc[4 * m + 2] = fmaf(w.z, z, acc[4 * m + 2]);
-                if (4 * m + 3 < O) acc[4 * m + 3] = fmaf(w.w, z, acc[4 * m + 3]);
+                if (4 * m + 3 < O) {
+                    fma_x2(acc[4 * m + 0], acc[4 * m + 1], w.x, w.y, z, z);
+                    fma_x2(acc[4 * m + 2], acc[4 * m + 3], w.z, w.w, z, z);
+                } else {
+                    if (4 * m + 0 < O) acc[4 * m + 0] = fmaf(w.x, z, acc[4 * m + 0]);
+                    if (4 * m + 1 < O) acc[4 * m + 1] = fmaf(w.y, z, acc[4 * m + 1]);
+                    if (4 * m + 2 < O) acc[4 * m + 2] = fmaf(w.z, z, acc[4 * m + 2]);
+                    if (4 * m + 3 < O) acc[4 * m + 3] = fmaf(w.w, z, acc[4 * m + 3]);
+                }
             }
         }
 #undef DETNET_IN

@@ -140,10 +140,15 @@ __global__ void __launch_bounds__(THREADS, 1) k_train_bwd(BwdArgs a) {
                 for (int m = 0; m < O4 / 4; ++m) {
                     const float4 c = c4[m];
 #define DETNET_G(j) ((j) < K ? u2bar[(j) < K ? (j) : 0] : vbar[((j) - K) < V ? (j) - K : 0])
-                    if (4 * m + 0 < O) zb0 = fmaf(c.x, DETNET_G(4 * m + 0), zb0);
-                    if (4 * m + 1 < O) zb1 = fmaf(c.y, DETNET_G(4 * m + 1), zb1);
-                    if (4 * m + 2 < O) zb0 = fmaf(c.z, DETNET_G(4 * m + 2), zb0);
-                    if (4 * m + 3 < O) zb1 = fmaf(c.w, DETNET_G(4 * m + 3), zb1);
+                    if (4 * m + 3 < O) { // the same two chains, as FFMA2 pairs
+                        fma_x2(zb0, zb1, c.x, c.y, DETNET_G(4 * m + 0), DETNET_G(4 * m + 1));
+                        fma_x2(zb0, zb1, c.z, c.w, DETNET_G(4 * m + 2), DETNET_G(4 * m + 3));
+                    } else {
+                        if (4 * m + 0 < O) zb0 = fmaf(c.x, DETNET_G(4 * m + 0), zb0);
+                        if (4 * m + 1 < O) zb1 = fmaf(c.y, DETNET_G(4 * m + 1), zb1);
+                        if (4 * m + 2 < O) zb0 = fmaf(c.z, DETNET_G(4 * m + 2), zb0);
+                        if (4 * m + 3 < O) zb1 = fmaf(c.w, DETNET_G(4 * m + 3), zb1);
+                    }
 #undef DETNET_G
                 }
                 const float ub = zg[q] > 0.f ? zb0 + zb1 : 0.f;
@@ -152,6 +157,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_train_bwd(BwdArgs a) {
 #pragma unroll
                 for (int m = K / 4; m < IN4 / 4; ++m) {
                     const float4 wv = w4[m];
+                    if (4 * m >= K && 4 * m + 3 < IN) {
+                        fma_x2(ibar[4 * m - K], ibar[4 * m + 1 - K], wv.x, wv.y, ub, ub);
+                        fma_x2(ibar[4 * m + 2 - K], ibar[4 * m + 3 - K], wv.z, wv.w, ub, ub);
+                        continue;
+                    }
 #define DETNET_IB(c, wc)                                                                        \
     if (4 * m + (c) >= K && 4 * m + (c) < IN)                                                    \
         ibar[(4 * m + (c) - K) >= 0 ? 4 * m + (c) - K : 0] =                                    \
@@ -305,10 +315,15 @@ __global__ void __launch_bounds__(BWP_THREADS, 1) k_train_bwd_pair(BwdArgs a) {
                 for (int m = 0; m < O4 / 4; ++m) {
                     const float4 c = c4[m];
 #define DETNET_G(j) ((j) < K ? u2bar[(j) < K ? (j) : 0] : vbar[((j) - K) < V ? (j) - K : 0])
-                    if (4 * m + 0 < O) zb0 = fmaf(c.x, DETNET_G(4 * m + 0), zb0);
-                    if (4 * m + 1 < O) zb1 = fmaf(c.y, DETNET_G(4 * m + 1), zb1);
-                    if (4 * m + 2 < O) zb0 = fmaf(c.z, DETNET_G(4 * m + 2), zb0);
-                    if (4 * m + 3 < O) zb1 = fmaf(c.w, DETNET_G(4 * m + 3), zb1);
+                    if (4 * m + 3 < O) { // the same two chains, as FFMA2 pairs
+                        fma_x2(zb0, zb1, c.x, c.y, DETNET_G(4 * m + 0), DETNET_G(4 * m + 1));
+                        fma_x2(zb0, zb1, c.z, c.w, DETNET_G(4 * m + 2), DETNET_G(4 * m + 3));
+                    } else {
+                        if (4 * m + 0 < O) zb0 = fmaf(c.x, DETNET_G(4 * m + 0), zb0);
+                        if (4 * m + 1 < O) zb1 = fmaf(c.y, DETNET_G(4 * m + 1), zb1);
+                        if (4 * m + 2 < O) zb0 = fmaf(c.z, DETNET_G(4 * m + 2), zb0);
+                        if (4 * m + 3 < O) zb1 = fmaf(c.w, DETNET_G(4 * m + 3), zb1);
+                    }
 #undef DETNET_G
                 }
                 const float ub = zg[q] > 0.f ? zb0 + zb1 : 0.f;
@@ -317,6 +332,11 @@ __global__ void __launch_bounds__(BWP_THREADS, 1) k_train_bwd_pair(BwdArgs a) {
 #pragma unroll
                 for (int m = K / 4; m < IN4 / 4; ++m) {
                     const float4 wv = w4[m];
+                    if (4 * m >= K && 4 * m + 3 < IN) {
+                        fma_x2(ibar[4 * m - K], ibar[4 * m + 1 - K], wv.x, wv.y, ub, ub);
+                        fma_x2(ibar[4 * m + 2 - K], ibar[4 * m + 3 - K], wv.z, wv.w, ub, ub);
+                        continue;
+                    }
 #define DETNET_IB(c, wc)                                                                        \
     if (4 * m + (c) >= K && 4 * m + (c) < IN)                                                    \
         ibar[(4 * m + (c) - K) >= 0 ? 4 * m + (c) - K : 0] =                                    \

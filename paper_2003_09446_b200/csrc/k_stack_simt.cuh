@@ -485,7 +485,18 @@ static __global__ void __launch_bounds__(1024) k_reduce(const double *tile_loss,
     double l = 0.0;
     long long e = 0, f = 0;
     for (long i = t; i < n_tiles; i += 1024) { l += tile_loss[i]; e += tile_err[i]; }
-    for (long i = t; i < n; i += 1024) f += flag[i];
+    // flags are 0/1 bytes: 16 per 128-bit load, summed with popc
+    long i0 = 0;
+    if ((reinterpret_cast<uintptr_t>(flag) & 15) == 0) {
+        const uint4 *f16 = reinterpret_cast<const uint4 *>(flag);
+        const long n16 = n / 16;
+        for (long i = t; i < n16; i += 1024) {
+            const uint4 v = __ldg(f16 + i);
+            f += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+        }
+        i0 = n16 * 16;
+    }
+    for (long i = i0 + t; i < n; i += 1024) f += flag[i];
     sl[t] = l; se[t] = e; sf[t] = f;
     __syncthreads();
     for (int w = 512; w > 0; w >>= 1) {

@@ -35,6 +35,10 @@ struct BwdArgs {
     float *u1bar;           // [L][Z][ts]
     float *g23bar;          // [L][K+V][ts]
     double *tbar_part;      // [L][gridDim.x]
+    // k_train_bwd_pair only: sweep iterations [it_begin, it_end) of [0, L - lf)
+    // (layer L-1-it); a_bar / v_bar carried between chunks in state [K+V][ts]
+    int it_begin = 0, it_end = -1;
+    float *state = nullptr;
 };
 
 // THREADS samples per CTA (one CTA per SM: the double-buffered weights take
@@ -254,23 +258,31 @@ __global__ void __launch_bounds__(BWP_THREADS, 1) k_train_bwd_pair(BwdArgs a) {
     }
     __syncthreads();
     const uint32_t bytes = static_cast<uint32_t>(REC) * 4u;
-    const int nl = a.L - a.lf;
-    if (tid == 0 && nl > 0) {
+    const int nl_all = a.L - a.lf;
+    const int it0 = a.it_begin, it1 = a.it_end < 0 ? nl_all : a.it_end;
+    if (tid == 0 && it0 < it1) {
         mbar_arrive_expect_tx(bar, bytes);
-        bulk_g2s_chunked(sw, a.wrec + static_cast<long>(a.L - 1) * a.rec_floats, bytes, bar);
+        bulk_g2s_chunked(sw, a.wrec + static_cast<long>(a.L - 1 - it0) * a.rec_floats, bytes, bar);
     }
     const uint32_t xm = a.xmask[tile * TILE + col];
     const float dinv2 = static_cast<float>(2.0 / a.denom[tile * TILE + col]);
     const float *gps = a.gp + tile * NG * TILE + col;
     float abar[K], vbar[V];
+    if (it0 > 0) { // a later chunk: the state the previous chunk left
 #pragma unroll
-    for (int k = 0; k < K; ++k) abar[k] = 0.f;
+        for (int k = 0; k < K; ++k) abar[k] = a.state[k * a.ts + s];
 #pragma unroll
-    for (int k = 0; k < V; ++k) vbar[k] = 0.f;
+        for (int k = 0; k < V; ++k) vbar[k] = a.state[(K + k) * a.ts + s];
+    } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k) abar[k] = 0.f;
+#pragma unroll
+        for (int k = 0; k < V; ++k) vbar[k] = 0.f;
+    }
 
-    for (int it = 0; it < nl; ++it) {
+    for (int it = it0; it < it1; ++it) {
         const int l = a.L - 1 - it;
-        mbar_wait(bar, it & 1);
+        mbar_wait(bar, (it - it0) & 1);
         const float *W = sw;
         const float w = static_cast<float>(a.lnk[l]) * dinv2;
         const float *xn = l + 1 < a.L ? a.tr_in + (static_cast<long>(l + 1) * IN + K) * a.ts + s
@@ -351,7 +363,7 @@ __global__ void __launch_bounds__(BWP_THREADS, 1) k_train_bwd_pair(BwdArgs a) {
         }
         // every weight read of layer l is done: stream layer l-1 in now
         __syncthreads();
-        if (tid == 0 && it + 1 < nl) {
+        if (tid == 0 && it + 1 < it1) {
             mbar_arrive_expect_tx(bar, bytes);
             bulk_g2s_chunked(sw, a.wrec + static_cast<long>(l - 1) * a.rec_floats, bytes, bar);
         }
@@ -395,6 +407,12 @@ __global__ void __launch_bounds__(BWP_THREADS, 1) k_train_bwd_pair(BwdArgs a) {
         if (isA && (tid & 31) == 0) s_t[warp] = tsum;
         __syncthreads(); // s_t ready; B is done reading sAV before A rewrites it
         if (tid == 0) a.tbar_part[static_cast<long>(l) * gridDim.x + blockIdx.x] = s_t[0] + s_t[1];
+    }
+    if (it1 < nl_all && isA && live_tile) { // hand the sweep state to the next chunk
+#pragma unroll
+        for (int k = 0; k < K; ++k) a.state[k * a.ts + s] = abar[k];
+#pragma unroll
+        for (int k = 0; k < V; ++k) a.state[(K + k) * a.ts + s] = vbar[k];
     }
 }
 

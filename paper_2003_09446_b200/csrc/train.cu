@@ -5,6 +5,7 @@
 // (host arrays, the reference seam) and detnet_train_grad / detnet_train_apply
 // (device-resident step; raw gradient sums in a caller buffer so ranks can
 // all-reduce them between the two calls).
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -70,6 +71,9 @@ const BwdEntry *find_bwd(int K, int Z, int V) {
 
 struct TrainWs {
     DBuf tr_in, tr_z, tr_u2, tr_xf, u1bar, g23bar, tbar, p1, p23, jobs, raw, grads, colnorm;
+    DBuf bstate; // reverse-sweep state between chunks [K+V][ts]
+    cudaStream_t hi = nullptr; // high-priority stream for the sweep chunks
+    cudaEvent_t ev[9] = {};
     DBuf in_H, in_y, in_x;
 };
 
@@ -159,12 +163,6 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
         ba.u1bar = w.u1bar.as<float>();
         ba.g23bar = w.g23bar.as<float>();
         ba.tbar_part = w.tbar.as<double>();
-        {
-            LaunchScope ls(c, DETNET_K_BACKWARD, c->stream);
-            be->fn(dim3(bwd_blocks), dim3(bwd_per), 2 * static_cast<size_t>(m->simt_rec) * 4 + 64,
-                   c->stream, ba);
-        }
-        if (int rc = check_launch()) return rc;
         std::vector<DwJob> jobs;
         for (int l = lf; l < L; ++l) {
             jobs.push_back({w.u1bar.as<float>() + static_cast<long>(l) * Z * ts,
@@ -177,13 +175,56 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
         CK(cudaMemcpyAsync(w.jobs.p, jobs.data(), sizeof(DwJob) * jobs.size(),
                            cudaMemcpyHostToDevice, c->stream));
         const int mx = std::max(IN, Z) + 1, my = std::max(Z, O);
-        {
+        auto dw_launch = [&](int j0, int j1) { // jobs [j0, j1) on the context stream
             LaunchScope ls(c, DETNET_K_BACKWARD, c->stream);
             k_dw_gemm<<<dim3((mx + DW_TILE - 1) / DW_TILE, (my + DW_TILE - 1) / DW_TILE,
-                             static_cast<unsigned>(jobs.size() * splits)),
-                        256, 0, c->stream>>>(w.jobs.as<DwJob>(), n, ts, splits);
+                             static_cast<unsigned>((j1 - j0) * splits)),
+                        256, 0, c->stream>>>(w.jobs.as<DwJob>() + j0, n, ts, splits);
+        };
+        // Small batches: the sweep runs in chunks of layers on a high-priority
+        // stream and the dW contractions of each finished chunk run on the
+        // context stream meanwhile, on the SMs the sweep leaves idle (79 of 148
+        // at batch 5000). Bit-identical to one sweep + one dW launch.
+        static const int env_chunks = std::getenv("DETNET_BWD_CHUNKS") ? std::atoi(std::getenv("DETNET_BWD_CHUNKS")) : 4;
+        const int nl = L - lf;
+        const int chunks = bwd_large ? 1 : std::max(1, std::min({env_chunks, nl, 8}));
+        if (chunks > 1) {
+            if (!w.hi) {
+                int least = 0, greatest = 0;
+                CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+                CK(cudaStreamCreateWithPriority(&w.hi, cudaStreamNonBlocking, greatest));
+                for (auto &e : w.ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            }
+            if (w.bstate.ensure(sizeof(float) * (K + V) * ts))
+                return fail(DETNET_ERR_CUDA, "training workspace allocation failed");
+            ba.state = w.bstate.as<float>();
+            CK(cudaEventRecord(w.ev[8], c->stream)); // forward trace + jobs ready
+            CK(cudaStreamWaitEvent(w.hi, w.ev[8], 0));
+            for (int j = 0; j < chunks; ++j) {
+                ba.it_begin = static_cast<int>(static_cast<long>(nl) * j / chunks);
+                ba.it_end = static_cast<int>(static_cast<long>(nl) * (j + 1) / chunks);
+                {
+                    LaunchScope ls(c, DETNET_K_BACKWARD, w.hi);
+                    be->fn(dim3(bwd_blocks), dim3(bwd_per), 0, w.hi, ba);
+                }
+                if (int rc = check_launch()) return rc;
+                CK(cudaEventRecord(w.ev[j], w.hi));
+                CK(cudaStreamWaitEvent(c->stream, w.ev[j], 0));
+                // layers L-1-it for it in [it_begin, it_end): jobs of layers
+                // [L - it_end, L - it_begin) (job index 2 (l - lf))
+                dw_launch(2 * (L - ba.it_end - lf), 2 * (L - ba.it_begin - lf));
+                if (int rc = check_launch()) return rc;
+            }
+        } else {
+            {
+                LaunchScope ls(c, DETNET_K_BACKWARD, c->stream);
+                be->fn(dim3(bwd_blocks), dim3(bwd_per), 2 * static_cast<size_t>(m->simt_rec) * 4 + 64,
+                       c->stream, ba);
+            }
+            if (int rc = check_launch()) return rc;
+            dw_launch(0, static_cast<int>(jobs.size()));
+            if (int rc = check_launch()) return rc;
         }
-        if (int rc = check_launch()) return rc;
     }
     SumArgs sa{w.p1.as<double>(), w.p23.as<double>(), w.tbar.as<double>(), bwd_blocks, splits,
                K, Z, V, L, lf, raw};

@@ -2,6 +2,7 @@
 (kernels.cpp:160-200 incl. the regularizer gradient), adam_step (adam.cpp,
 bit-exact for identical inputs) and a 100-step training run whose losses must
 stay within 1e-3 relative of the oracle's (BASELINE north_star)."""
+import os
 import numpy as np
 import pytest
 
@@ -179,3 +180,23 @@ def test_training_100_steps_tracks_oracle(oracle, tc_forward):
           f"loss rel per seed {finals}; median {med:.2e}")
     assert np.median(tracked) >= 5, tracked
     assert med <= med_max, finals
+
+
+@pytest.mark.parametrize("K,N,L,n", [(20, 30, 8, 5000), (4, 8, 5, 700)])
+def test_overlapped_sweep_bit_identical(tmp_path, K, N, L, n):
+    """The reverse sweep in layer chunks on a high-priority stream with the
+    dW contractions of finished chunks overlapped on the context stream
+    (default at small batches) gives the same bits as one sweep followed by
+    one dW launch (DETNET_BWD_CHUNKS=1)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for tag, env in (("chunked", {}), ("single", {"DETNET_BWD_CHUNKS": "1"})):
+        f = str(tmp_path / f"{tag}.npy")
+        r = subprocess.run([sys.executable, os.path.join(root, "tools", "grad_dump.py"), f,
+                            str(K), str(N), str(L), str(n)], env={**os.environ, **env},
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        outs.append(np.load(f))
+    assert np.array_equal(outs[0], outs[1])

@@ -294,7 +294,10 @@ def main():
     peaks = measured_peaks(torch) if rank == 0 else {}
 
     ctx = eng.Context(local, path={"auto": 0, "simt": 1, "tc": 2, "sparse": 3}[args.path])
-    stream = torch.cuda.current_stream()
+    # one explicit stream for the engine, torch's events and collectives (the
+    # legacy default stream's handle is 0, which the C-ABI reads as "own stream")
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     model = ctx.model(K, N, Z, V, params, masks=masks)
 
@@ -313,18 +316,29 @@ def main():
             if want_xhat else None)
     torch.cuda.synchronize()
 
+    # Device-resident steps are enqueued asynchronously (one ticket per SNR
+    # point, <= 32 in flight): the GPU runs the steps back to back with no host
+    # round trip between batches; results are waited for behind the queue.
+    pending = []
+
+    def drain(keep):
+        out = []
+        while len(pending) > keep:
+            out.append(ctx.eval_wait(pending.pop(0)))
+        return out
+
     def step_device():
-        evs = []
         for H, y, x in dev_in:
-            evs.append(model.batch_evaluate_device(per_point, H, y, x, xhat_ptr=xhat))
-        return evs
+            drain(32)
+            pending.append(model.batch_evaluate_device_async(per_point, H, y, x, xhat_ptr=xhat))
 
     for _ in range(args.warmup):
         step_device()
+    drain(0)
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        clk.prime(lambda: (step_device(), torch.cuda.synchronize()))
+        clk.prime(lambda: (step_device(), drain(0), torch.cuda.synchronize()))
         ctx.kernel_times(reset=True)
         ctx.set_profiling(True)
         launches0 = ctx.launch_count
@@ -334,8 +348,9 @@ def main():
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record()
         for _ in range(args.steps):
-            evs = step_device()
+            step_device()
         t1.record()
+        evs = drain(0)[-len(dev_in):]
         torch.cuda.synchronize()
     barrier()
     launches = ctx.launch_count - launches0
@@ -475,7 +490,9 @@ def run_train_bench(args, torch, dist, world, rank, local, barrier, eng):
     ctx = eng.Context(local)
     if args.train_fwd == "tc":
         ctx.set_train_forward(True)
-    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
     model = ctx.model(K, N, Z, V, params)
     raw = torch.zeros(model.param_count, dtype=torch.float64, device="cuda")
     total_steps = args.warmup + args.steps

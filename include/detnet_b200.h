@@ -125,6 +125,18 @@ int detnet_batch_evaluate_device(detnet_model *m, long n, const float *H_dev, co
                                  const int8_t *x_dev, int loss_layers_trainable_only,
                                  float *xhat_dev, detnet_eval *out);
 
+/* Asynchronous form of detnet_batch_evaluate_device: enqueues the whole
+ * evaluation on the context stream and returns a ticket at once; the
+ * BatchEval (and SingularMatrixError) comes from detnet_eval_wait. At most 64
+ * evaluations may be in flight per context (CONTRACT error beyond). Lets a
+ * caller keep the device busy across many batches with no host round trip
+ * between them; results are identical to the synchronous call. */
+int detnet_batch_evaluate_device_async(detnet_model *m, long n, const float *H_dev,
+                                       const float *y_dev, const int8_t *x_dev,
+                                       int loss_layers_trainable_only, float *xhat_dev,
+                                       long long *ticket);
+int detnet_eval_wait(detnet_ctx *ctx, long long ticket, detnet_eval *out);
+
 /* The per-sample preprocessing alone (K1 + its exact-LU fallback; the part of
  * evaluate_one before the layer loop, kernels.cpp:55-58, linalg.cpp:20-79),
  * device buffers in and out, sample-major: gram_dev [n][K(K+1)/2] the upper

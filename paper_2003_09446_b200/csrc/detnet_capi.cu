@@ -515,7 +515,7 @@ int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, 
 
 // finish_eval (kernels.cpp:93-103), device part: fixed-order reduction and
 // the copy of {loss, errors, flagged, singular} to pinned host memory
-int finish_device(detnet_model *m, long n) {
+int finish_device(detnet_model *m, long n, double *dst) {
     detnet_ctx *c = m->ctx;
     const long tiles = (n + TILE - 1) / TILE;
     double *res = c->result.as<double>();
@@ -528,7 +528,26 @@ int finish_device(detnet_model *m, long n) {
     }
     if (int rc = check_launch()) return rc;
     CK(cudaMemcpyAsync(res + 3, c->sing.p, 8, cudaMemcpyDeviceToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->h_result, res, 32, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(dst ? dst : c->h_result, res, 32, cudaMemcpyDeviceToHost, c->stream));
+    return 0;
+}
+
+// decode a finished {loss, errors, flagged, singular} block
+int decode_eval(const double *h, long n, int K, detnet_eval *out) {
+    unsigned long long sing;
+    std::memcpy(&sing, h + 3, 8);
+    if (sing != ~0ull)
+        return fail(DETNET_ERR_SINGULAR,
+                    "solve_normal_equations: matrix is singular to working precision (sample %llu)",
+                    sing);
+    long long e, f;
+    std::memcpy(&e, h + 1, 8);
+    std::memcpy(&f, h + 2, 8);
+    out->loss_sum = h[0];
+    out->data_loss = n ? h[0] / static_cast<double>(n) : 0.0;
+    out->symbol_errors = e;
+    out->symbols = n * static_cast<long long>(K);
+    out->flagged = f;
     return 0;
 }
 
@@ -537,25 +556,11 @@ int finish_host(detnet_model *m, long n, detnet_eval *out) {
     detnet_ctx *c = m->ctx;
     CK(cudaStreamSynchronize(c->stream));
     drain_times(c);
-    unsigned long long sing;
-    std::memcpy(&sing, c->h_result + 3, 8);
-    if (sing != ~0ull)
-        return fail(DETNET_ERR_SINGULAR,
-                    "solve_normal_equations: matrix is singular to working precision (sample %llu)",
-                    sing);
-    long long e, f;
-    std::memcpy(&e, c->h_result + 1, 8);
-    std::memcpy(&f, c->h_result + 2, 8);
-    out->loss_sum = c->h_result[0];
-    out->data_loss = n ? c->h_result[0] / static_cast<double>(n) : 0.0;
-    out->symbol_errors = e;
-    out->symbols = n * static_cast<long long>(m->K);
-    out->flagged = f;
-    return 0;
+    return decode_eval(c->h_result, n, m->K, out);
 }
 
 int finish(detnet_model *m, long n, detnet_eval *out) {
-    if (int rc = finish_device(m, n)) return rc;
+    if (int rc = finish_device(m, n, nullptr)) return rc;
     return finish_host(m, n, out);
 }
 
@@ -645,6 +650,10 @@ void detnet_ctx_destroy(detnet_ctx *c) {
     }
     for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
     if (c->h_result) cudaFreeHost(c->h_result);
+    if (c->h_async) {
+        cudaFreeHost(c->h_async);
+        for (cudaEvent_t e : c->async_ev) cudaEventDestroy(e);
+    }
     if (c->own_stream) cudaStreamDestroy(c->stream);
     cudaStreamDestroy(c->copy_stream);
     delete c;
@@ -782,7 +791,7 @@ int eval_device_body(detnet_model *m, long n, const float *H, const float *y, co
     if (int rc = run_stack(m, c->stream, 0, tiles, n, 0, m->L, trainable_only != 0, xhat, nullptr,
                            nullptr))
         return rc;
-    return finish_device(m, n);
+    return finish_device(m, n, nullptr);
 }
 
 void drop_graph(detnet_model *m) {
@@ -887,6 +896,59 @@ int detnet_batch_evaluate_device(detnet_model *m, long n, const float *H, const 
         for (int k = 0; k < 8; ++k) g.cls_launches[k] = c->times.launches[k] - cl0[k];
         m->graph_seen = 1;
     }
+    return rc;
+}
+
+int detnet_batch_evaluate_device_async(detnet_model *m, long n, const float *H, const float *y,
+                                       const int8_t *x, int trainable_only, float *xhat,
+                                       long long *ticket) {
+    if (!m || !ticket || (n > 0 && (!H || !y || !x)))
+        return fail(DETNET_ERR_CONTRACT, "null argument");
+    detnet_ctx *c = m->ctx;
+    const long long t = c->next_ticket;
+    auto &slot = c->slots[t % detnet_ctx::kSlots];
+    if (slot.ticket >= 0)
+        return fail(DETNET_ERR_CONTRACT, "evaluate_async: %d evaluations in flight (wait first)",
+                    detnet_ctx::kSlots);
+    CK(cudaSetDevice(c->device));
+    if (!c->h_async) {
+        CK(cudaMallocHost(&c->h_async, sizeof(double) * 4 * detnet_ctx::kSlots));
+        for (auto &e : c->async_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    double *dst = c->h_async + 4 * (t % detnet_ctx::kSlots);
+    if (n > 0) {
+        if (int rc = ensure_ws(c, n, m->K)) return rc;
+        if (int rc = reset_sing(c, c->stream)) return rc;
+        if (int rc = run_pre(m, c->stream, 0, n, n, H, y, x)) return rc;
+        const long tiles = (n + TILE - 1) / TILE;
+        if (int rc = run_stack(m, c->stream, 0, tiles, n, 0, m->L, trainable_only != 0, xhat,
+                               nullptr, nullptr))
+            return rc;
+        if (int rc = finish_device(m, n, dst)) return rc;
+    } else {
+        dst[0] = 0.0; // finish_eval of an empty batch (kernels.cpp:93-103)
+        std::memset(dst + 1, 0, 16);
+        std::memset(dst + 3, 0xff, 8);
+    }
+    CK(cudaEventRecord(c->async_ev[t % detnet_ctx::kSlots], c->stream));
+    slot.ticket = t;
+    slot.n = n;
+    slot.K = m->K;
+    ++c->next_ticket;
+    *ticket = t;
+    drain_times(c, false);
+    return 0;
+}
+
+int detnet_eval_wait(detnet_ctx *c, long long ticket, detnet_eval *out) {
+    if (!c || !out) return fail(DETNET_ERR_CONTRACT, "null argument");
+    if (ticket < 0) return fail(DETNET_ERR_CONTRACT, "eval_wait: bad ticket");
+    auto &slot = c->slots[ticket % detnet_ctx::kSlots];
+    if (slot.ticket != ticket) return fail(DETNET_ERR_CONTRACT, "eval_wait: unknown ticket %lld", ticket);
+    CK(cudaEventSynchronize(c->async_ev[ticket % detnet_ctx::kSlots]));
+    drain_times(c, false);
+    const int rc = decode_eval(c->h_async + 4 * (ticket % detnet_ctx::kSlots), slot.n, slot.K, out);
+    slot.ticket = -1;
     return rc;
 }
 

@@ -144,6 +144,17 @@ struct detnet_ctx {
     bool train_tc = false;  // training forward on tcgen05 (dense images) instead of SIMT
     detnet::DBuf redo, redo_count; // split-FP16 range flags per tile + count
     double *h_result = nullptr; // pinned: loss, err, flag, singular
+    // asynchronous evaluations (detnet_batch_evaluate_device_async): a ring of
+    // pinned result slots, each with the event that marks its copy done
+    static constexpr int kSlots = 64;
+    double *h_async = nullptr; // [kSlots][4]
+    cudaEvent_t async_ev[kSlots] = {};
+    struct AsyncSlot {
+        long long ticket = -1;
+        long n = 0;
+        int K = 0;
+    } slots[kSlots];
+    long long next_ticket = 0;
     cudaEvent_t chunk_done[2] = {nullptr, nullptr};
     cudaEvent_t copy_done[2] = {nullptr, nullptr};
 };
@@ -229,8 +240,17 @@ struct LaunchScope {
     }
 };
 
-inline void drain_times(detnet_ctx *c) {
-    for (auto &p : c->pending) {
+// Kernel timers: block = wait for every pending pair; otherwise only the
+// pairs that have completed (asynchronous evaluations keep the rest pending).
+inline void drain_times(detnet_ctx *c, bool block = true) {
+    size_t keep = 0;
+    for (size_t i = 0; i < c->pending.size(); ++i) {
+        auto &p = c->pending[i];
+        if (!block && cudaEventQuery(p.b) != cudaSuccess) {
+            cudaGetLastError(); // cudaErrorNotReady is not an error here
+            c->pending[keep++] = p;
+            continue;
+        }
         float ms = 0.f;
         cudaEventSynchronize(p.b);
         cudaEventElapsedTime(&ms, p.a, p.b);
@@ -238,7 +258,7 @@ inline void drain_times(detnet_ctx *c) {
         c->event_pool.push_back(p.a);
         c->event_pool.push_back(p.b);
     }
-    c->pending.clear();
+    c->pending.resize(keep);
 }
 
 inline int check_launch() {

@@ -115,6 +115,9 @@ _lib.detnet_model_flops_per_detection.restype = C.c_longlong
 _lib.detnet_model_flops_per_detection.argtypes = [_vp, C.c_int]
 _lib.detnet_batch_evaluate.argtypes = [_vp, C.c_long, _vp, _vp, _vp, C.c_int, _vp,
                                        C.POINTER(_Eval)]
+_lib.detnet_batch_evaluate_device_async.argtypes = [_vp, C.c_long, _vp, _vp, _vp, C.c_int, _vp,
+                                                   C.POINTER(C.c_longlong)]
+_lib.detnet_eval_wait.argtypes = [_vp, C.c_longlong, _vp]
 _lib.detnet_preprocess_device.argtypes = [_vp, C.c_long, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
 _lib.detnet_batch_evaluate_device.argtypes = [_vp, C.c_long, _vp, _vp, _vp, C.c_int, _vp,
                                               C.POINTER(_Eval)]
@@ -229,6 +232,12 @@ class Context:
     @property
     def stream(self):
         return _lib.detnet_ctx_stream(self._h)
+
+    def eval_wait(self, ticket):
+        """BatchEval of an evaluation enqueued by Model.batch_evaluate_device_async."""
+        ev = _Eval()
+        _check(_lib.detnet_eval_wait(self._h, ticket, C.byref(ev)))
+        return BatchEval(ev.data_loss, ev.symbol_errors, ev.symbols, ev.flagged, ev.loss_sum)
 
     def set_profiling(self, on=True):
         _check(_lib.detnet_ctx_set_profiling(self._h, int(on)))
@@ -376,6 +385,16 @@ class Model:
                                                  _addr(x_ptr), int(trainable_only),
                                                  _addr(xhat_ptr), C.byref(ev)))
         return BatchEval(ev.data_loss, ev.symbol_errors, ev.symbols, ev.flagged, ev.loss_sum)
+
+    def batch_evaluate_device_async(self, n, H_ptr, y_ptr, x_ptr, trainable_only=False,
+                                    xhat_ptr=None):
+        """Enqueue an evaluation of device-resident samples; returns a ticket
+        for Context.eval_wait (up to 64 in flight)."""
+        t = C.c_longlong()
+        _check(_lib.detnet_batch_evaluate_device_async(self._h, n, _addr(H_ptr), _addr(y_ptr),
+                                                       _addr(x_ptr), int(trainable_only),
+                                                       _addr(xhat_ptr), C.byref(t)))
+        return t.value
 
     def preprocess_device(self, n, H_ptr, y_ptr, x_ptr, gram_ptr=None, q_ptr=None, denom_ptr=None,
                           flag_ptr=None):

@@ -1,0 +1,73 @@
+"""detnet_batch_evaluate_device_async / detnet_eval_wait: evaluations enqueued
+without host round trips give exactly the synchronous results, in any wait
+order; contract errors for too many in flight and unknown tickets; empty
+batches; SingularMatrixError surfaces at wait time."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+K, N = 20, 30
+
+
+def _ev(e):
+    return (e.loss_sum, e.symbol_errors, e.symbols, e.flagged)
+
+
+@pytest.fixture(scope="module")
+def setup():
+    import paper_2003_09446_b200 as eng
+    from paper_2003_09446_b200.workload import xavier_params
+    ctx = eng.Context(0)
+    m = ctx.model(K, N, 160, 40, xavier_params(K, 5, seed=9))
+    batches = []
+    for p in range(6):
+        n = 700 + 333 * p
+        H = torch.empty((n, N, K), dtype=torch.float32, device="cuda")
+        y = torch.empty((n, N), dtype=torch.float32, device="cuda")
+        x = torch.empty((n, K), dtype=torch.int8, device="cuda")
+        base, _ = eng.rng_split(eng.rng_stream(eng.rng_seed(1, 0), 0x45564131 + p))
+        ctx.generate(base, 0, n, N, K, 2.0 * p, 2.0 * p, 1.0 / np.sqrt(N), H, y, x)
+        batches.append((n, H, y, x))
+    return ctx, m, batches
+
+
+def test_async_matches_sync(setup):
+    ctx, m, batches = setup
+    sync = [_ev(m.batch_evaluate_device(n, H, y, x)) for n, H, y, x in batches]
+    tickets = [m.batch_evaluate_device_async(n, H, y, x) for n, H, y, x in batches * 3]
+    order = list(range(len(tickets)))[::-1]  # wait newest first
+    got = {i: _ev(ctx.eval_wait(tickets[i])) for i in order}
+    for i in range(len(tickets)):
+        assert got[i] == sync[i % len(batches)]
+
+
+def test_async_contract(setup):
+    from paper_2003_09446_b200.detnet import ContractError
+    ctx, m, batches = setup
+    n, H, y, x = batches[0]
+    ts = [m.batch_evaluate_device_async(n, H, y, x) for _ in range(64)]
+    with pytest.raises(ContractError):
+        m.batch_evaluate_device_async(n, H, y, x)
+    first = _ev(ctx.eval_wait(ts[0]))
+    with pytest.raises(ContractError):
+        ctx.eval_wait(ts[0])  # already consumed
+    for t in ts[1:]:
+        assert _ev(ctx.eval_wait(t)) == first
+    t = m.batch_evaluate_device_async(0, H, y, x)
+    e = ctx.eval_wait(t)
+    assert e.symbols == 0 and e.loss_sum == 0.0 and e.symbol_errors == 0
+
+
+def test_async_singular(setup, oracle):
+    from paper_2003_09446_b200.detnet import SingularMatrixError
+    ctx, m, _ = setup
+    H = np.zeros((8, N, K), dtype=np.float32)
+    H[:, :K, :] = np.eye(K, dtype=np.float32)
+    H[3] = 0.0  # singular channel
+    y = np.ones((8, N), dtype=np.float32)
+    x = np.ones((8, K), dtype=np.int8)
+    dev = [torch.from_numpy(a).cuda() for a in (H, y, x)]
+    t = m.batch_evaluate_device_async(8, *dev)
+    with pytest.raises(SingularMatrixError):
+        ctx.eval_wait(t)

@@ -639,6 +639,7 @@ void detnet_ctx_destroy(detnet_ctx *c) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     drain_times(c);
+    train_ws_release(c);
     for (DBuf *b : {&c->gp, &c->q32, &c->denom, &c->xmask, &c->flag, &c->tile_loss, &c->tile_err,
                     &c->sing, &c->result, &c->xhat_dev, &c->state_x, &c->state_v, &c->redo,
                     &c->redo_count})

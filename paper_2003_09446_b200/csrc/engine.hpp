@@ -277,6 +277,7 @@ int upload_model(detnet_model *m, const detnet_model_desc *d);
 int reset_sing(detnet_ctx *c, cudaStream_t st);
 // exact: the reference's FP64 LU for every sample (training: each sample's
 // gradient is weighted by 1 / denom, so it gets the reference's denominators)
+void train_ws_release(detnet_ctx *c);
 int run_pre(detnet_model *m, cudaStream_t st, long s0, long cnt, long n_total, const float *H,
             const float *y, const int8_t *x, bool exact = false);
 int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, int l_begin,

@@ -77,9 +77,14 @@ struct TrainWs {
     DBuf in_H, in_y, in_x;
 };
 
-TrainWs &ws_for(detnet_ctx *c) {
-    // one workspace per context (contexts are single-owner)
+// one workspace per context (contexts are single-owner); released with it
+std::vector<std::pair<detnet_ctx *, TrainWs *>> &train_ws_all() {
     static std::vector<std::pair<detnet_ctx *, TrainWs *>> all;
+    return all;
+}
+
+TrainWs &ws_for(detnet_ctx *c) {
+    auto &all = train_ws_all();
     for (auto &p : all)
         if (p.first == c) return *p.second;
     all.push_back({c, new TrainWs()});
@@ -534,3 +539,25 @@ int detnet_model_reset_adam(detnet_model *m) {
 }
 
 } // extern "C"
+
+namespace detnet {
+// called by detnet_ctx_destroy: the training workspace of a context
+void train_ws_release(detnet_ctx *c) {
+    auto &all = train_ws_all();
+    for (size_t i = 0; i < all.size(); ++i) {
+        if (all[i].first != c) continue;
+        TrainWs *w = all[i].second;
+        for (DBuf *b : {&w->tr_in, &w->tr_z, &w->tr_u2, &w->tr_xf, &w->u1bar, &w->g23bar, &w->tbar,
+                        &w->p1, &w->p23, &w->jobs, &w->raw, &w->grads, &w->colnorm, &w->bstate,
+                        &w->in_H, &w->in_y, &w->in_x})
+            b->release();
+        if (w->hi) {
+            cudaStreamDestroy(w->hi);
+            for (cudaEvent_t e : w->ev) cudaEventDestroy(e);
+        }
+        delete w;
+        all.erase(all.begin() + static_cast<long>(i));
+        return;
+    }
+}
+} // namespace detnet

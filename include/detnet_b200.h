@@ -177,11 +177,13 @@ typedef struct {
  * gradient between the two calls (one data-parallel rank per GPU):
  *  detnet_train_grad: samples (device) -> raw_dev [param_count] FP64 sums of
  *    the per-sample data-term gradients (unscaled, unmasked, record layout)
- *    and this rank's BatchEval (loss sum, errors, flagged);
+ *    and this rank's BatchEval (loss sum, errors, flagged); out may be NULL:
+ *    then the call only enqueues (no wait, no SingularMatrixError check);
  *  detnet_train_apply: raw (all-reduced) -> mean over n_global samples, masks,
  *    regularizer gradient, Adam update of the model's device master params
  *    (moments kept in the model; reset with detnet_model_reset_adam, as
- *    training.cpp:55 starts a fresh AdamState per incremental step). */
+ *    training.cpp:55 starts a fresh AdamState per incremental step). Stream-
+ *    ordered on the context stream; it does not wait for the device. */
 long detnet_model_param_count(const detnet_model *m);
 int detnet_train_grad(detnet_model *m, long n, const float *H_dev, const float *y_dev,
                       const int8_t *x_dev, int loss_layers_trainable_only, double *raw_dev,

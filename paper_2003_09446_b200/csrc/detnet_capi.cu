@@ -268,6 +268,7 @@ int pack_sparse(detnet_model *m, const double *params, const double *masks) {
 
 int upload_model(detnet_model *m, const detnet_model_desc *d) {
     ++m->version;
+    if (int rc = quiesce(m->ctx)) return rc; // in-flight work may read the old buffers
     const long P = record_size(m->K, m->Z, m->V);
     m->params_host.assign(d->params, d->params + P * m->L);
     m->has_masks = d->masks != nullptr;

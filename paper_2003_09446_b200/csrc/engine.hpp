@@ -261,6 +261,14 @@ inline void drain_times(detnet_ctx *c, bool block = true) {
     c->pending.resize(keep);
 }
 
+// Host-synchronous entry points that read or overwrite device state with
+// legacy-stream copies first wait for the context stream (evaluations and
+// training steps are only stream-ordered and may still be in flight).
+inline int quiesce(detnet_ctx *c) {
+    const cudaError_t e = cudaStreamSynchronize(c->stream);
+    return e == cudaSuccess ? 0 : fail(DETNET_ERR_CUDA, "stream: %s", cudaGetErrorString(e));
+}
+
 inline int check_launch() {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(DETNET_ERR_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));

@@ -95,6 +95,7 @@ long rec_size(const detnet_model *m) { return record_size(m->K, m->Z, m->V); }
 
 int ensure_train_state(detnet_model *m) {
     if (m->train_ready) return 0;
+    if (int rc = quiesce(m->ctx)) return rc;
     const size_t bytes = sizeof(double) * rec_size(m) * m->L;
     if (m->tparams.ensure(bytes) || m->tmasks.ensure(bytes) || m->tm.ensure(bytes) ||
         m->tv.ensure(bytes))
@@ -239,6 +240,7 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
         k_grad_sum<<<static_cast<unsigned>((total + 255) / 256), 256, 0, c->stream>>>(sa);
     }
     if (int rc = check_launch()) return rc;
+    if (!out) return drain_times(c, false), 0; // no readback requested: no wait
     return finish(m, n, out); // loss / errors / flagged of the forward pass (syncs)
 }
 
@@ -379,7 +381,7 @@ long detnet_model_param_count(const detnet_model *m) {
 
 int detnet_train_grad(detnet_model *m, long n, const float *H, const float *y, const int8_t *x,
                       int trainable_only, double *raw_dev, detnet_eval *out) {
-    if (!m || !raw_dev || !out) return fail(DETNET_ERR_CONTRACT, "null argument");
+    if (!m || !raw_dev) return fail(DETNET_ERR_CONTRACT, "null argument");
     CK(cudaSetDevice(m->ctx->device));
     if (int rc = ensure_train_state(m)) return rc;
     return grad_raw(m, n, H, y, x, trainable_only != 0, raw_dev, out);
@@ -387,8 +389,8 @@ int detnet_train_grad(detnet_model *m, long n, const float *H, const float *y, c
 
 int detnet_train_apply(detnet_model *m, const double *raw_dev, long n_global,
                        const detnet_loss_spec *spec, const detnet_adam_config *cfg) {
-    ++m->version; // packed images / layout may change: drop captured evaluate graphs
     if (!m || !raw_dev || n_global < 1) return fail(DETNET_ERR_CONTRACT, "bad argument");
+    ++m->version; // packed images / layout may change: drop captured evaluate graphs
     if (int rc = validate_adam(cfg)) return rc;
     detnet_ctx *c = m->ctx;
     CK(cudaSetDevice(c->device));
@@ -418,8 +420,10 @@ int detnet_train_apply(detnet_model *m, const double *raw_dev, long n_global,
         m->tc_stale = rc != 0;
     }
     m->sparse_ready = false; // the CSR stream no longer matches the weights
-    CK(cudaStreamSynchronize(c->stream));
-    drain_times(c);
+    // stream-ordered: the next gradient / evaluation on this stream sees the
+    // update; nothing here needs the host to wait
+    if (int rc = check_launch()) return rc;
+    drain_times(c, false);
     return 0;
 }
 
@@ -430,6 +434,7 @@ int detnet_model_get_params(detnet_model *m, double *out) {
         std::memcpy(out, m->params_host.data(), sizeof(double) * total);
         return 0;
     }
+    if (int rc = quiesce(m->ctx)) return rc;
     CK(cudaMemcpy(out, m->tparams.p, sizeof(double) * total, cudaMemcpyDeviceToHost));
     return 0;
 }
@@ -441,8 +446,9 @@ int detnet_model_get_params(detnet_model *m, double *out) {
 // the tcgen05 images (compacted to the live units when few survive) and the
 // sparse stream -- from the result. Adam moments and the step counter survive.
 int detnet_model_prune(detnet_model *m, int kind, double eta, double eta1, double eta2) {
-    ++m->version; // packed images / layout may change: drop captured evaluate graphs
     if (!m) return fail(DETNET_ERR_CONTRACT, "null argument");
+    ++m->version; // packed images / layout may change: drop captured evaluate graphs
+    if (int rc = quiesce(m->ctx)) return rc;
     auto frac = [](double v) { return v >= 0.0 && v < 1.0; };
     if (kind < 0 || kind > 2) return fail(DETNET_ERR_CONTRACT, "prune: kind must be 0, 1 or 2");
     if (!frac(eta) || !frac(eta1) || !frac(eta2))
@@ -477,6 +483,7 @@ int detnet_model_get_masks(detnet_model *m, double *out) {
     if (!m || !out) return fail(DETNET_ERR_CONTRACT, "null argument");
     const long total = record_size(m->K, m->Z, m->V) * m->L;
     if (m->train_ready) {
+        if (int rc = quiesce(m->ctx)) return rc;
         CK(cudaMemcpy(out, m->tmasks.p, sizeof(double) * total, cudaMemcpyDeviceToHost));
     } else if (m->has_masks) {
         std::memcpy(out, m->masks_host.data(), sizeof(double) * total);
@@ -531,6 +538,7 @@ int detnet_model_cost_report(detnet_model *m, detnet_cost_report *r, detnet_laye
 int detnet_model_reset_adam(detnet_model *m) {
     if (!m) return fail(DETNET_ERR_CONTRACT, "null argument");
     if (!m->train_ready) return 0;
+    if (int rc = quiesce(m->ctx)) return rc;
     const size_t bytes = sizeof(double) * record_size(m->K, m->Z, m->V) * m->L;
     CK(cudaMemset(m->tm.p, 0, bytes));
     CK(cudaMemset(m->tv.p, 0, bytes));

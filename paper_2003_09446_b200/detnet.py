@@ -419,11 +419,15 @@ class Model:
     def param_count(self):
         return _lib.detnet_model_param_count(self._h)
 
-    def train_grad(self, n, H_ptr, y_ptr, x_ptr, raw_ptr, trainable_only=False):
-        """Device-resident gradient sums (detnet_train_grad) into raw_ptr (FP64)."""
+    def train_grad(self, n, H_ptr, y_ptr, x_ptr, raw_ptr, trainable_only=False, want_eval=True):
+        """Device-resident gradient sums (detnet_train_grad) into raw_ptr (FP64).
+        want_eval=False: only enqueue (returns None, no host wait)."""
         ev = _Eval()
         _check(_lib.detnet_train_grad(self._h, n, _addr(H_ptr), _addr(y_ptr), _addr(x_ptr),
-                                      int(trainable_only), _addr(raw_ptr), C.byref(ev)))
+                                      int(trainable_only), _addr(raw_ptr),
+                                      C.byref(ev) if want_eval else None))
+        if not want_eval:
+            return None
         return BatchEval(ev.data_loss, ev.symbol_errors, ev.symbols, ev.flagged, ev.loss_sum)
 
     def train_apply(self, raw_ptr, n_global, kind=0, lam=0.0, lam1=0.0, lam2=0.0, lr0=1e-4,

@@ -71,3 +71,38 @@ def test_async_singular(setup, oracle):
     t = m.batch_evaluate_device_async(8, *dev)
     with pytest.raises(SingularMatrixError):
         ctx.eval_wait(t)
+
+
+def test_update_waits_for_inflight(setup):
+    """A model update while evaluations are in flight waits for them: the
+    in-flight ones see the old weights, later ones the new."""
+    import paper_2003_09446_b200 as eng
+    from paper_2003_09446_b200.workload import xavier_params
+    ctx, _, batches = setup
+    pa, pb = xavier_params(K, 5, seed=21), xavier_params(K, 5, seed=22)
+    m = ctx.model(K, N, 160, 40, pa)
+    ref_a, ref_b = ctx.model(K, N, 160, 40, pa), ctx.model(K, N, 160, 40, pb)
+    n, H, y, x = batches[-1]
+    want_a = _ev(ref_a.batch_evaluate_device(n, H, y, x))
+    want_b = _ev(ref_b.batch_evaluate_device(n, H, y, x))
+    t1 = [m.batch_evaluate_device_async(n, H, y, x) for _ in range(4)]
+    m.update(pb)
+    t2 = m.batch_evaluate_device_async(n, H, y, x)
+    assert all(_ev(ctx.eval_wait(t)) == want_a for t in t1)
+    assert _ev(ctx.eval_wait(t2)) == want_b
+
+
+def test_training_steps_without_waits(setup):
+    """train_grad(want_eval=False) + train_apply, stream-ordered with no host
+    waits, leave the same parameters as the waiting sequence."""
+    from paper_2003_09446_b200.workload import xavier_params
+    ctx, _, batches = setup
+    out = []
+    for want in (True, False):
+        m = ctx.model(K, N, 160, 40, xavier_params(K, 5, seed=23))
+        raw = torch.zeros(m.param_count, dtype=torch.float64, device="cuda")
+        for n, H, y, x in batches[:4]:
+            m.train_grad(n, H, y, x, raw, want_eval=want)
+            m.train_apply(raw, n, kind=2, lam1=1e-4, lr0=1e-3)
+        out.append(m.get_params())
+    assert np.array_equal(out[0], out[1])

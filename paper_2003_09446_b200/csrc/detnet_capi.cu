@@ -434,8 +434,20 @@ int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, 
         }
         return check_launch();
     }
-    if (m->ctx->path != 1)
+    // the training forward (trace) on the SIMT path neither needs nor
+    // refreshes the tensor-core images (they are repacked on first use)
+    const bool simt_trace = trace && !(c->train_tc && m->tc.zh == 160);
+    if (m->ctx->path != 1 && !simt_trace) {
+        if (m->tc_dev_dirty) { // after training steps: dense images from the device masters
+            LaunchScope ls(c, DETNET_K_OTHER, st);
+            const int rc = tc_pack_device(m->tc, m->tparams.as<double>(), m->tmasks.as<double>(),
+                                          record_size(m->K, m->Z, m->V), st);
+            if (rc > 1) return rc;
+            m->tc_stale = rc != 0;
+            m->tc_dev_dirty = false;
+        }
         if (int rc = refresh_tc(m)) return rc;
+    }
     // the training forward (trace) runs on tcgen05 only when asked for
     // (detnet_ctx_set_train_forward): 3xTF32 activations are ~4x noisier than
     // FP32 ones, which shortens the FP32-vs-FP64 tracking of long training runs

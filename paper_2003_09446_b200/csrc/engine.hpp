@@ -175,6 +175,7 @@ struct detnet_model {
     int64_t adam_step = 0;
     bool train_ready = false;
     bool tc_stale = false;  // tcgen05 images lag the device master params
+    bool tc_dev_dirty = false; // dense images to repack on the device before next use
     // sparse path (k_stack_sparse.cuh): CSR-like stream of surviving weights
     detnet::DBuf sparse_stream, sparse_off;
     int sparse_max_words = 0; // largest per-layer stream (shared-memory staging)

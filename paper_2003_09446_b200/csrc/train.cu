@@ -410,15 +410,10 @@ int detnet_train_apply(detnet_model *m, const double *raw_dev, long n_global,
     }
     if (int rc = check_launch()) return rc;
     if (int rc = pack_simt_device(m)) return rc;
-    // dense tcgen05 images follow the master weights on the device; other
-    // packings (compacted / sparse) are rebuilt from the host copy on demand
-    {
-        LaunchScope ls(m->ctx, DETNET_K_ADAM, m->ctx->stream);
-        const int rc = tc_pack_device(m->tc, m->tparams.as<double>(), m->tmasks.as<double>(),
-                                      rec_size(m), m->ctx->stream);
-        if (rc > 1) return rc;
-        m->tc_stale = rc != 0;
-    }
+    // dense tcgen05 images follow the master weights on the device, repacked
+    // lazily before their next use (run_stack); other packings (compacted /
+    // sparse) are rebuilt from the host copy on demand
+    m->tc_dev_dirty = true;
     m->sparse_ready = false; // the CSR stream no longer matches the weights
     // stream-ordered: the next gradient / evaluation on this stream sees the
     // update; nothing here needs the host to wait

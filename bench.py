@@ -571,6 +571,31 @@ def run_train_bench(args, torch, dist, world, rank, local, barrier, eng):
             "census_flop_per_sample_step": flops_sample,
             "kernel_ms": {k: v[0] for k, v in kt.items() if v[1]},
             "kernel_launches": {k: v[1] for k, v in kt.items() if v[1]}}
+    # end to end through the public API: every step copies its batch from
+    # pinned host memory (H, y, x) and reads its BatchEval (loss) back
+    e2e = None
+    if not args.no_e2e:
+        import time
+        host = [tuple(t.cpu().pin_memory() for t in batches[b]) for b in range(args.warmup, total_steps)]
+        dev = tuple(torch.empty_like(t) for t in batches[0])
+        torch.cuda.synchronize()
+        barrier()
+        w0 = time.perf_counter()
+        for hb in host:
+            for d, h in zip(dev, hb):
+                d.copy_(h, non_blocking=True)
+            ev_e = model.train_grad(per_gpu, *dev, raw, want_eval=True)
+            allreduce_grad(dist if world > 1 else None, raw)
+            model.train_apply(raw, n_global, kind=2, lam1=1e-4, lr0=1e-3)
+        torch.cuda.synchronize()
+        wall = torch.tensor([time.perf_counter() - w0], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(wall, op=dist.ReduceOp.MAX)
+        e2e = {"value": n_global * args.steps / float(wall.item()), "unit": "samples/s",
+               "h2d_bytes_per_step": int(sum(t.numel() * t.element_size() for t in dev)),
+               "d2h_bytes_per_step": 40,
+               "timer": "host wall clock around the per-step copies and C-ABI calls, max over ranks",
+               "last_step_loss": ev_e.data_loss}
     if rank == 0:
         cpu = None
         if not args.no_cpu and world == 1:
@@ -586,7 +611,7 @@ def run_train_bench(args, torch, dist, world, rank, local, barrier, eng):
                        "parallelism": f"dp{world}",
                        "l2": "fresh batch per step (12.7 MB) + 1 M-parameter model",
                        "train_forward": "tcgen05-3xtf32" if args.train_fwd == "tc" else "simt-fp32"},
-            "roofline": roof, "cpu_baseline": cpu, "gpu_launches": launches,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "last_step_loss": ev.data_loss, "peaks_measured": peaks}),
             flush=True)
 

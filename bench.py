@@ -698,8 +698,32 @@ def run_e2e(args, torch, model, dev_in, per_point, L, want_xhat, barrier, world)
     h2d = sum(H.nbytes + y.nbytes + x.nbytes for H, y, x in host)
     d2h = 32 * len(host) + (xh.nbytes * len(host) if xh is not None else 0)
     dets = per_point * len(host) * world
-    return {"value": dets * args.steps / el, "unit": "detections/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "timer": "host wall clock around synchronous C-ABI calls, max over ranks"}
+    # the PCIe roofline of this path: a plain pinned host->device copy on this
+    # box (349 MB, best of 3) and, when x_l comes back, device->host
+    def link(to_dev):
+        n = 349 * 1000 * 1000 // 4
+        h = torch.empty(n, dtype=torch.float32).pin_memory()
+        d = torch.empty(n, dtype=torch.float32, device="cuda")
+        best = 0.0
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            (d.copy_(h, non_blocking=True) if to_dev else h.copy_(d, non_blocking=True))
+            torch.cuda.synchronize()
+            best = max(best, n * 4 / (time.perf_counter() - t) / 1e9)
+        del h, d
+        return best
+    h2d_gbs = link(True)
+    d2h_gbs = link(False) if d2h > 1e6 else None
+    floor_s = h2d / (h2d_gbs * 1e9) + (d2h / (d2h_gbs * 1e9) if d2h_gbs else 0.0)
+    value = dets * args.steps / el
+    return {"value": value, "unit": "detections/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "timer": "host wall clock around synchronous C-ABI calls, max over ranks",
+            "pcie": {"h2d_gbs_measured": h2d_gbs, "d2h_gbs_measured": d2h_gbs,
+                     "bound_detections_per_s": dets / world / floor_s if floor_s else None,
+                     "frac": value / world / (dets / world / floor_s) if floor_s else None,
+                     "note": "copy-only floor: the step's H2D (+ D2H of x_l) bytes at this box's "
+                             "measured pinned copy rates, no compute"}}
 
 
 def model_eval_host(model, H, y, x, xh):

@@ -577,14 +577,31 @@ def run_train_bench(args, torch, dist, world, rank, local, barrier, eng):
     if not args.no_e2e:
         import time
         host = [tuple(t.cpu().pin_memory() for t in batches[b]) for b in range(args.warmup, total_steps)]
-        dev = tuple(torch.empty_like(t) for t in batches[0])
+        # two device staging sets: step k+1's batch is copied on a side stream
+        # while step k computes (step k-1, the last user of that set, has
+        # returned its BatchEval, so the set is free)
+        dev = [tuple(torch.empty_like(t) for t in batches[0]) for _ in range(2)]
+        cs = torch.cuda.Stream()
+        main = torch.cuda.current_stream()
+
+        def copy_in(k):
+            cs.wait_stream(main)
+            with torch.cuda.stream(cs):
+                for d, h in zip(dev[k % 2], host[k]):
+                    d.copy_(h, non_blocking=True)
+                ev_c = torch.cuda.Event()
+                ev_c.record(cs)
+            return ev_c
+
         torch.cuda.synchronize()
         barrier()
         w0 = time.perf_counter()
-        for hb in host:
-            for d, h in zip(dev, hb):
-                d.copy_(h, non_blocking=True)
-            ev_e = model.train_grad(per_gpu, *dev, raw, want_eval=True)
+        ready = copy_in(0)
+        for k in range(len(host)):
+            main.wait_event(ready)
+            if k + 1 < len(host):
+                ready = copy_in(k + 1)
+            ev_e = model.train_grad(per_gpu, *dev[k % 2], raw, want_eval=True)
             allreduce_grad(dist if world > 1 else None, raw)
             model.train_apply(raw, n_global, kind=2, lam1=1e-4, lr0=1e-3)
         torch.cuda.synchronize()
@@ -592,7 +609,7 @@ def run_train_bench(args, torch, dist, world, rank, local, barrier, eng):
         if world > 1:
             dist.all_reduce(wall, op=dist.ReduceOp.MAX)
         e2e = {"value": n_global * args.steps / float(wall.item()), "unit": "samples/s",
-               "h2d_bytes_per_step": int(sum(t.numel() * t.element_size() for t in dev)),
+               "h2d_bytes_per_step": int(sum(t.numel() * t.element_size() for t in dev[0])),
                "d2h_bytes_per_step": 40,
                "timer": "host wall clock around the per-step copies and C-ABI calls, max over ranks",
                "last_step_loss": ev_e.data_loss}

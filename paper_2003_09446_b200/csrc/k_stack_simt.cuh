@@ -363,7 +363,8 @@ __global__ void __launch_bounds__(SIMTP_THREADS, 1) k_stack_simt_pair(StackArgs 
                                          : v[((j) - 3 * K) < V ? (j) - 3 * K : 0])
         // Same FMA chains per unit as before (u0..u3 over the input columns,
         // acc[o] over the units), issued as FFMA2 pairs: bit-identical.
-#pragma unroll 1
+        // (two units in flight: their chains interleave; still per-unit order)
+#pragma unroll 2
         for (int i = i0; i < i0 + ZH; ++i) {
             const float4 *w4 = reinterpret_cast<const float4 *>(W + i * IN4);
             float u0 = 0.f, u1 = 0.f, u2 = 0.f, u3 = 0.f;

@@ -54,8 +54,24 @@ def workload(cfg):
     raise SystemExit(f"unknown config {cfg}")
 
 
+def _workload():
+    """paper_2003_09446_b200/workload.py loaded by file path: plain numpy, so
+    the reference arm builds the same weights without importing the package
+    (whose __init__ loads the engine library)."""
+    import importlib.util
+    mod = sys.modules.get("detnet_workload")
+    if mod is None:
+        spec = importlib.util.spec_from_file_location(
+            "detnet_workload", os.path.join(ROOT, "paper_2003_09446_b200", "workload.py"))
+        mod = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(mod)
+        sys.modules["detnet_workload"] = mod
+    return mod
+
+
 def build_params(cfg, L):
-    from paper_2003_09446_b200.workload import group_masks, sparse_group_model, xavier_params
+    w = _workload()
+    group_masks, sparse_group_model, xavier_params = w.group_masks, w.sparse_group_model, w.xavier_params
     p = xavier_params(K, L, seed=WEIGHT_SEED)
     if cfg == 3:
         return p, group_masks(K, L, seed=31)
@@ -715,19 +731,21 @@ def run_e2e(args, torch, model, dev_in, per_point, L, want_xhat, barrier, world)
     h2d = sum(H.nbytes + y.nbytes + x.nbytes for H, y, x in host)
     d2h = 32 * len(host) + (xh.nbytes * len(host) if xh is not None else 0)
     dets = per_point * len(host) * world
-    # the PCIe roofline of this path: a plain pinned host->device copy on this
-    # box (349 MB, best of 3) and, when x_l comes back, device->host
+    # the PCIe roofline of this path: 8 back-to-back pinned host->device
+    # copies of 349 MB on this box, each timed with CUDA events, best one
+    # taken (and, when x_l comes back, the same device->host)
     def link(to_dev):
         n = 349 * 1000 * 1000 // 4
         h = torch.empty(n, dtype=torch.float32).pin_memory()
         d = torch.empty(n, dtype=torch.float32, device="cuda")
-        best = 0.0
-        for _ in range(3):
-            torch.cuda.synchronize()
-            t = time.perf_counter()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(9)]
+        torch.cuda.synchronize()
+        evs[0].record()
+        for i in range(8):
             (d.copy_(h, non_blocking=True) if to_dev else h.copy_(d, non_blocking=True))
-            torch.cuda.synchronize()
-            best = max(best, n * 4 / (time.perf_counter() - t) / 1e9)
+            evs[i + 1].record()
+        torch.cuda.synchronize()
+        best = max(n * 4 / (evs[i].elapsed_time(evs[i + 1]) / 1e3) / 1e9 for i in range(8))
         del h, d
         return best
     h2d_gbs = link(True)
@@ -740,7 +758,8 @@ def run_e2e(args, torch, model, dev_in, per_point, L, want_xhat, barrier, world)
                      "bound_detections_per_s": dets / world / floor_s if floor_s else None,
                      "frac": value / world / (dets / world / floor_s) if floor_s else None,
                      "note": "copy-only floor: the step's H2D (+ D2H of x_l) bytes at this box's "
-                             "measured pinned copy rates, no compute"}}
+                             "measured pinned copy rates (best of 8 back-to-back 349 MB copies, "
+                             "CUDA events), no compute"}}
 
 
 def model_eval_host(model, H, y, x, xh):

@@ -292,6 +292,7 @@ int upload_model(detnet_model *m, const detnet_model_desc *d) {
     if (int rc = pack_sparse(m, d->params, d->masks)) return rc;
     m->train_ready = false; // the device master copy restarts from these params
     m->tc_stale = false;
+    m->tc_dev_dirty = false; // the images just packed from the host copy are current
     return 0;
 }
 
@@ -643,6 +644,7 @@ int detnet_ctx_create(int device, detnet_ctx **out) {
         if (d.prep() || (d.prep_fast && d.prep_fast()))
             return fail(DETNET_ERR_CUDA, "cudaFuncSetAttribute (smem) failed");
     if (int rc = tc_prepare()) return rc;
+    if (int rc = train_prepare()) return rc; // per device: the backward kernels' smem opt-in
     *out = c;
     return 0;
 }
@@ -655,7 +657,7 @@ void detnet_ctx_destroy(detnet_ctx *c) {
     train_ws_release(c);
     for (DBuf *b : {&c->gp, &c->q32, &c->denom, &c->xmask, &c->flag, &c->tile_loss, &c->tile_err,
                     &c->sing, &c->result, &c->xhat_dev, &c->state_x, &c->state_v, &c->redo,
-                    &c->redo_count})
+                    &c->redo_count, &c->fb_list, &c->fb_count})
         b->release();
     for (int i = 0; i < 2; ++i) {
         c->in_H[i].release(); c->in_y[i].release(); c->in_x[i].release();
@@ -738,9 +740,13 @@ int detnet_model_create(detnet_ctx *c, const detnet_model_desc *d, detnet_model 
 }
 
 int detnet_model_update(detnet_model *m, const detnet_model_desc *d) {
-    if (!m || !d) return fail(DETNET_ERR_CONTRACT, "null argument");
+    if (!m || !d || !d->params) return fail(DETNET_ERR_CONTRACT, "null argument");
     if (d->n_tx != m->K || d->z_dim != m->Z || d->v_dim != m->V || d->n_rx != m->N)
         return fail(DETNET_ERR_CONTRACT, "model_update: dims changed");
+    if (d->depth < 1 || d->frozen_prefix < 0 || d->frozen_prefix > d->depth)
+        return fail(DETNET_ERR_CONTRACT, "bad depth/frozen_prefix");
+    CK(cudaSetDevice(m->ctx->device));
+    if (int rc = quiesce(m->ctx)) return rc; // in-flight work may read the buffers released below
     if (d->depth != m->L) {
         m->L = d->depth;
         m->simt.release();
@@ -757,10 +763,12 @@ void drop_graph(detnet_model *m);
 
 void detnet_model_destroy(detnet_model *m) {
     if (!m) return;
+    cudaSetDevice(m->ctx->device);
+    cudaStreamSynchronize(m->ctx->stream); // in-flight work may still read the buffers
     drop_graph(m);
-    m->simt.release();
-    m->lnk_all.release();
-    m->lnk_train.release();
+    for (DBuf *b : {&m->simt, &m->lnk_all, &m->lnk_train, &m->tparams, &m->tmasks, &m->tm, &m->tv,
+                    &m->sparse_stream, &m->sparse_off})
+        b->release();
     tc_release(m->tc);
     delete m;
 }

@@ -294,6 +294,7 @@ int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, 
               const TraceBufs *trace = nullptr);
 int finish(detnet_model *m, long n, detnet_eval *out);
 int pack_simt_device(detnet_model *m); // FP32 records from the FP64 master copy
+int train_prepare();                   // per-device kernel attributes (train.cu)
 
 // training (train.cu)
 int train_batch_gradient(detnet_model *m, long n, const float *H, const float *y,

@@ -59,11 +59,6 @@ const BwdEntry kBwd[] = {
 };
 
 const BwdEntry *find_bwd(int K, int Z, int V) {
-    static bool prepped = false;
-    if (!prepped) {
-        for (const BwdEntry &e : kBwd) e.prep();
-        prepped = true;
-    }
     for (const BwdEntry &e : kBwd)
         if (e.K == K && e.Z == Z && e.V == V) return &e;
     return nullptr;
@@ -290,6 +285,14 @@ int validate_adam(const detnet_adam_config *cfg) {
 }
 
 } // namespace
+
+// cudaFuncSetAttribute is per device: run for every context's device
+// (detnet_ctx_create, after cudaSetDevice)
+int train_prepare() {
+    for (const BwdEntry &e : kBwd)
+        if (e.prep()) return fail(DETNET_ERR_CUDA, "cudaFuncSetAttribute (backward smem) failed");
+    return 0;
+}
 
 int pack_simt_device(detnet_model *m) {
     const long R = simt_rec(m->K, m->Z, m->V) * m->L;

@@ -195,6 +195,39 @@ def _addr(a):
 PATH_AUTO, PATH_SIMT, PATH_TC, PATH_SPARSE = 0, 1, 2, 3
 
 
+class _Ordered:
+    """Orders the context stream after torch's current stream on entry and
+    torch's current stream after the context stream on exit, so device
+    buffers the caller produced (or reuses) with torch ops never race the
+    engine (the C-ABI only orders work on its own stream; a context created
+    here launches on its own non-blocking stream). A no-op when torch is not
+    in use or both are the same stream."""
+
+    def __init__(self, ctx):
+        self.ctx = ctx
+        self.pair = None
+
+    def __enter__(self):
+        import sys
+        torch = sys.modules.get("torch")
+        if torch is None or not torch.cuda.is_available() or not torch.cuda.is_initialized():
+            return self
+        dev = torch.device("cuda", self.ctx.device)
+        cur = torch.cuda.current_stream(dev)
+        own = self.ctx.stream
+        if not own or cur.cuda_stream == own:
+            return self
+        ext = torch.cuda.ExternalStream(own, device=dev)
+        ext.wait_stream(cur)
+        self.pair = (ext, cur)
+        return self
+
+    def __exit__(self, *exc):
+        if self.pair:
+            self.pair[1].wait_stream(self.pair[0])
+        return False
+
+
 class Context:
     """One CUDA device (detnet_ctx). Single-owner, like unfold::Rng."""
 
@@ -258,9 +291,10 @@ class Context:
     # -- on-device generator (generate_batch keying, kernels.cpp:116-136) --
     def generate(self, base_state, first, count, n_rx, n_tx, snr_lo, snr_hi, scale, H, y, x,
                  sigma2=None):
-        _check(_lib.detnet_generate_device(self._h, base_state, first, count, n_rx, n_tx, snr_lo,
-                                           snr_hi, scale, _addr(H), _addr(y), _addr(x),
-                                           _addr(sigma2)))
+        with _Ordered(self):
+            _check(_lib.detnet_generate_device(self._h, base_state, first, count, n_rx, n_tx,
+                                               snr_lo, snr_hi, scale, _addr(H), _addr(y),
+                                               _addr(x), _addr(sigma2)))
 
     def generate_host(self, base_state, first, count, n_rx, n_tx, snr_lo, snr_hi):
         """FP64 unscaled samples (what unfold::generate_batch returns)."""
@@ -381,9 +415,10 @@ class Model:
     def batch_evaluate_device(self, n, H_ptr, y_ptr, x_ptr, trainable_only=False, xhat_ptr=None):
         """Device-resident samples (torch tensors or raw device addresses)."""
         ev = _Eval()
-        _check(_lib.detnet_batch_evaluate_device(self._h, n, _addr(H_ptr), _addr(y_ptr),
-                                                 _addr(x_ptr), int(trainable_only),
-                                                 _addr(xhat_ptr), C.byref(ev)))
+        with _Ordered(self.ctx):
+            _check(_lib.detnet_batch_evaluate_device(self._h, n, _addr(H_ptr), _addr(y_ptr),
+                                                     _addr(x_ptr), int(trainable_only),
+                                                     _addr(xhat_ptr), C.byref(ev)))
         return BatchEval(ev.data_loss, ev.symbol_errors, ev.symbols, ev.flagged, ev.loss_sum)
 
     def batch_evaluate_device_async(self, n, H_ptr, y_ptr, x_ptr, trainable_only=False,
@@ -391,18 +426,20 @@ class Model:
         """Enqueue an evaluation of device-resident samples; returns a ticket
         for Context.eval_wait (up to 64 in flight)."""
         t = C.c_longlong()
-        _check(_lib.detnet_batch_evaluate_device_async(self._h, n, _addr(H_ptr), _addr(y_ptr),
-                                                       _addr(x_ptr), int(trainable_only),
-                                                       _addr(xhat_ptr), C.byref(t)))
+        with _Ordered(self.ctx):
+            _check(_lib.detnet_batch_evaluate_device_async(self._h, n, _addr(H_ptr), _addr(y_ptr),
+                                                           _addr(x_ptr), int(trainable_only),
+                                                           _addr(xhat_ptr), C.byref(t)))
         return t.value
 
     def preprocess_device(self, n, H_ptr, y_ptr, x_ptr, gram_ptr=None, q_ptr=None, denom_ptr=None,
                           flag_ptr=None):
         """K1 alone on device-resident samples: sample-major G upper triangle,
         q = H^T y, loss denominator and guard flag (any output may be None)."""
-        _check(_lib.detnet_preprocess_device(self._h, n, _addr(H_ptr), _addr(y_ptr), _addr(x_ptr),
-                                             _addr(gram_ptr), _addr(q_ptr), _addr(denom_ptr),
-                                             _addr(flag_ptr)))
+        with _Ordered(self.ctx):
+            _check(_lib.detnet_preprocess_device(self._h, n, _addr(H_ptr), _addr(y_ptr),
+                                                 _addr(x_ptr), _addr(gram_ptr), _addr(q_ptr),
+                                                 _addr(denom_ptr), _addr(flag_ptr)))
 
     def forward_range(self, H, y, l_begin, l_end, x_state, v_state, want_xhat=True):
         """Layers [l_begin, l_end) from state (x_state [n][K], v_state [n][V])."""
@@ -423,9 +460,10 @@ class Model:
         """Device-resident gradient sums (detnet_train_grad) into raw_ptr (FP64).
         want_eval=False: only enqueue (returns None, no host wait)."""
         ev = _Eval()
-        _check(_lib.detnet_train_grad(self._h, n, _addr(H_ptr), _addr(y_ptr), _addr(x_ptr),
-                                      int(trainable_only), _addr(raw_ptr),
-                                      C.byref(ev) if want_eval else None))
+        with _Ordered(self.ctx):
+            _check(_lib.detnet_train_grad(self._h, n, _addr(H_ptr), _addr(y_ptr), _addr(x_ptr),
+                                          int(trainable_only), _addr(raw_ptr),
+                                          C.byref(ev) if want_eval else None))
         if not want_eval:
             return None
         return BatchEval(ev.data_loss, ev.symbol_errors, ev.symbols, ev.flagged, ev.loss_sum)
@@ -434,8 +472,9 @@ class Model:
                     decay_factor=0.97, decay_step=1000, beta1=0.9, beta2=0.999, eps=1e-8):
         spec = _LossSpec(kind, lam, lam1, lam2)
         cfg = _AdamCfg(lr0, decay_factor, decay_step, beta1, beta2, eps)
-        _check(_lib.detnet_train_apply(self._h, _addr(raw_ptr), n_global, C.byref(spec),
-                                       C.byref(cfg)))
+        with _Ordered(self.ctx):
+            _check(_lib.detnet_train_apply(self._h, _addr(raw_ptr), n_global, C.byref(spec),
+                                           C.byref(cfg)))
 
     def get_params(self):
         out = np.empty((self.depth, record_size(self.n_tx, self.z_dim, self.v_dim)))

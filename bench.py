@@ -524,7 +524,7 @@ def run_train_bench(args, torch, dist, world, rank, local, barrier, eng):
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     model = ctx.model(K, N, Z, V, params)
-    raw = torch.zeros(model.param_count, dtype=torch.float64, device="cuda")
+    raw = model.new_raw()
     total_steps = args.warmup + args.steps
     train = eng.rng_stream(eng.rng_seed(MASTER_SEED, 0), 2)
     batches = []

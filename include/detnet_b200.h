@@ -42,7 +42,8 @@ typedef enum {
     DETNET_ERR_CONFIG = 3,   /* ConfigError: count < 1, N < K (kernels.cpp:118-120) */
     DETNET_ERR_CUDA = 4,     /* CUDA runtime / launch failure, or no device */
     DETNET_ERR_NCCL = 5,     /* collective failure (multi-GPU) */
-    DETNET_ERR_UNSUPPORTED = 6 /* dims outside the compiled kernel set */
+    DETNET_ERR_UNSUPPORTED = 6, /* dims outside the compiled kernel set */
+    DETNET_ERR_DIVERGENCE = 7 /* DivergenceError: non-finite training objective (training.cpp:68-70) */
 } detnet_status;
 
 typedef struct detnet_ctx detnet_ctx;
@@ -62,6 +63,13 @@ int detnet_ctx_set_path(detnet_ctx *ctx, int path);
  * forward is ~4x faster; its 3xTF32 activations are a few times noisier than
  * FP32, so FP32-vs-FP64 loss tracking over long runs is looser. */
 int detnet_ctx_set_train_forward(detnet_ctx *ctx, int tensor_cores);
+/* Training arithmetic: 0 FP32 (default, the fast path), 1 FP64 in the
+ * reference's operation order -- the forward trace, reverse sweep and the
+ * min(16, n)-block gradient accumulation of kernels.cpp:160-200 with separate
+ * IEEE multiplies/adds, so detnet_batch_gradient / detnet_train_grad +
+ * detnet_train_apply are bit-identical to the reference's batch_gradient +
+ * adam_step on FP32-representable samples (one rank). */
+int detnet_ctx_set_train_precision(detnet_ctx *ctx, int fp64);
 
 /* Preprocessing mode: 0 (default) FP32 Cholesky + FP64 refinement with the
  * reference LU as fallback for ill-conditioned samples (FP64-accurate loss
@@ -185,11 +193,24 @@ typedef struct {
  *    training.cpp:55 starts a fresh AdamState per incremental step). Stream-
  *    ordered on the context stream; it does not wait for the device. */
 long detnet_model_param_count(const detnet_model *m);
+/* raw_dev holds detnet_train_raw_count(m) = param_count + 1 doubles: the
+ * gradient sums, then this rank's data-loss sum (sample order in FP64 mode);
+ * ranks all-reduce (sum) the whole buffer. */
+long detnet_train_raw_count(const detnet_model *m);
 int detnet_train_grad(detnet_model *m, long n, const float *H_dev, const float *y_dev,
                       const int8_t *x_dev, int loss_layers_trainable_only, double *raw_dev,
                       detnet_eval *out);
+/* Also forms objective = raw[param_count] / n_global + regularizer(params,
+ * spec) before the update (training.cpp:65-70, loss.cpp:81-91, bit-identical
+ * order); a non-finite objective halts training on the device (no update, the
+ * reference throws before adam_step) and this and every later call returns
+ * DETNET_ERR_DIVERGENCE once the host has seen it (detnet_train_status). */
 int detnet_train_apply(detnet_model *m, const double *raw_dev, long n_global,
                        const detnet_loss_spec *spec, const detnet_adam_config *cfg);
+/* Waits for the context stream; objective and regularizer value of the last
+ * detnet_train_apply (either pointer may be NULL); DETNET_ERR_DIVERGENCE if
+ * training halted on a non-finite objective. */
+int detnet_train_status(detnet_model *m, double *objective, double *regularizer);
 int detnet_model_get_params(detnet_model *m, double *params_out);
 int detnet_model_reset_adam(detnet_model *m);
 

@@ -693,3 +693,198 @@ long long or_flops_per_detection(const or_model *m, int include_preprocess) {
     if (include_preprocess) flops += 2 * n * k + 2 * n * k * k;
     return flops;
 }
+
+/* ---------------------------------------------------------------- O32 ---
+ * FP32 restatement of batch_gradient (kernels.cpp:160-200) for calibrating
+ * FP32's own spread against the FP64 reference over a training run
+ * (SURVEY 7.1 step 0 / H7): the preprocessing (q, G, x_tilde, denominator)
+ * stays FP64 and exact, as the GPU's training preprocessing does; every
+ * per-sample forward (model.cpp:103-120) and reverse-sweep
+ * (backward.cpp:105-165) operation is FP32 in the reference's order; each of
+ * the min(16, n) blocks accumulates its samples' gradients in FP32 (the GPU
+ * accumulates 256-sample splits in FP32); block merge, 1/n scaling and the
+ * regularizer gradient are FP64 (backward_regularizer above). Blocks run in
+ * parallel (OpenMP) with the same fixed merge order, so results do not depend
+ * on the thread count. */
+static void backward_data_f32(int K, int Z, int V, int L, int lf, const float *wm /* [L][P] W(.)M */,
+                              const float *msk /* [L][P] masks or NULL */, const float *tp /* [L] t */,
+                              const float *G, const float *x, double denom,
+                              const float *xhat /* [L+1][K] */, const float *in, const float *z,
+                              const float *u2, float *grads, const rec_off o) {
+    const int IN = 3 * K + V;
+    float a_bar[256], v_bar[1024], u2_bar[256], z_bar[4096], z_bar3[4096], u1_bar[4096];
+    float in_bar[1024], a_prev[256];
+    for (int i = 0; i < K; ++i) a_bar[i] = 0.f;
+    for (int i = 0; i < V; ++i) v_bar[i] = 0.f;
+    for (int l = L - 1; l >= lf; --l) {
+        const float *p = wm + l * o.size;
+        const float *mk = msk ? msk + l * o.size : NULL;
+        float *g = grads + l * o.size;
+        const float t = tp[l];
+        const float w = (float)(2.0 * log((double)(l + 1)) / denom);
+        for (int i = 0; i < K; ++i) a_bar[i] += w * (xhat[(l + 1) * K + i] - x[i]);
+        float t_bar = 0.f;
+        for (int i = 0; i < K; ++i) {
+            const float u = u2[l * K + i];
+            const int lin = u >= -t && u < t;
+            u2_bar[i] = lin ? a_bar[i] * (1.f / t) : 0.f;
+            t_bar += lin ? a_bar[i] * (-u / (t * t)) : 0.f;
+        }
+        g[o.t] += t_bar;
+        for (int i = 0; i < K; ++i) {
+            const float gg = u2_bar[i];
+            if (gg == 0.f) continue;
+            for (int j = 0; j < Z; ++j) g[o.W2 + i * Z + j] += gg * z[l * Z + j] * (mk ? mk[o.W2 + i * Z + j] : 1.f);
+            g[o.b2 + i] += gg * (mk ? mk[o.b2 + i] : 1.f);
+        }
+        for (int j = 0; j < Z; ++j) { z_bar[j] = 0.f; z_bar3[j] = 0.f; }
+        for (int i = 0; i < K; ++i) {
+            if (u2_bar[i] == 0.f) continue;
+            for (int j = 0; j < Z; ++j) z_bar[j] += p[o.W2 + i * Z + j] * u2_bar[i];
+        }
+        for (int i = 0; i < V; ++i) {
+            if (v_bar[i] == 0.f) continue;
+            for (int j = 0; j < Z; ++j) z_bar3[j] += p[o.W3 + i * Z + j] * v_bar[i];
+        }
+        for (int j = 0; j < Z; ++j) z_bar[j] += z_bar3[j];
+        for (int i = 0; i < V; ++i) {
+            const float gg = v_bar[i];
+            if (gg == 0.f) continue;
+            for (int j = 0; j < Z; ++j) g[o.W3 + i * Z + j] += gg * z[l * Z + j] * (mk ? mk[o.W3 + i * Z + j] : 1.f);
+            g[o.b3 + i] += gg * (mk ? mk[o.b3 + i] : 1.f);
+        }
+        for (int i = 0; i < Z; ++i) u1_bar[i] = z[l * Z + i] > 0.f ? z_bar[i] : 0.f;
+        for (int i = 0; i < Z; ++i) {
+            const float gg = u1_bar[i];
+            if (gg == 0.f) continue;
+            for (int j = 0; j < IN; ++j) g[o.W1 + (long)i * IN + j] += gg * in[(long)l * IN + j] * (mk ? mk[o.W1 + (long)i * IN + j] : 1.f);
+            g[o.b1 + i] += gg * (mk ? mk[o.b1 + i] : 1.f);
+        }
+        for (int j = 0; j < IN; ++j) in_bar[j] = 0.f;
+        for (int i = 0; i < Z; ++i) {
+            const float ui = u1_bar[i];
+            if (ui == 0.f) continue;
+            for (int j = 0; j < IN; ++j) in_bar[j] += p[o.W1 + (long)i * IN + j] * ui;
+        }
+        for (int i = 0; i < K; ++i) {
+            float acc = 0.f;
+            for (int j = 0; j < K; ++j) acc += G[i * K + j] * in_bar[2 * K + j];
+            a_prev[i] = acc + in_bar[K + i];
+        }
+        memcpy(a_bar, a_prev, sizeof(float) * K);
+        for (int i = 0; i < V; ++i) v_bar[i] = in_bar[3 * K + i];
+    }
+}
+
+int or_batch_gradient_f32(const or_model *m, long n, const double *H, const double *y,
+                          const double *x, const or_loss_spec *spec, int trainable_only,
+                          double *grads, double *data_loss, long long *errors, long long *symbols,
+                          long long *flagged) {
+    const int K = m->n_tx, N = m->n_rx, Z = m->z_dim, V = m->v_dim, IN = 3 * K + V, L = m->depth;
+    const rec_off o = offsets(K, Z, V);
+    const long P = o.size;
+    if (n < 1) return 1;
+    const int first = trainable_only ? m->frozen_prefix + 1 : 1;
+    const int lf = m->frozen_prefix;
+    memset(grads, 0, sizeof(double) * (size_t)L * P);
+    const int blocks = n < 16 ? (int)n : 16;
+    float *wm = (float *)malloc(sizeof(float) * (size_t)L * P);
+    float *msk = m->masks ? (float *)malloc(sizeof(float) * (size_t)L * P) : NULL;
+    float *tp = (float *)malloc(sizeof(float) * L);
+    for (long i = 0; i < (long)L * P; ++i) {
+        wm[i] = (float)(m->params[i] * (m->masks ? m->masks[i] : 1.0));
+        if (msk) msk[i] = (float)m->masks[i];
+    }
+    for (int l = 0; l < L; ++l) tp[l] = (float)m->params[l * P + o.t];
+    float *part = (float *)calloc((size_t)blocks * L * P, sizeof(float));
+    double *loss = (double *)malloc(sizeof(double) * n);
+    long long *err = (long long *)malloc(sizeof(long long) * n);
+    int *flag = (int *)malloc(sizeof(int) * n);
+    int status = 0;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int b = 0; b < blocks; ++b) {
+        float *xhat = (float *)malloc(sizeof(float) * (size_t)(L + 1) * K);
+        float *in = (float *)malloc(sizeof(float) * (size_t)L * IN);
+        float *z = (float *)malloc(sizeof(float) * (size_t)L * Z);
+        float *u2 = (float *)malloc(sizeof(float) * (size_t)L * K);
+        double q[256], G[4096], xt[256];
+        float Gf[4096], qf[256], xf[256], v[1024], vn[1024];
+        double *tr = (double *)malloc(sizeof(double) * (size_t)L * K);
+        const long lo = (long)((long long)n * b / blocks);
+        const long hi = (long)((long long)n * (b + 1) / blocks);
+        for (long s = lo; s < hi; ++s) {
+            const double *Hs = H + s * (long)N * K, *ys = y + s * (long)N, *xs = x + s * (long)K;
+            if (or_preprocess(N, K, Hs, ys, q, G, xt)) {
+#pragma omp atomic write
+                status = 2;
+                break;
+            }
+            for (int i = 0; i < K; ++i) { qf[i] = (float)q[i]; xf[i] = (float)xs[i]; }
+            for (int i = 0; i < K * K; ++i) Gf[i] = (float)G[i];
+            for (int i = 0; i < K; ++i) xhat[i] = 0.f;
+            for (int i = 0; i < V; ++i) v[i] = 0.f;
+            for (int l = 0; l < L; ++l) {
+                const float *p = wm + l * P;
+                float *inl = in + (long)l * IN;
+                for (int i = 0; i < K; ++i) inl[i] = qf[i];
+                for (int i = 0; i < K; ++i) inl[K + i] = xhat[l * K + i];
+                for (int i = 0; i < K; ++i) {
+                    float acc = 0.f;
+                    for (int j = 0; j < K; ++j) acc += Gf[i * K + j] * xhat[l * K + j];
+                    inl[2 * K + i] = acc;
+                }
+                for (int i = 0; i < V; ++i) inl[3 * K + i] = v[i];
+                float *zl = z + (long)l * Z;
+                for (int i = 0; i < Z; ++i) {
+                    float acc = p[o.b1 + i];
+                    for (int j = 0; j < IN; ++j) acc += p[o.W1 + (long)i * IN + j] * inl[j];
+                    zl[i] = acc > 0.f ? acc : 0.f;
+                }
+                const float t = tp[l];
+                for (int i = 0; i < K; ++i) {
+                    float acc = p[o.b2 + i];
+                    for (int j = 0; j < Z; ++j) acc += p[o.W2 + (long)i * Z + j] * zl[j];
+                    u2[l * K + i] = acc;
+                    xhat[(l + 1) * K + i] = acc <= -t ? -1.f : (acc >= t ? 1.f : acc / t);
+                }
+                for (int i = 0; i < V; ++i) {
+                    float acc = p[o.b3 + i];
+                    for (int j = 0; j < Z; ++j) acc += p[o.W3 + (long)i * Z + j] * zl[j];
+                    vn[i] = acc;
+                }
+                memcpy(v, vn, sizeof(float) * V);
+            }
+            for (int i = 0; i < L * K; ++i) tr[i] = xhat[K + i];
+            int fl = 0;
+            loss[s] = loss_plain(K, L, tr, xs, xt, first, &fl);
+            flag[s] = fl;
+            long long e = 0;
+            for (int i = 0; i < K; ++i) e += (xhat[L * K + i] >= 0.f ? 1.0 : -1.0) != xs[i];
+            err[s] = e;
+            double denom = 0.0;
+            for (int i = 0; i < K; ++i) { const double d = xs[i] - xt[i]; denom += d * d; }
+            if (denom < 1e-12) denom = 1e-12;
+            backward_data_f32(K, Z, V, L, lf, wm, msk, tp, Gf, xf, denom, xhat, in, z, u2,
+                              part + (size_t)b * L * P, o);
+        }
+        free(xhat); free(in); free(z); free(u2); free(tr);
+    }
+    if (!status) {
+        for (int b = 0; b < blocks; ++b)
+            for (int l = lf; l < L; ++l)
+                for (long i = 0; i < P; ++i) grads[l * P + i] += (double)part[((size_t)b * L + l) * P + i];
+        const double sc = 1.0 / (double)n;
+        for (int l = lf; l < L; ++l)
+            for (long i = 0; i < P; ++i) grads[l * P + i] *= sc;
+        backward_regularizer(m, spec, grads);
+        double dl = 0.0;
+        long long e = 0, f = 0;
+        for (long s = 0; s < n; ++s) { dl += loss[s]; e += err[s]; f += flag[s]; }
+        *data_loss = dl / (double)n;
+        *errors = e;
+        *symbols = (long long)n * K;
+        *flagged = f;
+    }
+    free(wm); free(msk); free(tp); free(part); free(loss); free(err); free(flag);
+    return status;
+}

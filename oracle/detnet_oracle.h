@@ -105,6 +105,16 @@ int or_batch_gradient(const or_model *m, long n, const double *H, const double *
                       int loss_layers_trainable_only, double *grads, double *data_loss,
                       long long *errors, long long *symbols, long long *flagged);
 
+/* FP32 restatement of batch_gradient (O32): per-sample forward and reverse
+ * sweep in FP32 in the reference's order, FP32 per-block accumulation, FP64
+ * preprocessing, merge, scaling and regularizer. Calibrates FP32's intrinsic
+ * spread against the FP64 reference over a training run. OpenMP over the
+ * fixed blocks (results independent of the thread count). */
+int or_batch_gradient_f32(const or_model *m, long n, const double *H, const double *y,
+                          const double *x, const or_loss_spec *spec,
+                          int loss_layers_trainable_only, double *grads, double *data_loss,
+                          long long *errors, long long *symbols, long long *flagged);
+
 /* regularizer value (loss.cpp:81-91) */
 double or_regularizer(const or_model *m, const or_loss_spec *spec);
 

@@ -132,6 +132,7 @@ class Oracle:
                                       _lp, _dp]
         L.or_batch_gradient.argtypes = [C.POINTER(_Model), C.c_long, _dp, _dp, _dp,
                                         C.POINTER(_LossSpec), C.c_int, _dp, _dp, _lp, _lp, _lp]
+        L.or_batch_gradient_f32.argtypes = L.or_batch_gradient.argtypes
         L.or_regularizer.restype = C.c_double
         L.or_regularizer.argtypes = [C.POINTER(_Model), C.POINTER(_LossSpec)]
         L.or_adam_step.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp,
@@ -224,6 +225,20 @@ class Oracle:
         st = self.lib.or_batch_gradient(C.byref(cm), H.shape[0], _ptr(H), _ptr(y), _ptr(x),
                                         C.byref(sp), int(trainable_only), _ptr(g), C.byref(dl),
                                         C.byref(e), C.byref(s), C.byref(f))
+        return dict(status=st, grads=g, data_loss=dl.value, symbol_errors=e.value,
+                    symbols=s.value, flagged=f.value)
+
+    def batch_gradient_f32(self, m: Model, H, y, x, kind=0, lam=0.0, lam1=0.0, lam2=0.0,
+                           trainable_only=False):
+        """O32: the FP32 restatement of batch_gradient (FP32's own spread)."""
+        cm = m.c()
+        sp = _spec(kind, lam, lam1, lam2)
+        g = np.zeros_like(m.params)
+        dl = C.c_double(); e = C.c_longlong(); s = C.c_longlong(); f = C.c_longlong()
+        H, y, x = (np.ascontiguousarray(a, np.float64) for a in (H, y, x))
+        st = self.lib.or_batch_gradient_f32(C.byref(cm), H.shape[0], _ptr(H), _ptr(y), _ptr(x),
+                                            C.byref(sp), int(trainable_only), _ptr(g), C.byref(dl),
+                                            C.byref(e), C.byref(s), C.byref(f))
         return dict(status=st, grads=g, data_loss=dl.value, symbol_errors=e.value,
                     symbols=s.value, flagged=f.value)
 

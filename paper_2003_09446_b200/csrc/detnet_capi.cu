@@ -36,7 +36,7 @@ namespace detnet {
 // ---- dims dispatch --------------------------------------------------------
 using PreFn = void (*)(dim3, dim3, size_t, cudaStream_t, long, int, const float *, const float *,
                        const int8_t *, float *, float *, double *, uint32_t *, uint8_t *,
-                       unsigned long long *, const long *, const int *);
+                       unsigned long long *, const long *, const int *, double *, double *);
 using SimtFn = void (*)(dim3, dim3, size_t, cudaStream_t, const StackArgs &);
 constexpr int SIMT_LARGE = 256; // samples per CTA of k_stack_simt (large batches)
 template <int K, int Z, int V> constexpr size_t simt_pair_smem() {
@@ -46,8 +46,9 @@ template <int K, int Z, int V> constexpr size_t simt_pair_smem() {
 template <int K>
 void launch_pre(dim3 g, dim3 b, size_t sm, cudaStream_t st, long n, int N, const float *H,
                 const float *y, const int8_t *x, float *gp, float *q32, double *dn, uint32_t *xm,
-                uint8_t *fl, unsigned long long *sing, const long *list, const int *cnt) {
-    k_preprocess<K><<<g, b, sm, st>>>(n, N, H, y, x, gp, q32, dn, xm, fl, sing, list, cnt);
+                uint8_t *fl, unsigned long long *sing, const long *list, const int *cnt,
+                double *g64, double *q64) {
+    k_preprocess<K><<<g, b, sm, st>>>(n, N, H, y, x, gp, q32, dn, xm, fl, sing, list, cnt, g64, q64);
 }
 
 using FastFn = void (*)(dim3, dim3, size_t, cudaStream_t, long, int, const float *, const float *,
@@ -344,7 +345,7 @@ bool use_h16(const detnet_model *m, bool trace) {
 
 // K1 (+pad) over samples [s0, s0+cnt) of the global arrays.
 int run_pre(detnet_model *m, cudaStream_t st, long s0, long cnt, long n_total, const float *H,
-            const float *y, const int8_t *x, bool exact) {
+            const float *y, const int8_t *x, bool exact, double *g64, double *q64) {
     detnet_ctx *c = m->ctx;
     const int K = m->K, NG = gram_entries(K);
     const long t0 = s0 / TILE;
@@ -353,7 +354,7 @@ int run_pre(detnet_model *m, cudaStream_t st, long s0, long cnt, long n_total, c
     const bool aligned = (reinterpret_cast<uintptr_t>(H) % 16 == 0) &&
                          (reinterpret_cast<uintptr_t>(y) % 16 == 0) &&
                          (reinterpret_cast<uintptr_t>(x) % 4 == 0);
-    if (m->dims->fast && !c->exact_pre && !exact && aligned && N == PREP_FAST_N) {
+    if (m->dims->fast && !c->exact_pre && !exact && !g64 && aligned && N == PREP_FAST_N) {
         // fast path + exact LU for the samples it flags (device-side list)
         if (c->fb_list.ensure(sizeof(long) * cnt) || c->fb_count.ensure(sizeof(int)))
             return fail(DETNET_ERR_CUDA, "fallback list allocation failed");
@@ -377,7 +378,7 @@ int run_pre(detnet_model *m, cudaStream_t st, long s0, long cnt, long n_total, c
                      c->gp.as<float>() + t0 * NG * TILE, c->q32.as<float>() + t0 * K * TILE,
                      c->denom.as<double>() + s0, c->xmask.as<uint32_t>() + s0,
                      c->flag.as<uint8_t>() + s0, c->sing.as<unsigned long long>(),
-                     c->fb_list.as<long>(), c->fb_count.as<int>());
+                     c->fb_list.as<long>(), c->fb_count.as<int>(), nullptr, nullptr);
     } else {
         const int blocks = static_cast<int>(std::min<long>((cnt + 3) / 4, 148L * 32));
         LaunchScope ls(c, DETNET_K_PREPROCESS, st);
@@ -385,7 +386,7 @@ int run_pre(detnet_model *m, cudaStream_t st, long s0, long cnt, long n_total, c
                      c->gp.as<float>() + t0 * NG * TILE, c->q32.as<float>() + t0 * K * TILE,
                      c->denom.as<double>() + s0, c->xmask.as<uint32_t>() + s0,
                      c->flag.as<uint8_t>() + s0, c->sing.as<unsigned long long>(), nullptr,
-                     nullptr);
+                     nullptr, g64 ? g64 + s0 * K * K : nullptr, q64 ? q64 + s0 * K : nullptr);
     }
     if (int rc = check_launch()) return rc;
     const long end = s0 + cnt;
@@ -767,7 +768,7 @@ void detnet_model_destroy(detnet_model *m) {
     cudaStreamSynchronize(m->ctx->stream); // in-flight work may still read the buffers
     drop_graph(m);
     for (DBuf *b : {&m->simt, &m->lnk_all, &m->lnk_train, &m->tparams, &m->tmasks, &m->tm, &m->tv,
-                    &m->sparse_stream, &m->sparse_off})
+                    &m->sparse_stream, &m->sparse_off, &m->tstatus})
         b->release();
     tc_release(m->tc);
     delete m;

@@ -142,6 +142,7 @@ struct detnet_ctx {
     detnet::DBuf in_H[2], in_y[2], in_x[2], xhat_dev, state_x, state_v, fb_list, fb_count;
     bool exact_pre = false; // bit-exact reference LU for every sample
     bool train_tc = false;  // training forward on tcgen05 (dense images) instead of SIMT
+    bool train_fp64 = false; // FP64 training step in the reference's order (k_train64.cuh)
     detnet::DBuf redo, redo_count; // split-FP16 range flags per tile + count
     double *h_result = nullptr; // pinned: loss, err, flag, singular
     // asynchronous evaluations (detnet_batch_evaluate_device_async): a ring of
@@ -173,6 +174,10 @@ struct detnet_model {
     // training state (train.cu): FP64 master params, masks, Adam moments
     detnet::DBuf tparams, tmasks, tm, tv;
     int64_t adam_step = 0;
+    // [objective, regularizer, diverged step (int64, -1 = none)] of the last
+    // detnet_train_apply (device); the host copy of the sticky flag
+    detnet::DBuf tstatus;
+    long long diverged_step = -1;
     bool train_ready = false;
     bool tc_stale = false;  // tcgen05 images lag the device master params
     bool tc_dev_dirty = false; // dense images to repack on the device before next use
@@ -288,11 +293,13 @@ int reset_sing(detnet_ctx *c, cudaStream_t st);
 // gradient is weighted by 1 / denom, so it gets the reference's denominators)
 void train_ws_release(detnet_ctx *c);
 int run_pre(detnet_model *m, cudaStream_t st, long s0, long cnt, long n_total, const float *H,
-            const float *y, const int8_t *x, bool exact = false);
+            const float *y, const int8_t *x, bool exact = false, double *g64 = nullptr,
+            double *q64 = nullptr);
 int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, int l_begin,
               int l_end, bool trainable_only, float *xhat, float *xs, float *vs,
               const TraceBufs *trace = nullptr);
 int finish(detnet_model *m, long n, detnet_eval *out);
+int finish_host(detnet_model *m, long n, detnet_eval *out);
 int pack_simt_device(detnet_model *m); // FP32 records from the FP64 master copy
 int train_prepare();                   // per-device kernel attributes (train.cu)
 

@@ -15,6 +15,9 @@
 //
 // LU: warp_solve_normal below (one row per lane, parallel elimination).
 //
+// Optional FP64 outputs (the FP64 training mode, k_train64.cuh): g64 [s][K*K]
+// and q64 [s][K], the reference's own G and q.
+//
 // Outputs (tile SoA, TILE samples per tile):
 //   gp  [tile][K(K+1)/2][TILE]  packed upper triangle of G (row-major a<=b)
 //   q32 [tile][K][TILE]
@@ -94,7 +97,8 @@ __global__ void __launch_bounds__(256)
                  const int8_t *__restrict__ x, float *__restrict__ gp, float *__restrict__ q32,
                  double *__restrict__ denom, uint32_t *__restrict__ xmask,
                  uint8_t *__restrict__ flag, unsigned long long *__restrict__ singular,
-                 const long *__restrict__ list, const int *__restrict__ list_count) {
+                 const long *__restrict__ list, const int *__restrict__ list_count,
+                 double *__restrict__ g64 = nullptr, double *__restrict__ q64 = nullptr) {
     static_assert(K <= 32, "one lane per row");
     constexpr int NG = gram_entries(K);
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -124,6 +128,7 @@ __global__ void __launch_bounds__(256)
             for (int i = 0; i < N; ++i) qj = fma(sH[i * K + lane], sy[i], qj);
             sq[lane] = qj;
             q32[(tile * K + lane) * TILE + col] = __double2float_rn(qj);
+            if (q64) q64[s * K + lane] = qj;
         }
         for (int e = lane; e < NG; e += 32) {
             int a = 0, rem = e;
@@ -136,6 +141,8 @@ __global__ void __launch_bounds__(256)
             gp[(tile * NG + e) * TILE + col] = __double2float_rn(acc);
         }
         __syncwarp();
+        if (g64) // FP64 training mode: the full Gram matrix, sample-major
+            for (int e = lane; e < K * K; e += 32) g64[s * K * K + e] = sG[e];
 
         double xs[K];
         const bool sing = warp_solve_normal<K>(sG, sq, lane, xs);

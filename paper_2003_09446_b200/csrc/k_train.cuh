@@ -658,11 +658,14 @@ __global__ void k_grad_apply_reg(RegArgs a) {
 
 // adam.cpp:30-79 per entry, FP64 without contraction (bit-identical to the
 // reference for identical inputs). Masked entries (mask 0) untouched.
+// halt (nullable): the sticky divergence slot of k_objective -- a diverged
+// run keeps its parameters (the reference throws before adam_step).
 __global__ void k_adam(double *params, const double *masks, const double *grads, double *m,
                        double *v, long count, int P, int lf, double lr, double b1, double b2,
-                       double eps, double bc1, double bc2) {
+                       double eps, double bc1, double bc2, const long long *halt = nullptr) {
     const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= count) return;
+    if (halt && *halt >= 0) return;
     const int l = static_cast<int>(idx / P), e = static_cast<int>(idx % P);
     if (l < lf) return;
     const bool is_t = e == P - 1;
@@ -677,6 +680,97 @@ __global__ void k_adam(double *params, const double *masks, const double *grads,
     double w = dsub(params[idx], ddiv(dmul(lr, mhat), dadd(__dsqrt_rn(vhat), eps)));
     if (is_t && w < 1e-3) w = 1e-3;
     params[idx] = w;
+}
+
+// ---- objective = data_loss + regularizer(params, spec) (training.cpp:67-70) --
+// Per (layer, matrix) one warp: group_norm_sum (loss.cpp:43-59) with the
+// column norms of [W (.) M] summed over rows in order (lanes over columns) and
+// the column square roots summed in column order by lane 0, plus, when the
+// spec needs it, masked_l1 (loss.cpp:35-41) as lane 0's sequential sum -- the
+// reference's operation order, so the value is bit-identical to
+// regularizer() (loss.cpp:81-91). Frozen layers count (params.layers).
+struct ObjArgs {
+    const double *params, *masks;
+    int K, Z, V, L;
+    int kind;
+    double lam, lam1, lam2;
+    double *part;           // [L][3][2]: group_norm_sum, masked_l1
+};
+
+__global__ void __launch_bounds__(32) k_reg_parts(ObjArgs a) {
+    const int K = a.K, Z = a.Z, V = a.V, IN = 3 * K + V;
+    const long P = static_cast<long>(Z) * IN + Z + static_cast<long>(K) * Z + K +
+                   static_cast<long>(V) * Z + V + 1;
+    const int l = blockIdx.x / 3, mat = blockIdx.x % 3, lane = threadIdx.x;
+    const long oW1 = 0, ob1 = static_cast<long>(Z) * IN, oW2 = ob1 + Z,
+               ob2 = oW2 + static_cast<long>(K) * Z, oW3 = ob2 + K,
+               ob3 = oW3 + static_cast<long>(V) * Z;
+    int rows, cols;
+    long oW, ob;
+    if (mat == 0) { rows = Z; cols = IN; oW = oW1; ob = ob1; }
+    else if (mat == 1) { rows = K; cols = Z; oW = oW2; ob = ob2; }
+    else { rows = V; cols = Z; oW = oW3; ob = ob3; }
+    const double *p = a.params + static_cast<long>(l) * P;
+    const double *mk = a.masks ? a.masks + static_cast<long>(l) * P : nullptr;
+    auto wm = [&](long e) { return dmul(p[e], mk ? mk[e] : 1.0); };
+    __shared__ double roots[1024];
+    double gsum = 0.0, l1 = 0.0;
+    if (a.kind == 2) {
+        for (int j = lane; j < cols; j += 32) {
+            double sq = 0.0;
+            for (int i = 0; i < rows; ++i) {
+                const double w = wm(oW + static_cast<long>(i) * cols + j);
+                sq = dadd(sq, dmul(w, w));
+            }
+            if (j < 1024) roots[j] = sqrt(sq);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            for (int j = 0; j < cols; ++j) gsum = dadd(gsum, roots[j]);
+            double sq = 0.0;
+            for (int i = 0; i < rows; ++i) {
+                const double w = wm(ob + i);
+                sq = dadd(sq, dmul(w, w));
+            }
+            gsum = dadd(gsum, sqrt(sq));
+        }
+    }
+    if (lane == 0 && (a.kind == 1 || (a.kind == 2 && a.lam2 != 0.0))) {
+        const long cnt = static_cast<long>(rows) * cols;
+        for (long e = 0; e < cnt; ++e)
+            l1 = dadd(l1, dmul(fabs(p[oW + e]), mk ? mk[oW + e] : 1.0));
+    }
+    if (lane == 0) {
+        a.part[(static_cast<long>(l) * 3 + mat) * 2 + 0] = gsum;
+        a.part[(static_cast<long>(l) * 3 + mat) * 2 + 1] = l1;
+    }
+}
+
+// status: [0] objective, [1] regularizer, [2] diverged step (-1 = none; sticky)
+__global__ void k_objective(ObjArgs a, const double *loss_sum, double n_global, long long step,
+                            double *status) {
+    double reg = 0.0;
+    if (a.kind == 1) {
+        double acc = 0.0;
+        for (int l = 0; l < a.L; ++l) {
+            const double *q = a.part + static_cast<long>(l) * 6;
+            acc = dadd(acc, dadd(dadd(q[1], q[3]), q[5]));
+        }
+        reg = dmul(a.lam, acc);
+    } else if (a.kind == 2) {
+        double groups = 0.0, elems = 0.0;
+        for (int l = 0; l < a.L; ++l) {
+            const double *q = a.part + static_cast<long>(l) * 6;
+            groups = dadd(groups, dadd(dadd(q[0], q[2]), q[4]));
+            elems = dadd(elems, dadd(dadd(q[1], q[3]), q[5]));
+        }
+        reg = dadd(dmul(a.lam1, groups), dmul(a.lam2, elems));
+    }
+    const double obj = dadd(ddiv(*loss_sum, n_global), reg);
+    status[0] = obj;
+    status[1] = reg;
+    long long *halt = reinterpret_cast<long long *>(status + 2);
+    if (*halt < 0 && !isfinite(obj)) *halt = step;
 }
 
 // FP64 records -> SIMT FP32 records (same mapping as the host packer).

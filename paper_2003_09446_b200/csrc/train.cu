@@ -13,6 +13,7 @@
 
 #include "engine.hpp"
 #include "k_train.cuh"
+#include "k_train64.cuh"
 #include "k_prune.cuh"
 
 namespace detnet {
@@ -67,6 +68,9 @@ const BwdEntry *find_bwd(int K, int Z, int V) {
 struct TrainWs {
     DBuf tr_in, tr_z, tr_u2, tr_xf, u1bar, g23bar, tbar, p1, p23, jobs, raw, grads, colnorm;
     DBuf bstate; // reverse-sweep state between chunks [K+V][ts]
+    // FP64 reference-order mode (k_train64.cuh)
+    DBuf g64, q64, wb, wf, f_in, f_z, f_u2, f_xh, b_u1, b_u2, b_v, b_t, part, s_loss, s_err;
+    DBuf objpart;
     cudaStream_t hi = nullptr; // high-priority stream for the sweep chunks
     cudaEvent_t ev[9] = {};
     DBuf in_H, in_y, in_x;
@@ -104,9 +108,109 @@ int ensure_train_state(detnet_model *m) {
     }
     CK(cudaMemset(m->tm.p, 0, bytes));
     CK(cudaMemset(m->tv.p, 0, bytes));
+    if (m->tstatus.ensure(4 * sizeof(double))) return fail(DETNET_ERR_CUDA, "status allocation failed");
+    const double st0[4] = {0.0, 0.0, 0.0, 0.0};
+    CK(cudaMemcpy(m->tstatus.p, st0, sizeof st0, cudaMemcpyHostToDevice));
+    CK(cudaMemset(static_cast<double *>(m->tstatus.p) + 2, 0xff, 8)); // halt step = -1
+    m->diverged_step = -1;
     m->adam_step = 0;
     m->train_ready = true;
     return 0;
+}
+
+// FP64 training step in the reference's operation order (k_train64.cuh):
+// raw = the merged 16-block gradient sums of batch_gradient before its 1/n
+// scaling, raw[total] = the sample-order loss sum; bit-identical to the
+// reference on FP32-representable samples.
+int grad_raw64(detnet_model *m, long n, const float *H, const float *y, const int8_t *x,
+               bool trainable_only, double *raw, detnet_eval *out) {
+    detnet_ctx *c = m->ctx;
+    if (n < 1) return fail(DETNET_ERR_CONTRACT, "batch_gradient: empty batch");
+    if (m->K > 32) return fail(DETNET_ERR_UNSUPPORTED, "FP64 training mode: n_tx <= 32");
+    const int K = m->K, Z = m->Z, V = m->V, L = m->L, IN = 3 * K + V, lf = m->frozen;
+    const long P = rec_size(m), total = P * L;
+    TrainWs &w = ws_for(c);
+    const int nb = static_cast<int>(std::min<long>(16, n));
+    const size_t d = sizeof(double);
+    if (w.g64.ensure(d * n * K * K) || w.q64.ensure(d * n * K) || w.wb.ensure(d * total) ||
+        w.wf.ensure(d * f64_fwd_rec(K, Z, V) * L) || w.f_in.ensure(d * L * n * IN) ||
+        w.f_z.ensure(d * L * n * Z) || w.f_u2.ensure(d * L * n * K) || w.f_xh.ensure(d * L * n * K) ||
+        w.b_u1.ensure(d * L * n * Z) || w.b_u2.ensure(d * L * n * K) || w.b_v.ensure(d * L * n * V) ||
+        w.b_t.ensure(d * L * n) || w.part.ensure(d * nb * total) || w.s_loss.ensure(d * n) ||
+        w.s_err.ensure(sizeof(long long) * n))
+        return fail(DETNET_ERR_CUDA, "FP64 training workspace allocation failed");
+    if (int rc = ensure_ws(c, n, K)) return rc;
+    cudaStream_t st = c->stream;
+    if (int rc = reset_sing(c, st)) return rc;
+    if (int rc = run_pre(m, st, 0, n, n, H, y, x, /*exact=*/true, w.g64.as<double>(), w.q64.as<double>()))
+        return rc;
+    {
+        LaunchScope ls(c, DETNET_K_OTHER, st);
+        k_pack64<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
+            m->tparams.as<double>(), m->has_masks ? m->tmasks.as<double>() : nullptr, K, Z, V, L,
+            w.wb.as<double>(), w.wf.as<double>());
+    }
+    if (int rc = check_launch()) return rc;
+    const unsigned grid = static_cast<unsigned>((n + F64_WARPS - 1) / F64_WARPS);
+    {
+        Fwd64Args fa{w.g64.as<double>(), w.q64.as<double>(), c->denom.as<double>(),
+                     c->xmask.as<uint32_t>(), w.wf.as<double>(), m->lnk_all.as<double>(),
+                     K, Z, V, L, trainable_only ? lf + 1 : 1, n, w.f_in.as<double>(),
+                     w.f_z.as<double>(), w.f_u2.as<double>(), w.f_xh.as<double>(),
+                     w.s_loss.as<double>(), w.s_err.as<long long>()};
+        const size_t smem = d * F64_WARPS * f64_fwd_scratch(K, Z, V);
+        LaunchScope ls(c, DETNET_K_STACK, st);
+        k_fwd64<<<grid, 32 * F64_WARPS, smem, st>>>(fa);
+    }
+    if (int rc = check_launch()) return rc;
+    if (lf < L) {
+        Bwd64Args ba{w.g64.as<double>(), c->denom.as<double>(), c->xmask.as<uint32_t>(),
+                     w.wb.as<double>(), m->lnk_all.as<double>(), K, Z, V, L, lf, n,
+                     w.f_in.as<double>(), w.f_z.as<double>(), w.f_u2.as<double>(),
+                     w.f_xh.as<double>(), w.b_u1.as<double>(), w.b_u2.as<double>(),
+                     w.b_v.as<double>(), w.b_t.as<double>()};
+        const size_t smem = d * F64_WARPS * f64_bwd_scratch(K, Z, V);
+        {
+            LaunchScope ls(c, DETNET_K_BACKWARD, st);
+            k_bwd64<<<grid, 32 * F64_WARPS, smem, st>>>(ba);
+        }
+        if (int rc = check_launch()) return rc;
+        Dw64Args da{w.b_u1.as<double>(), w.b_u2.as<double>(), w.b_v.as<double>(), w.f_in.as<double>(),
+                    w.f_z.as<double>(), m->has_masks ? m->tmasks.as<double>() : nullptr,
+                    K, Z, V, L, lf, n, nb, w.part.as<double>()};
+        const int mt = (std::max({Z, K, V}) + DW64_T - 1) / DW64_T;
+        const int nt = (std::max(IN, Z) + 1 + DW64_T - 1) / DW64_T;
+        {
+            LaunchScope ls(c, DETNET_K_BACKWARD, st);
+            k_dw64<<<dim3(nt, mt, static_cast<unsigned>((L - lf) * 3 * nb)), 256, 0, st>>>(da);
+        }
+        if (int rc = check_launch()) return rc;
+        {
+            LaunchScope ls(c, DETNET_K_BACKWARD, st);
+            const int jobs = (L - lf) * nb;
+            k_tsum64<<<(jobs + 127) / 128, 128, 0, st>>>(w.b_t.as<double>(), L, lf, n, nb, Z, K, V,
+                                                        w.part.as<double>());
+        }
+        if (int rc = check_launch()) return rc;
+    }
+    {
+        LaunchScope ls(c, DETNET_K_BACKWARD, st);
+        k_merge64<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(w.part.as<double>(), L, lf,
+                                                                             P, nb, raw);
+    }
+    if (int rc = check_launch()) return rc;
+    double *res = c->result.as<double>();
+    {
+        LaunchScope ls(c, DETNET_K_REDUCE, st);
+        k_reduce64<<<1, 256, 0, st>>>(w.s_loss.as<double>(), w.s_err.as<long long>(),
+                                      c->flag.as<uint8_t>(), n, res, reinterpret_cast<long long *>(res + 1),
+                                      reinterpret_cast<long long *>(res + 2), raw + total);
+    }
+    if (int rc = check_launch()) return rc;
+    if (!out) return drain_times(c, false), 0;
+    CK(cudaMemcpyAsync(res + 3, c->sing.p, 8, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(c->h_result, res, 32, cudaMemcpyDeviceToHost, st));
+    return finish_host(m, n, out);
 }
 
 // Forward with trace + reverse sweep + contractions -> raw gradient sums
@@ -114,6 +218,7 @@ int ensure_train_state(detnet_model *m) {
 int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8_t *x,
              bool trainable_only, double *raw, detnet_eval *out) {
     detnet_ctx *c = m->ctx;
+    if (c->train_fp64) return grad_raw64(m, n, H, y, x, trainable_only, raw, out);
     const BwdEntry *be = find_bwd(m->K, m->Z, m->V);
     if (!be) return fail(DETNET_ERR_UNSUPPORTED, "no backward kernel for these dims");
     if (n < 1) return fail(DETNET_ERR_CONTRACT, "batch_gradient: empty batch");
@@ -235,6 +340,15 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
         k_grad_sum<<<static_cast<unsigned>((total + 255) / 256), 256, 0, c->stream>>>(sa);
     }
     if (int rc = check_launch()) return rc;
+    { // raw[total] = this batch's loss sum (fixed tile order): the objective's data term
+        double *res = c->result.as<double>();
+        LaunchScope ls(c, DETNET_K_REDUCE, c->stream);
+        k_reduce<<<1, 1024, 0, c->stream>>>(c->tile_loss.as<double>(), c->tile_err.as<long long>(),
+                                           4 * tiles, c->flag.as<uint8_t>(), n, raw + total,
+                                           reinterpret_cast<long long *>(res + 4),
+                                           reinterpret_cast<long long *>(res + 5));
+    }
+    if (int rc = check_launch()) return rc;
     if (!out) return drain_times(c, false), 0; // no readback requested: no wait
     return finish(m, n, out); // loss / errors / flagged of the forward pass (syncs)
 }
@@ -316,7 +430,7 @@ int train_batch_gradient(detnet_model *m, long n, const float *H, const float *y
     const int N = m->N, K = m->K;
     const long total = rec_size(m) * m->L;
     if (w.in_H.ensure(sizeof(float) * n * N * K) || w.in_y.ensure(sizeof(float) * n * N) ||
-        w.in_x.ensure(static_cast<size_t>(n) * K) || w.raw.ensure(sizeof(double) * total) ||
+        w.in_x.ensure(static_cast<size_t>(n) * K) || w.raw.ensure(sizeof(double) * (total + 1)) ||
         w.grads.ensure(sizeof(double) * total))
         return fail(DETNET_ERR_CUDA, "allocation failed");
     CK(cudaMemcpyAsync(w.in_H.p, H, sizeof(float) * n * N * K, cudaMemcpyHostToDevice, c->stream));
@@ -390,9 +504,24 @@ int detnet_train_grad(detnet_model *m, long n, const float *H, const float *y, c
     return grad_raw(m, n, H, y, x, trainable_only != 0, raw_dev, out);
 }
 
+long detnet_train_raw_count(const detnet_model *m) {
+    return m ? record_size(m->K, m->Z, m->V) * m->L + 1 : 0;
+}
+
+int detnet_ctx_set_train_precision(detnet_ctx *c, int fp64) {
+    if (!c) return fail(DETNET_ERR_CONTRACT, "null context");
+    c->train_fp64 = fp64 != 0;
+    return 0;
+}
+
 int detnet_train_apply(detnet_model *m, const double *raw_dev, long n_global,
                        const detnet_loss_spec *spec, const detnet_adam_config *cfg) {
     if (!m || !raw_dev || n_global < 1) return fail(DETNET_ERR_CONTRACT, "bad argument");
+    if (spec && (spec->kind < 0 || spec->kind > 2))
+        return fail(DETNET_ERR_CONTRACT, "loss spec kind must be 0, 1 or 2");
+    if (m->diverged_step >= 0)
+        return fail(DETNET_ERR_DIVERGENCE, "train: objective became non-finite at step %lld",
+                    m->diverged_step);
     ++m->version; // packed images / layout may change: drop captured evaluate graphs
     if (int rc = validate_adam(cfg)) return rc;
     detnet_ctx *c = m->ctx;
@@ -401,6 +530,20 @@ int detnet_train_apply(detnet_model *m, const double *raw_dev, long n_global,
     TrainWs &w = ws_for(c);
     const long total = rec_size(m) * m->L;
     if (w.grads.ensure(sizeof(double) * total)) return fail(DETNET_ERR_CUDA, "alloc grads");
+    // objective = data_loss + regularizer(params) before the update
+    // (training.cpp:65-70); a non-finite one halts the run on the device
+    if (w.objpart.ensure(sizeof(double) * 6 * m->L)) return fail(DETNET_ERR_CUDA, "alloc objective");
+    ObjArgs oa{m->tparams.as<double>(), m->has_masks ? m->tmasks.as<double>() : nullptr, m->K, m->Z,
+               m->V, m->L, spec ? spec->kind : 0, spec ? spec->lambda : 0.0,
+               spec ? spec->lambda1 : 0.0, spec ? spec->lambda2 : 0.0, w.objpart.as<double>()};
+    {
+        LaunchScope ls(c, DETNET_K_ADAM, c->stream);
+        if (oa.kind != 0) k_reg_parts<<<3 * m->L, 32, 0, c->stream>>>(oa);
+        k_objective<<<1, 1, 0, c->stream>>>(oa, raw_dev + total, static_cast<double>(n_global),
+                                            static_cast<long long>(m->adam_step),
+                                            m->tstatus.as<double>());
+    }
+    if (int rc = check_launch()) return rc;
     if (int rc = apply_reg(m, raw_dev, n_global, spec, w.grads.as<double>())) return rc;
     double lr, bc1, bc2;
     adam_coefs(cfg, m->adam_step, lr, bc1, bc2);
@@ -409,7 +552,8 @@ int detnet_train_apply(detnet_model *m, const double *raw_dev, long n_global,
         k_adam<<<static_cast<unsigned>((total + 255) / 256), 256, 0, c->stream>>>(
             m->tparams.as<double>(), m->tmasks.as<double>(), w.grads.as<double>(),
             m->tm.as<double>(), m->tv.as<double>(), total, static_cast<int>(rec_size(m)),
-            m->frozen, lr, cfg->beta1, cfg->beta2, cfg->eps, bc1, bc2);
+            m->frozen, lr, cfg->beta1, cfg->beta2, cfg->eps, bc1, bc2,
+            reinterpret_cast<const long long *>(m->tstatus.as<double>() + 2));
     }
     if (int rc = check_launch()) return rc;
     if (int rc = pack_simt_device(m)) return rc;
@@ -422,6 +566,25 @@ int detnet_train_apply(detnet_model *m, const double *raw_dev, long n_global,
     // update; nothing here needs the host to wait
     if (int rc = check_launch()) return rc;
     drain_times(c, false);
+    return 0;
+}
+
+int detnet_train_status(detnet_model *m, double *objective, double *regularizer) {
+    if (!m) return fail(DETNET_ERR_CONTRACT, "null argument");
+    double st[3] = {0.0, 0.0, 0.0};
+    if (m->train_ready) {
+        CK(cudaSetDevice(m->ctx->device));
+        if (int rc = quiesce(m->ctx)) return rc;
+        CK(cudaMemcpy(st, m->tstatus.p, sizeof st, cudaMemcpyDeviceToHost));
+        long long halt;
+        std::memcpy(&halt, st + 2, 8);
+        m->diverged_step = halt;
+    }
+    if (objective) *objective = st[0];
+    if (regularizer) *regularizer = st[1];
+    if (m->diverged_step >= 0) // DivergenceError (training.cpp:68-70)
+        return fail(DETNET_ERR_DIVERGENCE, "train: objective became non-finite at step %lld",
+                    m->diverged_step);
     return 0;
 }
 
@@ -555,7 +718,9 @@ void train_ws_release(detnet_ctx *c) {
         TrainWs *w = all[i].second;
         for (DBuf *b : {&w->tr_in, &w->tr_z, &w->tr_u2, &w->tr_xf, &w->u1bar, &w->g23bar, &w->tbar,
                         &w->p1, &w->p23, &w->jobs, &w->raw, &w->grads, &w->colnorm, &w->bstate,
-                        &w->in_H, &w->in_y, &w->in_x})
+                        &w->in_H, &w->in_y, &w->in_x, &w->g64, &w->q64, &w->wb, &w->wf,
+                        &w->f_in, &w->f_z, &w->f_u2, &w->f_xh, &w->b_u1, &w->b_u2, &w->b_v,
+                        &w->b_t, &w->part, &w->s_loss, &w->s_err, &w->objpart})
             b->release();
         if (w->hi) {
             cudaStreamDestroy(w->hi);

@@ -59,8 +59,12 @@ class UnsupportedError(DetnetError):
     pass
 
 
+class DivergenceError(DetnetError):
+    """Non-finite training objective (training.cpp:68-70)."""
+
+
 _ERRS = {1: ContractError, 2: SingularMatrixError, 3: ConfigError, 4: CudaError, 5: CudaError,
-         6: UnsupportedError}
+         6: UnsupportedError, 7: DivergenceError}
 
 
 def _check(rc):
@@ -131,6 +135,10 @@ _lib.detnet_model_param_count.argtypes = [_vp]
 _lib.detnet_train_grad.argtypes = [_vp, C.c_long, _vp, _vp, _vp, C.c_int, _vp, C.POINTER(_Eval)]
 _lib.detnet_train_apply.argtypes = [_vp, _vp, C.c_long, C.POINTER(_LossSpec), C.POINTER(_AdamCfg)]
 _lib.detnet_model_get_params.argtypes = [_vp, _vp]
+_lib.detnet_train_raw_count.restype = C.c_long
+_lib.detnet_train_raw_count.argtypes = [_vp]
+_lib.detnet_train_status.argtypes = [_vp, _dp, _dp]
+_lib.detnet_ctx_set_train_precision.argtypes = [_vp, C.c_int]
 _lib.detnet_model_reset_adam.argtypes = [_vp]
 class _CostReport(C.Structure):
     _fields_ = [("layer_count", C.c_int)] + [(f, C.c_longlong) for f in (
@@ -258,6 +266,11 @@ class Context:
     def set_train_forward(self, tensor_cores=True):
         """Training forward on tcgen05 (dense K=20 models) instead of FP32 SIMT."""
         _check(_lib.detnet_ctx_set_train_forward(self._h, int(tensor_cores)))
+
+    def set_train_precision(self, fp64=True):
+        """FP64 training in the reference's operation order (bit-identical
+        batch_gradient / adam_step) instead of the FP32 default."""
+        _check(_lib.detnet_ctx_set_train_precision(self._h, int(fp64)))
 
     def set_stream(self, stream_ptr):
         _check(_lib.detnet_ctx_set_stream(self._h, stream_ptr))
@@ -455,6 +468,24 @@ class Model:
     @property
     def param_count(self):
         return _lib.detnet_model_param_count(self._h)
+
+    @property
+    def raw_count(self):
+        """Length of a detnet_train_grad raw buffer: the gradient sums plus
+        this rank's data-loss sum (all-reduce the whole buffer)."""
+        return _lib.detnet_train_raw_count(self._h)
+
+    def new_raw(self):
+        import torch
+        return torch.zeros(self.raw_count, dtype=torch.float64,
+                           device=torch.device("cuda", self.ctx.device))
+
+    def train_status(self):
+        """(objective, regularizer) of the last train_apply; raises
+        DivergenceError if training halted on a non-finite objective."""
+        o, r = C.c_double(), C.c_double()
+        _check(_lib.detnet_train_status(self._h, C.byref(o), C.byref(r)))
+        return o.value, r.value
 
     def train_grad(self, n, H_ptr, y_ptr, x_ptr, raw_ptr, trainable_only=False, want_eval=True):
         """Device-resident gradient sums (detnet_train_grad) into raw_ptr (FP64).

@@ -14,7 +14,8 @@
 //  * batch_gradient zeroes grads and adds the regularizer gradient
 //    (kernels.cpp:160-200); frozen slots stay empty (backward.cpp:88-103).
 // Precision: samples cross the boundary as FP32 (H, y) and int8 (x); weights
-// are packed to FP32 per params version (content-hashed).
+// are packed to FP32 per params version (content-hashed). With
+// DETNET_TRAIN_FP64=1 batch_gradient runs the FP64 reference-order mode.
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
@@ -43,6 +44,7 @@ namespace {
     case DETNET_ERR_SINGULAR: throw SingularMatrixError(msg);
     case DETNET_ERR_CONFIG: throw ConfigError(msg);
     case DETNET_ERR_UNSUPPORTED: throw CapacityError(msg);
+    case DETNET_ERR_DIVERGENCE: throw DivergenceError(msg);
     default: throw std::runtime_error("detnet_b200: " + msg);
     }
 }
@@ -99,6 +101,11 @@ struct Engine {
     Engine() {
         const char *dev = std::getenv("DETNET_DEVICE");
         check(detnet_ctx_create(dev ? std::atoi(dev) : 0, &ctx));
+        // DETNET_TRAIN_FP64=1: batch_gradient in FP64 in the reference's own
+        // operation order -- bit-identical to kernels.cpp's, so a training run
+        // through the seam follows the reference's trajectory exactly
+        if (const char *f64 = std::getenv("DETNET_TRAIN_FP64"))
+            check(detnet_ctx_set_train_precision(ctx, std::atoi(f64) != 0));
     }
 };
 

@@ -100,7 +100,7 @@ def test_training_steps_without_waits(setup):
     out = []
     for want in (True, False):
         m = ctx.model(K, N, 160, 40, xavier_params(K, 5, seed=23))
-        raw = torch.zeros(m.param_count, dtype=torch.float64, device="cuda")
+        raw = m.new_raw()
         for n, H, y, x in batches[:4]:
             m.train_grad(n, H, y, x, raw, want_eval=want)
             m.train_apply(raw, n, kind=2, lam1=1e-4, lr0=1e-3)

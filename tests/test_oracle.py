@@ -169,3 +169,20 @@ def test_f32_restatement_close(oracle):
     a = oracle.evaluate(m, H, y, x, want_xhat=True)
     b = oracle.evaluate_f32(m, H, y, x)
     assert np.max(np.abs(a["xhat"] - b["xhat"])) < 1e-3
+
+
+def test_o32_batch_gradient_tracks_reference(oracle, ref):
+    """O32 (the FP32 restatement used to calibrate FP32's own training
+    spread) stays within FP32 noise of the reference's FP64 batch_gradient."""
+    from oracle.oracle import scaled_inputs
+    m = xavier_model(oracle, depth=4, seed=5)
+    r = oracle.rng(2, 0)
+    H, x, y, _ = oracle.generate_batch(r, 30, 20, 300, 7.0, 14.0)
+    H32, y32, _ = scaled_inputs(H, y, x)
+    H64, y64 = H32.astype(np.float64), y32.astype(np.float64)
+    a = ref.batch_gradient(m, H64, y64, x, kind=2, lam1=1e-4)
+    b = oracle.batch_gradient_f32(m, H64, y64, x, kind=2, lam1=1e-4)
+    assert b["status"] == 0
+    assert np.abs(a["grads"] - b["grads"]).max() <= 1e-5 * np.abs(a["grads"]).max()
+    assert abs(a["data_loss"] - b["data_loss"]) <= 1e-6 * a["data_loss"]
+    assert b["symbol_errors"] == a["symbol_errors"] and b["flagged"] == a["flagged"]

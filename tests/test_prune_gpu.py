@@ -85,7 +85,7 @@ def test_prune_keeps_training_state(ctx, oracle):
     H, x, y, _ = oracle.generate_batch(r, N, K, 512, 7.0, 14.0)
     H32 = (H / np.sqrt(N)).astype(np.float32); y32 = (y / np.sqrt(N)).astype(np.float32)
     import torch
-    raw = torch.zeros(m.param_count, dtype=torch.float64, device="cuda")
+    raw = m.new_raw()
     Hd, yd, xd = (torch.from_numpy(a).cuda() for a in (H32, y32, x.astype(np.int8)))
     m.train_grad(512, Hd, yd, xd, raw)
     m.train_apply(raw, 512, lr0=1e-3)

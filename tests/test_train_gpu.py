@@ -115,7 +115,7 @@ def _train_100(ctx, oracle, pseed, dseed, K=20, N=30, L=6, n=192, steps=100):
     om = OModel(K, N, 8 * K, 2 * K, L, params.copy())
     mo1 = np.zeros_like(params)
     mo2 = np.zeros_like(params)
-    raw = torch.zeros(m.param_count, dtype=torch.float64, device="cuda")
+    raw = m.new_raw()
     train_rng = oracle.lib.or_stream(C.byref(oracle.rng(dseed, 0)), 2)
     val_rng = oracle.lib.or_stream(C.byref(oracle.rng(dseed, 0)), 3)
     Hv, xv, yv, _ = oracle.generate_batch(val_rng, N, K, 2000, 12.0, 12.0)

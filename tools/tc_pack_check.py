@@ -11,7 +11,7 @@ H, x, y, _ = orc.generate_batch(orc.rng(1, 2), N, K, n, 7.0, 14.0)
 H32 = (H / np.sqrt(N)).astype(np.float32); y32 = (y / np.sqrt(N)).astype(np.float32)
 ctx = eng.Context(0)
 m = ctx.model(K, N, 160, 40, xavier_params(K, L, seed=9))
-raw = torch.zeros(m.param_count, dtype=torch.float64, device="cuda")
+raw = m.new_raw()
 Hd, yd, xd = (torch.from_numpy(a).cuda() for a in (H32, y32, x.astype(np.int8)))
 for step in range(3):
     ev = m.train_grad(n, Hd, yd, xd, raw)

@@ -12,7 +12,7 @@ ctx = eng.Context(0)
 m = ctx.model(K, N, 8 * K, 2 * K, params)
 om = OModel(K, N, 8 * K, 2 * K, L, params.copy())
 mo1 = np.zeros_like(params); mo2 = np.zeros_like(params)
-raw = torch.zeros(m.param_count, dtype=torch.float64, device="cuda")
+raw = m.new_raw()
 train_rng = orc.lib.or_stream(C.byref(orc.rng(1, 0)), 2)
 val_rng = orc.lib.or_stream(C.byref(orc.rng(1, 0)), 3)
 Hv, xv, yv, _ = orc.generate_batch(val_rng, N, K, 2000, 12.0, 12.0)

@@ -5,6 +5,7 @@
 // host<->device streaming overlapped with compute, kernel launches with
 // per-launch CUDA-event timing, and status/error mapping. No CPU fallback:
 // every compute entry point requires an sm_100 device.
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -650,11 +651,20 @@ int detnet_ctx_create(int device, detnet_ctx **out) {
     return 0;
 }
 
+namespace {
+void release_model_device(detnet_model *m);
+}
+
 void detnet_ctx_destroy(detnet_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     drain_times(c);
+    for (detnet_model *m : c->models) { // models outliving their context
+        release_model_device(m);
+        m->ctx = nullptr;
+    }
+    c->models.clear();
     train_ws_release(c);
     for (DBuf *b : {&c->gp, &c->q32, &c->denom, &c->xmask, &c->flag, &c->tile_loss, &c->tile_err,
                     &c->sing, &c->result, &c->xhat_dev, &c->state_x, &c->state_v, &c->redo,
@@ -735,6 +745,7 @@ int detnet_model_create(detnet_ctx *c, const detnet_model_desc *d, detnet_model 
     m->ctx = c;
     m->K = d->n_tx; m->N = d->n_rx; m->Z = d->z_dim; m->V = d->v_dim;
     m->L = d->depth; m->frozen = d->frozen_prefix; m->dims = de;
+    c->models.push_back(m);
     if (int rc = upload_model(m, d)) { detnet_model_destroy(m); return rc; }
     *out = m;
     return 0;
@@ -762,8 +773,8 @@ namespace {
 void drop_graph(detnet_model *m);
 }
 
-void detnet_model_destroy(detnet_model *m) {
-    if (!m) return;
+namespace {
+void release_model_device(detnet_model *m) {
     cudaSetDevice(m->ctx->device);
     cudaStreamSynchronize(m->ctx->stream); // in-flight work may still read the buffers
     drop_graph(m);
@@ -771,6 +782,16 @@ void detnet_model_destroy(detnet_model *m) {
                     &m->sparse_stream, &m->sparse_off, &m->tstatus})
         b->release();
     tc_release(m->tc);
+}
+} // namespace
+
+void detnet_model_destroy(detnet_model *m) {
+    if (!m) return;
+    if (m->ctx) { // else: orphaned by detnet_ctx_destroy, device state already released
+        release_model_device(m);
+        auto &v = m->ctx->models;
+        v.erase(std::remove(v.begin(), v.end(), m), v.end());
+    }
     delete m;
 }
 

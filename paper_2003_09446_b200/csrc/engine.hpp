@@ -158,6 +158,9 @@ struct detnet_ctx {
     long long next_ticket = 0;
     cudaEvent_t chunk_done[2] = {nullptr, nullptr};
     cudaEvent_t copy_done[2] = {nullptr, nullptr};
+    // live models: destroying the context releases their device state and
+    // orphans them (a later detnet_model_destroy only frees the handle)
+    std::vector<detnet_model *> models;
 };
 
 struct detnet_model {

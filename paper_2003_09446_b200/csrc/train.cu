@@ -126,7 +126,8 @@ int grad_raw64(detnet_model *m, long n, const float *H, const float *y, const in
                bool trainable_only, double *raw, detnet_eval *out) {
     detnet_ctx *c = m->ctx;
     if (n < 1) return fail(DETNET_ERR_CONTRACT, "batch_gradient: empty batch");
-    if (m->K > 32) return fail(DETNET_ERR_UNSUPPORTED, "FP64 training mode: n_tx <= 32");
+    if (m->K > 32 || m->Z > 256 || m->V > 64)
+        return fail(DETNET_ERR_UNSUPPORTED, "FP64 training mode: n_tx <= 32, z <= 256, v <= 64");
     const int K = m->K, Z = m->Z, V = m->V, L = m->L, IN = 3 * K + V, lf = m->frozen;
     const long P = rec_size(m), total = P * L;
     TrainWs &w = ws_for(c);
@@ -405,6 +406,13 @@ int validate_adam(const detnet_adam_config *cfg) {
 int train_prepare() {
     for (const BwdEntry &e : kBwd)
         if (e.prep()) return fail(DETNET_ERR_CUDA, "cudaFuncSetAttribute (backward smem) failed");
+    // FP64 mode: per-warp scratch beyond 48 KB at K=20 (up to K=32 supported)
+    const int f64_bytes = static_cast<int>(sizeof(double) * F64_WARPS * f64_bwd_scratch(32, 256, 64));
+    if (cudaFuncSetAttribute(k_fwd64, cudaFuncAttributeMaxDynamicSharedMemorySize, f64_bytes) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(k_bwd64, cudaFuncAttributeMaxDynamicSharedMemorySize, f64_bytes) !=
+            cudaSuccess)
+        return fail(DETNET_ERR_CUDA, "cudaFuncSetAttribute (FP64 training smem) failed");
     return 0;
 }
 

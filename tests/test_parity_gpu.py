@@ -118,7 +118,10 @@ def test_end_to_end_statistics(ctx, oracle, L, n):
     if not near0.any():
         assert ev.symbol_errors == int(ref["errors"].sum())
     frac = float(np.mean(_close(xh, ref["xhat"])))
-    assert frac > 0.99, f"only {frac:.4f} of soft outputs within 1e-4"
+    print(f"L={L}: {frac:.5f} of end-to-end soft outputs within rtol 1e-4 + atol 1e-5")
+    # measured: 0.99726 at L=90, >= 0.999 at L=40 (untrained stacks amplify
+    # last-bit differences layer to layer; teacher-forced layers are all in)
+    assert frac >= (0.997 if L == 90 else 0.999), f"only {frac:.4f} of soft outputs within 1e-4"
     rel = abs(ev.data_loss - ref["loss"].mean()) / abs(ref["loss"].mean())
     assert rel < 1e-4, rel
     assert ev.flagged == int(ref["flagged"].sum())
@@ -284,3 +287,31 @@ def test_sparse_group_model_paths(ctx, oracle, path):
     assert ok, stats
     assert ev.symbol_errors == int(ref["errors"].sum())
     assert abs(ev.data_loss - ref["loss"].mean()) <= 1e-4 * abs(ref["loss"].mean())
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+@pytest.mark.parametrize("path", [0, 2, 1])
+def test_masked_configs_full_depth(ctx, oracle, ref, cfg, path):
+    """Configs 3 (group-pruned, compacted tensor-core images) and 4 (sparse
+    group) at their full depth L=40: 2,048 samples against the reference
+    library (error and flag counts equal, data loss within 1e-4) and the
+    first 256 samples' soft outputs end to end against the oracle."""
+    from paper_2003_09446_b200.workload import group_masks, sparse_group_model, xavier_params
+    L = 40
+    params = xavier_params(K, L, seed=9)
+    masks = group_masks(K, L, seed=31)
+    if cfg == 4:
+        params, masks = sparse_group_model(params, masks, K)
+    H, y, x = _inputs(oracle, 2048, seed=7)
+    ctx.set_path(path)
+    m = ctx.model(K, N, 160, 40, params, masks=masks)
+    ev, xh = m.batch_evaluate(H, y, x, want_xhat=True)
+    ctx.set_path(0)
+    om = _omodel(params, masks=masks)
+    r = ref.batch_evaluate(om, H.astype(np.float64), y.astype(np.float64), x.astype(np.float64))
+    assert ev.symbol_errors == r["symbol_errors"] and ev.flagged == r["flagged"]
+    assert abs(ev.data_loss - r["data_loss"]) <= 1e-4 * abs(r["data_loss"])
+    e = oracle.evaluate(om, H[:256].astype(np.float64), y[:256].astype(np.float64),
+                        x[:256].astype(np.float64), want_xhat=True)
+    ok, stats = _e2e_ok(xh[:256], e["xhat"])
+    assert ok, stats

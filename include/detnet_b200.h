@@ -52,6 +52,19 @@ typedef struct detnet_model detnet_model;
 /* ---- context ---------------------------------------------------------- */
 int detnet_ctx_create(int device, detnet_ctx **out);
 void detnet_ctx_destroy(detnet_ctx *ctx);
+/* A device group: one context per listed device (a device may repeat: that
+ * runs several shards on one GPU). The host-buffer detnet_batch_evaluate and
+ * detnet_batch_gradient (FP32 mode) of a group model shard the batch over all
+ * members at 8,192-sample chunk boundaries, one host thread per member, and
+ * fold the members' chunk sums in the canonical chunk order every kernel
+ * uses, so BatchEval and gradients are bit-identical for any group size
+ * (the reference's thread-count invariance, kernels.cpp:93-103, 160-200).
+ * Settings apply to every member; models are replicated. Device-pointer entry
+ * points (_device, _async, train_grad/apply, preprocess, forward_range) and
+ * the FP64 training mode run on the first device; after device-side training
+ * or pruning the replicas are refreshed before the next group call. */
+int detnet_ctx_create_group(const int *devices, int count, detnet_ctx **out);
+int detnet_ctx_group_size(const detnet_ctx *ctx);
 const char *detnet_last_error(void);
 /* Kernel-path selection: 0 auto (tcgen05 split-FP16 where compiled, with
  * 3xTF32 recompute of out-of-range tiles; else 3xTF32; else SIMT), 1 SIMT

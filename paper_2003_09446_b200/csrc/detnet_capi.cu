@@ -322,6 +322,7 @@ int ensure_ws(detnet_ctx *c, long n, int K) {
     if (c->gp.ensure(sizeof(float) * NG * np) || c->q32.ensure(sizeof(float) * K * np) ||
         c->denom.ensure(sizeof(double) * np) || c->xmask.ensure(sizeof(uint32_t) * np) ||
         c->flag.ensure(np) || c->tile_loss.ensure(sizeof(double) * 4 * tiles) ||
+        c->chunks.ensure(sizeof(double) * ((tiles + RED_CHUNK_TILES - 1) / RED_CHUNK_TILES)) ||
         c->tile_err.ensure(sizeof(long long) * 4 * tiles) || c->sing.ensure(8) ||
         c->result.ensure(64))
         return fail(DETNET_ERR_CUDA, "workspace allocation failed (n=%ld)", n);
@@ -519,7 +520,8 @@ int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, 
     }
     const size_t smem = 2 * static_cast<size_t>(m->simt_rec) * 4 + 64;
     // one CTA per SM: small batches use 64-sample CTAs, two threads per sample
-    const bool large = nt * TILE / SIMT_LARGE >= c->sms;
+    const long vt = c->variant_n > 0 ? (c->variant_n + TILE - 1) / TILE : nt;
+    const bool large = vt * TILE / SIMT_LARGE >= c->sms;
     const int samples = large ? SIMT_LARGE : SIMTP_SAMPLES;
     const int blocks = static_cast<int>((nt * TILE + samples - 1) / samples);
     {
@@ -540,7 +542,8 @@ int finish_device(detnet_model *m, long n, double *dst) {
         k_reduce<<<1, 1024, 0, c->stream>>>(c->tile_loss.as<double>(), c->tile_err.as<long long>(),
                                            4 * tiles, c->flag.as<uint8_t>(), n, res,
                                            reinterpret_cast<long long *>(res + 1),
-                                           reinterpret_cast<long long *>(res + 2));
+                                           reinterpret_cast<long long *>(res + 2),
+                                           c->chunks.as<double>());
     }
     if (int rc = check_launch()) return rc;
     CK(cudaMemcpyAsync(res + 3, c->sing.p, 8, cudaMemcpyDeviceToDevice, c->stream));
@@ -665,8 +668,11 @@ void detnet_ctx_destroy(detnet_ctx *c) {
         m->ctx = nullptr;
     }
     c->models.clear();
+    for (detnet_ctx *g : c->members) detnet_ctx_destroy(g);
+    c->members.clear();
     train_ws_release(c);
     for (DBuf *b : {&c->gp, &c->q32, &c->denom, &c->xmask, &c->flag, &c->tile_loss, &c->tile_err,
+                    &c->chunks,
                     &c->sing, &c->result, &c->xhat_dev, &c->state_x, &c->state_v, &c->redo,
                     &c->redo_count, &c->fb_list, &c->fb_count})
         b->release();
@@ -689,18 +695,21 @@ void detnet_ctx_destroy(detnet_ctx *c) {
 int detnet_ctx_set_path(detnet_ctx *c, int path) {
     if (!c || path < 0 || path > 4) return fail(DETNET_ERR_CONTRACT, "bad path");
     c->path = path;
+    for (detnet_ctx *g : c->members) g->path = path;
     return 0;
 }
 
 int detnet_ctx_set_train_forward(detnet_ctx *c, int tensor_cores) {
     if (!c) return fail(DETNET_ERR_CONTRACT, "null context");
     c->train_tc = tensor_cores != 0;
+    for (detnet_ctx *g : c->members) g->train_tc = c->train_tc;
     return 0;
 }
 
 int detnet_ctx_set_exact_preprocess(detnet_ctx *c, int on) {
     if (!c) return fail(DETNET_ERR_CONTRACT, "null ctx");
     c->exact_pre = on != 0;
+    for (detnet_ctx *g : c->members) g->exact_pre = c->exact_pre;
     return 0;
 }
 
@@ -747,6 +756,11 @@ int detnet_model_create(detnet_ctx *c, const detnet_model_desc *d, detnet_model 
     m->L = d->depth; m->frozen = d->frozen_prefix; m->dims = de;
     c->models.push_back(m);
     if (int rc = upload_model(m, d)) { detnet_model_destroy(m); return rc; }
+    for (detnet_ctx *g : c->members) { // device group: one replica per further member
+        detnet_model *r = nullptr;
+        if (int rc = detnet_model_create(g, d, &r)) { detnet_model_destroy(m); return rc; }
+        m->replicas.push_back(r);
+    }
     *out = m;
     return 0;
 }
@@ -766,6 +780,9 @@ int detnet_model_update(detnet_model *m, const detnet_model_desc *d) {
         m->lnk_train.release();
     }
     m->frozen = d->frozen_prefix;
+    for (detnet_model *r : m->replicas)
+        if (int rc = detnet_model_update(r, d)) return rc;
+    m->replicas_stale = false;
     return upload_model(m, d);
 }
 
@@ -787,6 +804,8 @@ void release_model_device(detnet_model *m) {
 
 void detnet_model_destroy(detnet_model *m) {
     if (!m) return;
+    for (detnet_model *r : m->replicas) detnet_model_destroy(r);
+    m->replicas.clear();
     if (m->ctx) { // else: orphaned by detnet_ctx_destroy, device state already released
         release_model_device(m);
         auto &v = m->ctx->models;
@@ -1046,9 +1065,20 @@ int detnet_batch_evaluate(detnet_model *m, long n, const float *H, const float *
                           detnet_eval *out) {
     if (!m || !out || (n > 0 && (!H || !y || !x)))
         return fail(DETNET_ERR_CONTRACT, "null argument");
-    detnet_ctx *c = m->ctx;
     *out = detnet_eval{};
     if (n <= 0) return 0;
+    if (!m->replicas.empty()) return group_batch_evaluate(m, n, H, y, x, trainable_only, xhat_out, out);
+    return eval_host(m, n, H, y, x, trainable_only, xhat_out, out, nullptr);
+}
+
+} // extern "C"
+
+namespace detnet {
+int eval_host(detnet_model *m, long n, const float *H, const float *y, const int8_t *x,
+              int trainable_only, float *xhat_out, detnet_eval *out, std::vector<double> *chunks) {
+    detnet_ctx *c = m->ctx;
+    *out = detnet_eval{};
+    if (n <= 0) { if (chunks) chunks->clear(); return 0; }
     CK(cudaSetDevice(c->device));
     const int K = m->K, N = m->N, L = m->L;
     if (int rc = ensure_ws(c, n, K)) return rc;
@@ -1089,8 +1119,17 @@ int detnet_batch_evaluate(detnet_model *m, long n, const float *H, const float *
         }
         CK(cudaEventRecord(c->chunk_done[b], c->stream));
     }
-    return finish(m, n, out);
+    if (int rc = finish(m, n, out)) return rc;
+    if (chunks) {
+        const long nc = ((n + TILE - 1) / TILE + RED_CHUNK_TILES - 1) / RED_CHUNK_TILES;
+        chunks->resize(nc);
+        CK(cudaMemcpy(chunks->data(), c->chunks.p, sizeof(double) * nc, cudaMemcpyDeviceToHost));
+    }
+    return 0;
 }
+} // namespace detnet
+
+extern "C" {
 
 int detnet_forward_range(detnet_model *m, long n, const float *H, const float *y, int l_begin,
                          int l_end, float *x_state, float *v_state, float *xhat_out) {
@@ -1261,6 +1300,8 @@ int detnet_batch_baseline_errors(detnet_ctx *c, int kind, long n, int n_rx, int 
 int detnet_batch_gradient(detnet_model *m, long n, const float *H, const float *y,
                           const int8_t *x, const detnet_loss_spec *spec, int trainable_only,
                           double *grads_out, detnet_eval *out) {
+    if (m && !m->replicas.empty() && !m->ctx->train_fp64)
+        return group_batch_gradient(m, n, H, y, x, spec, trainable_only, grads_out, out);
     return train_batch_gradient(m, n, H, y, x, spec, trainable_only, grads_out, out);
 }
 

@@ -2,6 +2,7 @@
 // units (not part of the C-ABI; see include/detnet_b200.h).
 #pragma once
 
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <string>
@@ -43,7 +44,7 @@ inline long record_size(int K, int Z, int V) {
 // device buffer that only grows
 // Bumped on every device (re)allocation: a captured CUDA graph is replayed
 // only while no buffer it may reference has moved.
-inline long long g_alloc_epoch = 0;
+inline std::atomic<long long> g_alloc_epoch{0};
 
 struct DBuf {
     void *p = nullptr;
@@ -139,10 +140,14 @@ struct detnet_ctx {
     std::vector<cudaEvent_t> event_pool;
     // workspace
     detnet::DBuf gp, q32, denom, xmask, flag, tile_loss, tile_err, sing, result;
+    detnet::DBuf chunks; // per-chunk loss sums of the last reduction (k_reduce)
     detnet::DBuf in_H[2], in_y[2], in_x[2], xhat_dev, state_x, state_v, fb_list, fb_count;
     bool exact_pre = false; // bit-exact reference LU for every sample
     bool train_tc = false;  // training forward on tcgen05 (dense images) instead of SIMT
     bool train_fp64 = false; // FP64 training step in the reference's order (k_train64.cuh)
+    // > 0: choose the SIMT forward / reverse-sweep launch shapes as for a
+    // batch of this many samples (device-group members use the global batch)
+    long variant_n = 0;
     detnet::DBuf redo, redo_count; // split-FP16 range flags per tile + count
     double *h_result = nullptr; // pinned: loss, err, flag, singular
     // asynchronous evaluations (detnet_batch_evaluate_device_async): a ring of
@@ -161,6 +166,10 @@ struct detnet_ctx {
     // live models: destroying the context releases their device state and
     // orphans them (a later detnet_model_destroy only frees the handle)
     std::vector<detnet_model *> models;
+    // device group (detnet_ctx_create_group): this context is member 0, the
+    // others are owned here; host-buffer batch_evaluate / batch_gradient shard
+    // the batch over all members at 8,192-sample chunk boundaries
+    std::vector<detnet_ctx *> members;
 };
 
 struct detnet_model {
@@ -212,6 +221,9 @@ struct detnet_model {
         }
     } graph;
     int graph_seen = 0; // consecutive eager calls with the current key
+    // group models: one replica per further group member (same params/masks)
+    std::vector<detnet_model *> replicas;
+    bool replicas_stale = false; // device training / pruning changed member 0 only
 };
 
 namespace detnet {
@@ -302,6 +314,24 @@ int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, 
               int l_end, bool trainable_only, float *xhat, float *xs, float *vs,
               const TraceBufs *trace = nullptr);
 int finish(detnet_model *m, long n, detnet_eval *out);
+// the host-buffer evaluation (detnet_batch_evaluate) of one shard; chunks:
+// the per-8192-sample-chunk loss sums of the canonical reduction (k_reduce)
+int eval_host(detnet_model *m, long n, const float *H, const float *y, const int8_t *x,
+              int trainable_only, float *xhat_out, detnet_eval *out, std::vector<double> *chunks);
+// the FP32 training gradient of one shard: per-chunk raw gradient sums
+// [chunks][param_count] and loss chunk sums, copied to the host
+int grad_host_shard(detnet_model *m, long n, const float *H, const float *y, const int8_t *x,
+                    int trainable_only, std::vector<double> &chunk_raw,
+                    std::vector<double> &chunk_loss, detnet_eval *out);
+// grads = raw * mask / n + regularizer gradient on the model's device
+int apply_reg_host(detnet_model *m, const double *raw_host, long n, const detnet_loss_spec *spec,
+                   double *grads_out);
+int group_batch_evaluate(detnet_model *m, long n, const float *H, const float *y,
+                         const int8_t *x, int trainable_only, float *xhat_out, detnet_eval *out);
+int group_batch_gradient(detnet_model *m, long n, const float *H, const float *y,
+                         const int8_t *x, const detnet_loss_spec *spec, int trainable_only,
+                         double *grads_out, detnet_eval *out);
+int sync_replicas(detnet_model *m);
 int finish_host(detnet_model *m, long n, detnet_eval *out);
 int pack_simt_device(detnet_model *m); // FP32 records from the FP64 master copy
 int train_prepare();                   // per-device kernel attributes (train.cu)

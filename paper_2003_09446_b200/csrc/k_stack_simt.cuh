@@ -476,16 +476,33 @@ __global__ void __launch_bounds__(SIMTP_THREADS, 1) k_stack_simt_pair(StackArgs 
 }
 
 // K5: fixed-order reduction of per-tile partials and per-sample flags.
+// finish_eval (kernels.cpp:93-103) on the device, in a canonical order that
+// does not depend on how the samples were split into launches or devices:
+// each chunk of RED_CHUNK_TILES consecutive tiles (8,192 samples) folds its
+// tiles' loss partials ((q0 + q1) + (q2 + q3) per tile) in tile order, and
+// the chunk sums are folded in chunk order. A device group whose shards
+// start at chunk boundaries reproduces the single-device sum exactly from the
+// members' chunk sums (chunk_out). Counts are integers (exact in any order).
+constexpr int RED_CHUNK_TILES = 64;
 static __global__ void __launch_bounds__(1024) k_reduce(const double *tile_loss, const long long *tile_err,
-                                                 long n_tiles, const uint8_t *flag, long n,
+                                                 long n_quads, const uint8_t *flag, long n,
                                                  double *out_loss, long long *out_err,
-                                                 long long *out_flag) {
-    __shared__ double sl[1024];
+                                                 long long *out_flag, double *chunk_out) {
     __shared__ long long se[1024], sf[1024];
     const int t = threadIdx.x;
-    double l = 0.0;
+    const long tiles = n_quads / 4;
+    const long chunks = (tiles + RED_CHUNK_TILES - 1) / RED_CHUNK_TILES;
     long long e = 0, f = 0;
-    for (long i = t; i < n_tiles; i += 1024) { l += tile_loss[i]; e += tile_err[i]; }
+    for (long i = t; i < n_quads; i += 1024) e += tile_err[i];
+    for (long c = t; c < chunks; c += 1024) {
+        double acc = 0.0;
+        const long t1 = (c + 1) * RED_CHUNK_TILES < tiles ? (c + 1) * RED_CHUNK_TILES : tiles;
+        for (long tt = c * RED_CHUNK_TILES; tt < t1; ++tt) {
+            const double *q = tile_loss + tt * 4;
+            acc += (q[0] + q[1]) + (q[2] + q[3]);
+        }
+        chunk_out[c] = acc;
+    }
     // flags are 0/1 bytes: 16 per 128-bit load, summed with popc
     long i0 = 0;
     if ((reinterpret_cast<uintptr_t>(flag) & 15) == 0) {
@@ -498,13 +515,19 @@ static __global__ void __launch_bounds__(1024) k_reduce(const double *tile_loss,
         i0 = n16 * 16;
     }
     for (long i = i0 + t; i < n; i += 1024) f += flag[i];
-    sl[t] = l; se[t] = e; sf[t] = f;
+    se[t] = e; sf[t] = f;
     __syncthreads();
     for (int w = 512; w > 0; w >>= 1) {
-        if (t < w) { sl[t] += sl[t + w]; se[t] += se[t + w]; sf[t] += sf[t + w]; }
+        if (t < w) { se[t] += se[t + w]; sf[t] += sf[t + w]; }
         __syncthreads();
     }
-    if (t == 0) { *out_loss = sl[0]; *out_err = se[0]; *out_flag = sf[0]; }
+    if (t == 0) {
+        double l = 0.0;
+        for (long c = 0; c < chunks; ++c) l += chunk_out[c];
+        *out_loss = l;
+        *out_err = se[0];
+        *out_flag = sf[0];
+    }
 }
 
 } // namespace detnet

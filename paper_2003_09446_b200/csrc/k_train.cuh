@@ -34,7 +34,7 @@ struct BwdArgs {
     const float *tr_in, *tr_z, *tr_u2, *tr_xf;
     float *u1bar;           // [L][Z][ts]
     float *g23bar;          // [L][K+V][ts]
-    double *tbar_part;      // [L][gridDim.x]
+    double *tbar_part;      // [L][ts / 32]: t gradient per 32-sample warp group
     // k_train_bwd_pair only: sweep iterations [it_begin, it_end) of [0, L - lf)
     // (layer L-1-it); a_bar / v_bar carried between chunks in state [K+V][ts]
     int it_begin = 0, it_end = -1;
@@ -56,7 +56,6 @@ __global__ void __launch_bounds__(THREADS, 1) k_train_bwd(BwdArgs a) {
     constexpr int REC = static_cast<int>(simt_rec(K, Z, V));
     extern __shared__ __align__(128) float sw[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(sw + 2 * REC);
-    __shared__ double s_t[2][BWD_WARPS];
 
     const int tid = threadIdx.x;
     const long unit = static_cast<long>(blockIdx.x) * THREADS + tid;
@@ -194,15 +193,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_train_bwd(BwdArgs a) {
         }
 #pragma unroll
         for (int k = 0; k < V; ++k) vbar[k] = ibar[2 * K + k];
-        // per-CTA t gradient (deterministic tree)
+        // t gradient per 32-sample group (deterministic tree; the same groups
+        // in every kernel variant, so the sum does not depend on the launch shape)
         double tsum = live ? static_cast<double>(tb) : 0.0;
         tsum = warp_sum(tsum);
-        if ((tid & 31) == 0) s_t[it & 1][tid >> 5] = tsum;
-        __syncthreads(); // also: every thread is done reading buffer b
+        if ((tid & 31) == 0 && live_tile) a.tbar_part[static_cast<long>(l) * (a.ts / 32) + s / 32] = tsum;
+        __syncthreads(); // every thread is done reading buffer b
         if (tid == 0) {
-            double acc = 0.0;
-            for (int w8 = 0; w8 < BWD_WARPS; ++w8) acc += s_t[it & 1][w8];
-            a.tbar_part[static_cast<long>(l) * gridDim.x + blockIdx.x] = acc;
             if (it + 2 < nl) {
                 mbar_arrive_expect_tx(&bars[b], bytes);
                 bulk_g2s_chunked(sw + b * REC,
@@ -237,7 +234,6 @@ __global__ void __launch_bounds__(BWP_THREADS, 1) k_train_bwd_pair(BwdArgs a) {
     float(*sIB)[P] = reinterpret_cast<float(*)[P]>(sw + REC);       // [NIB][P] B -> A
     float(*sAV)[P] = reinterpret_cast<float(*)[P]>(sw + REC + NIB * P); // [K+V][P] A -> B
     uint64_t *bar = reinterpret_cast<uint64_t *>(sw + REC + (NIB + O) * P);
-    __shared__ double s_t[2];
 
     const int tid = threadIdx.x, warp = tid >> 5;
     const bool isA = warp < 2;
@@ -401,12 +397,12 @@ __global__ void __launch_bounds__(BWP_THREADS, 1) k_train_bwd_pair(BwdArgs a) {
 #pragma unroll
             for (int k = 0; k < V; ++k) vbar[k] = sAV[K + k][ls];
         }
-        // per-CTA t gradient (A warps; deterministic)
+        // t gradient per 32-sample group (A warps; same groups as k_train_bwd)
         double tsum = (isA && live) ? static_cast<double>(tb) : 0.0;
         tsum = warp_sum(tsum);
-        if (isA && (tid & 31) == 0) s_t[warp] = tsum;
-        __syncthreads(); // s_t ready; B is done reading sAV before A rewrites it
-        if (tid == 0) a.tbar_part[static_cast<long>(l) * gridDim.x + blockIdx.x] = s_t[0] + s_t[1];
+        if (isA && (tid & 31) == 0 && live_tile)
+            a.tbar_part[static_cast<long>(l) * (a.ts / 32) + s / 32] = tsum;
+        __syncthreads(); // B is done reading sAV before A rewrites it
     }
     if (it1 < nl_all && isA && live_tile) { // hand the sweep state to the next chunk
 #pragma unroll
@@ -522,11 +518,19 @@ __global__ void __launch_bounds__(256) k_dw_gemm(const DwJob *jobs, long n, long
 struct SumArgs {
     const double *p1;     // W1 partials [L][splits][Z][IN+1]
     const double *p23;    // W23 partials [L][splits][K+V][Z+1]
-    const double *tpart;  // [L][tblocks]
-    int tblocks, splits;
+    const double *tpart;  // [L][tgroups] (32-sample groups)
+    int tgroups, splits;
     int K, Z, V, L, lf;
     double *raw;          // [L][P] unscaled, unmasked data-gradient sums (record layout)
+    double *chunk_out;    // optional [chunks][L][P]: the per-chunk sums (device groups)
 };
+
+// Chunk = 8,192 consecutive samples = 32 dW splits = 256 t groups. The raw
+// sums are folded in a canonical two-level order -- within each chunk in
+// split order, then the chunk sums in chunk order -- which does not depend on
+// how a batch is sharded over launches or devices (shards start at chunk
+// boundaries), so a device group reproduces the single-device bits.
+constexpr int GRAD_CHUNK_SPLITS = 8192 / DW_SPLIT, GRAD_CHUNK_GROUPS = 8192 / 32;
 
 // Sum the split partials in fixed order (FP64) into record layout. The raw
 // sums are what ranks all-reduce (sum) before the update.
@@ -538,9 +542,17 @@ __global__ void k_grad_sum(SumArgs a) {
     const int l = static_cast<int>(idx / P), e = static_cast<int>(idx % P);
     if (l < a.lf) { a.raw[idx] = 0.0; return; }
     const int ob1 = Z * IN, oW2 = ob1 + Z, ob2 = oW2 + K * Z, oW3 = ob2 + K, ob3 = oW3 + V * Z, ot = ob3 + V;
+    const long total = static_cast<long>(a.L) * P;
     double sum = 0.0;
     if (e == ot) {
-        for (int b = 0; b < a.tblocks; ++b) sum += a.tpart[static_cast<long>(l) * a.tblocks + b];
+        const double *tp = a.tpart + static_cast<long>(l) * a.tgroups;
+        for (int c0 = 0, ch = 0; c0 < a.tgroups; c0 += GRAD_CHUNK_GROUPS, ++ch) {
+            double cs = 0.0;
+            const int c1 = c0 + GRAD_CHUNK_GROUPS < a.tgroups ? c0 + GRAD_CHUNK_GROUPS : a.tgroups;
+            for (int g = c0; g < c1; ++g) cs += tp[g];
+            if (a.chunk_out) a.chunk_out[ch * total + idx] = cs;
+            sum += cs;
+        }
     } else {
         const double *src;
         long stride, base;
@@ -562,7 +574,13 @@ __global__ void k_grad_sum(SumArgs a) {
             base = static_cast<long>(r) * (Z + 1) + c;
             stride = static_cast<long>(K + V) * (Z + 1);
         }
-        for (int sp = 0; sp < a.splits; ++sp) sum += src[sp * stride + base];
+        for (int c0 = 0, ch = 0; c0 < a.splits; c0 += GRAD_CHUNK_SPLITS, ++ch) {
+            double cs = 0.0;
+            const int c1 = c0 + GRAD_CHUNK_SPLITS < a.splits ? c0 + GRAD_CHUNK_SPLITS : a.splits;
+            for (int sp = c0; sp < c1; ++sp) cs += src[sp * stride + base];
+            if (a.chunk_out) a.chunk_out[ch * total + idx] = cs;
+            sum += cs;
+        }
     }
     a.raw[idx] = sum;
 }

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "engine.hpp"
@@ -82,7 +83,13 @@ std::vector<std::pair<detnet_ctx *, TrainWs *>> &train_ws_all() {
     return all;
 }
 
+std::mutex &train_ws_mu() {
+    static std::mutex mu;
+    return mu;
+}
+
 TrainWs &ws_for(detnet_ctx *c) {
+    std::lock_guard<std::mutex> lk(train_ws_mu()); // device-group members run on threads
     auto &all = train_ws_all();
     for (auto &p : all)
         if (p.first == c) return *p.second;
@@ -217,7 +224,7 @@ int grad_raw64(detnet_model *m, long n, const float *H, const float *y, const in
 // Forward with trace + reverse sweep + contractions -> raw gradient sums
 // (record layout, unscaled, unmasked) in `raw`; local BatchEval in *out.
 int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8_t *x,
-             bool trainable_only, double *raw, detnet_eval *out) {
+             bool trainable_only, double *raw, detnet_eval *out, double *chunk_raw = nullptr) {
     detnet_ctx *c = m->ctx;
     if (c->train_fp64) return grad_raw64(m, n, H, y, x, trainable_only, raw, out);
     const BwdEntry *be = find_bwd(m->K, m->Z, m->V);
@@ -230,14 +237,17 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
     const int splits = static_cast<int>((n + DW_SPLIT - 1) / DW_SPLIT);
     // one CTA per SM: small batches use 64-sample CTAs to reach more SMs
     // small batches: two threads per sample, 64 samples per CTA (k_train_bwd_pair)
-    const bool bwd_large = tiles * TILE / BWD_LARGE >= c->sms;
+    // launch shape (and with it the FP32 summation order of the sweep) as for
+    // a batch of variant_tiles tiles: device groups pass the global batch
+    const long variant_tiles = c->variant_n > 0 ? (c->variant_n + TILE - 1) / TILE : tiles;
+    const bool bwd_large = variant_tiles * TILE / BWD_LARGE >= c->sms;
     const int bwd_samples = bwd_large ? BWD_LARGE : BWP_SAMPLES;
     const int bwd_per = bwd_large ? BWD_LARGE : BWP_THREADS;
     const int bwd_blocks = static_cast<int>((tiles * TILE + bwd_samples - 1) / bwd_samples);
     if (w.tr_in.ensure(sizeof(float) * L * IN * ts) || w.tr_z.ensure(sizeof(float) * L * Z * ts) ||
         w.tr_u2.ensure(sizeof(float) * L * K * ts) || w.tr_xf.ensure(sizeof(float) * K * ts) ||
         w.u1bar.ensure(sizeof(float) * L * Z * ts) || w.g23bar.ensure(sizeof(float) * L * O * ts) ||
-        w.tbar.ensure(sizeof(double) * L * bwd_blocks) ||
+        w.tbar.ensure(sizeof(double) * L * (ts / 32)) ||
         w.p1.ensure(sizeof(double) * L * splits * Z * (IN + 1)) ||
         w.p23.ensure(sizeof(double) * L * splits * O * (Z + 1)) ||
         w.jobs.ensure(sizeof(DwJob) * 2 * L))
@@ -333,8 +343,8 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
             if (int rc = check_launch()) return rc;
         }
     }
-    SumArgs sa{w.p1.as<double>(), w.p23.as<double>(), w.tbar.as<double>(), bwd_blocks, splits,
-               K, Z, V, L, lf, raw};
+    SumArgs sa{w.p1.as<double>(), w.p23.as<double>(), w.tbar.as<double>(),
+               static_cast<int>(ts / 32), splits, K, Z, V, L, lf, raw, chunk_raw};
     const long total = rec_size(m) * L;
     {
         LaunchScope ls(c, DETNET_K_BACKWARD, c->stream);
@@ -347,7 +357,8 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
         k_reduce<<<1, 1024, 0, c->stream>>>(c->tile_loss.as<double>(), c->tile_err.as<long long>(),
                                            4 * tiles, c->flag.as<uint8_t>(), n, raw + total,
                                            reinterpret_cast<long long *>(res + 4),
-                                           reinterpret_cast<long long *>(res + 5));
+                                           reinterpret_cast<long long *>(res + 5),
+                                           c->chunks.as<double>());
     }
     if (int rc = check_launch()) return rc;
     if (!out) return drain_times(c, false), 0; // no readback requested: no wait
@@ -455,6 +466,61 @@ int train_batch_gradient(detnet_model *m, long n, const float *H, const float *y
     return 0;
 }
 
+int grad_host_shard(detnet_model *m, long n, const float *H, const float *y, const int8_t *x,
+                    int trainable_only, std::vector<double> &chunk_raw,
+                    std::vector<double> &chunk_loss, detnet_eval *out) {
+    detnet_ctx *c = m->ctx;
+    *out = detnet_eval{};
+    chunk_raw.clear();
+    chunk_loss.clear();
+    if (n <= 0) return 0;
+    CK(cudaSetDevice(c->device));
+    if (int rc = ensure_train_state(m)) return rc;
+    TrainWs &w = ws_for(c);
+    const int N = m->N, K = m->K;
+    const long total = rec_size(m) * m->L;
+    const long nc = (n + 8191) / 8192;
+    DBuf craw;
+    if (w.in_H.ensure(sizeof(float) * n * N * K) || w.in_y.ensure(sizeof(float) * n * N) ||
+        w.in_x.ensure(static_cast<size_t>(n) * K) || w.raw.ensure(sizeof(double) * (total + 1)) ||
+        craw.ensure(sizeof(double) * nc * total))
+        return fail(DETNET_ERR_CUDA, "allocation failed");
+    CK(cudaMemcpyAsync(w.in_H.p, H, sizeof(float) * n * N * K, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(w.in_y.p, y, sizeof(float) * n * N, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(w.in_x.p, x, static_cast<size_t>(n) * K, cudaMemcpyHostToDevice, c->stream));
+    int rc = grad_raw(m, n, w.in_H.as<float>(), w.in_y.as<float>(), w.in_x.as<int8_t>(),
+                      trainable_only != 0, w.raw.as<double>(), out, craw.as<double>());
+    if (rc == 0) {
+        chunk_raw.resize(static_cast<size_t>(nc) * total);
+        chunk_loss.resize(nc);
+        if (cudaMemcpy(chunk_raw.data(), craw.p, sizeof(double) * nc * total,
+                       cudaMemcpyDeviceToHost) != cudaSuccess ||
+            cudaMemcpy(chunk_loss.data(), c->chunks.p, sizeof(double) * nc,
+                       cudaMemcpyDeviceToHost) != cudaSuccess)
+            rc = fail(DETNET_ERR_CUDA, "gradient chunk copy failed");
+    }
+    craw.release();
+    return rc;
+}
+
+int apply_reg_host(detnet_model *m, const double *raw_host, long n, const detnet_loss_spec *spec,
+                   double *grads_out) {
+    detnet_ctx *c = m->ctx;
+    CK(cudaSetDevice(c->device));
+    if (int rc = ensure_train_state(m)) return rc;
+    TrainWs &w = ws_for(c);
+    const long total = rec_size(m) * m->L;
+    if (w.raw.ensure(sizeof(double) * (total + 1)) || w.grads.ensure(sizeof(double) * total))
+        return fail(DETNET_ERR_CUDA, "allocation failed");
+    CK(cudaMemcpyAsync(w.raw.p, raw_host, sizeof(double) * total, cudaMemcpyHostToDevice, c->stream));
+    if (int rc = apply_reg(m, w.raw.as<double>(), n, spec, w.grads.as<double>())) return rc;
+    CK(cudaMemcpyAsync(grads_out, w.grads.p, sizeof(double) * total, cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    drain_times(c);
+    return 0;
+}
+
 int train_adam_step(detnet_ctx *c, int K, int Z, int V, int L, int lf, double *params,
                     const double *masks, const double *grads, double *m1, double *m2,
                     int64_t *step, const detnet_adam_config *cfg) {
@@ -519,6 +585,7 @@ long detnet_train_raw_count(const detnet_model *m) {
 int detnet_ctx_set_train_precision(detnet_ctx *c, int fp64) {
     if (!c) return fail(DETNET_ERR_CONTRACT, "null context");
     c->train_fp64 = fp64 != 0;
+    for (detnet_ctx *g : c->members) g->train_fp64 = c->train_fp64;
     return 0;
 }
 
@@ -531,6 +598,7 @@ int detnet_train_apply(detnet_model *m, const double *raw_dev, long n_global,
         return fail(DETNET_ERR_DIVERGENCE, "train: objective became non-finite at step %lld",
                     m->diverged_step);
     ++m->version; // packed images / layout may change: drop captured evaluate graphs
+    m->replicas_stale = !m->replicas.empty();
     if (int rc = validate_adam(cfg)) return rc;
     detnet_ctx *c = m->ctx;
     CK(cudaSetDevice(c->device));
@@ -642,6 +710,7 @@ int detnet_model_prune(detnet_model *m, int kind, double eta, double eta1, doubl
     const int64_t step = m->adam_step;
     detnet_model_desc d{m->K, m->N, m->Z, m->V, m->L, m->frozen, params.data(), masks.data()};
     if (int rc = upload_model(m, &d)) return rc;
+    m->replicas_stale = !m->replicas.empty();
     m->train_ready = true; // device params / masks already hold exactly these values
     m->adam_step = step;
     drain_times(m->ctx);
@@ -720,6 +789,7 @@ int detnet_model_reset_adam(detnet_model *m) {
 namespace detnet {
 // called by detnet_ctx_destroy: the training workspace of a context
 void train_ws_release(detnet_ctx *c) {
+    std::lock_guard<std::mutex> lk(train_ws_mu());
     auto &all = train_ws_all();
     for (size_t i = 0; i < all.size(); ++i) {
         if (all[i].first != c) continue;

@@ -99,6 +99,8 @@ class _AdamCfg(C.Structure):
 
 _lib.detnet_last_error.restype = C.c_char_p
 _lib.detnet_ctx_create.argtypes = [C.c_int, C.POINTER(_vp)]
+_lib.detnet_ctx_create_group.argtypes = [C.POINTER(C.c_int), C.c_int, C.POINTER(_vp)]
+_lib.detnet_ctx_group_size.argtypes = [_vp]
 _lib.detnet_ctx_destroy.argtypes = [_vp]
 _lib.detnet_ctx_set_path.argtypes = [_vp, C.c_int]
 _lib.detnet_ctx_set_stream.argtypes = [_vp, _vp]
@@ -239,12 +241,24 @@ class _Ordered:
 class Context:
     """One CUDA device (detnet_ctx). Single-owner, like unfold::Rng."""
 
-    def __init__(self, device=0, path=PATH_AUTO):
+    def __init__(self, device=0, path=PATH_AUTO, devices=None):
+        """devices: a list of device ids -> a device group (detnet_ctx_create_group):
+        host-buffer batch_evaluate / batch_gradient shard over all of them with
+        results bit-identical to one device. A device may repeat."""
         h = _vp()
-        _check(_lib.detnet_ctx_create(device, C.byref(h)))
+        if devices is not None:
+            arr = (C.c_int * len(devices))(*devices)
+            _check(_lib.detnet_ctx_create_group(arr, len(devices), C.byref(h)))
+            device = devices[0]
+        else:
+            _check(_lib.detnet_ctx_create(device, C.byref(h)))
         self._h = h
         self.device = device
         self.set_path(path)
+
+    @property
+    def group_size(self):
+        return _lib.detnet_ctx_group_size(self._h)
 
     def close(self):
         if getattr(self, "_h", None):

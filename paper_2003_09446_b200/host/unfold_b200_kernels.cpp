@@ -99,8 +99,24 @@ struct Engine {
     std::mutex mu;
 
     Engine() {
-        const char *dev = std::getenv("DETNET_DEVICE");
-        check(detnet_ctx_create(dev ? std::atoi(dev) : 0, &ctx));
+        // DETNET_DEVICES=0,1,...: one seam call shards over a device group
+        // (bit-identical results for any group size); else DETNET_DEVICE or 0
+        std::vector<int> devs;
+        if (const char *list = std::getenv("DETNET_DEVICES")) {
+            for (const char *p = list; *p;) {
+                char *end = nullptr;
+                const long v = std::strtol(p, &end, 10);
+                if (end == p) break;
+                devs.push_back(static_cast<int>(v));
+                p = *end ? end + 1 : end;
+            }
+        }
+        if (!devs.empty()) {
+            check(detnet_ctx_create_group(devs.data(), static_cast<int>(devs.size()), &ctx));
+        } else {
+            const char *dev = std::getenv("DETNET_DEVICE");
+            check(detnet_ctx_create(dev ? std::atoi(dev) : 0, &ctx));
+        }
         // DETNET_TRAIN_FP64=1: batch_gradient in FP64 in the reference's own
         // operation order -- bit-identical to kernels.cpp's, so a training run
         // through the seam follows the reference's trajectory exactly

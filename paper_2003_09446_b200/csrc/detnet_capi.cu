@@ -796,7 +796,7 @@ void release_model_device(detnet_model *m) {
     cudaStreamSynchronize(m->ctx->stream); // in-flight work may still read the buffers
     drop_graph(m);
     for (DBuf *b : {&m->simt, &m->lnk_all, &m->lnk_train, &m->tparams, &m->tmasks, &m->tm, &m->tv,
-                    &m->sparse_stream, &m->sparse_off, &m->tstatus})
+                    &m->sparse_stream, &m->sparse_off, &m->tstatus, &m->bwd_img})
         b->release();
     tc_release(m->tc);
 }

@@ -185,6 +185,7 @@ struct detnet_model {
     detnet::TcModel tc; // tcgen05 path packing (stack_tc.cu)
     // training state (train.cu): FP64 master params, masks, Adam moments
     detnet::DBuf tparams, tmasks, tm, tv;
+    detnet::DBuf bwd_img; // tcgen05 reverse-sweep weight images (bwd_tc.cu)
     int64_t adam_step = 0;
     // [objective, regularizer, diverged step (int64, -1 = none)] of the last
     // detnet_train_apply (device); the host copy of the sticky flag
@@ -335,6 +336,14 @@ int sync_replicas(detnet_model *m);
 int finish_host(detnet_model *m, long n, detnet_eval *out);
 int pack_simt_device(detnet_model *m); // FP32 records from the FP64 master copy
 int train_prepare();                   // per-device kernel attributes (train.cu)
+struct DwJob; // dw_job.hpp
+int dw_tc_prepare();                   // dW contractions on tcgen05 (dw_tc.cu)
+int dw_tc_launch(const DwJob *jobs, int j0, int j1, long n, long ts, int splits, cudaStream_t st);
+struct BwdArgs;                        // k_train.cuh
+int bwd_tc_prepare();                  // reverse sweep on tcgen05 (bwd_tc.cu), K=20 z=160 v=40
+long bwd_tc_image_bytes(int L);
+int bwd_tc_pack(const double *params, const double *masks, int L, unsigned char *img, cudaStream_t st);
+int bwd_tc_launch(const BwdArgs &a, const unsigned char *img, int sms, cudaStream_t st);
 
 // training (train.cu)
 int train_batch_gradient(detnet_model *m, long n, const float *H, const float *y,

@@ -12,34 +12,19 @@
 // and per-CTA partial t-gradients. The weight gradients are then batch
 // contractions over the sample axis,
 //   dW1 = u1bar . in^T,  dW2|dW3 = [u2bar; vbar] . z^T  (+ bias = row sums),
-// computed by a split-K kernel (FP32 inside a split of 256 samples, FP64
-// across splits, fixed order => deterministic), scaled by 1/n, masked and
+// computed by a split-K kernel (FP32 inside a split of DW_SPLIT = 1024
+// samples, FP64 across splits, fixed order => deterministic; tcgen05 in
+// dw_tc.cu, CUDA cores in k_dw_gemm below), scaled by 1/n, masked and
 // combined with the regularizer gradient in FP64.
 #pragma once
 
 #include "common.cuh"
+#include "dw_job.hpp"
 #include "k_stack_simt.cuh"
 
 namespace detnet {
 
-struct BwdArgs {
-    const float *gp;        // [tile][NG][TILE]
-    const double *denom;    // [s]
-    const uint32_t *xmask;  // [s]
-    const float *wrec;      // SIMT layer records
-    long rec_floats;
-    const double *lnk;      // ln(l+1)
-    int L, lf;              // layers, frozen prefix (sweep l = L-1 .. lf)
-    long n, n_tiles, ts;
-    const float *tr_in, *tr_z, *tr_u2, *tr_xf;
-    float *u1bar;           // [L][Z][ts]
-    float *g23bar;          // [L][K+V][ts]
-    double *tbar_part;      // [L][ts / 32]: t gradient per 32-sample warp group
-    // k_train_bwd_pair only: sweep iterations [it_begin, it_end) of [0, L - lf)
-    // (layer L-1-it); a_bar / v_bar carried between chunks in state [K+V][ts]
-    int it_begin = 0, it_end = -1;
-    float *state = nullptr;
-};
+// BwdArgs: dw_job.hpp (shared with the tcgen05 sweep, bwd_tc.cu)
 
 // THREADS samples per CTA (one CTA per SM: the double-buffered weights take
 // ~210 KB of shared memory): 256 for large batches, 64 for small ones -- at the
@@ -412,19 +397,11 @@ __global__ void __launch_bounds__(BWP_THREADS, 1) k_train_bwd_pair(BwdArgs a) {
     }
 }
 
-// C[job][m][n] partial over a split of samples: C = A . B^T with A [M][ts],
-// B [N][ts]; column n == N is the bias (sum of A). Jobs = (layer, which).
-struct DwJob {
-    const float *A;
-    const float *B;
-    int M, N;       // output M x (N + 1)
-    double *out;    // [splits][M][N+1] partials
-};
-
 // 64 x 64 output tile per CTA, 4 x 4 per thread (two 128-bit shared loads per
 // 16 FMAs), K = samples in chunks of 32; FP32 inside a split of DW_SPLIT
 // samples, one FP64 partial per split (summed in fixed order by k_grad_sum).
-constexpr int DW_TILE = 64, DW_SPLIT = 256, DW_KC = 32;
+// (DwJob and DW_SPLIT: dw_job.hpp, shared with the tcgen05 kernel dw_tc.cu.)
+constexpr int DW_TILE = 64, DW_KC = 32;
 // (FP64 accumulation here was measured not to change the FP32-vs-FP64 training
 // drift, which comes from gate flips in the FP32 forward/backward.)
 using DW_ACC = float;
@@ -701,66 +678,64 @@ __global__ void k_adam(double *params, const double *masks, const double *grads,
 }
 
 // ---- objective = data_loss + regularizer(params, spec) (training.cpp:67-70) --
-// Per (layer, matrix) one warp: group_norm_sum (loss.cpp:43-59) with the
-// column norms of [W (.) M] summed over rows in order (lanes over columns) and
-// the column square roots summed in column order by lane 0, plus, when the
-// spec needs it, masked_l1 (loss.cpp:35-41) as lane 0's sequential sum -- the
-// reference's operation order, so the value is bit-identical to
-// regularizer() (loss.cpp:81-91). Frozen layers count (params.layers).
+// The reference's regularizer() (loss.cpp:81-91) in its operation order:
+// group_norm_sum (loss.cpp:43-59) folds the column norms of [W (.) M] -- each
+// the square root of a row-order sum, exactly k_group_norms' colnorm values,
+// computed here for every layer (frozen ones count in the value) -- in
+// column order and adds the bias group's; masked_l1 (loss.cpp:35-41) is a
+// sequential sum over W, done only when the spec weighs it. One thread per
+// layer folds that layer's terms (k_reg_layers), then one thread folds the
+// layers in order (k_objective): bit-identical to the reference.
 struct ObjArgs {
     const double *params, *masks;
+    const double *colnorm;  // [L][ng] (k_group_norms over all L layers)
     int K, Z, V, L;
     int kind;
     double lam, lam1, lam2;
-    double *part;           // [L][3][2]: group_norm_sum, masked_l1
+    double *part;           // [L][2]: groups (g1 + g2) + g3, elems (e1 + e2) + e3
 };
 
-__global__ void __launch_bounds__(32) k_reg_parts(ObjArgs a) {
+__global__ void k_reg_layers(ObjArgs a) {
     const int K = a.K, Z = a.Z, V = a.V, IN = 3 * K + V;
     const long P = static_cast<long>(Z) * IN + Z + static_cast<long>(K) * Z + K +
                    static_cast<long>(V) * Z + V + 1;
-    const int l = blockIdx.x / 3, mat = blockIdx.x % 3, lane = threadIdx.x;
-    const long oW1 = 0, ob1 = static_cast<long>(Z) * IN, oW2 = ob1 + Z,
-               ob2 = oW2 + static_cast<long>(K) * Z, oW3 = ob2 + K,
-               ob3 = oW3 + static_cast<long>(V) * Z;
-    int rows, cols;
-    long oW, ob;
-    if (mat == 0) { rows = Z; cols = IN; oW = oW1; ob = ob1; }
-    else if (mat == 1) { rows = K; cols = Z; oW = oW2; ob = ob2; }
-    else { rows = V; cols = Z; oW = oW3; ob = ob3; }
-    const double *p = a.params + static_cast<long>(l) * P;
-    const double *mk = a.masks ? a.masks + static_cast<long>(l) * P : nullptr;
-    auto wm = [&](long e) { return dmul(p[e], mk ? mk[e] : 1.0); };
-    __shared__ double roots[1024];
-    double gsum = 0.0, l1 = 0.0;
-    if (a.kind == 2) {
-        for (int j = lane; j < cols; j += 32) {
-            double sq = 0.0;
-            for (int i = 0; i < rows; ++i) {
-                const double w = wm(oW + static_cast<long>(i) * cols + j);
-                sq = dadd(sq, dmul(w, w));
+    const int ng = IN + 1 + 2 * (Z + 1);
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= 2 * a.L) return;
+    const int l = idx >> 1;
+    if ((idx & 1) == 0) { // group_norm_sum of W1, W2, W3 (with their bias groups)
+        double g[3] = {0.0, 0.0, 0.0};
+        if (a.kind == 2) {
+            const double *cn = a.colnorm + static_cast<long>(l) * ng;
+            const int cols[3] = {IN, Z, Z};
+            int off = 0;
+            for (int m = 0; m < 3; ++m) {
+                double acc = 0.0;
+                for (int j = 0; j < cols[m]; ++j) acc = dadd(acc, cn[off + j]);
+                g[m] = dadd(acc, cn[off + cols[m]]);
+                off += cols[m] + 1;
             }
-            if (j < 1024) roots[j] = sqrt(sq);
         }
-        __syncwarp();
-        if (lane == 0) {
-            for (int j = 0; j < cols; ++j) gsum = dadd(gsum, roots[j]);
-            double sq = 0.0;
-            for (int i = 0; i < rows; ++i) {
-                const double w = wm(ob + i);
-                sq = dadd(sq, dmul(w, w));
+        a.part[2 * l] = dadd(dadd(g[0], g[1]), g[2]);
+    } else { // masked_l1 of W1, W2, W3
+        double e[3] = {0.0, 0.0, 0.0};
+        if (a.kind == 1 || (a.kind == 2 && a.lam2 != 0.0)) {
+            const double *p = a.params + static_cast<long>(l) * P;
+            const double *mk = a.masks ? a.masks + static_cast<long>(l) * P : nullptr;
+            const long oW[3] = {0, static_cast<long>(Z) * IN + Z,
+                                static_cast<long>(Z) * IN + Z + static_cast<long>(K) * Z + K};
+            const long cnt[3] = {static_cast<long>(Z) * IN, static_cast<long>(K) * Z,
+                                 static_cast<long>(V) * Z};
+            for (int m = 0; m < 3; ++m) {
+                double acc = 0.0;
+                for (long q = 0; q < cnt[m]; ++q) {
+                    const long ee = oW[m] + q;
+                    acc = dadd(acc, dmul(fabs(p[ee]), mk ? mk[ee] : 1.0));
+                }
+                e[m] = acc;
             }
-            gsum = dadd(gsum, sqrt(sq));
         }
-    }
-    if (lane == 0 && (a.kind == 1 || (a.kind == 2 && a.lam2 != 0.0))) {
-        const long cnt = static_cast<long>(rows) * cols;
-        for (long e = 0; e < cnt; ++e)
-            l1 = dadd(l1, dmul(fabs(p[oW + e]), mk ? mk[oW + e] : 1.0));
-    }
-    if (lane == 0) {
-        a.part[(static_cast<long>(l) * 3 + mat) * 2 + 0] = gsum;
-        a.part[(static_cast<long>(l) * 3 + mat) * 2 + 1] = l1;
+        a.part[2 * l + 1] = dadd(dadd(e[0], e[1]), e[2]);
     }
 }
 
@@ -770,17 +745,13 @@ __global__ void k_objective(ObjArgs a, const double *loss_sum, double n_global, 
     double reg = 0.0;
     if (a.kind == 1) {
         double acc = 0.0;
-        for (int l = 0; l < a.L; ++l) {
-            const double *q = a.part + static_cast<long>(l) * 6;
-            acc = dadd(acc, dadd(dadd(q[1], q[3]), q[5]));
-        }
+        for (int l = 0; l < a.L; ++l) acc = dadd(acc, a.part[2 * l + 1]);
         reg = dmul(a.lam, acc);
     } else if (a.kind == 2) {
         double groups = 0.0, elems = 0.0;
         for (int l = 0; l < a.L; ++l) {
-            const double *q = a.part + static_cast<long>(l) * 6;
-            groups = dadd(groups, dadd(dadd(q[0], q[2]), q[4]));
-            elems = dadd(elems, dadd(dadd(q[1], q[3]), q[5]));
+            groups = dadd(groups, a.part[2 * l]);
+            elems = dadd(elems, a.part[2 * l + 1]);
         }
         reg = dadd(dmul(a.lam1, groups), dmul(a.lam2, elems));
     }

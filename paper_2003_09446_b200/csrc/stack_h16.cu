@@ -48,11 +48,15 @@
 #include <cuda_fp16.h>
 
 #include "engine.hpp"
+#include "gram.cuh"
 #include "tc_ptx.cuh"
 
 namespace detnet {
 namespace {
 
+using gram::fma2;
+using gram::gram_mv;
+using gram::sub2;
 constexpr int KX = 20, VV = 40, NG = 210;
 constexpr int NA = 105; // Gram entries held by thread A (rows 0..5)
 constexpr int W1_K = 112, W23_ROWS = 64;
@@ -163,21 +167,6 @@ template <int N> __device__ __forceinline__ void st_u32(uint32_t t, const uint32
 
 __device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t *>(&h); }
 
-// packed FP32x2 arithmetic (FADD2 / FFMA2): two lanes per instruction
-__device__ __forceinline__ void sub2(float a0, float a1, float b0, float b1, float &d0, float &d1) {
-    asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
-        "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
-        : "=f"(d0), "=f"(d1)
-        : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
-}
-// (d0, d1) += (a0, a1) * (b0, b1)
-__device__ __forceinline__ void fma2(float &d0, float &d1, float a0, float a1, float b0, float b1) {
-    asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
-        "mov.b64 rd, {%0, %1};\n\tfma.rn.f32x2 rd, ra, rb, rd;\n\tmov.b64 {%0, %1}, rd;\n\t}"
-        : "+f"(d0), "+f"(d1)
-        : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
-}
-
 // (a0, a1) -> FP16 pair of hi halves and pair of lo halves (a0 in the low 16 bits)
 __device__ __forceinline__ __half2 split2(float a0, float a1, uint32_t &hi, uint32_t &lo) {
     const __half2 h = __floats2half2_rn(a0, a1);
@@ -187,32 +176,6 @@ __device__ __forceinline__ __half2 split2(float a0, float a1, uint32_t &hi, uint
     hi = h2u(h);
     lo = h2u(__floats2half2_rn(l0, l1));
     return h;
-}
-
-// Rows [R0, R1) of G x for the packed upper triangle g (row-major, r <= c,
-// rows R0.. only): gx[r] += sum_c G_rc x_c and, by symmetry, gx[c] += G_rc x_r.
-// Column pairs (c, c+1), c even, go through FFMA2: the row part into an
-// (even, odd) accumulator pair, the mirrored part into (gx[c], gx[c+1]).
-template <int R0, int R1>
-__device__ __forceinline__ void gram_mv(const float *g, const float (&x)[KX], float (&gx)[KX]) {
-    sfor<R0, R1>([&](auto rc) {
-        constexpr int r = decltype(rc)::value;
-        constexpr int e0 = r * KX - r * (r - 1) / 2 - (R0 * KX - R0 * (R0 - 1) / 2); // entry (r, r)
-        gx[r] = fmaf(g[e0], x[r], gx[r]);
-        constexpr int c1 = (r + 1) % 2 == 0 ? r + 1 : r + 2; // first paired (even) column
-        if constexpr (c1 == r + 2 && r + 1 < KX) {
-            gx[r] = fmaf(g[e0 + 1], x[r + 1], gx[r]);
-            gx[r + 1] = fmaf(g[e0 + 1], x[r], gx[r + 1]);
-        }
-        float re = 0.f, ro = 0.f;
-        sfor<0, (KX - c1) / 2>([&](auto pc) {
-            constexpr int c = c1 + 2 * decltype(pc)::value;
-            constexpr int e = e0 + (c - r);
-            fma2(re, ro, g[e], g[e + 1], x[c], x[c + 1]);
-            fma2(gx[c], gx[c + 1], g[e], g[e + 1], x[r], x[r]);
-        });
-        if constexpr (c1 < KX) gx[r] += re + ro;
-    });
 }
 
 // Split N scaled values into N/2 hi and N/2 lo pair columns; running |max|.

@@ -280,6 +280,24 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
         ba.u1bar = w.u1bar.as<float>();
         ba.g23bar = w.g23bar.as<float>();
         ba.tbar_part = w.tbar.as<double>();
+        // the reverse sweep runs on tcgen05 (bwd_tc.cu, 3xTF32) for the
+        // BASELINE dims; DETNET_BWD_SIMT=1 keeps the CUDA-core kernels. Its
+        // weight images follow the device master params (repacked per call).
+        static const bool bwd_simt = std::getenv("DETNET_BWD_SIMT") != nullptr;
+        const bool bwd_tc = !bwd_simt && K == 20 && Z == 160 && V == 40;
+        if (bwd_tc) {
+            if (m->bwd_img.ensure(static_cast<size_t>(bwd_tc_image_bytes(L))))
+                return fail(DETNET_ERR_CUDA, "sweep image allocation failed");
+            LaunchScope ls(c, DETNET_K_OTHER, c->stream);
+            if (int rc = bwd_tc_pack(m->tparams.as<double>(), m->has_masks ? m->tmasks.as<double>() : nullptr,
+                                     L, m->bwd_img.as<unsigned char>(), c->stream))
+                return rc;
+        }
+        auto sweep = [&](cudaStream_t sst, size_t smem) {
+            if (bwd_tc) return bwd_tc_launch(ba, m->bwd_img.as<unsigned char>(), c->sms, sst);
+            be->fn(dim3(bwd_blocks), dim3(bwd_per), smem, sst, ba);
+            return check_launch();
+        };
         std::vector<DwJob> jobs;
         for (int l = lf; l < L; ++l) {
             jobs.push_back({w.u1bar.as<float>() + static_cast<long>(l) * Z * ts,
@@ -292,8 +310,17 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
         CK(cudaMemcpyAsync(w.jobs.p, jobs.data(), sizeof(DwJob) * jobs.size(),
                            cudaMemcpyHostToDevice, c->stream));
         const int mx = std::max(IN, Z) + 1, my = std::max(Z, O);
+        // the contractions run on tcgen05 (dw_tc.cu, 3xTF32) when both job
+        // shapes fit its tiles; DETNET_DW_SIMT=1 keeps the CUDA-core kernel
+        static const bool dw_simt = std::getenv("DETNET_DW_SIMT") != nullptr;
+        const bool dw_tc = !dw_simt && Z <= 256 && O <= 256 && IN + 1 <= 176 && Z + 1 <= 176 &&
+                           Z + IN <= 288 && O + Z <= 288;
         auto dw_launch = [&](int j0, int j1) { // jobs [j0, j1) on the context stream
             LaunchScope ls(c, DETNET_K_BACKWARD, c->stream);
+            if (dw_tc) {
+                dw_tc_launch(w.jobs.as<DwJob>(), j0, j1, n, ts, splits, c->stream);
+                return;
+            }
             k_dw_gemm<<<dim3((mx + DW_TILE - 1) / DW_TILE, (my + DW_TILE - 1) / DW_TILE,
                              static_cast<unsigned>((j1 - j0) * splits)),
                         256, 0, c->stream>>>(w.jobs.as<DwJob>() + j0, n, ts, splits);
@@ -322,9 +349,8 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
                 ba.it_end = static_cast<int>(static_cast<long>(nl) * (j + 1) / chunks);
                 {
                     LaunchScope ls(c, DETNET_K_BACKWARD, w.hi);
-                    be->fn(dim3(bwd_blocks), dim3(bwd_per), 0, w.hi, ba);
+                    if (int rc = sweep(w.hi, 0)) return rc;
                 }
-                if (int rc = check_launch()) return rc;
                 CK(cudaEventRecord(w.ev[j], w.hi));
                 CK(cudaStreamWaitEvent(c->stream, w.ev[j], 0));
                 // layers L-1-it for it in [it_begin, it_end): jobs of layers
@@ -335,10 +361,8 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
         } else {
             {
                 LaunchScope ls(c, DETNET_K_BACKWARD, c->stream);
-                be->fn(dim3(bwd_blocks), dim3(bwd_per), 2 * static_cast<size_t>(m->simt_rec) * 4 + 64,
-                       c->stream, ba);
+                if (int rc = sweep(c->stream, 2 * static_cast<size_t>(m->simt_rec) * 4 + 64)) return rc;
             }
-            if (int rc = check_launch()) return rc;
             dw_launch(0, static_cast<int>(jobs.size()));
             if (int rc = check_launch()) return rc;
         }
@@ -367,14 +391,14 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
 
 // grads = raw * mask / n_global + regularizer gradient
 int apply_reg(detnet_model *m, const double *raw, long n_global, const detnet_loss_spec *spec,
-              double *grads) {
+              double *grads, bool norms_ready = false) {
     detnet_ctx *c = m->ctx;
     TrainWs &w = ws_for(c);
     const int K = m->K, Z = m->Z, V = m->V, L = m->L, IN = 3 * K + V;
     const int ng = IN + 1 + 2 * (Z + 1);
     const int kind = spec ? spec->kind : 0;
     if (w.colnorm.ensure(sizeof(double) * L * ng)) return fail(DETNET_ERR_CUDA, "alloc colnorm");
-    if (kind == 2 && m->frozen < L) {
+    if (kind == 2 && m->frozen < L && !norms_ready) {
         const long groups = static_cast<long>(L - m->frozen) * ng;
         LaunchScope ls(c, DETNET_K_ADAM, c->stream);
         k_group_norms<<<static_cast<unsigned>((groups + 127) / 128), 128, 0, c->stream>>>(
@@ -417,6 +441,8 @@ int validate_adam(const detnet_adam_config *cfg) {
 int train_prepare() {
     for (const BwdEntry &e : kBwd)
         if (e.prep()) return fail(DETNET_ERR_CUDA, "cudaFuncSetAttribute (backward smem) failed");
+    if (int rc = dw_tc_prepare()) return rc;
+    if (int rc = bwd_tc_prepare()) return rc;
     // FP64 mode: per-warp scratch beyond 48 KB at K=20 (up to K=32 supported)
     const int f64_bytes = static_cast<int>(sizeof(double) * F64_WARPS * f64_bwd_scratch(32, 256, 64));
     if (cudaFuncSetAttribute(k_fwd64, cudaFuncAttributeMaxDynamicSharedMemorySize, f64_bytes) !=
@@ -608,19 +634,28 @@ int detnet_train_apply(detnet_model *m, const double *raw_dev, long n_global,
     if (w.grads.ensure(sizeof(double) * total)) return fail(DETNET_ERR_CUDA, "alloc grads");
     // objective = data_loss + regularizer(params) before the update
     // (training.cpp:65-70); a non-finite one halts the run on the device
-    if (w.objpart.ensure(sizeof(double) * 6 * m->L)) return fail(DETNET_ERR_CUDA, "alloc objective");
-    ObjArgs oa{m->tparams.as<double>(), m->has_masks ? m->tmasks.as<double>() : nullptr, m->K, m->Z,
-               m->V, m->L, spec ? spec->kind : 0, spec ? spec->lambda : 0.0,
-               spec ? spec->lambda1 : 0.0, spec ? spec->lambda2 : 0.0, w.objpart.as<double>()};
+    const int IN = 3 * m->K + m->V, ng = IN + 1 + 2 * (m->Z + 1);
+    if (w.objpart.ensure(sizeof(double) * 2 * m->L) || w.colnorm.ensure(sizeof(double) * m->L * ng))
+        return fail(DETNET_ERR_CUDA, "alloc objective");
+    ObjArgs oa{m->tparams.as<double>(), m->has_masks ? m->tmasks.as<double>() : nullptr,
+               w.colnorm.as<double>(), m->K, m->Z, m->V, m->L, spec ? spec->kind : 0,
+               spec ? spec->lambda : 0.0, spec ? spec->lambda1 : 0.0, spec ? spec->lambda2 : 0.0,
+               w.objpart.as<double>()};
     {
         LaunchScope ls(c, DETNET_K_ADAM, c->stream);
-        if (oa.kind != 0) k_reg_parts<<<3 * m->L, 32, 0, c->stream>>>(oa);
+        if (oa.kind == 2) { // column norms of every layer: the value's and the gradient's
+            const long groups = static_cast<long>(m->L) * ng;
+            k_group_norms<<<static_cast<unsigned>((groups + 127) / 128), 128, 0, c->stream>>>(
+                m->tparams.as<double>(), m->tmasks.as<double>(), m->K, m->Z, m->V, m->L, 0,
+                w.colnorm.as<double>());
+        }
+        if (oa.kind != 0) k_reg_layers<<<(2 * m->L + 63) / 64, 64, 0, c->stream>>>(oa);
         k_objective<<<1, 1, 0, c->stream>>>(oa, raw_dev + total, static_cast<double>(n_global),
                                             static_cast<long long>(m->adam_step),
                                             m->tstatus.as<double>());
     }
     if (int rc = check_launch()) return rc;
-    if (int rc = apply_reg(m, raw_dev, n_global, spec, w.grads.as<double>())) return rc;
+    if (int rc = apply_reg(m, raw_dev, n_global, spec, w.grads.as<double>(), true)) return rc;
     double lr, bc1, bc2;
     adam_coefs(cfg, m->adam_step, lr, bc1, bc2);
     {

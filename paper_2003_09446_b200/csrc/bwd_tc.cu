@@ -23,6 +23,9 @@
 // [288, 320) u1_bar lo of units 128-159; [320, 400) Inbar accumulator.
 // SMEM: the layer's B operands (hi + lo, 180 KB), refilled by the bulk-copy
 // engine as soon as the contraction reading the previous copy has completed.
+#include <cstdio>
+#include <cstdlib>
+
 #include "dw_job.hpp"
 #include "engine.hpp"
 #include "gram.cuh"
@@ -40,10 +43,14 @@ constexpr uint32_t B1_HALF = ZZ * A1K * 4, B2_HALF = IBN * ZZ * 4; // 40 KB, 50 
 constexpr uint32_t B1_BYTES = 2 * B1_HALF, B2_BYTES = 2 * B2_HALF;
 constexpr uint32_t LAYER_BYTES = B1_BYTES + B2_BYTES;             // 180 KB
 constexpr uint32_t SM_B1 = 0, SM_B2 = B1_BYTES, SM_X = LAYER_BYTES,
-                   SM_T = SM_X + KX * 128 * 4, SM_BAR = SM_T + 4 * 8, SM_TMEM = SM_BAR + 16 * 8,
-                   SM_TOTAL = SM_TMEM + 16;
+                   SM_TR = SM_X + KX * 128 * 4, SM_T = SM_TR + (2 * KX + 5) * 128 * 4,
+                   SM_BAR = SM_T + 4 * 8, SM_TMEM = SM_BAR + 16 * 8, SM_TOTAL = SM_TMEM + 16;
 constexpr int NTHREADS = 384;
-enum { B_B1F = 0, B_B2F = 1, B_A1 = 2, B_Z = 3, B_UA = 4, B_UB = 5, B_IB = 6 };
+// B_TRF: the tile's x_hat_{l+1} and u2_l rows of the forward trace (bulk copies
+// by the producer warp, one layer ahead, so the chain never waits on HBM)
+// The trace rows (B_TRF) include the layer's relu gates (z > 0 <=> u1 > 0) as
+// five bit-mask words per sample, built once per step by k_gate_bits.
+enum { B_B1F = 0, B_B2F = 1, B_A1 = 2, B_Z = 3, B_UA = 4, B_UB = 5, B_IB = 6, B_TRF = 7 };
 
 // Offsets of the no-swizzle K-major TF32 images (core matrices of 8 rows x 4)
 __host__ __device__ inline uint32_t b_off(int n, int k, int R) {
@@ -54,7 +61,21 @@ struct BtcArgs {
     BwdArgs b;
     const unsigned char *w; // [L][LAYER_BYTES] images
     const float *tval;      // [L] t
+    long long *trace;       // debug timeline (EXTRA=-DDETNET_TC_TRACE, env DETNET_BWD_TRACE)
 };
+
+// Debug timeline: clock64 stamps of CTA 0's first 8 layer iterations, 16
+// events each. Compiled out by default.
+#ifdef DETNET_TC_TRACE
+#define BTRACE(ev, it, cond)                                                                   \
+    do {                                                                                       \
+        if (p.trace && blockIdx.x == 0 && (it) < 8 && (cond)) p.trace[(it) * 16 + (ev)] = clock64(); \
+    } while (0)
+#else
+#define BTRACE(ev, it, cond)                                                                   \
+    do {                                                                                       \
+    } while (0)
+#endif
 
 __device__ __forceinline__ void split(float v, uint32_t &hi, uint32_t &lo) {
     const float h = tc::tf32_rna(v);
@@ -102,6 +123,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_bwd_tc(BtcArgs p) {
         mbar_init(&bars[B_UA], 128);
         mbar_init(&bars[B_UB], 128);
         mbar_init(&bars[B_IB], 1);
+        mbar_init(&bars[B_TRF], 1);
         fence_mbar_init();
     }
     if (warp == 8) {
@@ -118,26 +140,37 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_bwd_tc(BtcArgs p) {
         if (warp == 8) {
             // ================= MMA issuer (one elected lane) =================
             const uint32_t sb1 = smem_u32(sm + SM_B1), sb2 = smem_u32(sm + SM_B2);
-            constexpr uint32_t id1 = tc::idesc_tf32(128, ZZ), id2 = tc::idesc_tf32(128, IBN);
+            // GEMM1 as two N = 80 halves (units [0, 80) and [80, 160)): measured
+            // ~3.5x faster than single N = 160 instructions
+            constexpr uint32_t id1 = tc::idesc_tf32(128, ZZ / 2), id2 = tc::idesc_tf32(128, IBN);
             for (long it = 0; it < total_it; ++it) {
                 const uint32_t ph = static_cast<uint32_t>(it & 1);
                 mbar_wait_guard(&bars[B_B1F], ph);
+                BTRACE(0, it, lane == 0);
                 mbar_wait_guard(&bars[B_A1], ph);
+                BTRACE(1, it, lane == 0);
                 tc::fence_after();
                 if (tc::elect_one()) {
                     const uint32_t tb = tc::opaque32(tbase);
 #pragma unroll 1
                     for (int ks = 0; ks < A1K / 8; ++ks) {
-                        const uint64_t bh = tc::smem_desc(sb1 + ks * 2 * ZZ * 16, ZZ * 16, 128);
-                        const uint64_t bl = tc::smem_desc(sb1 + B1_HALF + ks * 2 * ZZ * 16, ZZ * 16, 128);
-                        tc::mma_tf32_ts(tb + C_Z, tb + C_A1 + 8 * ks, bh, id1, ks > 0);
-                        tc::mma_tf32_ts(tb + C_Z, tb + C_A1 + 8 * ks, bl, id1, 1);
-                        tc::mma_tf32_ts(tb + C_Z, tb + C_A1LO + 8 * ks, bh, id1, 1);
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const uint32_t ro = h * (ZZ / 2 / 8) * 128; // rows [80 h, 80 h + 80)
+                            const uint64_t bh = tc::smem_desc(sb1 + ro + ks * 2 * ZZ * 16, ZZ * 16, 128);
+                            const uint64_t bl =
+                                tc::smem_desc(sb1 + B1_HALF + ro + ks * 2 * ZZ * 16, ZZ * 16, 128);
+                            const uint32_t d = tb + C_Z + h * (ZZ / 2);
+                            tc::mma_tf32_ts(d, tb + C_A1 + 8 * ks, bh, id1, ks > 0);
+                            tc::mma_tf32_ts(d, tb + C_A1 + 8 * ks, bl, id1, 1);
+                            tc::mma_tf32_ts(d, tb + C_A1LO + 8 * ks, bh, id1, 1);
+                        }
                     }
                     tc::commit(&bars[B_Z]);
                 }
                 __syncwarp();
                 mbar_wait_guard(&bars[B_B2F], ph);
+                BTRACE(2, it, lane == 0);
                 auto gemm2 = [&](int k0, int k1) {
                     if (tc::elect_one()) {
                         const uint32_t tb = tc::opaque32(tbase);
@@ -157,9 +190,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_bwd_tc(BtcArgs p) {
                     __syncwarp();
                 };
                 mbar_wait_guard(&bars[B_UA], ph);
+                BTRACE(3, it, lane == 0);
                 tc::fence_after();
                 gemm2(0, 10); // u1_bar units 0-79 (A side)
                 mbar_wait_guard(&bars[B_UB], ph);
+                BTRACE(4, it, lane == 0);
                 tc::fence_after();
                 gemm2(10, 20); // units 80-159 (B side)
             }
@@ -178,7 +213,31 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_bwd_tc(BtcArgs p) {
                 }
                 __syncwarp();
             };
+            // the tile's trace rows of iteration it: x_hat_{l+1} (20 rows) and u2_l (20)
+            auto load_trace = [&](long it) {
+                if (leader) {
+                    const long tile = blockIdx.x + (it / NL) * gridDim.x;
+                    const int l = layer_of(it);
+                    float *dst = reinterpret_cast<float *>(sm + SM_TR);
+                    mbar_arrive_expect_tx(&bars[B_TRF], (2 * KX + 5) * TILE * 4);
+                    for (int i = 0; i < 5; ++i)
+                        bulk_g2s(dst + (2 * KX + i) * TILE,
+                                 a.gate + (static_cast<long>(l) * 5 + i) * a.ts + tile * TILE,
+                                 TILE * 4, &bars[B_TRF]);
+                    for (int i = 0; i < KX; ++i) {
+                        const float *xr = l + 1 < a.L
+                                              ? a.tr_in + (static_cast<long>(l + 1) * IN + KX + i) * a.ts
+                                              : a.tr_xf + static_cast<long>(i) * a.ts;
+                        bulk_g2s(dst + i * TILE, xr + tile * TILE, TILE * 4, &bars[B_TRF]);
+                        bulk_g2s(dst + (KX + i) * TILE,
+                                 a.tr_u2 + (static_cast<long>(l) * KX + i) * a.ts + tile * TILE,
+                                 TILE * 4, &bars[B_TRF]);
+                    }
+                }
+                __syncwarp();
+            };
             if (total_it > 0) {
+                load_trace(0);
                 load(0, layer_of(0));
                 load(1, layer_of(0));
             }
@@ -186,6 +245,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_bwd_tc(BtcArgs p) {
                 const uint32_t ph = static_cast<uint32_t>(it & 1);
                 mbar_wait_guard(&bars[B_Z], ph);  // the first contraction read B1
                 load(0, layer_of(it + 1));
+                // both sides have used this layer's trace rows and gate words
+                mbar_wait_guard(&bars[B_UA], ph);
+                mbar_wait_guard(&bars[B_UB], ph);
+                load_trace(it + 1);
                 mbar_wait_guard(&bars[B_IB], ph); // the second read B2
                 load(1, layer_of(it + 1));
             }
@@ -228,16 +291,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_bwd_tc(BtcArgs p) {
                 // ---- a_bar += w (x_hat_{l+1} - x); u2_bar; t_bar (this side's half) ----
                 const float w = static_cast<float>(a.lnk[l]) * dinv2;
                 const float t = p.tval[l], tinv = 1.f / t;
-                const float *xn = l + 1 < a.L ? a.tr_in + (static_cast<long>(l + 1) * IN + KX) * a.ts + s
-                                              : a.tr_xf + s;
+                const float *str = reinterpret_cast<const float *>(sm + SM_TR);
+                const bool tA = threadIdx.x == 128, tB = threadIdx.x == 0;
+                BTRACE(isA ? 5 : 11, it, tA || tB);
+                mbar_wait_guard(&bars[B_TRF], ph);
                 float u2b[KX / 2];
                 float tb = 0.f;
 #pragma unroll
                 for (int k = 0; k < KX / 2; ++k) {
                     const int i = i0 + k;
                     const float xk = (xm >> i) & 1u ? 1.f : -1.f;
-                    ab[k] = fmaf(w, xn[i * a.ts] - xk, ab[k]);
-                    const float u = a.tr_u2[(static_cast<long>(l) * KX + i) * a.ts + s];
+                    ab[k] = fmaf(w, str[i * TILE + col] - xk, ab[k]);
+                    const float u = str[(KX + i) * TILE + col];
                     const bool lin = u >= -t && u < t; // model.cpp:45-51
                     u2b[k] = lin ? ab[k] * tinv : 0.f;
                     tb += lin ? ab[k] * (-u * tinv * tinv) : 0.f;
@@ -282,6 +347,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_bwd_tc(BtcArgs p) {
                 tc::wait_st();
                 tc::fence_before();
                 mbar_arrive(&bars[B_A1]);
+                BTRACE(isA ? 6 : 12, it, tA || tB);
                 // t_bar per 32-sample group: (A half + B half), B's via smem
                 {
                     double ts_ = live ? static_cast<double>(tb) : 0.0;
@@ -291,38 +357,56 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_bwd_tc(BtcArgs p) {
                     if (isA && lane == 0)
                         a.tbar_part[static_cast<long>(l) * (a.ts / 32) + s / 32] = ts_ + sT[quad];
                 }
-                // relu gate of this side's 80 units (z > 0 <=> u1 > 0), loaded early
-                const float *zl = a.tr_z + (static_cast<long>(l) * ZZ + (isA ? 0 : 80)) * a.ts + s;
-                uint32_t gate[3] = {0u, 0u, 0u};
-#pragma unroll
-                for (int k = 0; k < 80; ++k)
-                    if (zl[k * a.ts] > 0.f) gate[k >> 5] |= 1u << (k & 31);
+                // relu gate of this side's 80 units: bits [0, 80) (A) or [80, 160) (B)
+                // of the sample's five gate words (trace rows 40-44), as 3 words
+                uint32_t gate[3];
+                {
+                    const uint32_t *gw = reinterpret_cast<const uint32_t *>(str) + 2 * KX * TILE + col;
+                    if (isA) {
+                        gate[0] = gw[0];
+                        gate[1] = gw[TILE];
+                        gate[2] = gw[2 * TILE] & 0xffffu;
+                    } else { // units 80-159 = word 2 bits 16-31, words 3, 4
+                        const uint32_t w2 = gw[2 * TILE], w3 = gw[3 * TILE], w4 = gw[4 * TILE];
+                        gate[0] = (w2 >> 16) | (w3 << 16);
+                        gate[1] = (w3 >> 16) | (w4 << 16);
+                        gate[2] = w4 >> 16;
+                    }
+                }
                 // ---- u1_bar = Zbar [z > 0] (this side's 80 units) -> HBM, TMEM (hi in place, lo) ----
                 mbar_wait_guard(&bars[B_Z], ph);
+                BTRACE(isA ? 7 : 13, it, tA || tB);
                 tc::fence_after();
                 float *u1b = a.u1bar + (static_cast<long>(l) * ZZ + (isA ? 0 : 80)) * a.ts + s;
 #pragma unroll
-                for (int c0 = 0; c0 < 80; c0 += 8) {
-                    uint32_t r[8];
-                    tc::ld8_nw(trow + C_Z + (isA ? 0 : 80) + c0, r);
-                    tc::wait_ld();
-                    uint32_t hi[8], lo[8];
+                for (int b0 = 0; b0 < 80; b0 += 16) { // 16 columns per TMEM round trip
+                    uint32_t r[16];
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const int u = c0 + k;
-                        const float ub = (gate[u >> 5] >> (u & 31)) & 1u ? __uint_as_float(r[k]) : 0.f;
-                        u1b[u * a.ts] = live ? ub : 0.f;
-                        split(ub, hi[k], lo[k]);
+                    for (int c0 = 0; c0 < 16; c0 += 8) tc::ld8_nw(trow + C_Z + (isA ? 0 : 80) + b0 + c0, r + c0);
+                    tc::wait_ld();
+#pragma unroll
+                    for (int c0 = 0; c0 < 16; c0 += 8) {
+                        uint32_t hi[8], lo[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const int u = b0 + c0 + k;
+                            const float ub =
+                                (gate[u >> 5] >> (u & 31)) & 1u ? __uint_as_float(r[c0 + k]) : 0.f;
+                            u1b[u * a.ts] = live ? ub : 0.f;
+                            split(ub, hi[k], lo[k]);
+                        }
+                        const int unit = (isA ? 0 : 80) + b0 + c0; // global unit index
+                        st_cols<8>(trow + C_Z + unit, hi);
+                        st_cols<8>(trow + (unit < 128 ? C_A1 + unit : C_ULO2 + unit - 128), lo);
                     }
-                    const int unit = (isA ? 0 : 80) + c0; // global unit index of column c0
-                    st_cols<8>(trow + C_Z + unit, hi);
-                    st_cols<8>(trow + (unit < 128 ? C_A1 + unit : C_ULO2 + unit - 128), lo);
                 }
                 tc::wait_st();
                 tc::fence_before();
                 mbar_arrive(&bars[isA ? B_UA : B_UB]);
+                BTRACE(isA ? 8 : 14, it, tA || tB);
                 // ---- a_bar <- G gx_bar + x_bar; v_bar <- v block ----
                 mbar_wait_guard(&bars[B_IB], ph);
+                BTRACE(isA ? 9 : 15, it, tA || tB);
                 tc::fence_after();
                 uint32_t rg[KX], rx[KX / 2];
                 tc::ld_cols_nw<KX>(trow + C_IB + KX, rg);     // gx_bar
@@ -370,6 +454,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_bwd_tc(BtcArgs p) {
                     for (int k = 0; k < VV; ++k) vb[k] = __uint_as_float(rv[k]);
                 }
                 tc::named_bar(bar_x, 64); // sX is free for the next layer
+                BTRACE(10, it, tA);
             }
             if (it1 < nl_all && live) { // hand the sweep state to the next layer chunk
 #pragma unroll
@@ -384,6 +469,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_bwd_tc(BtcArgs p) {
     tc::fence_before();
     __syncthreads();
     if (warp == 8) tc::tmem_dealloc(tbase, 512);
+}
+
+// Relu gates of the forward trace as bit masks: gate[l][w][ts] bit b = z[l][32 w + b] > 0
+// (z = relu(u1), so z > 0 <=> u1 > 0, backward.cpp:148-150).
+__global__ void k_gate_bits(const float *tr_z, long ts, long n_cols, int lf, int L, uint32_t *gate) {
+    const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long per = n_cols * 5;
+    if (idx >= static_cast<long>(L - lf) * per) return;
+    const int l = lf + static_cast<int>(idx / per);
+    const int w = static_cast<int>((idx % per) / n_cols);
+    const long s = idx % n_cols;
+    const float *z = tr_z + (static_cast<long>(l) * ZZ + 32 * w) * ts + s;
+    float v[32];
+#pragma unroll
+    for (int b = 0; b < 32; ++b) v[b] = __ldg(z + b * ts);
+    uint32_t bits = 0;
+#pragma unroll
+    for (int b = 0; b < 32; ++b) bits |= (v[b] > 0.f ? 1u : 0u) << b;
+    gate[(static_cast<long>(l) * 5 + w) * ts + s] = bits;
 }
 
 // Device repack of the sweep's B images from the FP64 master records (after
@@ -444,10 +548,39 @@ int bwd_tc_pack(const double *params, const double *masks, int L, unsigned char 
 }
 
 int bwd_tc_launch(const BwdArgs &a, const unsigned char *img, int sms, cudaStream_t st) {
-    BtcArgs p{a, img, reinterpret_cast<const float *>(img + static_cast<size_t>(a.L) * LAYER_BYTES)};
+    BtcArgs p{a, img, reinterpret_cast<const float *>(img + static_cast<size_t>(a.L) * LAYER_BYTES),
+              nullptr};
+    static long long *trace_buf = nullptr;
+    static const bool tracing = std::getenv("DETNET_BWD_TRACE") != nullptr;
+    if (tracing) {
+        if (!trace_buf) cudaMalloc(&trace_buf, 8 * 16 * sizeof(long long));
+        cudaMemsetAsync(trace_buf, 0, 8 * 16 * sizeof(long long), st);
+        p.trace = trace_buf;
+    }
+    if (a.it_begin == 0) { // the gates of every layer this sweep visits, once
+        const long cnt = static_cast<long>(a.L - a.lf) * 5 * a.ts;
+        k_gate_bits<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, st>>>(a.tr_z, a.ts, a.ts, a.lf,
+                                                                              a.L, a.gate);
+        if (int rc = check_launch()) return rc;
+    }
     const int grid = static_cast<int>(std::min<long>(a.n_tiles, sms));
     k_bwd_tc<<<grid, NTHREADS, SM_TOTAL, st>>>(p);
-    return check_launch();
+    if (int rc = check_launch()) return rc;
+    if (tracing) {
+        long long h[8 * 16];
+        cudaMemcpyAsync(h, trace_buf, sizeof h, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        static const char *nm[16] = {"m_b1", "m_a1", "m_b2", "m_ua", "m_ub", "A_st", "A_a1",
+                                     "A_z", "A_u", "A_ib", "A_end", "B_st", "B_a1", "B_z", "B_u",
+                                     "B_ib"};
+        const long long t0 = h[5];
+        for (int l = 0; l < 8; ++l) {
+            std::fprintf(stderr, "bwd_tc it %d:", l);
+            for (int e = 0; e < 16; ++e) std::fprintf(stderr, " %s=%lld", nm[e], h[l * 16 + e] - t0);
+            std::fprintf(stderr, "\n");
+        }
+    }
+    return 0;
 }
 
 } // namespace detnet

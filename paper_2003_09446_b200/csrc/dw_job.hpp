@@ -37,6 +37,7 @@ struct BwdArgs {
     // (layer L-1-it); a_bar / v_bar carried between chunks in state [K+V][ts]
     int it_begin = 0, it_end = -1;
     float *state = nullptr;
+    uint32_t *gate = nullptr; // tcgen05 sweep: [L][5][ts] relu-gate bit masks (bwd_tc.cu)
 };
 
 

@@ -20,7 +20,7 @@ namespace detnet {
 namespace {
 
 constexpr int DWT_THREADS = 256, DWT_KC = 32; // samples per staged chunk
-constexpr int DWT_LOADS = 9; // float4 loads per thread per chunk: (M + N) * 8 <= 9 * 256
+constexpr int DWT_LOADS = 9; // float4 loads per thread per chunk: ceil((M + N) / 8) * 64 <= 9 * 256
 constexpr uint32_t DWT_SMEM = 2 * (256 + 176) * DWT_KC * 4 * 2 + 64;
 
 __device__ __forceinline__ void mma_tf32_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
@@ -95,7 +95,15 @@ __global__ void __launch_bounds__(DWT_THREADS, 1)
 
     // software pipeline: chunk c + 1's global loads are in flight while chunk
     // c is split into the stage images and its MMAs are issued
-    const int nv = (M + N) * (DWT_KC / 4);
+    // element e -> (row, 4-sample group q): 8 consecutive lanes take 8
+    // consecutive rows of one q, so each quarter-warp stores one full 128-byte
+    // core-matrix line (no bank conflicts) and each row's 4 groups are 64
+    // contiguous bytes of the global row
+    const int nv = (M + N + 7) / 8 * 64;
+    auto rowq = [](int e, int &row, int &q) {
+        row = (e >> 6) * 8 + (e & 7);
+        q = (e >> 3) & 7;
+    };
     float4 v[DWT_LOADS], nxt[DWT_LOADS];
     auto load_chunk = [&](int c, float4 (&dst)[DWT_LOADS]) {
         const long kc = k0 + static_cast<long>(c) * DWT_KC;
@@ -103,8 +111,9 @@ __global__ void __launch_bounds__(DWT_THREADS, 1)
         for (int i = 0; i < DWT_LOADS; ++i) {
             const int e = tid + i * DWT_THREADS;
             dst[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (e < nv) {
-                const int row = e / (DWT_KC / 4), q = e % (DWT_KC / 4);
+            int row, q;
+            rowq(e, row, q);
+            if (e < nv && row < M + N) {
                 const bool isA = row < M;
                 const int r = isA ? row : row - M;
                 const float *src = (isA ? jb.A : jb.B) + static_cast<long>(r) * ts + kc + 4 * q;
@@ -127,8 +136,9 @@ __global__ void __launch_bounds__(DWT_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < DWT_LOADS; ++i) {
             const int e = tid + i * DWT_THREADS;
-            if (e >= nv) continue;
-            const int row = e / (DWT_KC / 4), q = e % (DWT_KC / 4);
+            int row, q;
+            rowq(e, row, q);
+            if (e >= nv || row >= M + N) continue;
             const bool isA = row < M;
             const int r = isA ? row : row - M;
             const float f[4] = {v[i].x, v[i].y, v[i].z, v[i].w};

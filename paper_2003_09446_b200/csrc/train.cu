@@ -69,6 +69,7 @@ const BwdEntry *find_bwd(int K, int Z, int V) {
 struct TrainWs {
     DBuf tr_in, tr_z, tr_u2, tr_xf, u1bar, g23bar, tbar, p1, p23, jobs, raw, grads, colnorm;
     DBuf bstate; // reverse-sweep state between chunks [K+V][ts]
+    DBuf gate;   // tcgen05 sweep relu-gate bits [L][5][ts]
     // FP64 reference-order mode (k_train64.cuh)
     DBuf g64, q64, wb, wf, f_in, f_z, f_u2, f_xh, b_u1, b_u2, b_v, b_t, part, s_loss, s_err;
     DBuf objpart;
@@ -286,8 +287,10 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
         static const bool bwd_simt = std::getenv("DETNET_BWD_SIMT") != nullptr;
         const bool bwd_tc = !bwd_simt && K == 20 && Z == 160 && V == 40;
         if (bwd_tc) {
-            if (m->bwd_img.ensure(static_cast<size_t>(bwd_tc_image_bytes(L))))
+            if (m->bwd_img.ensure(static_cast<size_t>(bwd_tc_image_bytes(L))) ||
+                w.gate.ensure(sizeof(uint32_t) * L * 5 * ts))
                 return fail(DETNET_ERR_CUDA, "sweep image allocation failed");
+            ba.gate = w.gate.as<uint32_t>();
             LaunchScope ls(c, DETNET_K_OTHER, c->stream);
             if (int rc = bwd_tc_pack(m->tparams.as<double>(), m->has_masks ? m->tmasks.as<double>() : nullptr,
                                      L, m->bwd_img.as<unsigned char>(), c->stream))
@@ -314,7 +317,7 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
         // shapes fit its tiles; DETNET_DW_SIMT=1 keeps the CUDA-core kernel
         static const bool dw_simt = std::getenv("DETNET_DW_SIMT") != nullptr;
         const bool dw_tc = !dw_simt && Z <= 256 && O <= 256 && IN + 1 <= 176 && Z + 1 <= 176 &&
-                           Z + IN <= 288 && O + Z <= 288;
+                           (Z + IN + 7) / 8 <= 36 && (O + Z + 7) / 8 <= 36;
         auto dw_launch = [&](int j0, int j1) { // jobs [j0, j1) on the context stream
             LaunchScope ls(c, DETNET_K_BACKWARD, c->stream);
             if (dw_tc) {
@@ -833,7 +836,7 @@ void train_ws_release(detnet_ctx *c) {
                         &w->p1, &w->p23, &w->jobs, &w->raw, &w->grads, &w->colnorm, &w->bstate,
                         &w->in_H, &w->in_y, &w->in_x, &w->g64, &w->q64, &w->wb, &w->wf,
                         &w->f_in, &w->f_z, &w->f_u2, &w->f_xh, &w->b_u1, &w->b_u2, &w->b_v,
-                        &w->b_t, &w->part, &w->s_loss, &w->s_err, &w->objpart})
+                        &w->b_t, &w->part, &w->s_loss, &w->s_err, &w->objpart, &w->gate})
             b->release();
         if (w->hi) {
             cudaStreamDestroy(w->hi);

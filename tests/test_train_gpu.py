@@ -200,3 +200,62 @@ def test_overlapped_sweep_bit_identical(tmp_path, K, N, L, n):
         assert r.returncode == 0, r.stderr
         outs.append(np.load(f))
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("tc_forward", [False, True])
+def test_fp32_training_config5_shape_within_fp32_spread(oracle, ref, tc_forward):
+    """Config-5 shape (L=40, batch 5000, 100 Adam steps, group LASSO 1e-4)
+    from the seeds of the reference trajectories in tests/golden/
+    train_ref_k20_l40.json. FP32's own distance from the FP64 reference after
+    100 steps is measured by O32 -- the FP32 restatement of the reference's
+    algorithm (oracle/detnet_oracle.c) -- over six seeds
+    (tools/train_reference_runs.py -> profiles/r2_train_spread.json: median
+    ~1e-2, max ~6e-2 in final validation loss): the trajectory is chaotic, so
+    no FP32 implementation meets the north star's 1e-3 here (the FP64 mode
+    does, at 0: test_train64_gpu.py). The FP32 GPU runs must stay inside that
+    measured FP32 band: each final validation loss (the reference evaluating
+    both final models on the same 2,000 samples) within 1.5x O32's largest
+    distance, the median within 3x O32's median; step 0 (identical weights)
+    agrees to 1e-6."""
+    import ctypes as Cc
+    import json
+
+    import torch
+    from paper_2003_09446_b200 import Context
+    from paper_2003_09446_b200.workload import xavier_params
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    gold = json.load(open(os.path.join(root, "tests", "golden", "train_ref_k20_l40.json")))
+    spread = json.load(open(os.path.join(root, "profiles", "r2_train_spread.json")))
+    K, N = 20, 30
+    ctx = Context(0)
+    ctx.set_train_forward(tc_forward)
+    finals = []
+    for run in gold["runs"]:
+        L, n, steps = run["layers"], run["batch"], run["steps"]
+        params = xavier_params(K, L, seed=run["pseed"])
+        m = ctx.model(K, N, 8 * K, 2 * K, params)
+        raw = m.new_raw()
+        train = oracle.lib.or_stream(Cc.byref(oracle.rng(run["dseed"], 0)), 2)
+        first = None
+        for step in range(steps):
+            H, x, y, _ = oracle.generate_batch(train, N, K, n, 7.0, 14.0)
+            Hd = torch.from_numpy((H / np.sqrt(N)).astype(np.float32)).cuda()
+            yd = torch.from_numpy((y / np.sqrt(N)).astype(np.float32)).cuda()
+            xd = torch.from_numpy(x.astype(np.int8)).cuda()
+            ev = m.train_grad(n, Hd, yd, xd, raw, want_eval=step == 0)
+            if step == 0:
+                first = ev.data_loss
+            m.train_apply(raw, n, kind=2, lam1=1e-4, lr0=1e-3)
+        assert abs(first - run["data_loss"][0]) <= 1e-6 * run["data_loss"][0]
+        val = oracle.lib.or_stream(Cc.byref(oracle.rng(run["dseed"], 0)), 3)
+        Hv, xv, yv, _ = oracle.generate_batch(val, N, K, 2000, 12.0, 12.0)
+        Hv = (Hv / np.sqrt(N)).astype(np.float32).astype(np.float64)
+        yv = (yv / np.sqrt(N)).astype(np.float32).astype(np.float64)
+        vg = ref.batch_evaluate(OModel(K, N, 8 * K, 2 * K, L, m.get_params()), Hv, yv, xv)["data_loss"]
+        finals.append(abs(vg - run["val_loss_final"]) / run["val_loss_final"])
+    med = float(np.median(finals))
+    print(f"FP32 GPU (tc forward {tc_forward}) vs reference after 100 config-5 steps: final "
+          f"validation loss rel {finals}, median {med:.3e}; O32 median {spread['median']:.3e} "
+          f"max {spread['max']:.3e}")
+    assert max(finals) <= 1.5 * spread["max"], finals
+    assert med <= 3.0 * spread["median"], finals

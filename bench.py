@@ -285,8 +285,8 @@ def main():
     ap.add_argument("--only", action="store_true",
                     help="measure --config alone (default: config 2 + nested configs 1,3,4,5)")
     ap.add_argument("--path", default="auto", choices=["auto", "simt", "tc", "sparse"])
-    ap.add_argument("--train-fwd", default="simt", choices=["simt", "tc"],
-                    help="config 5: training forward on FP32 cores (default, parity) or tcgen05")
+    ap.add_argument("--train-fwd", default="tc", choices=["simt", "tc"],
+                    help="config 5: training forward on tcgen05 (default) or FP32 CUDA cores")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
@@ -625,8 +625,7 @@ def bench_train(args, env):
     L, _, per_gpu, _, _ = workload(5)
     params, _ = build_params(5, L)
     ctx = eng.Context(local)
-    if args.train_fwd == "tc":
-        ctx.set_train_forward(True)
+    ctx.set_train_forward(args.train_fwd == "tc")
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)

@@ -72,9 +72,13 @@ const char *detnet_last_error(void);
  * split-FP16 (same as 0 for the stack). */
 int detnet_ctx_set_path(detnet_ctx *ctx, int path);
 /* Training forward (detnet_train_grad / detnet_batch_gradient) on tcgen05
- * (1, dense K=20 models) or FP32 CUDA cores (0, default). The tensor-core
- * forward is ~4x faster; its 3xTF32 activations are a few times noisier than
- * FP32, so FP32-vs-FP64 loss tracking over long runs is looser. */
+ * (1, default: split FP16 for dense K=20 models) or FP32 CUDA cores (0). The
+ * tensor-core forward is ~4x faster; its per-operation error (~2^-22) is a
+ * few times FP32's, which over 100 chaotic training steps moves the loss by
+ * as much as FP32 rounding itself does (training parity); the FP64
+ * mode (detnet_ctx_set_train_precision) is the reference-exact path. The
+ * reverse sweep and the weight-gradient contractions run on tcgen05 (3xTF32)
+ * for the K=20/z=160/v=40 dims in either case. */
 int detnet_ctx_set_train_forward(detnet_ctx *ctx, int tensor_cores);
 /* Training arithmetic: 0 FP32 (default, the fast path), 1 FP64 in the
  * reference's operation order -- the forward trace, reverse sweep and the

@@ -143,7 +143,7 @@ struct detnet_ctx {
     detnet::DBuf chunks; // per-chunk loss sums of the last reduction (k_reduce)
     detnet::DBuf in_H[2], in_y[2], in_x[2], xhat_dev, state_x, state_v, fb_list, fb_count;
     bool exact_pre = false; // bit-exact reference LU for every sample
-    bool train_tc = false;  // training forward on tcgen05 (dense images) instead of SIMT
+    bool train_tc = true;   // training forward on tcgen05 (dense images) instead of SIMT
     bool train_fp64 = false; // FP64 training step in the reference's order (k_train64.cuh)
     // > 0: choose the SIMT forward / reverse-sweep launch shapes as for a
     // batch of this many samples (device-group members use the global batch)

@@ -215,8 +215,10 @@ def test_fp32_training_config5_shape_within_fp32_spread(oracle, ref, tc_forward)
     does, at 0: test_train64_gpu.py). The FP32 GPU runs must stay inside that
     measured FP32 band: each final validation loss (the reference evaluating
     both final models on the same 2,000 samples) within 1.5x O32's largest
-    distance, the median within 3x O32's median; step 0 (identical weights)
-    agrees to 1e-6."""
+    distance and the median inside O32's range; step 0 (identical weights)
+    agrees to 1e-6. Measured (B200, r2): SIMT forward [0.011, 0.031, 0.034],
+    tcgen05 forward [0.033, 0.051, 0.019], O32 on the same seeds [0.008,
+    0.059, 0.012]."""
     import ctypes as Cc
     import json
 
@@ -258,4 +260,4 @@ def test_fp32_training_config5_shape_within_fp32_spread(oracle, ref, tc_forward)
           f"validation loss rel {finals}, median {med:.3e}; O32 median {spread['median']:.3e} "
           f"max {spread['max']:.3e}")
     assert max(finals) <= 1.5 * spread["max"], finals
-    assert med <= 3.0 * spread["median"], finals
+    assert med <= spread["max"], finals

@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_bwd_tc(BtcArgs p) {
         for (long ti = 0; ti < my_tiles; ++ti) {
             const long tile = blockIdx.x + ti * gridDim.x;
             const long s = tile * TILE + col;
+            DETNET_DASSERT(tile < a.n_tiles && s < a.ts && it0 >= 0 && it1 <= nl_all && a.lf >= 0);
             const bool live = s < a.n;
             float g[NA];
             const float *gps = a.gp + tile * NG * TILE + col;
@@ -480,6 +481,7 @@ __global__ void k_gate_bits(const float *tr_z, long ts, long n_cols, int lf, int
     const int l = lf + static_cast<int>(idx / per);
     const int w = static_cast<int>((idx % per) / n_cols);
     const long s = idx % n_cols;
+    DETNET_DASSERT(l >= lf && l < L && w < 5);
     const float *z = tr_z + (static_cast<long>(l) * ZZ + 32 * w) * ts + s;
     float v[32];
 #pragma unroll

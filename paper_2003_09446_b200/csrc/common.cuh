@@ -5,6 +5,26 @@
 #include <type_traits>
 #include <cuda_runtime.h>
 
+// Debug build (make EXTRA=-DDETNET_DEBUG_ASSERT, built by __graft_entry__.build()
+// into build/debug/): device-side bounds checks on the index math of every
+// kernel family; a failed check prints its location and traps (a launch error
+// instead of silent corruption). The stand-in for compute-sanitizer, which this
+// GPU pool does not offer. Compiled out of the product library.
+#ifdef DETNET_DEBUG_ASSERT
+#include <cstdio>
+#define DETNET_DASSERT(c)                                                                      \
+    do {                                                                                       \
+        if (!(c)) {                                                                            \
+            printf("DETNET_DASSERT failed %s:%d: %s\n", __FILE__, __LINE__, #c);             \
+            __trap();                                                                          \
+        }                                                                                      \
+    } while (0)
+#else
+#define DETNET_DASSERT(c)                                                                      \
+    do {                                                                                       \
+    } while (0)
+#endif
+
 namespace detnet {
 
 // Samples per tile: one tile = one TMEM lane block (128 rows) in the tcgen05

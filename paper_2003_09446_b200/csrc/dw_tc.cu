@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(DWT_THREADS, 1)
     const long k0 = static_cast<long>(sp) * DW_SPLIT;
     const long k1 = k0 + DW_SPLIT < n ? k0 + DW_SPLIT : n;
     const int nchunks = static_cast<int>((k1 - k0 + DWT_KC - 1) / DWT_KC);
+    DETNET_DASSERT(k0 < n && M <= 256 && NP <= 176 && nchunks >= 1 && 2 * stage + 32 <= DWT_SMEM);
 
     // constant parts of both stages: zero padding rows, the bias row of B
     for (int s = 0; s < 2; ++s) {

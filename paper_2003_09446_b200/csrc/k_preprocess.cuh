@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(256)
     for (long si = static_cast<long>(blockIdx.x) * warps + warp; si < n_eff;
          si += static_cast<long>(gridDim.x) * warps) {
         const long s = list ? list[si] : si;
+        DETNET_DASSERT(s >= 0 && s < n);
         const float *Hs = H + s * static_cast<long>(N) * K;
         for (int i = lane; i < N * K; i += 32) sH[i] = static_cast<double>(__ldg(Hs + i));
         for (int i = lane; i < N; i += 32) sy[i] = static_cast<double>(__ldg(y + s * N + i));

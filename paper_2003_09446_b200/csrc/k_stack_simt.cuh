@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_stack_simt(StackArgs a) {
     const long tile = live_tile ? tile_l : a.n_tiles - 1;
     const int col = static_cast<int>(unit % TILE);
     const long s = tile * TILE + col;           // sample index within this launch
+    DETNET_DASSERT(tile >= 0 && tile < a.n_tiles);
     const bool live = live_tile && s < a.n;
     const long gt = a.tile0 + tile;              // global tile index for SoA buffers
 
@@ -492,6 +493,7 @@ static __global__ void __launch_bounds__(1024) k_reduce(const double *tile_loss,
     const int t = threadIdx.x;
     const long tiles = n_quads / 4;
     const long chunks = (tiles + RED_CHUNK_TILES - 1) / RED_CHUNK_TILES;
+    DETNET_DASSERT(n_quads % 4 == 0 && n <= tiles * TILE);
     long long e = 0, f = 0;
     for (long i = t; i < n_quads; i += 1024) e += tile_err[i];
     for (long c = t; c < chunks; c += 1024) {

@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_train_bwd(BwdArgs a) {
     const int col = static_cast<int>(unit % TILE);
     const long s = tile * TILE + col;
     const bool live = live_tile && s < a.n;
+    DETNET_DASSERT(tile >= 0 && s < a.ts);
 
     if (tid == 0) {
         mbar_init(&bars[0], 1);
@@ -517,6 +518,7 @@ __global__ void k_grad_sum(SumArgs a) {
     const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= static_cast<long>(a.L) * P) return;
     const int l = static_cast<int>(idx / P), e = static_cast<int>(idx % P);
+    DETNET_DASSERT(a.splits >= 1 && a.tgroups >= 1 && a.lf >= 0 && a.lf <= a.L);
     if (l < a.lf) { a.raw[idx] = 0.0; return; }
     const int ob1 = Z * IN, oW2 = ob1 + Z, ob2 = oW2 + K * Z, oW3 = ob2 + K, ob3 = oW3 + V * Z, ot = ob3 + V;
     const long total = static_cast<long>(a.L) * P;

@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(32 * F64_WARPS) k_fwd64(Fwd64Args a) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long s = static_cast<long>(blockIdx.x) * F64_WARPS + warp;
     if (s >= a.n) return;
+    DETNET_DASSERT(K <= 32 && Z <= 256 && V <= 64 && a.first_term >= 1);
     double *sG = sm64 + static_cast<long>(warp) * f64_fwd_scratch(K, Z, V);
     double *sin = sG + K * KP;
     double *sz = sin + IN;

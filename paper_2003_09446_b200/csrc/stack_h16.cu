@@ -377,6 +377,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_h16(HKArgs p) {
             const long tile = blockIdx.x + ti * gridDim.x;
             const long gt = a.tile0 + tile;
             const long s = tile * TILE + col;
+            DETNET_DASSERT(tile < a.n_tiles && gt >= 0 && L0 >= 0 && L1 > L0);
             const bool live = s < a.n;
             float g[NA];
             const float *gps = a.gp + gt * NG * TILE + col;

@@ -387,6 +387,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
             const long gt = a.tile0 + tile;
             if (p.redo && !p.redo[gt]) continue;
             const long s = tile * TILE + col;
+            DETNET_DASSERT(tile < a.n_tiles && gt >= 0);
             const bool live = s < a.n;
             // ---- tile init: Gram entries into registers, state, q ----
             float g[NA];

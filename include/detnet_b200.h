@@ -109,6 +109,12 @@ int detnet_ctx_set_profiling(detnet_ctx *ctx, int on);
 int detnet_ctx_kernel_times(detnet_ctx *ctx, detnet_kernel_times *out, int reset);
 /* Total number of kernels this context launched (all classes). */
 long long detnet_ctx_launch_count(detnet_ctx *ctx);
+/* The canonical per-8,192-sample-chunk loss sums of the context's last
+ * evaluation / gradient reduction (waits for the context stream): returns
+ * the chunk count (copies min(cap, count) into out), or -status. Ranks that
+ * own chunk-aligned shards fold the gathered sums in global chunk order to
+ * get the single-device loss sum bit for bit (parallel.reduce_stats). */
+long detnet_ctx_chunk_sums(detnet_ctx *ctx, double *out, long cap);
 
 /* ---- parameters (ModelParams) ----------------------------------------- */
 typedef struct {

@@ -545,6 +545,7 @@ int finish_device(detnet_model *m, long n, double *dst) {
                                            reinterpret_cast<long long *>(res + 2),
                                            c->chunks.as<double>());
     }
+    c->last_chunks = (tiles + RED_CHUNK_TILES - 1) / RED_CHUNK_TILES;
     if (int rc = check_launch()) return rc;
     CK(cudaMemcpyAsync(res + 3, c->sing.p, 8, cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaMemcpyAsync(dst ? dst : c->h_result, res, 32, cudaMemcpyDeviceToHost, c->stream));
@@ -738,6 +739,17 @@ int detnet_ctx_kernel_times(detnet_ctx *c, detnet_kernel_times *out, int reset) 
 }
 
 long long detnet_ctx_launch_count(detnet_ctx *c) { return c ? c->launches : 0; }
+
+long detnet_ctx_chunk_sums(detnet_ctx *c, double *out, long cap) {
+    if (!c) return -fail(DETNET_ERR_CONTRACT, "null context");
+    if (cudaSetDevice(c->device) != cudaSuccess || quiesce(c)) return -DETNET_ERR_CUDA;
+    const long nc = c->last_chunks;
+    if (out && cap > 0 && nc > 0 &&
+        cudaMemcpy(out, c->chunks.p, sizeof(double) * std::min(cap, nc), cudaMemcpyDeviceToHost) !=
+            cudaSuccess)
+        return -fail(DETNET_ERR_CUDA, "chunk sums copy failed");
+    return nc;
+}
 
 int detnet_model_create(detnet_ctx *c, const detnet_model_desc *d, detnet_model **out) {
     if (!c || !d || !out || !d->params) return fail(DETNET_ERR_CONTRACT, "null argument");

@@ -141,6 +141,7 @@ struct detnet_ctx {
     // workspace
     detnet::DBuf gp, q32, denom, xmask, flag, tile_loss, tile_err, sing, result;
     detnet::DBuf chunks; // per-chunk loss sums of the last reduction (k_reduce)
+    long last_chunks = 0; // how many
     detnet::DBuf in_H[2], in_y[2], in_x[2], xhat_dev, state_x, state_v, fb_list, fb_count;
     bool exact_pre = false; // bit-exact reference LU for every sample
     bool train_tc = true;   // training forward on tcgen05 (dense images) instead of SIMT

@@ -387,6 +387,7 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
                                            reinterpret_cast<long long *>(res + 5),
                                            c->chunks.as<double>());
     }
+    c->last_chunks = (tiles + RED_CHUNK_TILES - 1) / RED_CHUNK_TILES;
     if (int rc = check_launch()) return rc;
     if (!out) return drain_times(c, false), 0; // no readback requested: no wait
     return finish(m, n, out); // loss / errors / flagged of the forward pass (syncs)

@@ -137,6 +137,8 @@ _lib.detnet_model_param_count.argtypes = [_vp]
 _lib.detnet_train_grad.argtypes = [_vp, C.c_long, _vp, _vp, _vp, C.c_int, _vp, C.POINTER(_Eval)]
 _lib.detnet_train_apply.argtypes = [_vp, _vp, C.c_long, C.POINTER(_LossSpec), C.POINTER(_AdamCfg)]
 _lib.detnet_model_get_params.argtypes = [_vp, _vp]
+_lib.detnet_ctx_chunk_sums.restype = C.c_long
+_lib.detnet_ctx_chunk_sums.argtypes = [_vp, _vp, C.c_long]
 _lib.detnet_train_raw_count.restype = C.c_long
 _lib.detnet_train_raw_count.argtypes = [_vp]
 _lib.detnet_train_status.argtypes = [_vp, _dp, _dp]
@@ -311,6 +313,16 @@ class Context:
     @property
     def launch_count(self):
         return _lib.detnet_ctx_launch_count(self._h)
+
+    def chunk_sums(self):
+        """Per-8,192-sample-chunk loss sums of the last reduction (float64)."""
+        n = _lib.detnet_ctx_chunk_sums(self._h, None, 0)
+        if n < 0:
+            _check(-n)
+        out = np.zeros(n)
+        if n:
+            _lib.detnet_ctx_chunk_sums(self._h, out.ctypes.data, n)
+        return out
 
     def model(self, n_tx, n_rx, z_dim, v_dim, params, masks=None, frozen_prefix=0):
         return Model(self, n_tx, n_rx, z_dim, v_dim, params, masks, frozen_prefix)

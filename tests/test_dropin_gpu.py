@@ -18,13 +18,24 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(ROOT, "oracle", "_ref", "dropin_test")
 
 
-@pytest.fixture(scope="module")
-def run():
+# desk scale (K=3, SIMT kernels), the BASELINE dims (K=20: tcgen05 kernels),
+# and the BASELINE dims with the FP64 training mode (DETNET_TRAIN_FP64=1)
+CASES = [("3", "5", "4", "157", ""), ("20", "30", "6", "2000", ""), ("20", "30", "6", "2000", "1")]
+
+
+@pytest.fixture(scope="module", params=CASES, ids=["k3", "k20", "k20-fp64"])
+def run(request):
     if not os.path.exists(BIN):
         pytest.skip("dropin_test not built (needs the reference tree at build time)")
-    out = subprocess.run([BIN, "3", "5", "4", "157"], capture_output=True, text=True, timeout=300)
+    K, N, L, n, fp64 = request.param
+    env = dict(os.environ)
+    if fp64:
+        env["DETNET_TRAIN_FP64"] = fp64
+    out = subprocess.run([BIN, K, N, L, n], capture_output=True, text=True, timeout=300, env=env)
     assert out.returncode == 0, out.stderr
-    return json.loads(out.stdout)
+    d = json.loads(out.stdout)
+    d["fp64"] = bool(fp64)
+    return d
 
 
 def _model(d, params=None):
@@ -62,7 +73,8 @@ def test_dropin_batch_evaluate(run, oracle):
     loss, errors, symbols, flagged = d["eval"]
     assert symbols == d["n"] * d["K"] and flagged == ref["flagged"]
     assert abs(loss - ref["data_loss"]) <= 1e-4 * abs(ref["data_loss"])
-    assert abs(errors - ref["symbol_errors"]) <= 2  # N(0,1) channels: rare FP32 sign flips
+    # N(0,1) channels (the reference's convention): rare FP32 sign flips
+    assert abs(errors - ref["symbol_errors"]) <= max(2, symbols // 2000)
     reft = oracle.batch_evaluate(m, H, y, x, trainable_only=True)
     assert abs(d["eval_trainable"][0] - reft["data_loss"]) <= 1e-4 * abs(reft["data_loss"])
 
@@ -75,8 +87,24 @@ def test_dropin_gradient_and_adam(run, oracle):
     H, y, x = _inputs(d)
     ref = oracle.batch_gradient(m, H, y, x, kind=2, lam1=0.04, lam2=0.04)
     g = np.array(d["grads"]).reshape(ref["grads"].shape)
-    scale = np.max(np.abs(ref["grads"]))
-    assert np.max(np.abs(g - ref["grads"])) <= 1e-3 * scale
+    if d["fp64"]:  # FP64 reference-order mode: bit-identical through the seam
+        assert np.array_equal(g, ref["grads"])
+    elif d["K"] <= 8:
+        scale = np.max(np.abs(ref["grads"]))
+        assert np.max(np.abs(g - ref["grads"])) <= 1e-3 * scale
+    else:
+        # K=20 on the reference's unscaled N(0,1) channels: per-sample gradients
+        # carry the weight 1 / ||x - x_ZF||^2, and a relu / soft-sign gate that
+        # flips under FP32-class rounding on one heavily weighted sample moves
+        # the batch gradient (per-sample gradients agree to ~5e-6,
+        # tools/grad_noise.py). Bound: the relative L2 distance within 10x that
+        # of O32 (the FP32 restatement) on the same batch, or 1e-3.
+        o32 = oracle.batch_gradient_f32(m, H, y, x, kind=2, lam1=0.04, lam2=0.04)["grads"]
+        nrm = np.linalg.norm(ref["grads"])
+        e_gpu = np.linalg.norm(g - ref["grads"]) / nrm
+        e_o32 = np.linalg.norm(o32 - ref["grads"]) / nrm
+        print(f"drop-in K=20 FP32 gradient: rel L2 {e_gpu:.2e} (O32 {e_o32:.2e})")
+        assert e_gpu <= max(10.0 * e_o32, 1e-3), (e_gpu, e_o32)
     assert d["train_steps"] == 1
     mo = np.zeros_like(m.params)
     vo = np.zeros_like(m.params)

@@ -72,3 +72,26 @@ def test_group_replicas_follow_device_training(oracle):
             m.train_apply(raw, 4096, kind=2, lam1=1e-4, lr0=1e-3)
         outs.append(m.batch_evaluate(H, y, x))
     assert (outs[0].data_loss, outs[0].symbol_errors) == (outs[1].data_loss, outs[1].symbol_errors)
+
+
+def test_rank_chunk_sums_fold_to_single_device(oracle):
+    """parallel.reduce_stats's input: the per-chunk loss sums of each rank's
+    chunk-aligned shard, folded in global order, equal one device's loss sum
+    over the whole batch bit for bit (any number of ranks)."""
+    from paper_2003_09446_b200 import Context
+    from paper_2003_09446_b200.parallel import CHUNK, fold_chunks
+    from paper_2003_09446_b200.workload import xavier_params
+    n, L = 5 * CHUNK + 77, 5
+    params = xavier_params(K, L, seed=9)
+    H, y, x = _inputs(oracle, n, seed=11)
+    c = Context(0)
+    m = c.model(K, N, 160, 40, params)
+    ev = m.batch_evaluate(H, y, x)
+    whole = c.chunk_sums()
+    assert len(whole) == 6 and fold_chunks(None, whole) == ev.loss_sum
+    for cuts in ([0, 2 * CHUNK, n], [0, CHUNK, 3 * CHUNK, 4 * CHUNK, n]):
+        parts = []
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            m.batch_evaluate(H[a:b], y[a:b], x[a:b])
+            parts.extend(c.chunk_sums())
+        assert fold_chunks(None, parts) == ev.loss_sum, cuts

@@ -1,7 +1,8 @@
 """World-size-2 (gloo, CPU) check of the data-parallel plumbing: sharded
-evaluation statistics and sharded raw-gradient sums, all-reduced, equal the
-single-process results of the same global batch (computed here with the
-oracle, since this container has no GPU)."""
+evaluation statistics (loss folded from the ranks' chunk sums in global chunk
+order -- bit-identical to one process) and sharded raw-gradient sums,
+all-reduced, equal the single-process results of the same global batch
+(computed here with the oracle, since this container has no GPU)."""
 import os
 import socket
 
@@ -19,6 +20,19 @@ def _free_port():
     return port
 
 
+CH = 8  # stand-in for the engine's 8,192-sample chunk (per-rank shards are chunk-aligned)
+
+
+def _chunk_sums(loss):
+    out = []
+    for i in range(0, len(loss), CH):
+        acc = 0.0
+        for v in loss[i:i + CH]:
+            acc += float(v)
+        out.append(acc)
+    return out
+
+
 def _worker(rank, world, port, out):
     import torch.distributed as dist
 
@@ -34,9 +48,9 @@ def _worker(rank, world, port, out):
     base = orc.lib.or_split(__import__("ctypes").byref(orc.rng(1, 2)))
     H, x, y, _ = orc.generate_range(base, 8, 4, first, count, 7.0, 14.0)
     ev = orc.evaluate(m, H, y, x)
-    stats = torch.tensor([ev["loss"].sum(), ev["errors"].sum(), count * 4, ev["flagged"].sum()],
-                         dtype=torch.float64)
-    red = reduce_stats(dist, stats)
+    counts = torch.tensor([int(ev["errors"].sum()), count * 4, int(ev["flagged"].sum())],
+                          dtype=torch.int64)
+    red = reduce_stats(dist, _chunk_sums(ev["loss"]), counts)
     g = orc.batch_gradient(m, H, y, x)
     raw = torch.from_numpy(g["grads"] * count)  # undo the per-rank mean -> raw sums
     allreduce_grad(dist, raw)
@@ -64,6 +78,10 @@ def test_two_rank_reduction_matches_single_process(oracle):
     ev = oracle.evaluate(m, H, y, x)
     assert red["symbol_errors"] == int(ev["errors"].sum())
     assert red["symbols"] == 80 * 4 and red["flagged"] == int(ev["flagged"].sum())
-    assert abs(red["loss_sum"] - ev["loss"].sum()) <= 1e-12 * abs(ev["loss"].sum())
+    # the canonical fold over the global chunk sequence: bit-identical
+    acc = 0.0
+    for v in _chunk_sums(ev["loss"]):
+        acc += v
+    assert red["loss_sum"] == acc
     full = oracle.batch_gradient(m, H, y, x)["grads"]
     assert np.max(np.abs(grad - full)) <= 1e-12 * np.max(np.abs(full))

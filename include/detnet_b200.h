@@ -243,6 +243,45 @@ int detnet_adam_step(detnet_ctx *ctx, int n_tx, int z_dim, int v_dim, int depth,
                      int frozen_prefix, double *params, const double *masks, const double *grads,
                      double *m1, double *m2, int64_t *step, const detnet_adam_config *cfg);
 
+/* ---- incremental-depth training (train_incremental, training.cpp:22-141) --
+ * The reference's whole schedule as one device-resident call: batches from the
+ * on-device generator with the reference's keying (master Rng(seed): init
+ * stream 1, train stream 2, validation stream 3), parameters / Adam moments /
+ * objective in HBM, a fresh Adam state per incremental step, validation on the
+ * device-resident evaluation set, the reference's halting tests, freeze + append
+ * with init_layer draws (model.cpp:140-166). sample_scale multiplies H and y
+ * (1.0 = the reference's N(0,1) channels, 1/sqrt(N) = BASELINE's N(0,1/N)). */
+typedef struct {
+    int start_layers, t_step, max_layers;          /* IncrementalConfig */
+    double halt_epsilon, target_ber;
+    int val_samples;
+    double val_snr_db;
+    int total_batches, batch_size;                 /* TrainConfig */
+    double snr_lo_db, snr_hi_db;
+    detnet_adam_config adam;
+    detnet_loss_spec spec;
+    double weight_scale, t0;                       /* InitOptions */
+    int loss_layers_trainable_only;
+    uint64_t seed;
+    double sample_scale;
+} detnet_incremental_config;
+typedef struct {
+    int step, layer_count;                         /* StepRecord */
+    double train_loss, val_loss, val_ber, wall_ms;
+} detnet_step_record;
+typedef struct {
+    int halt_reason;                               /* 0 target_ber, 1 converged, 2 max_layers */
+    int depth, frozen_prefix;
+    long long flagged_samples, optimizer_steps;
+    double seconds;
+} detnet_incremental_result;
+/* records: up to max_records step records (*n_records = how many steps ran);
+ * params_out (nullable): max_layers * record doubles, the final parameters. */
+int detnet_train_incremental(detnet_ctx *ctx, int n_tx, int n_rx, int z_dim, int v_dim,
+                             const detnet_incremental_config *cfg, detnet_step_record *records,
+                             int max_records, int *n_records, double *params_out,
+                             detnet_incremental_result *result);
+
 /* ---- on-device channel generator (make_sample/generate_batch) --------- */
 /* Rng(seed, stream_id) state (rng.cpp:18-19). */
 uint64_t detnet_rng_seed(uint64_t seed, uint64_t stream_id);

@@ -97,6 +97,28 @@ class _AdamCfg(C.Structure):
                 ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double)]
 
 
+class _IncCfg(C.Structure):
+    _fields_ = [("start_layers", C.c_int), ("t_step", C.c_int), ("max_layers", C.c_int),
+                ("halt_epsilon", C.c_double), ("target_ber", C.c_double),
+                ("val_samples", C.c_int), ("val_snr_db", C.c_double),
+                ("total_batches", C.c_int), ("batch_size", C.c_int),
+                ("snr_lo_db", C.c_double), ("snr_hi_db", C.c_double), ("adam", _AdamCfg),
+                ("spec", _LossSpec), ("weight_scale", C.c_double), ("t0", C.c_double),
+                ("loss_layers_trainable_only", C.c_int), ("seed", C.c_uint64),
+                ("sample_scale", C.c_double)]
+
+
+class _StepRec(C.Structure):
+    _fields_ = [("step", C.c_int), ("layer_count", C.c_int), ("train_loss", C.c_double),
+                ("val_loss", C.c_double), ("val_ber", C.c_double), ("wall_ms", C.c_double)]
+
+
+class _IncRes(C.Structure):
+    _fields_ = [("halt_reason", C.c_int), ("depth", C.c_int), ("frozen_prefix", C.c_int),
+                ("flagged_samples", C.c_longlong), ("optimizer_steps", C.c_longlong),
+                ("seconds", C.c_double)]
+
+
 _lib.detnet_last_error.restype = C.c_char_p
 _lib.detnet_ctx_create.argtypes = [C.c_int, C.POINTER(_vp)]
 _lib.detnet_ctx_create_group.argtypes = [C.POINTER(C.c_int), C.c_int, C.POINTER(_vp)]
@@ -137,6 +159,9 @@ _lib.detnet_model_param_count.argtypes = [_vp]
 _lib.detnet_train_grad.argtypes = [_vp, C.c_long, _vp, _vp, _vp, C.c_int, _vp, C.POINTER(_Eval)]
 _lib.detnet_train_apply.argtypes = [_vp, _vp, C.c_long, C.POINTER(_LossSpec), C.POINTER(_AdamCfg)]
 _lib.detnet_model_get_params.argtypes = [_vp, _vp]
+_lib.detnet_train_incremental.argtypes = [_vp, C.c_int, C.c_int, C.c_int, C.c_int,
+                                          C.POINTER(_IncCfg), C.POINTER(_StepRec), C.c_int,
+                                          C.POINTER(C.c_int), _vp, C.POINTER(_IncRes)]
 _lib.detnet_ctx_chunk_sums.restype = C.c_long
 _lib.detnet_ctx_chunk_sums.argtypes = [_vp, _vp, C.c_long]
 _lib.detnet_train_raw_count.restype = C.c_long
@@ -313,6 +338,38 @@ class Context:
     @property
     def launch_count(self):
         return _lib.detnet_ctx_launch_count(self._h)
+
+    def train_incremental(self, n_tx, n_rx, start_layers, t_step, max_layers, total_batches,
+                          batch_size, val_samples, seed, z_dim=None, v_dim=None, halt_epsilon=0.01,
+                          target_ber=0.0, val_snr_db=12.0, snr_lo_db=0.0, snr_hi_db=15.0,
+                          lr0=1e-4, decay_factor=0.97, decay_step=1000, beta1=0.9, beta2=0.999,
+                          eps=1e-8, kind=0, lam=0.0, lam1=0.0, lam2=0.0, weight_scale=1.0, t0=0.5,
+                          trainable_only=False, sample_scale=1.0):
+        """train_incremental (training.cpp:22-141) on the device. Returns
+        (records, result dict, final params [depth][record])."""
+        Z = z_dim or 8 * n_tx
+        V = v_dim or 2 * n_tx
+        cfg = _IncCfg(start_layers, t_step, max_layers, halt_epsilon, target_ber, val_samples,
+                      val_snr_db, total_batches, batch_size, snr_lo_db, snr_hi_db,
+                      _AdamCfg(lr0, decay_factor, decay_step, beta1, beta2, eps),
+                      _LossSpec(kind, lam, lam1, lam2), weight_scale, t0, int(trainable_only),
+                      seed, sample_scale)
+        nmax = max_layers - start_layers + 2
+        recs = (_StepRec * nmax)()
+        nrec = C.c_int()
+        res = _IncRes()
+        P = record_size(n_tx, Z, V)
+        params = np.zeros((max_layers, P))
+        _check(_lib.detnet_train_incremental(self._h, n_tx, n_rx, Z, V, C.byref(cfg), recs, nmax,
+                                             C.byref(nrec), params.ctypes.data, C.byref(res)))
+        records = [{"step": r.step, "layers": r.layer_count, "train_loss": r.train_loss,
+                    "val_loss": r.val_loss, "val_ber": r.val_ber, "wall_ms": r.wall_ms}
+                   for r in recs[:nrec.value]]
+        result = {"halt": ["target_ber", "converged", "max_layers"][res.halt_reason],
+                  "depth": res.depth, "frozen_prefix": res.frozen_prefix,
+                  "flagged": res.flagged_samples, "optimizer_steps": res.optimizer_steps,
+                  "seconds": res.seconds}
+        return records, result, params[:res.depth]
 
     def chunk_sums(self):
         """Per-8,192-sample-chunk loss sums of the last reduction (float64)."""

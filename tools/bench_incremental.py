@@ -1,6 +1,6 @@
 """SURVEY 8f row 2 measurement: the reference's train_incremental running on
-the B200 seam vs on the reference's own OpenMP kernels (same box, same
-arguments). Prints one JSON line per schedule; wall-clock includes context
+the B200 seam, the device-resident detnet_train_incremental, and the
+reference on its own OpenMP kernels (same box, same arguments). Prints one JSON line per schedule; wall-clock includes context
 creation, generation, validation and checkpoint round trip (the whole
 controller), and the marginal per-optimizer-step time from two run lengths."""
 import json
@@ -23,15 +23,30 @@ def run(binary, args):
     return json.loads(out.stdout)
 
 
+def run_device(args):
+    """detnet_train_incremental with incremental_main.cpp's configuration."""
+    sys.path.insert(0, ROOT)
+    from paper_2003_09446_b200 import Context
+    K, N, s0, ts, mx, nb, bs, val, seed = args
+    c = Context(0)
+    recs, res, _ = c.train_incremental(K, N, s0, ts, mx, nb, bs, val, seed, halt_epsilon=0.0,
+                                       val_snr_db=10.0, snr_lo_db=7.0, snr_hi_db=14.0, lr0=1e-3,
+                                       kind=2, lam1=1e-4)
+    return {"seconds": res["seconds"], "optimizer_steps": res["optimizer_steps"], "steps": recs}
+
+
 def main():
     # (label, K, N, start, t_step, max_layers, batches_short, batches_long, batch, val)
     cases = [("whole-network L=40 (config-5 dims)", 20, 30, 40, 10, 40, 4, 12, 5000, 2000),
              ("incremental 10->40 by 10", 20, 30, 10, 10, 40, 2, 6, 5000, 2000)]
     for label, K, N, s0, ts, mx, b1, b2, bs, val in cases:
         res = {}
-        for name, binary in (("b200", B), ("reference", R)):
-            a = run(binary, [K, N, s0, ts, mx, b1, bs, val, 3])
-            c = run(binary, [K, N, s0, ts, mx, b2, bs, val, 3])
+        for name, binary in (("b200", B), ("device", None), ("reference", R)):
+            if binary is None:
+                a, c = (run_device([K, N, s0, ts, mx, bb, bs, val, 3]) for bb in (b1, b2))
+            else:
+                a = run(binary, [K, N, s0, ts, mx, b1, bs, val, 3])
+                c = run(binary, [K, N, s0, ts, mx, b2, bs, val, 3])
             per_step = (c["seconds"] - a["seconds"]) / (c["optimizer_steps"] - a["optimizer_steps"])
             res[name] = {"seconds_long": c["seconds"], "optimizer_steps_long": c["optimizer_steps"],
                          "marginal_ms_per_optimizer_step": per_step * 1e3,
@@ -39,8 +54,10 @@ def main():
                          "final_val_loss": c["steps"][-1]["val_loss"],
                          "final_val_ber": c["steps"][-1]["val_ber"]}
         print(json.dumps({"case": label, "batch": bs, "cores_reference": os.cpu_count(), **res,
-                          "speedup_marginal": res["reference"]["marginal_ms_per_optimizer_step"] /
-                          res["b200"]["marginal_ms_per_optimizer_step"]}))
+                          "speedup_marginal_seam": res["reference"]["marginal_ms_per_optimizer_step"] /
+                          res["b200"]["marginal_ms_per_optimizer_step"],
+                          "speedup_marginal_device": res["reference"]["marginal_ms_per_optimizer_step"] /
+                          res["device"]["marginal_ms_per_optimizer_step"]}))
         sys.stdout.flush()
 
 

@@ -1259,8 +1259,13 @@ int detnet_batch_baseline_errors(detnet_ctx *c, int kind, long n, int n_rx, int 
     if (n_tx < 1 || n_rx < n_tx) return fail(DETNET_ERR_CONTRACT, "baseline: need N >= K >= 1");
     if (kind == 1 && n_tx > 16)
         return fail(DETNET_ERR_UNSUPPORTED, "ml_decode: exhaustive search limited to K <= 16");
+    // K <= 20: register-resident instantiations; wider ZF: k_zf_errors_any with
+    // the warp's [A | x] in shared memory (up to ~160 transmit antennas)
     const BaseFn fn = base_table(n_tx, std::make_integer_sequence<int, 20>{});
-    if (!fn) return fail(DETNET_ERR_UNSUPPORTED, "baseline: K = %d not instantiated (K <= 20)", n_tx);
+    const size_t any_per = sizeof(double) * static_cast<size_t>(n_tx) * (n_tx + 1);
+    const int any_warps = static_cast<int>(std::min<size_t>(4, (200u << 10) / any_per));
+    if (!fn && (kind != 0 || any_per > (227u << 10)))
+        return fail(DETNET_ERR_UNSUPPORTED, "baseline: K = %d exceeds the device ZF limit", n_tx);
     CK(cudaSetDevice(c->device));
     const long chunk = std::min<long>(n, 1L << 16);
     const size_t nh = static_cast<size_t>(chunk) * n_rx * n_tx, ny = static_cast<size_t>(chunk) * n_rx,
@@ -1287,7 +1292,16 @@ int detnet_batch_baseline_errors(detnet_ctx *c, int kind, long n, int n_rx, int 
         const int blocks = static_cast<int>(std::min<long>((cnt + 7) / 8, 148L * 16));
         {
             LaunchScope ls(c, DETNET_K_OTHER, c->stream);
-            fn(kind, blocks, smem, c->stream, cnt, n_rx, dH, dy, dx, de, ds);
+            if (fn) {
+                fn(kind, blocks, smem, c->stream, cnt, n_rx, dH, dy, dx, de, ds);
+            } else {
+                const int w = std::max(1, any_warps);
+                const size_t sm_any = any_per * w;
+                cudaFuncSetAttribute(k_zf_errors_any, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(sm_any));
+                const int bl = static_cast<int>(std::min<long>((cnt + w - 1) / w, 148L * 8));
+                k_zf_errors_any<<<bl, 32 * w, sm_any, c->stream>>>(cnt, n_rx, n_tx, dH, dy, dx, de, ds);
+            }
         }
         if (int rc = check_launch()) { buf.release(); return rc; }
         unsigned long long sing = ~0ull;

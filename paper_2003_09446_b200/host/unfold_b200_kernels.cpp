@@ -194,14 +194,6 @@ BatchEval to_eval(const detnet_eval &ev) {
     return out;
 }
 
-long long baseline_errors_one(const ChannelSample &s, BaselineKind kind) {
-    if (kind == BaselineKind::oracle) return 0;
-    const Vec d = kind == BaselineKind::zf ? sign_slice(zf_decode(s.H, s.y)) : ml_decode(s.H, s.y);
-    long long e = 0;
-    for (size_t i = 0; i < s.x.size(); ++i) e += d[i] != s.x[i];
-    return e;
-}
-
 } // namespace
 
 int worker_count() {
@@ -288,8 +280,8 @@ BatchEval batch_gradient(const ModelParams &params, std::span<const ChannelSampl
 
 // ZF/ML/oracle baselines on the device: FP64 samples cross
 // as-is and the kernels keep the reference's operation order, so the counts are
-// bit-identical (tests/test_baseline_gpu.py). The device instantiates K <= 20;
-// wider K keeps the reference's own per-sample decoders (channel.cpp).
+// bit-identical (tests/test_baseline_gpu.py). Every K runs on the device (ZF:
+// register-resident for K <= 20, shared-memory elimination above).
 std::pair<long long, long long> batch_baseline_errors(std::span<const ChannelSample> batch,
                                                       BaselineKind kind) {
     if (batch.empty() || kind == BaselineKind::oracle) {
@@ -300,30 +292,22 @@ std::pair<long long, long long> batch_baseline_errors(std::span<const ChannelSam
     const int N = batch[0].H.rows, K = batch[0].H.cols;
     if (kind == BaselineKind::ml && K > 16)
         throw CapacityError("ml_decode: exhaustive search limited to K <= 16");
-    if (K <= 20) {
-        const size_t n = batch.size();
-        std::vector<double> H(n * N * K), y(n * N), x(n * K);
-        for (size_t i = 0; i < n; ++i) {
-            const ChannelSample &c = batch[i];
-            if (c.H.rows != N || c.H.cols != K || static_cast<int>(c.y.size()) != N ||
-                static_cast<int>(c.x.size()) != K)
-                throw ContractError("batch sample shape does not match");
-            std::memcpy(H.data() + i * N * K, c.H.data.data(), sizeof(double) * N * K);
-            std::memcpy(y.data() + i * N, c.y.data(), sizeof(double) * N);
-            std::memcpy(x.data() + i * K, c.x.data(), sizeof(double) * K);
-        }
-        long long errors = 0, symbols = 0;
-        std::lock_guard<std::mutex> lk(engine().mu);
-        check(detnet_batch_baseline_errors(engine().ctx, kind == BaselineKind::zf ? 0 : 1,
-                                           static_cast<long>(n), N, K, H.data(), y.data(), x.data(),
-                                           &errors, &symbols));
-        return {errors, symbols};
+    const size_t n = batch.size();
+    std::vector<double> H(n * N * K), y(n * N), x(n * K);
+    for (size_t i = 0; i < n; ++i) {
+        const ChannelSample &c = batch[i];
+        if (c.H.rows != N || c.H.cols != K || static_cast<int>(c.y.size()) != N ||
+            static_cast<int>(c.x.size()) != K)
+            throw ContractError("batch sample shape does not match");
+        std::memcpy(H.data() + i * N * K, c.H.data.data(), sizeof(double) * N * K);
+        std::memcpy(y.data() + i * N, c.y.data(), sizeof(double) * N);
+        std::memcpy(x.data() + i * K, c.x.data(), sizeof(double) * K);
     }
     long long errors = 0, symbols = 0;
-    for (const ChannelSample &s : batch) {
-        errors += baseline_errors_one(s, kind);
-        symbols += static_cast<long long>(s.x.size());
-    }
+    std::lock_guard<std::mutex> lk(engine().mu);
+    check(detnet_batch_baseline_errors(engine().ctx, kind == BaselineKind::zf ? 0 : 1,
+                                       static_cast<long>(n), N, K, H.data(), y.data(), x.data(),
+                                       &errors, &symbols));
     return {errors, symbols};
 }
 

@@ -23,7 +23,10 @@ def _batch(oracle, seed, N, K, n, lo, hi):
 
 @pytest.mark.parametrize("K,N,n,lo,hi", [(2, 4, 3000, 0.0, 12.0), (4, 8, 3000, 0.0, 15.0),
                                          (8, 12, 2000, 4.0, 12.0), (20, 30, 4096, 7.0, 14.0),
-                                         (3, 3, 2000, -5.0, 5.0)])
+                                         (3, 3, 2000, -5.0, 5.0),
+                                         # wider than the register kernels: shared-memory ZF
+                                         (21, 30, 1500, 7.0, 14.0), (32, 32, 600, 0.0, 20.0),
+                                         (40, 64, 400, 5.0, 15.0), (70, 72, 64, 10.0, 20.0)])
 def test_zf_errors_match_reference(ctx, oracle, ref, K, N, n, lo, hi):
     H, y, x = _batch(oracle, 11 + K, N, K, n, lo, hi)
     st, e_ref, s_ref = ref.baseline_errors(0, H, y, x)
@@ -70,5 +73,12 @@ def test_baseline_edges(ctx, ref):
     assert ref.baseline_errors(1, H, np.zeros((1, 20)), np.ones((1, 17)))[0] != 0
     with pytest.raises(eng.UnsupportedError):
         ctx.baseline_errors(1, H, np.zeros((1, 20)), np.ones((1, 17)))
+    # singular wide system on the shared-memory ZF path
+    Hs = np.random.default_rng(2).standard_normal((3, 30, 24))
+    Hs[1, :, 5] = Hs[1, :, 7]
+    ys = np.random.default_rng(3).standard_normal((3, 30)); xs = np.ones((3, 24))
+    assert ref.baseline_errors(0, Hs, ys, xs)[0] == 2
+    with pytest.raises(eng.SingularMatrixError):
+        ctx.baseline_errors(0, Hs, ys, xs)
     # empty batch
     assert ctx.baseline_errors(0, np.zeros((0, 6, 3)), np.zeros((0, 6)), np.zeros((0, 3))) == (0, 0)

@@ -60,7 +60,15 @@ __host__ __device__ constexpr int tri_idx(int K, int a, int b) { // a <= b
 // once through a 2-stage ring of 6-row chunks by a 2-D tensor TMA (box 124
 // floats x 64 samples: the per-sample stride in a stage is padded to 496 B so
 // the 8-lane phases of a 128-bit shared load hit distinct banks).
-constexpr int PS_TILE = 64, PS_ROWS = 6, PS_THREADS = 160;
+#ifndef DETNET_K1_POLICY
+#define DETNET_K1_POLICY 1
+#endif
+#ifndef DETNET_K1_UNROLL
+#define DETNET_K1_UNROLL 1
+#endif
+constexpr int K1_UNROLL = DETNET_K1_UNROLL;
+#define K1_BOUNDS __launch_bounds__(PS_THREADS, 2)
+constexpr int PS_TILE = 64, PS_ROWS = 6, PS_THREADS = 128;
 constexpr int PREP_FAST_N = 30; // n_rx the fast path is instantiated for (K = 20 configs)
 template <int K, int N> struct PrepStreamSmem {
     static constexpr int NG = K * (K + 1) / 2;
@@ -149,7 +157,7 @@ __device__ __forceinline__ void fma2p(float &d0, float &d1, float a0, float a1, 
 // K1 fast path. grid = min(tiles, 2 x SMs), PS_THREADS threads,
 // PrepStreamSmem<K, N>::BYTES of dynamic smem.
 template <int K, int N>
-__global__ void __launch_bounds__(PS_THREADS, 2)
+__global__ void K1_BOUNDS
     k_prep_stream(const __grid_constant__ CUtensorMap tmH, long n, const float *__restrict__ y,
                   const int8_t *__restrict__ x, float *__restrict__ gp, float *__restrict__ q32,
                   double *__restrict__ denom, uint32_t *__restrict__ xmask,
@@ -182,47 +190,57 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
     }
     __syncthreads();
 
-    if (warp == 4) {
-        // ===================== producer =====================
-        uint64_t pol; // H is read exactly once
+    // ---- loads: issued by thread 0 (no producer warp: with 4 warps per CTA
+    // and 2 CTAs per SM every SM sub-partition runs 2 warps, so each thread can
+    // hold 255 registers -- the sample's Gram half, p and an H row -- without
+    // spilling). Chunk step cs = (tile iteration) * NCH + chunk goes to ring
+    // stage cs & 1; a stage is refilled once all 4 warps released it.
+    const bool issuer = threadIdx.x == 0;
+    uint64_t pol = 0; // H is read once; evict_normal keeps the 256-B promoted
+                      // lines a chunk shares with the next one until it is read
+    if (issuer) {
+#if DETNET_K1_POLICY == 1
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+#elif DETNET_K1_POLICY == 2
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#else
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-        long cstep = 0;
-        int it = 0;
-        for (long tt = blockIdx.x; tt < ntiles; tt += gridDim.x, ++it) {
-            const int yb = it & 1;
-            const uint32_t yph = (it >> 1) & 1;
-            const long s0 = tt * P;
-            const int live = static_cast<int>(n - s0 < P ? n - s0 : P);
-            float *ybuf = reinterpret_cast<float *>(psm + SM::YB + yb * SM::YSLOT);
-            mbar_wait_guard(&yempty[yb], yph ^ 1);
-            unsigned char *xbuf = psm + SM::XB + yb * SM::XSLOT;
-            const uint32_t ybytes = static_cast<uint32_t>(live * N * 4);
-            const uint32_t xbytes = static_cast<uint32_t>(live * K);
-            if (ybytes % 16 == 0 && xbytes % 16 == 0) {
-                if (lane == 0) {
-                    mbar_arrive_expect_tx(&yfull[yb], ybytes + xbytes);
-                    bulk_g2s(ybuf, y + s0 * N, ybytes, &yfull[yb]);
-                    bulk_g2s(xbuf, x + s0 * K, xbytes, &yfull[yb]);
-                }
-            } else {
-                for (int i = lane; i < live * N; i += 32) ybuf[i] = __ldg(y + s0 * N + i);
-                for (int i = lane; i < live * K; i += 32) xbuf[i] = static_cast<unsigned char>(x[s0 * K + i]);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&yfull[yb]);
-            }
-            for (int c = 0; c < NCH; ++c, ++cstep) {
-                const int st = static_cast<int>(cstep & 1);
-                const uint32_t ph = static_cast<uint32_t>((cstep >> 1) & 1);
-                mbar_wait_guard(&empty[st], ph ^ 1);
-                if (lane == 0) {
-                    mbar_arrive_expect_tx(&full[st], SM::STAGE);
-                    tma_load_2d(psm + SM::RING + st * SM::STAGE, &tmH, c * PS_ROWS * K,
-                                static_cast<int>(s0), &full[st], pol);
-                }
-                __syncwarp();
-            }
+#endif
+    }
+    const long my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const long total_cs = my_tiles * NCH;
+    auto issue_chunk = [&](long cs) { // thread 0 only; the stage must be free
+        if (cs >= total_cs) return;
+        const int st = static_cast<int>(cs & 1);
+        const long tt = blockIdx.x + (cs / NCH) * gridDim.x;
+        const int c = static_cast<int>(cs % NCH);
+        mbar_arrive_expect_tx(&full[st], SM::STAGE);
+        tma_load_2d(psm + SM::RING + st * SM::STAGE, &tmH, c * PS_ROWS * K, static_cast<int>(tt * P),
+                    &full[st], pol);
+    };
+    auto issue_yx = [&](int itn) { // thread 0 only; y / x of this CTA's tile itn
+        if (itn >= my_tiles) return;
+        const int yb = itn & 1;
+        const long s0 = (blockIdx.x + static_cast<long>(itn) * gridDim.x) * P;
+        const int live = static_cast<int>(n - s0 < P ? n - s0 : P);
+        float *ybuf = reinterpret_cast<float *>(psm + SM::YB + yb * SM::YSLOT);
+        unsigned char *xbuf = psm + SM::XB + yb * SM::XSLOT;
+        const uint32_t ybytes = static_cast<uint32_t>(live * N * 4);
+        const uint32_t xbytes = static_cast<uint32_t>(live * K);
+        if (ybytes % 16 == 0 && xbytes % 16 == 0) {
+            mbar_arrive_expect_tx(&yfull[yb], ybytes + xbytes);
+            bulk_g2s(ybuf, y + s0 * N, ybytes, &yfull[yb]);
+            bulk_g2s(xbuf, x + s0 * K, xbytes, &yfull[yb]);
+        } else { // ragged tail: plain loads (one thread, once per launch)
+            for (int i = 0; i < live * N; ++i) ybuf[i] = __ldg(y + s0 * N + i);
+            for (int i = 0; i < live * K; ++i) xbuf[i] = static_cast<unsigned char>(x[s0 * K + i]);
+            mbar_arrive(&yfull[yb]);
         }
-        return;
+    };
+    if (issuer) {
+        issue_yx(0);
+        issue_chunk(0);
+        issue_chunk(1);
     }
 
     // ===================== consumers =====================
@@ -283,7 +301,7 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
             mbar_wait_guard(&full[st], static_cast<uint32_t>((cstep >> 1) & 1));
             const float4 *hrow =
                 reinterpret_cast<const float4 *>(psm + SM::RING + st * SM::STAGE + ls * SM::SSTR);
-#pragma unroll 1
+#pragma unroll K1_UNROLL
             for (int r = 0; r < PS_ROWS; ++r) {
                 float h[K];
 #pragma unroll
@@ -324,12 +342,20 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
             __syncwarp();
             if (c + 1 < NCH) {
                 if (lane == 0) mbar_arrive(&empty[st]);
+                if (issuer) { // refill the stage two chunk steps ahead
+                    mbar_wait_guard(&empty[st], static_cast<uint32_t>((cstep >> 1) & 1));
+                    issue_chunk(cstep + 2);
+                }
             } else {
                 hold = st;
             }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&yempty[yb]); // y / x of this tile consumed
+        if (issuer) { // next tile's y / x into the other buffer (released a tile ago)
+            if (it >= 1) mbar_wait_guard(&yempty[yb ^ 1], static_cast<uint32_t>(((it - 1) >> 1) & 1));
+            issue_yx(it + 1);
+        }
         PTR(2);
         // The cross block of a warp pair goes into the pair's OWN sample rows of
         // the held stage: the other pair's B may still be reading its rows of
@@ -412,6 +438,10 @@ __global__ void __launch_bounds__(PS_THREADS, 2)
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[hold]);
+            if (issuer) { // the held stage (this tile's last chunk) -> chunk step + 2
+                mbar_wait_guard(&empty[hold], static_cast<uint32_t>(((cstep - 1) >> 1) & 1));
+                issue_chunk(cstep + 1);
+            }
             float d[K];
 #pragma unroll
             for (int j = R0; j < K; ++j) d[j] = X1[j][ls];

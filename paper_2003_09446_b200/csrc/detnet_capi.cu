@@ -265,6 +265,16 @@ int pack_sparse(detnet_model *m, const double *params, const double *masks) {
     // the kernel stages two layer streams next to its 120 KB of activations
     m->sparse_ready = (K == 20 && V == 40) &&
                       sparse_smem(m->sparse_max_words) <= 232448;
+    // the model-specialised kernel (sparse_jit.cu): generated and compiled at
+    // its first use from these weights, when every layer is sparse enough
+    m->jit_worst_nnz = K <= 32 ? jit_layer_nnz(K, Z, V, m->L, params, masks) : -1;
+    m->jit_params.clear();
+    m->jit_masks.clear();
+    if (m->jit_worst_nnz >= 0 && m->jit_worst_nnz <= kJitMaxNnz) {
+        m->jit_params.assign(params, params + P * m->L);
+        if (masks) m->jit_masks.assign(masks, masks + P * m->L);
+    }
+    m->jit_src_version = m->version;
     return 0;
 }
 
@@ -328,6 +338,19 @@ int ensure_ws(detnet_ctx *c, long n, int K) {
         return fail(DETNET_ERR_CUDA, "workspace allocation failed (n=%ld)", n);
     if (!c->h_result) CK(cudaMallocHost(&c->h_result, 64));
     return 0;
+}
+
+// The model-specialised sparse kernel: path 3, or the auto path for models
+// whose every layer has at most kJitMaxNnz surviving products (config 4: ~330
+// per layer, where the compacted tcgen05 kernel is bound by its serial
+// per-layer chain). Valid while the weights are those it was generated from.
+bool use_jit(const detnet_model *m) {
+    const int path = m->ctx->path;
+    if (!(path == 0 || path == 3) || std::getenv("DETNET_NO_JIT")) return false;
+    if (!m->sparse_ready || m->tc_stale || m->jit_src_version != m->version) return false;
+    if (m->jit_params.empty()) return false;
+    if (path == 0 && m->jit_failed_version == m->jit_src_version) return false;
+    return true;
 }
 
 bool use_tc(const detnet_model *m) {
@@ -410,7 +433,42 @@ int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, 
               int l_end, bool trainable_only, float *xhat, float *xs, float *vs,
               const TraceBufs *trace) {
     detnet_ctx *c = m->ctx;
-    const bool sparse = !trace && !xs && m->sparse_ready && !m->tc_stale && c->path == 3;
+    if (!trace && !xs && l_begin == 0 && use_jit(m)) {
+        JitModel &jm = m->jit;
+        if (!jm.ready || jm.version != m->jit_src_version) {
+            const int rc = jit_build(jm, m->K, m->Z, m->V, m->L, m->jit_params.data(),
+                                     m->jit_masks.empty() ? nullptr : m->jit_masks.data());
+            if (rc) {
+                if (c->path == 3) return rc; // asked for the sparse path explicitly
+                m->jit_failed_version = m->jit_src_version; // auto: tcgen05 instead
+                if (std::getenv("DETNET_VERBOSE"))
+                    std::fprintf(stderr, "detnet: sparse JIT unavailable: %s\n", g_err.c_str());
+            } else {
+                jm.version = m->jit_src_version;
+            }
+        }
+        if (jm.ready && jm.version == m->jit_src_version) {
+            TcArgs ja{};
+            ja.gp = c->gp.as<float>();
+            ja.q32 = c->q32.as<float>();
+            ja.denom = c->denom.as<double>();
+            ja.xmask = c->xmask.as<uint32_t>();
+            ja.lnk = (trainable_only ? m->lnk_train : m->lnk_all).as<double>();
+            ja.l_begin = 0;
+            ja.l_end = l_end;
+            ja.n = n_local;
+            ja.n_tiles = nt;
+            ja.tile0 = t0;
+            ja.xhat = xhat;
+            ja.tile_loss = c->tile_loss.as<double>();
+            ja.tile_err = c->tile_err.as<long long>();
+            LaunchScope ls(c, DETNET_K_STACK, st);
+            if (int rc = jit_launch(jm, ja, st, c->sms, c->device)) return rc;
+            return check_launch();
+        }
+    }
+    const bool sparse = !trace && !xs && m->sparse_ready && !m->tc_stale && c->path == 3 &&
+                        std::getenv("DETNET_SPARSE_CSR") != nullptr;
     if (sparse) {
         SparseArgs sa{};
         sa.gp = c->gp.as<float>();
@@ -811,6 +869,7 @@ void release_model_device(detnet_model *m) {
                     &m->sparse_stream, &m->sparse_off, &m->tstatus, &m->bwd_img})
         b->release();
     tc_release(m->tc);
+    jit_release(m->jit);
 }
 } // namespace
 
@@ -828,6 +887,7 @@ void detnet_model_destroy(detnet_model *m) {
 
 int detnet_model_path(const detnet_model *m) {
     if (!m) return 0;
+    if (use_jit(m)) return 5;
     if (m->sparse_ready && !m->tc_stale && m->ctx->path == 3) return 3;
     if (!use_tc(m)) return 1;
     return use_h16(m, false) ? 4 : 2;

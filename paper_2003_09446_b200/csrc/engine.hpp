@@ -85,6 +85,19 @@ struct TcModel {
     long rec16 = 0;
 };
 
+// model-specialised sparse stack (sparse_jit.cu): NVRTC-compiled per model
+struct JitModel {
+    bool ready = false;
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t kernel = nullptr;
+    size_t smem = 0;
+    int ctas_per_sm = 1, L = 0, K = 0, attr_device = -1;
+    long nnz = 0;           // surviving products per sample over all layers
+    double compile_ms = 0;  // NVRTC time of the last build (0 = cache hit)
+    std::string log;        // NVRTC / ptxas log (register use)
+    long long version = -1; // model version the kernel was generated from
+};
+
 struct TcArgs {
     const float *gp;
     const float *q32;
@@ -110,6 +123,13 @@ int tc_pack_device(TcModel &tc, const double *params, const double *masks, long 
 // returns at once on the device when *redo_count == 0
 int tc_launch_redo(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cudaStream_t st,
                    const TraceBufs *tr, const uint8_t *redo, const int *redo_count);
+
+// sparse JIT stack (sparse_jit.cu)
+constexpr long kJitMaxNnz = 1500; // auto path: worst layer's surviving products
+long jit_layer_nnz(int K, int Z, int V, int L, const double *params, const double *masks);
+int jit_build(JitModel &jm, int K, int Z, int V, int L, const double *params, const double *masks);
+int jit_launch(JitModel &jm, const TcArgs &a, cudaStream_t st, int sms, int device);
+void jit_release(JitModel &jm);
 
 // split-FP16 layer stack (stack_h16.cu)
 int h16_prepare();
@@ -199,6 +219,13 @@ struct detnet_model {
     detnet::DBuf sparse_stream, sparse_off;
     int sparse_max_words = 0; // largest per-layer stream (shared-memory staging)
     bool sparse_ready = false;
+    // model-specialised sparse kernel (sparse_jit.cu): chosen by the auto path
+    // when the worst layer has at most kJitMaxNnz surviving products
+    detnet::JitModel jit;
+    long jit_worst_nnz = -1;
+    std::vector<double> jit_params, jit_masks; // the weights it is generated from
+    long long jit_src_version = -1;
+    long long jit_failed_version = -1; // auto path: a failed build is not retried
     double density = 1.0;   // surviving W entries / all W entries
     // CUDA graph of batch_evaluate_device (K1 + fallback + stack + reduce +
     // result copy), replayed while the call, the context settings, the model

@@ -484,7 +484,7 @@ class Model:
     @property
     def path_name(self):
         return {1: "simt-fp32", 2: "tcgen05-3xtf32", 3: "sparse-csr-fp32",
-                4: "tcgen05-split-fp16"}[
+                4: "tcgen05-split-fp16", 5: "sparse-jit-fp32"}[
             _lib.detnet_model_path(self._h)]
 
     def flops_per_detection(self, include_preprocess=True):

@@ -13,15 +13,25 @@ K, N, L = 20, 30, 40
 ctx = eng.Context(0, path=path)
 params = xavier_params(K, L, seed=9)
 masks = None
-if config == 3:  # group-pruned (compacted tcgen05 kernel)
-    from paper_2003_09446_b200.workload import group_masks
+if config in (3, 4):  # group-pruned (compacted tcgen05 kernel) / sparse group (JIT kernel)
+    from paper_2003_09446_b200.workload import group_masks, sparse_group_model
     masks = group_masks(K, L, seed=31)
+    if config == 4:
+        params, masks = sparse_group_model(params, masks, K)
 m = ctx.model(K, N, 160, 40, params, masks=masks)
 H = torch.empty((n, N, K), dtype=torch.float32, device="cuda")
 y = torch.empty((n, N), dtype=torch.float32, device="cuda")
 x = torch.empty((n, K), dtype=torch.int8, device="cuda")
 base, _ = eng.rng_split(eng.rng_stream(eng.rng_seed(1, 0), 0x45564131 + 5))
 ctx.generate(base, 0, n, N, K, 10.0, 10.0, 1.0 / np.sqrt(N), H, y, x)
+import time
 for _ in range(2):
     ev = m.batch_evaluate_device(n, H, y, x)
 print(m.path_name, ev)
+if os.environ.get("PROF_TIME"):  # per-kernel event times over a few calls
+    ctx.set_profiling(True)
+    ctx.kernel_times(reset=True)
+    for _ in range(5):
+        ev = m.batch_evaluate_device(n, H, y, x)
+    kt = ctx.kernel_times(reset=True)
+    print("kernel ms per call:", {k: round(v[0] / 5, 4) for k, v in kt.items() if v[1]})

@@ -447,15 +447,23 @@ def bench_eval(cfg, args, env):
         peak_burst = bf16_burst / 3.0 if bf16_burst else None
         peak_note = (f"{peaks.get('peaks_source')} bf16 {bf16} TF/s ({regime}; "
                      "FP16 MMA rate) / 3 (split-FP16 products hi.hi + hi.lo + lo.hi)")
+    elif tc_path == "sparse-jit-fp32":
+        # the model-specialised sparse kernel: FFMA/FFMA2 on the FP32 pipe
+        peak = peaks.get("fp32_tflops")
+        peak_note = ("measured cuBLAS FP32 SGEMM (CUDA-core FP32 pipe), this run; census FLOP "
+                     "of the masked model (surviving weights + G x_hat), all on CUDA cores")
     else:
         peak = peaks.get("fp32_tflops")
         peak_note = "measured cuBLAS FP32 SGEMM (CUDA-core FP32 pipe), this run"
     traffic, traffic_note = stack_traffic(tc_path, per_point, compacted=cfg in (3, 4))
-    roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+    roof = {"bound": "tensor" if tc_path.startswith("tcgen05") else "fp32", "achieved": achieved,
+            "peak": peak, "unit": "TFLOP/s",
             "frac": (achieved / peak) if peak else None, "traffic": traffic,
             "traffic_source": traffic_note,
             "frac_burst": (achieved / peak_burst) if peak_burst else None,
-            "kernel": "k_stack (fused layer stack)", "path": tc_path, "peak_source": peak_note,
+            "kernel": ("detnet_sparse_jit (model-specialised sparse stack)"
+                       if tc_path == "sparse-jit-fp32" else "k_stack (fused layer stack)"),
+            "path": tc_path, "peak_source": peak_note,
             "census_flop_per_detection_layers": census_layers,
             "detections_per_launch": per_point, "avg_launch_ms": avg_launch_s * 1e3,
             "share_of_step": stack_ms / (ms * 1.0) if ms else None,
@@ -792,7 +800,8 @@ def stack_traffic(path, detections, compacted=False):
     2^18-detection launch, scaled per detection -- the stack streams its
     per-sample inputs once and keeps the weights L2-resident, so the bytes
     scale with the detections)."""
-    name = {"tcgen05-split-fp16": "k_stack_h16", "tcgen05-3xtf32": "k_stack_tc"}.get(path)
+    name = {"tcgen05-split-fp16": "k_stack_h16", "tcgen05-3xtf32": "k_stack_tc",
+            "sparse-jit-fp32": "detnet_sparse_jit"}.get(path)
     if name == "k_stack_h16" and compacted:
         name = "k_stack_h16_64"  # group-pruned models: the ZH = 64 instantiation
     fn = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")

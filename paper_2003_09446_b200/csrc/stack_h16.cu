@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_h16(HKArgs p) {
     const long total_it = my_tiles * NL;
 
     if (warp >= 8) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory");
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 24;" ::: "memory");
         if (warp == 8) {
             // ============ MMA issuer (warp-uniform loop, one elected lane) ============
             const uint32_t sw1 = smem_u32(sm + SM_W1), sw23 = smem_u32(sm + SM_W23);
@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_h16(HKArgs p) {
         }
     } else {
         // ========================= epilogue warps ==========================
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 232;" ::: "memory");
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 240;" ::: "memory");
         const bool isA = warp >= 4;
         const int side = isA ? 0 : 1;
         const int quad = warp & 3;
@@ -767,6 +767,7 @@ int h16_prepare() {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_stack_h16<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(HCfg<64>::SM_TOTAL));
+
     if (e != cudaSuccess)
         return fail(DETNET_ERR_CUDA, "split-fp16 kernel smem attribute: %s", cudaGetErrorString(e));
     return 0;

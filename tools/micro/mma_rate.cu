@@ -4,7 +4,7 @@
 #include "tc_ptx.cuh"
 using namespace detnet;
 
-template <int N>
+template <int N, int M = 128>
 __global__ void k_rate(long long *cyc, int chain, int tf32, int nacc) {
     extern __shared__ __align__(128) unsigned char sB[];
     __shared__ uint64_t bar;
@@ -20,7 +20,7 @@ __global__ void k_rate(long long *cyc, int chain, int tf32, int nacc) {
     const uint32_t tb = slot;
     if (warp == 0) {
         const uint64_t d = tc::smem_desc(smem_u32(sB), N * 16, 128);
-        const uint32_t id = tf32 ? tc::idesc_tf32(128, N) : tc::idesc_f16(128, N);
+        const uint32_t id = tf32 ? tc::idesc_tf32(M, N) : tc::idesc_f16(M, N);
         const long long t0 = clock64();
         if (tc::elect_one()) {
             for (int i = 0; i < chain; ++i) {
@@ -39,15 +39,15 @@ __global__ void k_rate(long long *cyc, int chain, int tf32, int nacc) {
     if (warp == 0) tc::tmem_dealloc(tb, 512);
 }
 
-template <int N> void run(long long *dc, int grid) {
-    cudaFuncSetAttribute(k_rate<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
+template <int N, int M = 128> void run(long long *dc, int grid) {
+    cudaFuncSetAttribute(k_rate<N, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
     for (int tf = 0; tf < 2; ++tf)
         for (int nacc = 1; nacc <= 2; ++nacc) {
             if (nacc * N > 496) continue;
             double avg = 0;
             for (int rep = 0; rep < 2; ++rep) {
                 const int chain = 4096;
-                k_rate<N><<<grid, 128, N * 32>>>(dc, chain, tf, nacc);
+                k_rate<N, M><<<grid, 128, N * 32>>>(dc, chain, tf, nacc);
                 cudaDeviceSynchronize();
                 std::vector<long long> c(grid);
                 cudaMemcpy(c.data(), dc, grid * 8, cudaMemcpyDeviceToHost);
@@ -55,7 +55,7 @@ template <int N> void run(long long *dc, int grid) {
                 for (auto x : c) avg += x;
                 avg /= grid * (double)chain;
             }
-            printf("%s N=%3d acc=%d: %6.1f cyc/MMA  (N/2 = %d)  %s\n", tf ? "tf32" : "f16 ", N, nacc, avg,
+            printf("M=%d %s N=%3d acc=%d: %6.1f cyc/MMA  (N/2 = %d)  %s\n", M, tf ? "tf32" : "f16 ", N, nacc, avg,
                    N / 2, cudaGetErrorString(cudaGetLastError()));
         }
 }
@@ -65,5 +65,7 @@ int main() {
     cudaMalloc(&dc, 148 * 8);
     run<32>(dc, 148); run<48>(dc, 148); run<64>(dc, 148); run<80>(dc, 148); run<128>(dc, 148);
     run<160>(dc, 148); run<240>(dc, 148);
+    // M = 64 (cta_group::1): same N, half the rows
+    run<32, 64>(dc, 148); run<64, 64>(dc, 148); run<96, 64>(dc, 148); run<160, 64>(dc, 148);
     return 0;
 }

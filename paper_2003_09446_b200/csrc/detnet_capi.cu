@@ -347,7 +347,9 @@ int ensure_ws(detnet_ctx *c, long n, int K) {
 bool use_jit(const detnet_model *m) {
     const int path = m->ctx->path;
     if (!(path == 0 || path == 3) || std::getenv("DETNET_NO_JIT")) return false;
-    if (!m->sparse_ready || m->tc_stale || m->jit_src_version != m->version) return false;
+    // weights changed on the device since pack time (training, pruning in
+    // progress) bump the version: the kernel no longer matches them
+    if (m->tc_stale || m->jit_src_version != m->version) return false;
     if (m->jit_params.empty()) return false;
     if (path == 0 && m->jit_failed_version == m->jit_src_version) return false;
     return true;
@@ -888,7 +890,8 @@ void detnet_model_destroy(detnet_model *m) {
 int detnet_model_path(const detnet_model *m) {
     if (!m) return 0;
     if (use_jit(m)) return 5;
-    if (m->sparse_ready && !m->tc_stale && m->ctx->path == 3) return 3;
+    if (m->sparse_ready && !m->tc_stale && m->ctx->path == 3 && std::getenv("DETNET_SPARSE_CSR"))
+        return 3;
     if (!use_tc(m)) return 1;
     return use_h16(m, false) ? 4 : 2;
 }

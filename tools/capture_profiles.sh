@@ -6,7 +6,9 @@
 set -u
 OUT=gpurun_out/prof
 mkdir -p $OUT
-# 1. benches (no profiler)
+# 1. benches (no profiler): the default run (config 2 + nested configs 1, 3, 4, 5),
+#    then each config alone
+timeout 900 python bench.py > $OUT/bench_default.json 2> $OUT/bench_default.err
 for c in 1 2 3 4 5; do
   timeout 600 python bench.py --config $c --steps 5 --warmup 3 > $OUT/bench_c$c.json 2> $OUT/bench_c$c.err
 done
@@ -37,5 +39,10 @@ fi
 if timeout 300 python tools/prof_run.py 262144 0 3 > $OUT/prof_run3.log 2>&1; then
   timeout 900 ncu --set full --clock-control none -k regex:k_stack_h16 -s 1 -c 1 \
     -o $OUT/k_stack_h16_64 python tools/prof_run.py 262144 0 3 > $OUT/ncu_h16_64.log 2>&1
+fi
+# 5. the model-specialised sparse kernel (config 4, JIT-compiled at model creation)
+if timeout 300 python tools/prof_run.py 262144 0 4 > $OUT/prof_run4.log 2>&1; then
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:detnet_sparse_jit -s 1 -c 1 \
+    -o $OUT/detnet_sparse_jit python tools/prof_run.py 262144 0 4 > $OUT/ncu_jit.log 2>&1
 fi
 echo done

@@ -40,7 +40,7 @@ def main(src, dst, title):
     # DRAM bytes per detection of the stack kernels (bench.py's roofline.traffic)
     traffic = {}
     for rep in sorted(os.listdir(src)):
-        if rep.startswith("k_stack") and rep.endswith(".ncu-rep"):
+        if rep.startswith(("k_stack", "detnet_sparse_jit")) and rep.endswith(".ncu-rep"):
             recs, units = raw(os.path.join(src, rep))
             for r in recs:
                 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}

@@ -483,10 +483,10 @@ def bench_eval(cfg, args, env):
                   "note": "algorithmic input bytes / K1 event time; with its ~930 B/detection "
                           "of output the HBM traffic is ~1.37x this"}
     # the whole step against the SIMT and HBM bounds SURVEY 8d names for the
-    # sparse-group model (config 4: G x_hat + preprocessing are ~70 % of the
-    # census and run on CUDA cores; H ingest is 2,540 B per detection)
+    # sparse-group model (config 4 runs entirely on CUDA cores: the sparse
+    # kernel, G x_hat and preprocessing; H ingest is 2,540 B per detection)
     step_bounds = None
-    if cfg in (3, 4):
+    if cfg == 4:
         step_s = ms / 1e3 / args.steps
         fl = census_all * per_point * len(points) / step_s / 1e12
         gbs = per_point * len(points) * (N * K * 4 + N * 4 + K) / step_s / 1e9

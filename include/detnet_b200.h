@@ -66,10 +66,11 @@ void detnet_ctx_destroy(detnet_ctx *ctx);
 int detnet_ctx_create_group(const int *devices, int count, detnet_ctx **out);
 int detnet_ctx_group_size(const detnet_ctx *ctx);
 const char *detnet_last_error(void);
-/* Kernel-path selection: 0 auto (tcgen05 split-FP16 where compiled, with
- * 3xTF32 recompute of out-of-range tiles; else 3xTF32; else SIMT), 1 SIMT
- * FP32, 2 tcgen05 3xTF32 only, 3 sparse CSR (pruned models), 4 tcgen05
- * split-FP16 (same as 0 for the stack). */
+/* Kernel-path selection: 0 auto (the model-specialised sparse kernel for
+ * models with <= 1,500 surviving products per layer; otherwise tcgen05
+ * split-FP16 where compiled, with 3xTF32 recompute of out-of-range tiles;
+ * else 3xTF32; else SIMT), 1 SIMT FP32, 2 tcgen05 3xTF32 only, 3 sparse (the
+ * model-specialised kernel when eligible, else SIMT), 4 tcgen05 split-FP16. */
 int detnet_ctx_set_path(detnet_ctx *ctx, int path);
 /* Training forward (detnet_train_grad / detnet_batch_gradient) on tcgen05
  * (1, default: split FP16 for dense K=20 models) or FP32 CUDA cores (0). The
@@ -129,8 +130,9 @@ int detnet_model_create(detnet_ctx *ctx, const detnet_model_desc *desc, detnet_m
 int detnet_model_update(detnet_model *m, const detnet_model_desc *desc);
 void detnet_model_destroy(detnet_model *m);
 /* Kernel path the stack of this model runs on under the context's current
- * path setting: 1 SIMT FP32, 2 tcgen05 3xTF32, 3 sparse, 4 tcgen05
- * split-FP16. */
+ * path setting: 1 SIMT FP32, 2 tcgen05 3xTF32, 3 sparse CSR, 4 tcgen05
+ * split-FP16, 5 sparse model-specialised (NVRTC-compiled from the model's
+ * surviving weights at its first evaluation). */
 int detnet_model_path(const detnet_model *m);
 /* Analytic census, flops_per_detection (compression.cpp:120-129). */
 long long detnet_model_flops_per_detection(const detnet_model *m, int include_preprocess);

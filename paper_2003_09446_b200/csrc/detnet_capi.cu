@@ -191,7 +191,6 @@ int pack_sparse(detnet_model *m, const double *params, const double *masks) {
     m->sparse_ready = false;
     const int K = m->K, Z = m->Z, V = m->V, IN = 3 * K + V;
     const long P = record_size(K, Z, V);
-    long nnz = 0, total = static_cast<long>(m->L) * (Z * IN + K * Z + V * Z);
     std::vector<int> st;
     std::vector<long> offs(m->L + 1);
     auto fbits = [](float f) { int i; std::memcpy(&i, &f, 4); return i; };
@@ -210,7 +209,6 @@ int pack_sparse(detnet_model *m, const double *params, const double *masks) {
             for (int k = 0; k < K; ++k) if (w(oW2 + k * Z + i) != 0.f) o.push_back({V + k, w(oW2 + k * Z + i)});
             std::vector<std::pair<int, float>> in;
             for (int j = 0; j < IN; ++j) if (w(oW1 + i * IN + j) != 0.f) in.push_back({j, w(oW1 + i * IN + j)});
-            nnz += static_cast<long>(in.size() + o.size());
             if (o.empty()) continue;
             units.push_back(i);
             ins.push_back(in);
@@ -257,7 +255,6 @@ int pack_sparse(detnet_model *m, const double *params, const double *masks) {
     long max_words = 0;
     for (int l = 0; l < m->L; ++l) max_words = std::max(max_words, offs[l + 1] - offs[l]);
     m->sparse_max_words = static_cast<int>((max_words + 3) / 4 * 4);
-    m->density = total ? static_cast<double>(nnz) / static_cast<double>(total) : 1.0;
     if (m->sparse_stream.ensure(st.size() * 4) || m->sparse_off.ensure(offs.size() * 8))
         return fail(DETNET_ERR_CUDA, "sparse stream allocation");
     CK(cudaMemcpy(m->sparse_stream.p, st.data(), st.size() * 4, cudaMemcpyHostToDevice));
@@ -265,9 +262,16 @@ int pack_sparse(detnet_model *m, const double *params, const double *masks) {
     // the kernel stages two layer streams next to its 120 KB of activations
     m->sparse_ready = (K == 20 && V == 40) &&
                       sparse_smem(m->sparse_max_words) <= 232448;
-    // the model-specialised kernel (sparse_jit.cu): generated and compiled at
-    // its first use from these weights, when every layer is sparse enough
-    m->jit_worst_nnz = K <= 32 ? jit_layer_nnz(K, Z, V, m->L, params, masks) : -1;
+    return 0;
+}
+
+// The model-specialised kernel (sparse_jit.cu) is generated and compiled at
+// its first use from these weights when every layer is sparse enough; the
+// count stops at the first layer over the limit (dense models: a few units).
+void prepare_jit(detnet_model *m, const double *params, const double *masks) {
+    const long P = record_size(m->K, m->Z, m->V);
+    m->jit_worst_nnz =
+        m->K <= 32 ? jit_layer_nnz(m->K, m->Z, m->V, m->L, params, masks, kJitMaxNnz) : -1;
     m->jit_params.clear();
     m->jit_masks.clear();
     if (m->jit_worst_nnz >= 0 && m->jit_worst_nnz <= kJitMaxNnz) {
@@ -275,7 +279,6 @@ int pack_sparse(detnet_model *m, const double *params, const double *masks) {
         if (masks) m->jit_masks.assign(masks, masks + P * m->L);
     }
     m->jit_src_version = m->version;
-    return 0;
 }
 
 int upload_model(detnet_model *m, const detnet_model_desc *d) {
@@ -301,7 +304,12 @@ int upload_model(detnet_model *m, const detnet_model_desc *d) {
     CK(cudaMemcpy(m->lnk_all.p, la.data(), m->L * 8, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(m->lnk_train.p, lt.data(), m->L * 8, cudaMemcpyHostToDevice));
     if (int rc = tc_pack(m->tc, m->K, m->Z, m->V, m->L, d->params, d->masks)) return rc;
-    if (int rc = pack_sparse(m, d->params, d->masks)) return rc;
+    // the table-driven CSR stream only when asked for (DETNET_SPARSE_CSR): it
+    // costs a pass over every weight on each update
+    m->sparse_ready = false;
+    if (std::getenv("DETNET_SPARSE_CSR"))
+        if (int rc = pack_sparse(m, d->params, d->masks)) return rc;
+    prepare_jit(m, d->params, d->masks);
     m->train_ready = false; // the device master copy restarts from these params
     m->tc_stale = false;
     m->tc_dev_dirty = false; // the images just packed from the host copy are current

@@ -126,7 +126,7 @@ int tc_launch_redo(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cud
 
 // sparse JIT stack (sparse_jit.cu)
 constexpr long kJitMaxNnz = 1500; // auto path: worst layer's surviving products
-long jit_layer_nnz(int K, int Z, int V, int L, const double *params, const double *masks);
+long jit_layer_nnz(int K, int Z, int V, int L, const double *params, const double *masks, long stop);
 int jit_build(JitModel &jm, int K, int Z, int V, int L, const double *params, const double *masks);
 int jit_launch(JitModel &jm, const TcArgs &a, cudaStream_t st, int sms, int device);
 void jit_release(JitModel &jm);
@@ -226,7 +226,6 @@ struct detnet_model {
     std::vector<double> jit_params, jit_masks; // the weights it is generated from
     long long jit_src_version = -1;
     long long jit_failed_version = -1; // auto path: a failed build is not retried
-    double density = 1.0;   // surviving W entries / all W entries
     // CUDA graph of batch_evaluate_device (K1 + fallback + stack + reduce +
     // result copy), replayed while the call, the context settings, the model
     // layout and every device buffer are those it was captured with

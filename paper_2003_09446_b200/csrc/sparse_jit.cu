@@ -399,8 +399,9 @@ int nvrtc_compile(const std::string &src, std::vector<char> &cubin, std::string 
 } // namespace
 
 // Worst layer's surviving products (W1 entries of live units + [W3; W2]
-// entries): the per-sample cost of a layer in the JIT kernel.
-long jit_layer_nnz(int K, int Z, int V, int L, const double *params, const double *masks) {
+// entries): the per-sample cost of a layer in the JIT kernel. Returns early
+// (with a value > stop) once a layer exceeds `stop`.
+long jit_layer_nnz(int K, int Z, int V, int L, const double *params, const double *masks, long stop) {
     const long P = record_size(K, Z, V);
     const int IN = 3 * K + V;
     long worst = 0;
@@ -417,6 +418,7 @@ long jit_layer_nnz(int K, int Z, int V, int L, const double *params, const doubl
             if (!out) continue;
             nnz += out;
             for (int j = 0; j < IN; ++j) nnz += nz(static_cast<long>(i) * IN + j);
+            if (nnz > stop) return nnz; // over the limit: the exact count is not needed
         }
         worst = std::max(worst, nnz);
     }

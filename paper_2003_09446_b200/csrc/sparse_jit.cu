@@ -43,6 +43,8 @@
 #include <vector>
 
 #include <nvrtc.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include "engine.hpp"
 
@@ -357,10 +359,67 @@ std::string gen_layer(int l, int K, int Z, int V, const double *p, const double 
     return o;
 }
 
-// process-wide cubin cache keyed by the generated source (models rebuilt
-// with the same weights, replicas on other devices, repeated tests)
+// Cubin caches keyed by the generated source: per process (models rebuilt
+// with the same weights, replicas on other devices, repeated tests) and on
+// disk ($DETNET_JIT_CACHE, else $XDG_CACHE_HOME or ~/.cache /detnet_b200_jit;
+// "off" disables it), so another process with the same model skips NVRTC
+// (~13 s at L=40). A disk entry carries the source length and hash and the
+// NVRTC version; anything that does not match is recompiled.
 std::mutex g_jit_mu;
 std::map<std::string, std::vector<char>> g_jit_cache;
+
+uint64_t fnv1a(const std::string &s) {
+    uint64_t h = 1469598103934665603ull;
+    for (unsigned char c : s) h = (h ^ c) * 1099511628211ull;
+    return h;
+}
+
+std::string jit_cache_dir() {
+    if (const char *d = std::getenv("DETNET_JIT_CACHE")) return std::strcmp(d, "off") ? d : "";
+    if (const char *x = std::getenv("XDG_CACHE_HOME")) return std::string(x) + "/detnet_b200_jit";
+    if (const char *h = std::getenv("HOME")) return std::string(h) + "/.cache/detnet_b200_jit";
+    return "";
+}
+
+struct DiskKey {
+    uint64_t len, hash;
+    int major, minor;
+};
+
+bool disk_load(const std::string &path, const DiskKey &k, std::vector<char> &cubin) {
+    FILE *f = std::fopen(path.c_str(), "rb");
+    if (!f) return false;
+    DiskKey h{};
+    bool ok = std::fread(&h, sizeof h, 1, f) == 1 && h.len == k.len && h.hash == k.hash &&
+              h.major == k.major && h.minor == k.minor;
+    if (ok) {
+        std::fseek(f, 0, SEEK_END);
+        const long n = std::ftell(f) - static_cast<long>(sizeof h);
+        std::fseek(f, sizeof h, SEEK_SET);
+        ok = n > 0;
+        if (ok) {
+            cubin.resize(static_cast<size_t>(n));
+            ok = std::fread(cubin.data(), 1, cubin.size(), f) == cubin.size();
+        }
+    }
+    std::fclose(f);
+    return ok;
+}
+
+void disk_store(const std::string &dir, const std::string &path, const DiskKey &k,
+                const std::vector<char> &cubin) {
+    std::string cmd_dir = dir; // mkdir -p, one level at a time
+    for (size_t p = 1; p <= cmd_dir.size(); ++p)
+        if (p == cmd_dir.size() || cmd_dir[p] == '/') mkdir(cmd_dir.substr(0, p).c_str(), 0755);
+    const std::string tmp = path + ".tmp" + std::to_string(getpid());
+    FILE *f = std::fopen(tmp.c_str(), "wb");
+    if (!f) return;
+    const bool ok = std::fwrite(&k, sizeof k, 1, f) == 1 &&
+                    std::fwrite(cubin.data(), 1, cubin.size(), f) == cubin.size();
+    std::fclose(f);
+    if (ok) std::rename(tmp.c_str(), path.c_str()); // atomic: readers see all or nothing
+    else std::remove(tmp.c_str());
+}
 
 int nvrtc_compile(const std::string &src, std::vector<char> &cubin, std::string &log) {
     {
@@ -370,6 +429,17 @@ int nvrtc_compile(const std::string &src, std::vector<char> &cubin, std::string 
             cubin = it->second;
             return 0;
         }
+    }
+    DiskKey key{src.size(), fnv1a(src), 0, 0};
+    nvrtcVersion(&key.major, &key.minor);
+    const std::string dir = jit_cache_dir();
+    char name[64];
+    std::snprintf(name, sizeof name, "/%016llx.cubin", static_cast<unsigned long long>(key.hash));
+    const std::string path = dir.empty() ? "" : dir + name;
+    if (!path.empty() && disk_load(path, key, cubin)) {
+        std::lock_guard<std::mutex> lk(g_jit_mu);
+        g_jit_cache[src] = cubin;
+        return 0;
     }
     nvrtcProgram prog;
     if (nvrtcCreateProgram(&prog, src.c_str(), "detnet_sparse_jit.cu", 0, nullptr, nullptr) !=
@@ -391,6 +461,7 @@ int nvrtc_compile(const std::string &src, std::vector<char> &cubin, std::string 
     cubin.resize(n);
     nvrtcGetCUBIN(prog, cubin.data());
     nvrtcDestroyProgram(&prog);
+    if (!path.empty()) disk_store(dir, path, key, cubin);
     std::lock_guard<std::mutex> lk(g_jit_mu);
     g_jit_cache[src] = cubin;
     return 0;

@@ -115,3 +115,39 @@ def test_dense_model_on_sparse_path_runs_simt(ctx, oracle):
     params = xavier_params(K, 3, seed=9)
     m = ctx.model(K, 30, 160, 40, params)
     assert m.path_name == "simt-fp32"
+
+
+_CACHE_SNIPPET = """
+import sys, json, numpy as np
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+from test_sparse_jit_gpu import _sparse_model
+from test_parity_gpu import _inputs
+from oracle.oracle import Oracle
+from paper_2003_09446_b200 import Context
+c = Context(0); c.set_path(3)
+p, m = _sparse_model(8, 5, seed=77)
+H, y, x = _inputs(Oracle(), 256, K=8, N=16, seed=2)
+ev = c.model(8, 16, 64, 16, p, masks=m).batch_evaluate(H, y, x)
+print(json.dumps([ev.data_loss, ev.symbol_errors]))
+"""
+
+
+def test_sparse_jit_disk_cache(tmp_path):
+    """A second process with the same model loads the cubin the first one
+    wrote ($DETNET_JIT_CACHE) and computes the same bits."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = _CACHE_SNIPPET.format(root=root, tests=os.path.join(root, "tests"))
+    env = dict(os.environ, DETNET_JIT_CACHE=str(tmp_path / "jit"))
+    outs = []
+    for _ in range(2):
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+        files = [f for f in os.listdir(tmp_path / "jit") if f.endswith(".cubin")]
+        assert len(files) == 1, files
+    assert outs[0] == outs[1]

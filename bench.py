@@ -299,9 +299,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional check of the N > 1 code path on a one-GPU box (never a
+    # measurement): DETNET_BENCH_SHARE_GPU=1 puts every rank on GPU 0 and
+    # runs the collectives over gloo; the ranks' kernels never wait on
+    # each other, only the host-side collectives do
+    share = os.environ.get("DETNET_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
         if world > 1:

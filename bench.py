@@ -436,17 +436,18 @@ def bench_eval(cfg, args, env):
     avg_launch_s = stack_ms / 1e3 / max(stack_launches, 1)
     achieved = flops_per_launch / avg_launch_s / 1e12
     tc_path = model.path_name
-    # B200_PROFILING.md: the burst bf16 figure for a kernel timed alone, the
-    # sustained (power-capped) one for a kernel timed inside a long step --
-    # steps of >= 10 ms of back-to-back launches run in the capped regime
-    long_step = ms / args.steps >= 10.0
-    regime = "sustained" if long_step else "burst"
-    bf16 = peaks.get("bf16_tflops_sustained" if long_step else "bf16_tflops")
-    bf16_burst = peaks.get("bf16_tflops")
-    peak_burst = None
+    # The roofline is quoted against the burst bf16 GEMM rate. B200_PROFILING.md
+    # allows the sustained (power-capped) figure for a kernel timed inside a
+    # long step, but MEASURED_PEAKS.json's sustained GEMM ran at a median
+    # ~1.36 GHz while this kernel holds ~1.8 GHz under the same cap, so the
+    # sustained fraction (frac_sustained, beside it) flatters the kernel.
+    regime = "burst"
+    bf16 = peaks.get("bf16_tflops")
+    bf16_sus = peaks.get("bf16_tflops_sustained")  # -> frac_sustained
+    peak_sus = None
     if tc_path == "tcgen05-3xtf32":
         peak = bf16 / 6.0 if bf16 else None
-        peak_burst = bf16_burst / 6.0 if bf16_burst else None
+        peak_sus = bf16_sus / 6.0 if bf16_sus else None
         peak_note = (f"{peaks.get('peaks_source')} bf16 {bf16} TF/s ({regime}) "
                      "/ 2 (TF32 rate) / 3 (3xTF32 split); this run's cuBLAS TF32 GEMM: "
                      f"{peaks.get('tf32_tflops', 0):.0f} TF/s")
@@ -454,7 +455,7 @@ def bench_eval(cfg, args, env):
         # FP16 MMAs run at the bf16 rate; every FP32-class product is three of
         # them (hi.hi + hi.lo + lo.hi)
         peak = bf16 / 3.0 if bf16 else None
-        peak_burst = bf16_burst / 3.0 if bf16_burst else None
+        peak_sus = bf16_sus / 3.0 if bf16_sus else None
         peak_note = (f"{peaks.get('peaks_source')} bf16 {bf16} TF/s ({regime}; "
                      "FP16 MMA rate) / 3 (split-FP16 products hi.hi + hi.lo + lo.hi)")
     elif tc_path == "sparse-jit-fp32":
@@ -470,7 +471,7 @@ def bench_eval(cfg, args, env):
             "peak": peak, "unit": "TFLOP/s",
             "frac": (achieved / peak) if peak else None, "traffic": traffic,
             "traffic_source": traffic_note,
-            "frac_burst": (achieved / peak_burst) if peak_burst else None,
+            "frac_sustained": (achieved / peak_sus) if peak_sus else None,
             "kernel": ("detnet_sparse_jit (model-specialised sparse stack)"
                        if tc_path == "sparse-jit-fp32" else "k_stack (fused layer stack)"),
             "path": tc_path, "peak_source": peak_note,
@@ -539,7 +540,7 @@ def bench_eval(cfg, args, env):
         large = {"detections": nb, "layers": L, "detections_per_s": nb / (msb / 1e3),
                  "ms_per_batch": msb, "stack_ms": sm_b, "roofline_achieved_tflops": ach_b,
                  "roofline_frac": (ach_b / peak) if peak else None,
-                 "roofline_frac_burst": (ach_b / peak_burst) if peak_burst else None,
+                 "roofline_frac_sustained": (ach_b / peak_sus) if peak_sus else None,
                  "note": "x_l not stored; inputs resident; same model and kernel"}
         del Hb, yb, xb
 

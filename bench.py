@@ -736,6 +736,10 @@ def bench_train(args, env):
                 ev_c.record(cs)
             return ev_c
 
+        # each step's loss sum (the raw buffer's last slot, after the
+        # all-reduce) is copied back to pinned host memory on the step's own
+        # stream: a device->host read per step that does not stall the host
+        losses = torch.empty(len(host), dtype=torch.float64).pin_memory()
         torch.cuda.synchronize()
         barrier()
         w0 = time.perf_counter()
@@ -744,8 +748,9 @@ def bench_train(args, env):
             main_s.wait_event(ready)
             if k + 1 < len(host):
                 ready = copy_in(k + 1)
-            ev_e = model.train_grad(per_gpu, *dev[k % 2], raw, want_eval=True)
+            model.train_grad(per_gpu, *dev[k % 2], raw, want_eval=False)
             allreduce_grad(dist if world > 1 else None, raw)
+            losses[k:k + 1].copy_(raw[-1:], non_blocking=True)
             model.train_apply(raw, n_global, kind=2, lam1=1e-4, lr0=1e-3)
         torch.cuda.synchronize()
         wall = torch.tensor([time.perf_counter() - w0], dtype=torch.float64, device="cuda")
@@ -753,9 +758,9 @@ def bench_train(args, env):
             dist.all_reduce(wall, op=dist.ReduceOp.MAX)
         e2e = {"value": n_global * args.steps / float(wall.item()), "unit": "samples/s",
                "h2d_bytes_per_step": int(sum(t.numel() * t.element_size() for t in dev[0])),
-               "d2h_bytes_per_step": 40,
+               "d2h_bytes_per_step": 8,
                "timer": "host wall clock around the per-step copies and C-ABI calls, max over ranks",
-               "last_step_loss": ev_e.data_loss}
+               "last_step_loss": float(losses[-1]) / n_global}
     out = None
     if rank == 0:
         cpu = None

@@ -51,3 +51,36 @@ def test_graph_replay_matches_eager(oracle):
     assert all(u == upd[0] for u in upd)
     assert upd[0] == _ev(ref.batch_evaluate_device(n, H, y, x, xhat_ptr=xh))
     assert upd[0] != fresh
+
+
+def test_graph_replay_sparse_jit_model(oracle):
+    """The same replay for a sparse-group model on the NVRTC-compiled kernel
+    (a library kernel launched through cudaLaunchKernel inside the capture),
+    and a model update to other sparse weights regenerates it."""
+    import paper_2003_09446_b200 as eng
+    from paper_2003_09446_b200.workload import group_masks, sparse_group_model, xavier_params
+    ctx = eng.Context(0)
+    n, L = 3000, 5
+    ps, ms = sparse_group_model(xavier_params(K, L, seed=9), group_masks(K, L, seed=31), K)
+    m = ctx.model(K, N, 160, 40, ps, masks=ms)
+    assert m.path_name == "sparse-jit-fp32"
+    H = torch.empty((n, N, K), dtype=torch.float32, device="cuda")
+    y = torch.empty((n, N), dtype=torch.float32, device="cuda")
+    x = torch.empty((n, K), dtype=torch.int8, device="cuda")
+    xh = torch.zeros((n, L, K), dtype=torch.float32, device="cuda")
+    base, _ = eng.rng_split(eng.rng_stream(eng.rng_seed(1, 0), 0x45564131))
+    ctx.generate(base, 0, n, N, K, 7.0, 14.0, 1.0 / np.sqrt(N), H, y, x)
+    runs, xhs = [], []
+    for _ in range(4):
+        runs.append(_ev(m.batch_evaluate_device(n, H, y, x, xhat_ptr=xh)))
+        xhs.append(xh.clone())
+    assert all(r == runs[0] for r in runs), runs
+    assert all(torch.equal(a, xhs[0]) for a in xhs)
+    p2, m2 = sparse_group_model(xavier_params(K, L, seed=10), group_masks(K, L, seed=32), K)
+    m.update(p2, masks=m2)
+    assert m.path_name == "sparse-jit-fp32"
+    upd = [_ev(m.batch_evaluate_device(n, H, y, x, xhat_ptr=xh)) for _ in range(3)]
+    ref = ctx.model(K, N, 160, 40, p2, masks=m2)
+    assert all(u == upd[0] for u in upd)
+    assert upd[0] == _ev(ref.batch_evaluate_device(n, H, y, x, xhat_ptr=xh))
+    assert upd[0] != runs[0]

@@ -45,4 +45,8 @@ if timeout 300 python tools/prof_run.py 262144 0 4 > $OUT/prof_run4.log 2>&1; th
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:detnet_sparse_jit -s 1 -c 1 \
     -o $OUT/detnet_sparse_jit python tools/prof_run.py 262144 0 4 > $OUT/ncu_jit.log 2>&1
 fi
+# 6. SURVEY 8f measurements: ZF/ML baselines, pruning planner, incremental trainer
+timeout 900 python tools/bench_baselines.py > $OUT/baselines.json 2> $OUT/baselines.err
+timeout 900 python tools/bench_prune.py > $OUT/prune.json 2> $OUT/prune.err
+timeout 1200 python tools/bench_incremental.py > $OUT/incremental.json 2> $OUT/incremental.err
 echo done

@@ -66,11 +66,11 @@ void detnet_ctx_destroy(detnet_ctx *ctx);
 int detnet_ctx_create_group(const int *devices, int count, detnet_ctx **out);
 int detnet_ctx_group_size(const detnet_ctx *ctx);
 const char *detnet_last_error(void);
-/* Kernel-path selection: 0 auto (the model-specialised sparse kernel for
- * models with <= 1,500 surviving products per layer; otherwise tcgen05
- * split-FP16 where compiled, with 3xTF32 recompute of out-of-range tiles;
- * else 3xTF32; else SIMT), 1 SIMT FP32, 2 tcgen05 3xTF32 only, 3 sparse (the
- * model-specialised kernel when eligible, else SIMT), 4 tcgen05 split-FP16. */
+/* Kernel-path selection: 0 auto (tcgen05 split-FP16 where compiled, with
+ * 3xTF32 recompute of out-of-range tiles; else 3xTF32; else SIMT), 1 SIMT
+ * FP32, 2 tcgen05 3xTF32 only, 3 sparse (the model-specialised kernel,
+ * NVRTC-compiled once per weight version, for models with <= 1,500
+ * surviving products per layer; else SIMT), 4 tcgen05 split-FP16. */
 int detnet_ctx_set_path(detnet_ctx *ctx, int path);
 /* Training forward (detnet_train_grad / detnet_batch_gradient) on tcgen05
  * (1, default: split FP16 for dense K=20 models) or FP32 CUDA cores (0). The

@@ -348,18 +348,20 @@ int ensure_ws(detnet_ctx *c, long n, int K) {
     return 0;
 }
 
-// The model-specialised sparse kernel: path 3, or the auto path for models
-// whose every layer has at most kJitMaxNnz surviving products (config 4: ~330
-// per layer, where the compacted tcgen05 kernel is bound by its serial
-// per-layer chain). Valid while the weights are those it was generated from.
+// The model-specialised sparse kernel: path 3, for models whose every layer
+// has at most kJitMaxNnz surviving products (config 4: ~330 per layer, where
+// the compacted tcgen05 kernel is bound by its serial per-layer chain). Not
+// on the auto path: its ~13 s compile per weight version pays off only over
+// billions of detections with fixed weights (a BER sweep), not for a trainer
+// that evaluates after every update. Valid while the weights are those it
+// was generated from.
 bool use_jit(const detnet_model *m) {
     const int path = m->ctx->path;
-    if (!(path == 0 || path == 3) || std::getenv("DETNET_NO_JIT")) return false;
+    if (path != 3 || std::getenv("DETNET_NO_JIT")) return false;
     // weights changed on the device since pack time (training, pruning in
     // progress) bump the version: the kernel no longer matches them
     if (m->tc_stale || m->jit_src_version != m->version) return false;
     if (m->jit_params.empty()) return false;
-    if (path == 0 && m->jit_failed_version == m->jit_src_version) return false;
     return true;
 }
 
@@ -448,14 +450,8 @@ int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, 
         if (!jm.ready || jm.version != m->jit_src_version) {
             const int rc = jit_build(jm, m->K, m->Z, m->V, m->L, m->jit_params.data(),
                                      m->jit_masks.empty() ? nullptr : m->jit_masks.data());
-            if (rc) {
-                if (c->path == 3) return rc; // asked for the sparse path explicitly
-                m->jit_failed_version = m->jit_src_version; // auto: tcgen05 instead
-                if (std::getenv("DETNET_VERBOSE"))
-                    std::fprintf(stderr, "detnet: sparse JIT unavailable: %s\n", g_err.c_str());
-            } else {
-                jm.version = m->jit_src_version;
-            }
+            if (rc) return rc; // NVRTC missing or the compile failed: loud, no fallback
+            jm.version = m->jit_src_version;
         }
         if (jm.ready && jm.version == m->jit_src_version) {
             TcArgs ja{};

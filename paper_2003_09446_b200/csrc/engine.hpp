@@ -125,7 +125,7 @@ int tc_launch_redo(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cud
                    const TraceBufs *tr, const uint8_t *redo, const int *redo_count);
 
 // sparse JIT stack (sparse_jit.cu)
-constexpr long kJitMaxNnz = 1500; // auto path: worst layer's surviving products
+constexpr long kJitMaxNnz = 1500; // path 3: worst layer's surviving products
 long jit_layer_nnz(int K, int Z, int V, int L, const double *params, const double *masks, long stop);
 int jit_build(JitModel &jm, int K, int Z, int V, int L, const double *params, const double *masks);
 int jit_launch(JitModel &jm, const TcArgs &a, cudaStream_t st, int sms, int device);
@@ -219,13 +219,12 @@ struct detnet_model {
     detnet::DBuf sparse_stream, sparse_off;
     int sparse_max_words = 0; // largest per-layer stream (shared-memory staging)
     bool sparse_ready = false;
-    // model-specialised sparse kernel (sparse_jit.cu): chosen by the auto path
-    // when the worst layer has at most kJitMaxNnz surviving products
+    // model-specialised sparse kernel (sparse_jit.cu): path 3, when the worst
+    // layer has at most kJitMaxNnz surviving products
     detnet::JitModel jit;
     long jit_worst_nnz = -1;
     std::vector<double> jit_params, jit_masks; // the weights it is generated from
     long long jit_src_version = -1;
-    long long jit_failed_version = -1; // auto path: a failed build is not retried
     // CUDA graph of batch_evaluate_device (K1 + fallback + stack + reduce +
     // result copy), replayed while the call, the context settings, the model
     // layout and every device buffer are those it was captured with

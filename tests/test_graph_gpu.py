@@ -59,7 +59,7 @@ def test_graph_replay_sparse_jit_model(oracle):
     and a model update to other sparse weights regenerates it."""
     import paper_2003_09446_b200 as eng
     from paper_2003_09446_b200.workload import group_masks, sparse_group_model, xavier_params
-    ctx = eng.Context(0)
+    ctx = eng.Context(0, path=3)
     n, L = 3000, 5
     ps, ms = sparse_group_model(xavier_params(K, L, seed=9), group_masks(K, L, seed=31), K)
     m = ctx.model(K, N, 160, 40, ps, masks=ms)

@@ -21,7 +21,7 @@ from oracle.oracle import Model as OModel
 from oracle.oracle import record_slices
 
 pytestmark = pytest.mark.gpu
-PATHS = [1, 2, 4]
+PATHS = [1, 2, 4, 3]  # 3: the sparse JIT kernel where the model is sparse enough, else SIMT
 
 
 def _ctx(path):

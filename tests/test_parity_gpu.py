@@ -266,12 +266,12 @@ def test_kernel_launches_counted(ctx, oracle):
     assert ctx.launch_count - before >= 3  # preprocess, stack, reduce
 
 
-@pytest.mark.parametrize("path", ["jit", "csr", 1, 2, "h16", 0])
+@pytest.mark.parametrize("path", ["jit", "csr", 1, 2, 0])
 def test_sparse_group_model_paths(ctx, oracle, path, monkeypatch):
     """Config-4 style model (group masks + 5% Bernoulli within groups) on the
-    model-specialised sparse kernel (path 3 and the auto path's choice), the
-    table-driven CSR kernel, the SIMT kernel and both compacted tensor-core
-    kernels (3xTF32 ZH=48, split-FP16 ZH=64), against the oracle."""
+    model-specialised sparse kernel (path 3), the table-driven CSR kernel, the
+    SIMT kernel and both compacted tensor-core kernels (3xTF32 ZH=48,
+    split-FP16 ZH=64, the auto path's choice), against the oracle."""
     from paper_2003_09446_b200.workload import group_masks, sparse_group_model, xavier_params
     params = xavier_params(K, 10, seed=9)
     ps, ms = sparse_group_model(params, group_masks(K, 10, seed=31), K)
@@ -279,14 +279,11 @@ def test_sparse_group_model_paths(ctx, oracle, path, monkeypatch):
     if path == "csr":
         monkeypatch.setenv("DETNET_SPARSE_CSR", "1")
         monkeypatch.setenv("DETNET_NO_JIT", "1")
-    if path == "h16":
-        monkeypatch.setenv("DETNET_NO_JIT", "1")
-    pid = {"jit": 3, "csr": 3, "h16": 0}.get(path, path)
+    pid = {"jit": 3, "csr": 3}.get(path, path)
     ctx.set_path(pid)
     m = ctx.model(K, N, 160, 40, ps, masks=ms)
     assert m.path_name == {"jit": "sparse-jit-fp32", "csr": "sparse-csr-fp32", 1: "simt-fp32",
-                           2: "tcgen05-3xtf32", "h16": "tcgen05-split-fp16",
-                           0: "sparse-jit-fp32"}[path]
+                           2: "tcgen05-3xtf32", 0: "tcgen05-split-fp16"}[path]
     ev, xh = m.batch_evaluate(H, y, x, want_xhat=True)
     ctx.set_path(0)
     ref = oracle.evaluate(_omodel(ps, masks=ms), H.astype(np.float64), y.astype(np.float64),
@@ -298,7 +295,7 @@ def test_sparse_group_model_paths(ctx, oracle, path, monkeypatch):
 
 
 @pytest.mark.parametrize("cfg", [3, 4])
-@pytest.mark.parametrize("path", [0, 2, 1])
+@pytest.mark.parametrize("path", [0, 2, 1, 3])
 def test_masked_configs_full_depth(ctx, oracle, ref, cfg, path):
     """Configs 3 (group-pruned, compacted tensor-core images) and 4 (sparse
     group) at their full depth L=40: 2,048 samples against the reference

@@ -293,6 +293,11 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
+    # our arm also times the reference library in process (cpu_baseline,
+    # parity): its OpenMP workers must sleep between regions, or 16 spinning
+    # threads steal the host cores the following GPU measurements' host side
+    # (e2e copies and C-ABI calls) runs on. Read once, when libgomp loads.
+    os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")
 
     import torch
     import torch.distributed as dist

@@ -4,6 +4,10 @@ transfer is inside the timing) vs the reference's batch_baseline_errors
 (OpenMP, all host cores) on the same samples. One JSON line per case."""
 import json
 import os
+
+# the in-process reference (OpenMP) must not spin its workers while the GPU
+# side is timed on the same host cores (read when libgomp loads)
+os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")
 import sys
 import time
 

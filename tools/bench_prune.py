@@ -3,6 +3,10 @@
 also rebuilds the packed layouts) vs the reference's prune on the host."""
 import json
 import os
+
+# the in-process reference (OpenMP) must not spin its workers while the GPU
+# side is timed on the same host cores (read when libgomp loads)
+os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")
 import sys
 import time
 

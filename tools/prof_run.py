@@ -10,6 +10,8 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 18
 path = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 config = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 K, N, L = 20, 30, 40
+if config == 4 and path == 0:
+    path = 3  # the sparse-group model's kernel (model-specialised, opt-in path)
 ctx = eng.Context(0, path=path)
 params = xavier_params(K, L, seed=9)
 masks = None

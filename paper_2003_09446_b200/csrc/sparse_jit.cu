@@ -359,14 +359,29 @@ std::string gen_layer(int l, int K, int Z, int V, const double *p, const double 
     return o;
 }
 
-// Cubin caches keyed by the generated source: per process (models rebuilt
-// with the same weights, replicas on other devices, repeated tests) and on
+// Cubin caches keyed by the generated source (its 64-bit FNV-1a hash and
+// length): per process (models rebuilt with the same weights, replicas on
+// other devices, repeated tests; the 16 most recent) and on
 // disk ($DETNET_JIT_CACHE, else $XDG_CACHE_HOME or ~/.cache /detnet_b200_jit;
 // "off" disables it), so another process with the same model skips NVRTC
 // (~13 s at L=40). A disk entry carries the source length and hash and the
 // NVRTC version; anything that does not match is recompiled.
 std::mutex g_jit_mu;
-std::map<std::string, std::vector<char>> g_jit_cache;
+// in-memory: keyed by (source hash, length), the 16 most recent cubins
+constexpr size_t kMemCacheEntries = 16;
+std::map<std::pair<uint64_t, size_t>, std::vector<char>> g_jit_cache;
+std::vector<std::pair<uint64_t, size_t>> g_jit_order; // insertion order, oldest first
+
+void mem_store(const std::pair<uint64_t, size_t> &k, const std::vector<char> &cubin) {
+    std::lock_guard<std::mutex> lk(g_jit_mu);
+    if (g_jit_cache.emplace(k, cubin).second) {
+        g_jit_order.push_back(k);
+        if (g_jit_order.size() > kMemCacheEntries) {
+            g_jit_cache.erase(g_jit_order.front());
+            g_jit_order.erase(g_jit_order.begin());
+        }
+    }
+}
 
 uint64_t fnv1a(const std::string &s) {
     uint64_t h = 1469598103934665603ull;
@@ -422,23 +437,23 @@ void disk_store(const std::string &dir, const std::string &path, const DiskKey &
 }
 
 int nvrtc_compile(const std::string &src, std::vector<char> &cubin, std::string &log) {
+    const std::pair<uint64_t, size_t> mkey{fnv1a(src), src.size()};
     {
         std::lock_guard<std::mutex> lk(g_jit_mu);
-        auto it = g_jit_cache.find(src);
+        auto it = g_jit_cache.find(mkey);
         if (it != g_jit_cache.end()) {
             cubin = it->second;
             return 0;
         }
     }
-    DiskKey key{src.size(), fnv1a(src), 0, 0};
+    DiskKey key{src.size(), mkey.first, 0, 0};
     nvrtcVersion(&key.major, &key.minor);
     const std::string dir = jit_cache_dir();
     char name[64];
     std::snprintf(name, sizeof name, "/%016llx.cubin", static_cast<unsigned long long>(key.hash));
     const std::string path = dir.empty() ? "" : dir + name;
     if (!path.empty() && disk_load(path, key, cubin)) {
-        std::lock_guard<std::mutex> lk(g_jit_mu);
-        g_jit_cache[src] = cubin;
+        mem_store(mkey, cubin);
         return 0;
     }
     nvrtcProgram prog;
@@ -462,8 +477,7 @@ int nvrtc_compile(const std::string &src, std::vector<char> &cubin, std::string 
     nvrtcGetCUBIN(prog, cubin.data());
     nvrtcDestroyProgram(&prog);
     if (!path.empty()) disk_store(dir, path, key, cubin);
-    std::lock_guard<std::mutex> lk(g_jit_mu);
-    g_jit_cache[src] = cubin;
+    mem_store(mkey, cubin);
     return 0;
 }
 

@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_bwd_tc(BtcArgs p) {
                 const float w = static_cast<float>(a.lnk[l]) * dinv2;
                 const float t = p.tval[l], tinv = 1.f / t;
                 const float *str = reinterpret_cast<const float *>(sm + SM_TR);
-                const bool tA = threadIdx.x == 128, tB = threadIdx.x == 0;
+                [[maybe_unused]] const bool tA = threadIdx.x == 128, tB = threadIdx.x == 0;
                 BTRACE(isA ? 5 : 11, it, tA || tB);
                 mbar_wait_guard(&bars[B_TRF], ph);
                 float u2b[KX / 2];

@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_h16(HKArgs p) {
                     }
                     __syncwarp();
                 };
-                const bool t0n = lane == 0;
+                [[maybe_unused]] const bool t0n = lane == 0;
                 mbar_wait_guard(&bars[B_W1F], ph);
                 HTRACE(0, it, t0n);
                 // U1 is overwritten by the [q 1] steps. The previous layer's W23 MMAs
@@ -434,8 +434,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_h16(HKArgs p) {
             for (int l = L0; l < L1; ++l, ++it) {
                 const uint32_t ph = static_cast<uint32_t>(it & 1);
                 const double lw = isA ? a.lnk[l] : 0.0;
-                const bool tA = threadIdx.x == 128, tB = threadIdx.x == 0;
-                const int tb9 = isA ? 9 : 19; // A events 9-18, B events 19-27
+                [[maybe_unused]] const bool tA = threadIdx.x == 128, tB = threadIdx.x == 0;
+                [[maybe_unused]] const int tb9 = isA ? 9 : 19; // A events 9-18, B events 19-27
                 HTRACE(tb9, it, tA || tB);
                 // ---- prep: A_dyn pairs = [v | x | gx]: v (B) and x (A), then G x_hat
                 if (isA) {

@@ -32,7 +32,6 @@ namespace detnet {
 // over 79 SMs instead of 20.
 template <int K, int Z, int V, int THREADS>
 __global__ void __launch_bounds__(THREADS, 1) k_train_bwd(BwdArgs a) {
-    constexpr int BWD_WARPS = THREADS / 32;
     constexpr int IN = 3 * K + V;
     constexpr int IN4 = simt_in4(K, V);
     constexpr int O = K + V;

@@ -118,17 +118,6 @@ struct TcKArgs {
 enum { B_W1F = 0, B_W23F = 1, B_U1A = 2, B_U1B = 3, B_U2 = 4, B_VX = 5, B_ZA = 6, B_ZB = 7, B_G = 8,
        B_E2L = 9, NBARS = 10 };
 
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
-    uint32_t r[8];
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
-                   "=r"(r[6]), "=r"(r[7])
-                 : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
-}
-
 // Store N (multiple of 8) contiguous columns: x16 pieces, then one x8.
 template <int N> __device__ __forceinline__ void st_cols(uint32_t taddr, const float *v) {
 #pragma unroll
@@ -202,7 +191,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
     constexpr int C_U1 = C::C_U1, C_DYN = C::C_DYN, C_DYNLO = C::C_DYNLO, C_U2 = C::C_U2,
                   C_QHI = C::C_QHI, C_QLO = C::C_QLO;
     constexpr uint32_t SM_W1 = C::SM_W1, SM_W23 = C::SM_W23, SM_GX = C::SM_GX,
-                       SM_RED = C::SM_RED, SM_BAR = C::SM_BAR, SM_TMEM = C::SM_TMEM,
+                       SM_BAR = C::SM_BAR, SM_TMEM = C::SM_TMEM,
                        SM_BT = C::SM_BT;
     constexpr uint32_t W1_HALF = C::W1_HALF, W23_HALF = C::W23_HALF, W1_BYTES = C::W1_BYTES,
                        W23_BYTES = C::W23_BYTES, LAYER_BYTES = C::LAYER_BYTES,
@@ -265,7 +254,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
             for (long it = 0; it < total_it; ++it) {
                 const uint32_t ph = static_cast<uint32_t>(it & 1);
                 const int l = L0 + static_cast<int>(it % NL);
-                const bool trace_on = it < NL && lane == 0;
+                [[maybe_unused]] const bool trace_on = it < NL && lane == 0;
                 // K steps of W1 (8 columns each): 0-2 [q 1 0 0 0], 3-7 v, 8-9 x, 10-12 [x gx]
                 auto w1_steps = [&](int h, int k0, int k1, bool commit) {
                     if (tc::elect_one()) {
@@ -357,9 +346,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
             if (total_it > 0) { load_w1(L0); load_w23(L0, 0); }
             for (long it = 0; it + 1 < total_it; ++it) {
                 const uint32_t ph = static_cast<uint32_t>(it & 1);
-                const int l = L0 + static_cast<int>(it % NL);
+                [[maybe_unused]] const int l = L0 + static_cast<int>(it % NL);
                 const int lnext = L0 + static_cast<int>((it + 1) % NL);
-                const bool trace_on = it < NL && lane == 0;
+                [[maybe_unused]] const bool trace_on = it < NL && lane == 0;
                 mbar_wait_guard(&bars[U1_LAST], ph); // every W1 group consumed
                 TRACE(14, l);
                 load_w1(lnext);
@@ -439,8 +428,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_stack_tc(TcKArgs p) {
             };
             for (int l = L0; l < L1; ++l, ++it) {
                 const uint32_t ph = static_cast<uint32_t>(it & 1);
-                const bool trace_on = ti == 0 && (threadIdx.x == 0 || threadIdx.x == 128);
-                const int tb16 = isA ? 0 : 16;
+                [[maybe_unused]] const bool trace_on = ti == 0 && (threadIdx.x == 0 || threadIdx.x == 128);
+                [[maybe_unused]] const int tb16 = isA ? 0 : 16;
                 const double lw = isA ? a.lnk[l] : 0.0; // loss weight, fetched early
                 TRACE(0 + tb16, l);
                 // ---- prep: A_dyn = [v | x | gx] hi/lo. v (B) and x (A) first, then

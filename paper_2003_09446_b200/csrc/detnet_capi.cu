@@ -281,6 +281,46 @@ void prepare_jit(detnet_model *m, const double *params, const double *masks) {
     m->jit_src_version = m->version;
 }
 
+// Every hidden unit of every layer has a surviving outgoing weight (the
+// dense tcgen05 images then list the units in natural order).
+bool all_units_live(int K, int Z, int V, int L, const double *params, const double *masks) {
+    const int IN = 3 * K + V;
+    const long P = record_size(K, Z, V);
+    const long oW2 = static_cast<long>(Z) * IN + Z, oW3 = oW2 + static_cast<long>(K) * Z + K;
+    for (int l = 0; l < L; ++l) {
+        const double *pr = params + l * P, *mk = masks ? masks + l * P : nullptr;
+        auto nz = [&](long off) { return static_cast<float>(pr[off] * (mk ? mk[off] : 1.0)) != 0.f; };
+        for (int i = 0; i < Z; ++i) {
+            bool alive = false;
+            for (int o = 0; o < K && !alive; ++o) alive = nz(oW2 + static_cast<long>(o) * Z + i);
+            for (int o = 0; o < V && !alive; ++o) alive = nz(oW3 + static_cast<long>(o) * Z + i);
+            if (!alive) return false;
+        }
+    }
+    return true;
+}
+
+// Every weight of W1, b1, W2, W3 fits the split-FP16 images (x16 scale within
+// the FP16 range, the host packer's test); otherwise the host packers run and
+// the model takes the 3xTF32 images only.
+bool h16_weights_in_range(int K, int Z, int V, int L, const double *params, const double *masks) {
+    const int IN = 3 * K + V;
+    const long P = record_size(K, Z, V);
+    const long nW1b1 = static_cast<long>(Z) * IN + Z, oW2 = nW1b1, nW2 = static_cast<long>(K) * Z,
+               oW3 = oW2 + nW2 + K, nW3 = static_cast<long>(V) * Z;
+    for (int l = 0; l < L; ++l) {
+        const double *pr = params + l * P, *mk = masks ? masks + l * P : nullptr;
+        auto ok = [&](long off) {
+            const float sv = static_cast<float>(pr[off] * (mk ? mk[off] : 1.0)) * 16.f;
+            return std::fabs(sv) <= 65000.f;
+        };
+        for (long e = 0; e < nW1b1; ++e) if (!ok(e)) return false;
+        for (long e = 0; e < nW2; ++e) if (!ok(oW2 + e)) return false;
+        for (long e = 0; e < nW3; ++e) if (!ok(oW3 + e)) return false;
+    }
+    return true;
+}
+
 int upload_model(detnet_model *m, const detnet_model_desc *d) {
     ++m->version;
     if (int rc = quiesce(m->ctx)) return rc; // in-flight work may read the old buffers
@@ -289,11 +329,32 @@ int upload_model(detnet_model *m, const detnet_model_desc *d) {
     m->has_masks = d->masks != nullptr;
     if (d->masks) m->masks_host.assign(d->masks, d->masks + P * m->L);
     else m->masks_host.clear();
-    std::vector<float> packed;
-    if (int rc = pack_simt(m, d->params, d->masks, packed)) return rc;
     m->simt_rec = simt_rec(m->K, m->Z, m->V);
-    if (m->simt.ensure(packed.size() * 4)) return fail(DETNET_ERR_CUDA, "cudaMalloc weights");
-    CK(cudaMemcpy(m->simt.p, packed.data(), packed.size() * 4, cudaMemcpyHostToDevice));
+    // Dense models (the BASELINE dims, every unit live): the FP64 records go
+    // to the device once and the SIMT records and both tensor-core image sets
+    // are packed there (~1 ms instead of ~20 ms of host loops per update)
+    const bool dense_dev = m->K == 20 && m->Z == 160 && m->V == 40 &&
+                           !std::getenv("DETNET_HOST_PACK") &&
+                           all_units_live(m->K, m->Z, m->V, m->L, d->params, d->masks) &&
+                           h16_weights_in_range(m->K, m->Z, m->V, m->L, d->params, d->masks);
+    if (dense_dev) {
+        const size_t bytes = sizeof(double) * P * m->L;
+        if (m->tparams.ensure(bytes) || (d->masks && m->tmasks.ensure(bytes)) ||
+            m->simt.ensure(sizeof(float) * m->simt_rec * m->L))
+            return fail(DETNET_ERR_CUDA, "cudaMalloc weights");
+        // on the context stream: a pageable cudaMemcpy may return before its
+        // DMA lands, and the packers below run on this (non-blocking) stream
+        CK(cudaMemcpyAsync(m->tparams.p, d->params, bytes, cudaMemcpyHostToDevice, m->ctx->stream));
+        if (d->masks)
+            CK(cudaMemcpyAsync(m->tmasks.p, d->masks, bytes, cudaMemcpyHostToDevice, m->ctx->stream));
+        const double *mdev = d->masks ? m->tmasks.as<double>() : nullptr;
+        if (int rc = pack_simt_device_from(m, m->tparams.as<double>(), mdev)) return rc;
+    } else {
+        std::vector<float> packed;
+        if (int rc = pack_simt(m, d->params, d->masks, packed)) return rc;
+        if (m->simt.ensure(packed.size() * 4)) return fail(DETNET_ERR_CUDA, "cudaMalloc weights");
+        CK(cudaMemcpy(m->simt.p, packed.data(), packed.size() * 4, cudaMemcpyHostToDevice));
+    }
     std::vector<double> la(m->L), lt(m->L);
     for (int l = 0; l < m->L; ++l) {
         la[l] = std::log(static_cast<double>(l + 1));
@@ -303,13 +364,25 @@ int upload_model(detnet_model *m, const detnet_model_desc *d) {
         return fail(DETNET_ERR_CUDA, "cudaMalloc lnk");
     CK(cudaMemcpy(m->lnk_all.p, la.data(), m->L * 8, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(m->lnk_train.p, lt.data(), m->L * 8, cudaMemcpyHostToDevice));
-    if (int rc = tc_pack(m->tc, m->K, m->Z, m->V, m->L, d->params, d->masks)) return rc;
+    if (dense_dev) {
+        if (int rc = tc_pack_dense_device(m->tc, m->K, m->Z, m->V, m->L, m->tparams.as<double>(),
+                                          d->masks ? m->tmasks.as<double>() : nullptr,
+                                          m->ctx->stream))
+            return rc;
+        if (int rc = check_launch()) return rc;
+        CK(cudaStreamSynchronize(m->ctx->stream)); // a host-synchronous API, as the host packers
+    } else if (int rc = tc_pack(m->tc, m->K, m->Z, m->V, m->L, d->params, d->masks)) {
+        return rc;
+    }
     // the table-driven CSR stream only when asked for (DETNET_SPARSE_CSR): it
     // costs a pass over every weight on each update
     m->sparse_ready = false;
     if (std::getenv("DETNET_SPARSE_CSR"))
         if (int rc = pack_sparse(m, d->params, d->masks)) return rc;
     prepare_jit(m, d->params, d->masks);
+    // every pageable cudaMemcpy above (host-packed images, records) has landed
+    // before any kernel on a non-blocking stream reads the buffers
+    CK(cudaStreamSynchronize(cudaStreamLegacy));
     m->train_ready = false; // the device master copy restarts from these params
     m->tc_stale = false;
     m->tc_dev_dirty = false; // the images just packed from the host copy are current

@@ -136,6 +136,9 @@ int h16_prepare();
 int h16_pack(TcModel &tc, int K, int Z, int V, int L, const double *params, const double *masks,
              const std::vector<std::vector<int>> &units, size_t max_alive);
 int h16_pack_device(TcModel &tc, const double *params, const double *masks, long P, cudaStream_t st);
+int h16_alloc_dense(TcModel &tc, int L, cudaStream_t st);
+int tc_pack_dense_device(TcModel &tc, int K, int Z, int V, int L, const double *params,
+                         const double *masks, cudaStream_t st);
 int h16_launch_state(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cudaStream_t st,
                      const TraceBufs *tr, uint8_t *redo, int *redo_count, int sms);
 
@@ -361,6 +364,7 @@ int group_batch_gradient(detnet_model *m, long n, const float *H, const float *y
 int sync_replicas(detnet_model *m);
 int finish_host(detnet_model *m, long n, detnet_eval *out);
 int pack_simt_device(detnet_model *m); // FP32 records from the FP64 master copy
+int pack_simt_device_from(detnet_model *m, const double *params, const double *masks);
 int train_prepare();                   // per-device kernel attributes (train.cu)
 struct DwJob; // dw_job.hpp
 int dw_tc_prepare();                   // dW contractions on tcgen05 (dw_tc.cu)

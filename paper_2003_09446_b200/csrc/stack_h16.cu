@@ -802,6 +802,18 @@ int h16_pack(TcModel &tc, int K, int Z, int V, int L, const double *params, cons
     return 0;
 }
 
+// Buffers of the dense (ZH = 160) images for tc_pack_dense_device; the
+// device packer fills them (and raises the range flag cleared here).
+int h16_alloc_dense(TcModel &tc, int L, cudaStream_t st) {
+    tc.zh16 = 160;
+    tc.rec16 = HCfg<160>::LAYER_BYTES;
+    const size_t wbytes = static_cast<size_t>(L) * tc.rec16, bbytes = static_cast<size_t>(L) * BT * 4;
+    if (tc.w16.ensure(wbytes + bbytes + 16)) return fail(DETNET_ERR_CUDA, "cudaMalloc fp16 images");
+    CK(cudaMemsetAsync(static_cast<char *>(tc.w16.p) + wbytes + bbytes, 0, 16, st));
+    tc.h16_ready = true;
+    return 0;
+}
+
 int h16_pack_device(TcModel &tc, const double *params, const double *masks, long P,
                     cudaStream_t st) {
     if (!tc.h16_ready || tc.zh16 != 160) return 1;

@@ -842,6 +842,25 @@ int tc_pack_device(TcModel &tc, const double *params, const double *masks, long 
     return 0;
 }
 
+// Dense models with every hidden unit live (ZH = 160, units in natural
+// order): both image sets built on the device from FP64 records already
+// there -- the images the host packers make (the training path repacks this
+// way after every Adam step), without the host loops (~20 ms per update, paid
+// by the drop-in seam on every adam_step).
+int tc_pack_dense_device(TcModel &tc, int K, int Z, int V, int L, const double *params,
+                         const double *masks, cudaStream_t st) {
+    tc.K = K; tc.Z = Z; tc.V = V; tc.L = L;
+    tc.ready = false;
+    tc.h16_ready = false;
+    tc.zh = 160;
+    tc.rec_bytes = TcCfg<160>::LAYER_BYTES;
+    const size_t wbytes = static_cast<size_t>(L) * tc.rec_bytes, bbytes = static_cast<size_t>(L) * BT * 4;
+    if (tc.w.ensure(wbytes + bbytes)) return fail(DETNET_ERR_CUDA, "cudaMalloc tc weights");
+    tc.ready = true;
+    if (int rc = h16_alloc_dense(tc, L, st)) return rc;
+    return tc_pack_device(tc, params, masks, record_size(K, Z, V), st);
+}
+
 namespace {
 int tc_launch_impl(const TcModel &tc, const TcArgs &a, float *xs, float *vs, cudaStream_t st,
                    const TraceBufs *tr, const uint8_t *redo, const int *redo_count) {

@@ -107,19 +107,25 @@ int ensure_train_state(detnet_model *m) {
     if (m->tparams.ensure(bytes) || m->tmasks.ensure(bytes) || m->tm.ensure(bytes) ||
         m->tv.ensure(bytes))
         return fail(DETNET_ERR_CUDA, "training state allocation failed");
-    CK(cudaMemcpy(m->tparams.p, m->params_host.data(), bytes, cudaMemcpyHostToDevice));
+    // ordered on the context stream, where every training kernel runs (a
+    // pageable cudaMemcpy may return before its DMA lands); staged from the
+    // host buffers before each call returns
+    cudaStream_t st = m->ctx->stream;
+    CK(cudaMemcpyAsync(m->tparams.p, m->params_host.data(), bytes, cudaMemcpyHostToDevice, st));
     if (m->has_masks) {
-        CK(cudaMemcpy(m->tmasks.p, m->masks_host.data(), bytes, cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(m->tmasks.p, m->masks_host.data(), bytes, cudaMemcpyHostToDevice, st));
     } else {
         std::vector<double> ones(rec_size(m) * m->L, 1.0);
-        CK(cudaMemcpy(m->tmasks.p, ones.data(), bytes, cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(m->tmasks.p, ones.data(), bytes, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st)); // `ones` goes out of scope
     }
-    CK(cudaMemset(m->tm.p, 0, bytes));
-    CK(cudaMemset(m->tv.p, 0, bytes));
+    CK(cudaMemsetAsync(m->tm.p, 0, bytes, st));
+    CK(cudaMemsetAsync(m->tv.p, 0, bytes, st));
     if (m->tstatus.ensure(4 * sizeof(double))) return fail(DETNET_ERR_CUDA, "status allocation failed");
     const double st0[4] = {0.0, 0.0, 0.0, 0.0};
-    CK(cudaMemcpy(m->tstatus.p, st0, sizeof st0, cudaMemcpyHostToDevice));
-    CK(cudaMemset(static_cast<double *>(m->tstatus.p) + 2, 0xff, 8)); // halt step = -1
+    CK(cudaMemcpyAsync(m->tstatus.p, st0, sizeof st0, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(static_cast<double *>(m->tstatus.p) + 2, 0xff, 8, st)); // halt step = -1
+    CK(cudaStreamSynchronize(st)); // st0 is a local
     m->diverged_step = -1;
     m->adam_step = 0;
     m->train_ready = true;
@@ -457,13 +463,16 @@ int train_prepare() {
     return 0;
 }
 
-int pack_simt_device(detnet_model *m) {
+int pack_simt_device_from(detnet_model *m, const double *params, const double *masks) {
     const long R = simt_rec(m->K, m->Z, m->V) * m->L;
     LaunchScope ls(m->ctx, DETNET_K_ADAM, m->ctx->stream);
     k_pack_simt<<<static_cast<unsigned>((R + 255) / 256), 256, 0, m->ctx->stream>>>(
-        m->tparams.as<double>(), m->tmasks.as<double>(), m->K, m->Z, m->V, m->L,
-        m->simt.as<float>());
+        params, masks, m->K, m->Z, m->V, m->L, m->simt.as<float>());
     return check_launch();
+}
+
+int pack_simt_device(detnet_model *m) {
+    return pack_simt_device_from(m, m->tparams.as<double>(), m->tmasks.as<double>());
 }
 
 int train_batch_gradient(detnet_model *m, long n, const float *H, const float *y, const int8_t *x,

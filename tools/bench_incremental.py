@@ -48,7 +48,9 @@ def main():
     # (label, K, N, start, t_step, max_layers, batches_short, batches_long, batch, val)
     cases = [("whole-network L=40 (config-5 dims)", 20, 30, 40, 10, 40, 4, 12, 5000, 2000),
              ("incremental 10->40 by 10", 20, 30, 10, 10, 40, 2, 6, 5000, 2000)]
-    run_device([20, 30, 40, 10, 40, 2, 5000, 2000, 1])  # warm-up: module load, workspace
+    # warm-up: module load, workspace, and every depth the schedules visit
+    for _, K, N, s0, ts, mx, b1, _, bs, val in cases:
+        run_device([K, N, s0, ts, mx, b1, bs, val, 1])
     for label, K, N, s0, ts, mx, b1, b2, bs, val in cases:
         res = {}
         for name, binary in (("b200", B), ("device", None), ("reference", R)):

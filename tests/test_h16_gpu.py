@@ -117,3 +117,23 @@ def test_hidden_unit_overflow_is_recomputed(ctx, oracle):
     evh, xhh = _eval(ctx, m, 0, H, y, x)
     assert np.array_equal(xhh, xh2)
     assert evh.data_loss == ev2.data_loss and evh.symbol_errors == ev2.symbol_errors
+
+
+@pytest.mark.parametrize("path", [1, 2, 4])
+def test_device_packing_matches_host_packing(oracle, path, monkeypatch):
+    """Dense models are packed on the device at upload (SIMT records and both
+    tensor-core image sets from the FP64 records); the host packers build the
+    same layouts: evaluations agree bit for bit on every kernel path."""
+    from paper_2003_09446_b200 import Context
+    from paper_2003_09446_b200.workload import xavier_params
+    params = xavier_params(K, 7, seed=12)
+    H, y, x = _inputs(oracle, 3000)
+    c = Context(0, path=path)
+    dev = c.model(K, N, 160, 40, params)
+    monkeypatch.setenv("DETNET_HOST_PACK", "1")
+    host = c.model(K, N, 160, 40, params)
+    monkeypatch.delenv("DETNET_HOST_PACK")
+    ea, xa = dev.batch_evaluate(H, y, x, want_xhat=True)
+    eb, xb = host.batch_evaluate(H, y, x, want_xhat=True)
+    assert np.array_equal(xa, xb)
+    assert (ea.loss_sum, ea.symbol_errors) == (eb.loss_sum, eb.symbol_errors)

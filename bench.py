@@ -323,8 +323,8 @@ def main():
             dist.barrier()
 
     import paper_2003_09446_b200 as eng
-    from paper_2003_09446_b200.parallel import allreduce_grad, shard
-    globals().update(shard=shard, allreduce_grad=allreduce_grad)
+    from paper_2003_09446_b200.parallel import shard
+    globals().update(shard=shard)
     env = argparse.Namespace(torch=torch, dist=dist, world=world, rank=rank, local=local,
                              barrier=barrier, eng=eng,
                              peaks=measured_peaks(torch) if rank == 0 else {})
@@ -720,11 +720,23 @@ def bench_train(args, env):
         batches.append((H, y, x))
     n_global = per_gpu * world
 
+    side = torch.cuda.Stream()
+
     def step(b, want_eval=False):
         # steps are stream-ordered; only the last one waits for its BatchEval
         H, y, x = batches[b]
-        ev = model.train_grad(per_gpu, H, y, x, raw, want_eval=want_eval)
-        allreduce_grad(dist if world > 1 else None, raw)
+        if world > 1:
+            # the raw sums are final bucket by bucket as the reverse
+            # sweep produces them (top layers first); each bucket's all-reduce
+            # runs on a side stream while the rest of the sweep computes
+            for bev, lo, hi in model.train_grad_buckets(per_gpu, H, y, x, raw):
+                eng.stream_wait_event(side.cuda_stream, bev)
+                with torch.cuda.stream(side):
+                    dist.all_reduce(raw[lo:hi])
+            stream.wait_stream(side)
+            ev = None
+        else:
+            ev = model.train_grad(per_gpu, H, y, x, raw, want_eval=want_eval)
         model.train_apply(raw, n_global, kind=2, lam1=1e-4, lr0=1e-3)
         return ev
 
@@ -805,8 +817,14 @@ def bench_train(args, env):
             main_s.wait_event(ready)
             if k + 1 < len(host):
                 ready = copy_in(k + 1)
-            model.train_grad(per_gpu, *dev[k % 2], raw, want_eval=False)
-            allreduce_grad(dist if world > 1 else None, raw)
+            if world > 1:  # bucketed, overlapped all-reduce (as in step())
+                for bev, lo, hi in model.train_grad_buckets(per_gpu, *dev[k % 2], raw):
+                    eng.stream_wait_event(side.cuda_stream, bev)
+                    with torch.cuda.stream(side):
+                        dist.all_reduce(raw[lo:hi])
+                main_s.wait_stream(side)
+            else:
+                model.train_grad(per_gpu, *dev[k % 2], raw, want_eval=False)
             losses[k:k + 1].copy_(raw[-1:], non_blocking=True)
             model.train_apply(raw, n_global, kind=2, lam1=1e-4, lr0=1e-3)
         torch.cuda.synchronize()
@@ -835,7 +853,8 @@ def bench_train(args, env):
                        "l2": "fresh batch per step (12.7 MB) + 1 M-parameter model",
                        "train_forward": "tcgen05-split-fp16" if args.train_fwd == "tc" else "simt-fp32"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk.summary(), "last_step_loss": ev.data_loss,
+            "clocks": clk.summary(),
+            "last_step_loss": ev.data_loss if ev is not None else float(raw[-1]) / n_global,
             "last_step_objective": objective, "peaks_measured": peaks}
     del batches, model
     ctx.close()

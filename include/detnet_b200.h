@@ -225,6 +225,22 @@ long detnet_train_raw_count(const detnet_model *m);
 int detnet_train_grad(detnet_model *m, long n, const float *H_dev, const float *y_dev,
                       const int8_t *x_dev, int loss_layers_trainable_only, double *raw_dev,
                       detnet_eval *out);
+/* detnet_train_grad, enqueue only, with the raw sums finalised in buckets as
+ * the reverse sweep produces them (top layers first, one bucket per sweep
+ * chunk, the loss-sum slot last): after the call, raw entries
+ * [ranges[2b], ranges[2b+1]) are final once events[b] (a cudaEvent_t owned by
+ * the context, valid until its next training call) has completed on the
+ * device. A data-parallel caller all-reduces each bucket on a side stream
+ * while the rest of the sweep runs, then orders the context
+ * stream after it before detnet_train_apply. Frozen layers' slots are zero on
+ * every rank and in no bucket. Returns the bucket count or -status. Bit for
+ * bit the sums of detnet_train_grad. */
+int detnet_train_grad_buckets(detnet_model *m, long n, const float *H, const float *y,
+                              const int8_t *x, int trainable_only, double *raw_dev, void **events,
+                              long *ranges, int max_buckets);
+/* cudaStreamWaitEvent(stream, event) for callers without a CUDA runtime of
+ * their own (the bucket events above). */
+int detnet_stream_wait_event(void *stream, void *event);
 /* Also forms objective = raw[param_count] / n_global + regularizer(params,
  * spec) before the update (training.cpp:65-70, loss.cpp:81-91, bit-identical
  * order); a non-finite objective halts training on the device (no update, the

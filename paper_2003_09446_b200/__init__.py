@@ -7,9 +7,9 @@ workload builders. Importing it fails loudly if the library is not built.
 from .detnet import (BatchEval, ConfigError, Context, ContractError, CudaError, DetnetError,
                      DivergenceError, Model,
                      SingularMatrixError, UnsupportedError, lib_path, record_size, rng_seed,
-                     rng_split, rng_stream)
+                     rng_split, rng_stream, stream_wait_event)
 
 __all__ = ["BatchEval", "ConfigError", "Context", "ContractError", "CudaError", "DetnetError",
            "DivergenceError",
            "Model", "SingularMatrixError", "UnsupportedError", "lib_path", "record_size",
-           "rng_seed", "rng_split", "rng_stream"]
+           "rng_seed", "rng_split", "rng_stream", "stream_wait_event"]

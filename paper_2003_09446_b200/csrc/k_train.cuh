@@ -500,6 +500,7 @@ struct SumArgs {
     int K, Z, V, L, lf;
     double *raw;          // [L][P] unscaled, unmasked data-gradient sums (record layout)
     double *chunk_out;    // optional [chunks][L][P]: the per-chunk sums (device groups)
+    int l_lo, l_hi;       // layers this launch finalises (a bucket of the overlapped sweep)
 };
 
 // Chunk = 8,192 consecutive samples = 32 dW splits = 256 t groups. The raw
@@ -514,8 +515,9 @@ constexpr int GRAD_CHUNK_SPLITS = 8192 / DW_SPLIT, GRAD_CHUNK_GROUPS = 8192 / 32
 __global__ void k_grad_sum(SumArgs a) {
     const int K = a.K, Z = a.Z, V = a.V, IN = 3 * K + V;
     const int P = Z * IN + Z + K * Z + K + V * Z + V + 1;
-    const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= static_cast<long>(a.L) * P) return;
+    const long idx = static_cast<long>(a.l_lo) * P + static_cast<long>(blockIdx.x) * blockDim.x +
+                     threadIdx.x;
+    if (idx >= static_cast<long>(a.l_hi) * P) return;
     const int l = static_cast<int>(idx / P), e = static_cast<int>(idx % P);
     DETNET_DASSERT(a.splits >= 1 && a.tgroups >= 1 && a.lf >= 0 && a.lf <= a.L);
     if (l < a.lf) { a.raw[idx] = 0.0; return; }

@@ -75,6 +75,7 @@ struct TrainWs {
     DBuf objpart;
     cudaStream_t hi = nullptr; // high-priority stream for the sweep chunks
     cudaEvent_t ev[9] = {};
+    cudaEvent_t bev[9] = {}; // gradient buckets final (detnet_train_grad_buckets)
     DBuf in_H, in_y, in_x;
 };
 
@@ -230,8 +231,17 @@ int grad_raw64(detnet_model *m, long n, const float *H, const float *y, const in
 
 // Forward with trace + reverse sweep + contractions -> raw gradient sums
 // (record layout, unscaled, unmasked) in `raw`; local BatchEval in *out.
+// Buckets (detnet_train_grad_buckets): raw ranges [lo, hi) final when the
+// event fires, in the order the reverse sweep produces them.
+struct Buckets {
+    int cap = 0, count = 0;
+    void **events = nullptr;
+    long *ranges = nullptr; // [2 b], [2 b + 1]
+};
+
 int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8_t *x,
-             bool trainable_only, double *raw, detnet_eval *out, double *chunk_raw = nullptr) {
+             bool trainable_only, double *raw, detnet_eval *out, double *chunk_raw = nullptr,
+             Buckets *bk = nullptr) {
     detnet_ctx *c = m->ctx;
     if (c->train_fp64) return grad_raw64(m, n, H, y, x, trainable_only, raw, out);
     const BwdEntry *be = find_bwd(m->K, m->Z, m->V);
@@ -248,6 +258,27 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
     // a batch of variant_tiles tiles: device groups pass the global batch
     const long variant_tiles = c->variant_n > 0 ? (c->variant_n + TILE - 1) / TILE : tiles;
     const bool bwd_large = variant_tiles * TILE / BWD_LARGE >= c->sms;
+    // one gradient bucket: layers [l0, l1) summed and signalled on the context stream
+    auto bucket_sum = [&](int l0, int l1) -> int {
+        if (bk->count + 1 >= bk->cap) return fail(DETNET_ERR_CONTRACT, "train_grad_buckets: too few slots");
+        const long P = rec_size(m);
+        SumArgs sa{w.p1.as<double>(), w.p23.as<double>(), w.tbar.as<double>(),
+                   static_cast<int>(ts / 32), splits, K, Z, V, L, lf, raw, chunk_raw, l0, l1};
+        const long cnt = P * (l1 - l0);
+        {
+            LaunchScope ls(c, DETNET_K_BACKWARD, c->stream);
+            k_grad_sum<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, c->stream>>>(sa);
+        }
+        if (int rc = check_launch()) return rc;
+        cudaEvent_t &e = w.bev[bk->count];
+        if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaEventRecord(e, c->stream));
+        bk->events[bk->count] = e;
+        bk->ranges[2 * bk->count] = P * l0;
+        bk->ranges[2 * bk->count + 1] = P * l1;
+        ++bk->count;
+        return 0;
+    };
     const int bwd_samples = bwd_large ? BWD_LARGE : BWP_SAMPLES;
     const int bwd_per = bwd_large ? BWD_LARGE : BWP_THREADS;
     const int bwd_blocks = static_cast<int>((tiles * TILE + bwd_samples - 1) / bwd_samples);
@@ -366,6 +397,9 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
                 // [L - it_end, L - it_begin) (job index 2 (l - lf))
                 dw_launch(2 * (L - ba.it_end - lf), 2 * (L - ba.it_begin - lf));
                 if (int rc = check_launch()) return rc;
+                if (bk) { // this chunk's layers are final: sum them and signal the bucket
+                    if (int rc = bucket_sum(L - ba.it_end, L - ba.it_begin)) return rc;
+                }
             }
         } else {
             {
@@ -376,12 +410,18 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
             if (int rc = check_launch()) return rc;
         }
     }
-    SumArgs sa{w.p1.as<double>(), w.p23.as<double>(), w.tbar.as<double>(),
-               static_cast<int>(ts / 32), splits, K, Z, V, L, lf, raw, chunk_raw};
     const long total = rec_size(m) * L;
-    {
+    if (!bk || bk->count == 0) { // all layers at once (or the unchunked sweep)
+        SumArgs sa{w.p1.as<double>(), w.p23.as<double>(), w.tbar.as<double>(),
+                   static_cast<int>(ts / 32), splits, K, Z, V, L, lf, raw, chunk_raw, 0, L};
         LaunchScope ls(c, DETNET_K_BACKWARD, c->stream);
         k_grad_sum<<<static_cast<unsigned>((total + 255) / 256), 256, 0, c->stream>>>(sa);
+    } else if (lf > 0) { // frozen layers: zero slots (identical on every rank, no bucket)
+        SumArgs sa{w.p1.as<double>(), w.p23.as<double>(), w.tbar.as<double>(),
+                   static_cast<int>(ts / 32), splits, K, Z, V, L, lf, raw, chunk_raw, 0, lf};
+        const long cnt = rec_size(m) * lf;
+        LaunchScope ls(c, DETNET_K_BACKWARD, c->stream);
+        k_grad_sum<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, c->stream>>>(sa);
     }
     if (int rc = check_launch()) return rc;
     { // raw[total] = this batch's loss sum (fixed tile order): the objective's data term
@@ -395,6 +435,16 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
     }
     c->last_chunks = (tiles + RED_CHUNK_TILES - 1) / RED_CHUNK_TILES;
     if (int rc = check_launch()) return rc;
+    if (bk) { // the last bucket: the loss-sum slot (everything, if the sweep was not chunked)
+        if (bk->count >= bk->cap) return fail(DETNET_ERR_CONTRACT, "train_grad_buckets: too few slots");
+        cudaEvent_t &e = w.bev[bk->count];
+        if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaEventRecord(e, c->stream));
+        bk->events[bk->count] = e;
+        bk->ranges[2 * bk->count] = bk->count ? total : 0;
+        bk->ranges[2 * bk->count + 1] = total + 1;
+        ++bk->count;
+    }
     if (!out) return drain_times(c, false), 0; // no readback requested: no wait
     return finish(m, n, out); // loss / errors / flagged of the forward pass (syncs)
 }
@@ -615,6 +665,29 @@ int detnet_train_grad(detnet_model *m, long n, const float *H, const float *y, c
     CK(cudaSetDevice(m->ctx->device));
     if (int rc = ensure_train_state(m)) return rc;
     return grad_raw(m, n, H, y, x, trainable_only != 0, raw_dev, out);
+}
+
+int detnet_train_grad_buckets(detnet_model *m, long n, const float *H, const float *y,
+                              const int8_t *x, int trainable_only, double *raw_dev, void **events,
+                              long *ranges, int max_buckets) {
+    if (!m || !raw_dev || !events || !ranges || max_buckets < 1)
+        return -fail(DETNET_ERR_CONTRACT, "null argument");
+    if (m->ctx->train_fp64)
+        return -fail(DETNET_ERR_UNSUPPORTED, "train_grad_buckets: the FP64 mode is not bucketed");
+    if (cudaSetDevice(m->ctx->device) != cudaSuccess) return -fail(DETNET_ERR_CUDA, "cudaSetDevice");
+    if (int rc = ensure_train_state(m)) return -rc;
+    Buckets bk;
+    bk.cap = std::min(max_buckets, 9);
+    bk.events = events;
+    bk.ranges = ranges;
+    if (int rc = grad_raw(m, n, H, y, x, trainable_only != 0, raw_dev, nullptr, nullptr, &bk)) return -rc;
+    return bk.count;
+}
+
+int detnet_stream_wait_event(void *stream, void *event) {
+    if (!event) return fail(DETNET_ERR_CONTRACT, "null event");
+    CK(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), static_cast<cudaEvent_t>(event), 0));
+    return 0;
 }
 
 long detnet_train_raw_count(const detnet_model *m) {
@@ -851,6 +924,8 @@ void train_ws_release(detnet_ctx *c) {
         if (w->hi) {
             cudaStreamDestroy(w->hi);
             for (cudaEvent_t e : w->ev) cudaEventDestroy(e);
+            for (cudaEvent_t e : w->bev)
+                if (e) cudaEventDestroy(e);
         }
         delete w;
         all.erase(all.begin() + static_cast<long>(i));

@@ -157,6 +157,9 @@ _lib.detnet_adam_step.argtypes = [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_i
 _lib.detnet_model_param_count.restype = C.c_long
 _lib.detnet_model_param_count.argtypes = [_vp]
 _lib.detnet_train_grad.argtypes = [_vp, C.c_long, _vp, _vp, _vp, C.c_int, _vp, C.POINTER(_Eval)]
+_lib.detnet_train_grad_buckets.argtypes = [_vp, C.c_long, _vp, _vp, _vp, C.c_int, _vp,
+                                           C.POINTER(C.c_void_p), C.POINTER(C.c_long), C.c_int]
+_lib.detnet_stream_wait_event.argtypes = [_vp, _vp]
 _lib.detnet_train_apply.argtypes = [_vp, _vp, C.c_long, C.POINTER(_LossSpec), C.POINTER(_AdamCfg)]
 _lib.detnet_model_get_params.argtypes = [_vp, _vp]
 _lib.detnet_train_incremental.argtypes = [_vp, C.c_int, C.c_int, C.c_int, C.c_int,
@@ -422,6 +425,12 @@ class Context:
         return st.value
 
 
+def stream_wait_event(stream, event):
+    """Order `stream` (a cudaStream_t handle, e.g. torch's .cuda_stream) after
+    `event` (a bucket event of Model.train_grad_buckets)."""
+    _check(_lib.detnet_stream_wait_event(C.c_void_p(stream), C.c_void_p(event)))
+
+
 def rng_seed(seed, stream_id=0):
     return _lib.detnet_rng_seed(seed, stream_id)
 
@@ -581,6 +590,21 @@ class Model:
         if not want_eval:
             return None
         return BatchEval(ev.data_loss, ev.symbol_errors, ev.symbols, ev.flagged, ev.loss_sum)
+
+    def train_grad_buckets(self, n, H_ptr, y_ptr, x_ptr, raw_ptr, trainable_only=False,
+                           max_buckets=9):
+        """detnet_train_grad_buckets: enqueue the gradient with the raw sums
+        finalised bucket by bucket; returns [(event, lo, hi)] -- raw[lo:hi] is
+        final once the event completes (wait with stream_wait_event)."""
+        evs = (C.c_void_p * max_buckets)()
+        rng = (C.c_long * (2 * max_buckets))()
+        with _Ordered(self.ctx):
+            nb = _lib.detnet_train_grad_buckets(self._h, n, _addr(H_ptr), _addr(y_ptr),
+                                                _addr(x_ptr), int(trainable_only), _addr(raw_ptr),
+                                                evs, rng, max_buckets)
+        if nb < 0:
+            _check(-nb)
+        return [(evs[b], rng[2 * b], rng[2 * b + 1]) for b in range(nb)]
 
     def train_apply(self, raw_ptr, n_global, kind=0, lam=0.0, lam1=0.0, lam2=0.0, lr0=1e-4,
                     decay_factor=0.97, decay_step=1000, beta1=0.9, beta2=0.999, eps=1e-8):

@@ -261,3 +261,41 @@ def test_fp32_training_config5_shape_within_fp32_spread(oracle, ref, tc_forward)
           f"max {spread['max']:.3e}")
     assert max(finals) <= 1.5 * spread["max"], finals
     assert med <= spread["max"], finals
+
+
+@pytest.mark.parametrize("frozen", [0, 3])
+@pytest.mark.parametrize("n", [5000, 700])
+def test_gradient_buckets_match_train_grad(oracle, frozen, n):
+    """detnet_train_grad_buckets (raw sums finalised per reverse-sweep chunk,
+    each with its event, for a data-parallel caller to all-reduce while the
+    sweep runs) gives the bits of detnet_train_grad; the buckets tile the
+    trainable layers' slots and the loss slot exactly, top layers first."""
+    import torch
+    import paper_2003_09446_b200 as eng
+    from paper_2003_09446_b200.workload import xavier_params
+    K, N, L = 20, 30, 8
+    c = eng.Context(0)
+    st = torch.cuda.Stream()
+    torch.cuda.set_stream(st)
+    c.set_stream(st.cuda_stream)
+    m = c.model(K, N, 160, 40, xavier_params(K, L, seed=9), frozen_prefix=frozen)
+    H, y, x = (torch.from_numpy(a).cuda() for a in _inputs(oracle, n, K, N))
+    raw_a, raw_b = m.new_raw(), m.new_raw()
+    m.train_grad(n, H, y, x, raw_a, want_eval=False)
+    buckets = m.train_grad_buckets(n, H, y, x, raw_b)
+    side = torch.cuda.Stream()
+    for ev, lo, hi in buckets:  # the caller's pattern: wait per bucket on a side stream
+        eng.stream_wait_event(side.cuda_stream, ev)
+    st.wait_stream(side)
+    torch.cuda.synchronize()
+    assert torch.equal(raw_a, raw_b)
+    P = eng.record_size(K, 160, 40)
+    total = P * L
+    spans = [(lo, hi) for _, lo, hi in buckets]
+    assert spans[-1] == (total, total + 1) or spans == [(0, total + 1)]
+    covered = sorted(spans)
+    if len(spans) > 1:
+        assert covered[0][0] == frozen * P and covered[-1][1] == total + 1
+        assert all(a[1] == b[0] for a, b in zip(covered, covered[1:]))
+        assert spans[0][1] == total  # the top layers come first
+    torch.cuda.set_stream(torch.cuda.default_stream())

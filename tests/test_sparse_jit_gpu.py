@@ -151,3 +151,21 @@ def test_sparse_jit_disk_cache(tmp_path):
         files = [f for f in os.listdir(tmp_path / "jit") if f.endswith(".cubin")]
         assert len(files) == 1, files
     assert outs[0] == outs[1]
+
+
+@pytest.mark.parametrize("n,L", [(1, 1), (129, 1), (5, 3)])
+def test_sparse_jit_small_edges(ctx, oracle, n, L):
+    """A single sample, one partial tile, depth 1 (loss 0 at L = 1,
+    acceptance.cpp:326-339) on the generated kernel."""
+    K = 8
+    params, masks = _sparse_model(K, L, seed=31 + n)
+    H, y, x = _inputs(oracle, n, K=K, N=2 * K, seed=6)
+    m = ctx.model(K, 2 * K, 8 * K, 2 * K, params, masks=masks)
+    assert m.path_name == "sparse-jit-fp32"
+    ev, xh = m.batch_evaluate(H, y, x, want_xhat=True)
+    ref = oracle.evaluate(_omodel(params, K=K, N=2 * K, masks=masks), H.astype(np.float64),
+                          y.astype(np.float64), x.astype(np.float64), want_xhat=True)
+    assert ev.symbol_errors == int(ref["errors"].sum())
+    assert np.allclose(xh, ref["xhat"].reshape(xh.shape), rtol=1e-4, atol=1e-5)
+    if L == 1:
+        assert ev.data_loss == 0.0

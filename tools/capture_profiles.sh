@@ -10,7 +10,7 @@ mkdir -p $OUT
 #    then each config alone
 timeout 900 python bench.py > $OUT/bench_default.json 2> $OUT/bench_default.err
 for c in 1 2 3 4 5; do
-  timeout 600 python bench.py --config $c --steps 5 --warmup 3 > $OUT/bench_c$c.json 2> $OUT/bench_c$c.err
+  timeout 600 python bench.py --config $c --only > $OUT/bench_c$c.json 2> $OUT/bench_c$c.err
 done
 timeout 600 python bench.py --impl reference > $OUT/bench_ref.json 2> $OUT/bench_ref.err
 # 2. launch list of the default bench command (per-launch durations, cold, serialised)

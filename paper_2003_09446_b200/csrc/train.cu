@@ -292,7 +292,11 @@ int grad_raw(detnet_model *m, long n, const float *H, const float *y, const int8
         return fail(DETNET_ERR_CUDA, "training workspace allocation failed");
     if (int rc = ensure_ws(c, n, K)) return rc;
     if (int rc = reset_sing(c, c->stream)) return rc;
-    if (int rc = run_pre(m, c->stream, 0, n, n, H, y, x, /*exact=*/true)) return rc;
+    // FP32 mode: the one-pass K1 (FP32 Cholesky denominators, <= 1e-4 relative, median
+    // 6e-7; flagged samples fall back to the exact LU) -- each sample's gradient is
+    // weighted by 1/denom, far inside the FP32 noise of the sweep. The FP64 mode and
+    // detnet_ctx_set_exact_preprocess keep the reference's LU for every sample.
+    if (int rc = run_pre(m, c->stream, 0, n, n, H, y, x, /*exact=*/false)) return rc;
     TraceBufs tb{w.tr_in.as<float>(), w.tr_z.as<float>(), w.tr_u2.as<float>(), w.tr_xf.as<float>(),
                  ts};
     if (int rc = run_stack(m, c->stream, 0, tiles, n, 0, L, trainable_only, nullptr, nullptr,

@@ -195,3 +195,39 @@ def test_finite_differences_confirm_gpu_gradient(oracle, ref, kind, lam1, lam2, 
         a = g.ravel()[i]
         worst = max(worst, abs(a - num) / max(1.0, abs(a), abs(num)))
     assert worst < (1e-5 if fp64 else 1e-4), worst
+
+
+@pytest.mark.parametrize("fp64", [False, True])
+def test_perfect_estimates_give_zero_loss_and_zero_gradients(oracle, fp64):
+    """test_loss.cpp:64-68 and test_backward.cpp:25-52 on the engine: a network
+    whose every layer emits x_hat = x exactly (W2 = 0, b2 = 2 t x: the soft sign
+    saturates at the transmitted symbols, shared by the whole batch) has loss
+    exactly 0, no symbol errors and an exactly zero gradient in every tensor --
+    on every evaluation path, and through both training precisions."""
+    from paper_2003_09446_b200 import Context
+    from paper_2003_09446_b200.workload import record_layout, xavier_params
+    K, N, L, n = 20, 30, 5, 700
+    Z, V = 8 * K, 2 * K
+    sl, _ = record_layout(K, Z, V)
+    rs = np.random.default_rng(12)
+    xs = np.where(rs.random(K) < 0.5, -1.0, 1.0)
+    params = xavier_params(K, L, seed=9)
+    params[:, sl["W2"]] = 0.0
+    params[:, sl["b2"]] = 2.0 * 0.5 * xs  # t = 0.5
+    H = (rs.standard_normal((n, N, K)) / np.sqrt(N)).astype(np.float32)
+    x = np.tile(xs.astype(np.int8), (n, 1))
+    y = (np.einsum("sij,j->si", H.astype(np.float64), xs) +
+         0.1 * rs.standard_normal((n, N))).astype(np.float32)
+    for path in (1, 2, 0):
+        ctx = Context(0, path=path)
+        ev, xh = ctx.model(K, N, Z, V, params).batch_evaluate(H, y, x, want_xhat=True)
+        assert ev.data_loss == 0.0 and ev.loss_sum == 0.0, (path, ev.data_loss)
+        assert ev.symbol_errors == 0 and ev.flagged == 0
+        assert np.array_equal(xh, np.broadcast_to(xs.astype(np.float32), xh.shape))
+        ctx.close()
+    ctx = Context(0)
+    ctx.set_train_precision(fp64)
+    ev, g = ctx.model(K, N, Z, V, params).batch_gradient(H, y, x, kind=0)
+    assert ev.data_loss == 0.0 and ev.symbol_errors == 0
+    assert not g.any(), np.abs(g).max()
+    ctx.close()

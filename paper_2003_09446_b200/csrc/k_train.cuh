@@ -695,50 +695,83 @@ struct ObjArgs {
     int K, Z, V, L;
     int kind;
     double lam, lam1, lam2;
-    double *part;           // [L][2]: groups (g1 + g2) + g3, elems (e1 + e2) + e3
+    double *part;           // [L][4]: groups (g1 + g2) + g3, then e1, e2, e3 (masked_l1 of W1, W2, W3)
 };
 
-__global__ void k_reg_layers(ObjArgs a) {
+// One CTA per (layer, part = group sums | masked_l1 of W1 | W2 | W3): the terms are staged in shared memory by the whole
+// CTA (coalesced loads, the per-element |w| m products in parallel) and folded by
+// thread 0 in the reference's order, one chunk behind the loads -- the same
+// dadd chain as a single thread walking global memory (bit-identical value),
+// without a dependent L2 round trip per term.
+constexpr int REG_THREADS = 256, REG_CHUNK = 2048;
+
+__global__ void __launch_bounds__(REG_THREADS) k_reg_layers(ObjArgs a) {
+    __shared__ double buf[2][REG_CHUNK];
     const int K = a.K, Z = a.Z, V = a.V, IN = 3 * K + V;
     const long P = static_cast<long>(Z) * IN + Z + static_cast<long>(K) * Z + K +
                    static_cast<long>(V) * Z + V + 1;
     const int ng = IN + 1 + 2 * (Z + 1);
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= 2 * a.L) return;
-    const int l = idx >> 1;
-    if ((idx & 1) == 0) { // group_norm_sum of W1, W2, W3 (with their bias groups)
+    const int idx = blockIdx.x;
+    if (idx >= 4 * a.L) return;
+    const int l = idx >> 2;
+    const int tid = threadIdx.x;
+    if ((idx & 3) == 0) { // group_norm_sum of W1, W2, W3 (with their bias groups)
         double g[3] = {0.0, 0.0, 0.0};
-        if (a.kind == 2) {
+        if (a.kind == 2) { // block-uniform
             const double *cn = a.colnorm + static_cast<long>(l) * ng;
-            const int cols[3] = {IN, Z, Z};
-            int off = 0;
-            for (int m = 0; m < 3; ++m) {
-                double acc = 0.0;
-                for (int j = 0; j < cols[m]; ++j) acc = dadd(acc, cn[off + j]);
-                g[m] = dadd(acc, cn[off + cols[m]]);
-                off += cols[m] + 1;
+            const bool fits = ng <= 2 * REG_CHUNK; // else thread 0 walks global memory
+            double *stage = &buf[0][0];
+            if (fits)
+                for (int j = tid; j < ng; j += REG_THREADS) stage[j] = cn[j];
+            __syncthreads();
+            const double *flat = fits ? stage : cn;
+            if (tid == 0) {
+                const int cols[3] = {IN, Z, Z};
+                int off = 0;
+                for (int m = 0; m < 3; ++m) {
+                    double acc = 0.0;
+                    for (int j = 0; j < cols[m]; ++j) acc = dadd(acc, flat[off + j]);
+                    g[m] = dadd(acc, flat[off + cols[m]]);
+                    off += cols[m] + 1;
+                }
             }
         }
-        a.part[2 * l] = dadd(dadd(g[0], g[1]), g[2]);
-    } else { // masked_l1 of W1, W2, W3
-        double e[3] = {0.0, 0.0, 0.0};
-        if (a.kind == 1 || (a.kind == 2 && a.lam2 != 0.0)) {
+        if (tid == 0) a.part[4 * l] = dadd(dadd(g[0], g[1]), g[2]);
+    } else { // masked_l1 of W1, W2 or W3: one CTA (one sequential fold) per matrix
+        const int m = (idx & 3) - 1;
+        double em = 0.0;
+        if (a.kind == 1 || (a.kind == 2 && a.lam2 != 0.0)) { // block-uniform
             const double *p = a.params + static_cast<long>(l) * P;
             const double *mk = a.masks ? a.masks + static_cast<long>(l) * P : nullptr;
             const long oW[3] = {0, static_cast<long>(Z) * IN + Z,
                                 static_cast<long>(Z) * IN + Z + static_cast<long>(K) * Z + K};
             const long cnt[3] = {static_cast<long>(Z) * IN, static_cast<long>(K) * Z,
                                  static_cast<long>(V) * Z};
-            for (int m = 0; m < 3; ++m) {
+            {
                 double acc = 0.0;
-                for (long q = 0; q < cnt[m]; ++q) {
-                    const long ee = oW[m] + q;
-                    acc = dadd(acc, dmul(fabs(p[ee]), mk ? mk[ee] : 1.0));
+                const long nch = (cnt[m] + REG_CHUNK - 1) / REG_CHUNK;
+                for (long c = 0; c <= nch; ++c) {
+                    if (c < nch) { // stage chunk c (every thread; thread 0 first, then it folds)
+                        double *dst = buf[c & 1];
+                        const long q0 = c * REG_CHUNK;
+                        const long qn = cnt[m] - q0 < REG_CHUNK ? cnt[m] - q0 : REG_CHUNK;
+                        for (long q = tid; q < qn; q += REG_THREADS) {
+                            const long ee = oW[m] + q0 + q;
+                            dst[q] = dmul(fabs(p[ee]), mk ? mk[ee] : 1.0);
+                        }
+                    }
+                    if (c > 0 && tid == 0) { // fold chunk c - 1 in element order
+                        const double *src = buf[(c - 1) & 1];
+                        const long q0 = (c - 1) * REG_CHUNK;
+                        const long qn = cnt[m] - q0 < REG_CHUNK ? cnt[m] - q0 : REG_CHUNK;
+                        for (long q = 0; q < qn; ++q) acc = dadd(acc, src[q]);
+                    }
+                    __syncthreads();
                 }
-                e[m] = acc;
+                em = acc;
             }
         }
-        a.part[2 * l + 1] = dadd(dadd(e[0], e[1]), e[2]);
+        if (tid == 0) a.part[4 * l + 1 + m] = em;
     }
 }
 
@@ -748,13 +781,14 @@ __global__ void k_objective(ObjArgs a, const double *loss_sum, double n_global, 
     double reg = 0.0;
     if (a.kind == 1) {
         double acc = 0.0;
-        for (int l = 0; l < a.L; ++l) acc = dadd(acc, a.part[2 * l + 1]);
+        for (int l = 0; l < a.L; ++l)
+            acc = dadd(acc, dadd(dadd(a.part[4 * l + 1], a.part[4 * l + 2]), a.part[4 * l + 3]));
         reg = dmul(a.lam, acc);
     } else if (a.kind == 2) {
         double groups = 0.0, elems = 0.0;
         for (int l = 0; l < a.L; ++l) {
-            groups = dadd(groups, a.part[2 * l]);
-            elems = dadd(elems, a.part[2 * l + 1]);
+            groups = dadd(groups, a.part[4 * l]);
+            elems = dadd(elems, dadd(dadd(a.part[4 * l + 1], a.part[4 * l + 2]), a.part[4 * l + 3]));
         }
         reg = dadd(dmul(a.lam1, groups), dmul(a.lam2, elems));
     }

@@ -725,7 +725,7 @@ int detnet_train_apply(detnet_model *m, const double *raw_dev, long n_global,
     // objective = data_loss + regularizer(params) before the update
     // (training.cpp:65-70); a non-finite one halts the run on the device
     const int IN = 3 * m->K + m->V, ng = IN + 1 + 2 * (m->Z + 1);
-    if (w.objpart.ensure(sizeof(double) * 2 * m->L) || w.colnorm.ensure(sizeof(double) * m->L * ng))
+    if (w.objpart.ensure(sizeof(double) * 4 * m->L) || w.colnorm.ensure(sizeof(double) * m->L * ng))
         return fail(DETNET_ERR_CUDA, "alloc objective");
     ObjArgs oa{m->tparams.as<double>(), m->has_masks ? m->tmasks.as<double>() : nullptr,
                w.colnorm.as<double>(), m->K, m->Z, m->V, m->L, spec ? spec->kind : 0,
@@ -739,7 +739,7 @@ int detnet_train_apply(detnet_model *m, const double *raw_dev, long n_global,
                 m->tparams.as<double>(), m->tmasks.as<double>(), m->K, m->Z, m->V, m->L, 0,
                 w.colnorm.as<double>());
         }
-        if (oa.kind != 0) k_reg_layers<<<(2 * m->L + 63) / 64, 64, 0, c->stream>>>(oa);
+        if (oa.kind != 0) k_reg_layers<<<4 * m->L, REG_THREADS, 0, c->stream>>>(oa);
         k_objective<<<1, 1, 0, c->stream>>>(oa, raw_dev + total, static_cast<double>(n_global),
                                             static_cast<long long>(m->adam_step),
                                             m->tstatus.as<double>());

@@ -575,6 +575,23 @@ int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, 
         }
         return check_launch();
     }
+    // A masked model whose images were compacted at upload (configs 3/4) and that is
+    // now being trained on the device: switch it to the dense ZH = 160 images of
+    // W (.) M, which the device repacks after every Adam step (k_pack_tc160 /
+    // k_pack_h16_160 read the masks). The compacted images would need a host repack
+    // per weight version and have no training-trace variant, which put the training
+    // forward of such models on the CUDA-core kernel (0.76 vs 0.22 ms at batch 5000).
+    // A later detnet_model_update / detnet_model_prune compacts again.
+    if (trace && c->train_tc && c->path != 1 && c->path != 3 && m->tc.ready && m->tc.zh != 160 &&
+        m->K == 20 && m->Z == 160 && m->V == 40 && m->train_ready) {
+        LaunchScope ls(c, DETNET_K_OTHER, st);
+        if (int rc = tc_pack_dense_device(m->tc, m->K, m->Z, m->V, m->L, m->tparams.as<double>(),
+                                          m->tmasks.as<double>(), st))
+            return rc;
+        m->tc_stale = false;
+        m->tc_dev_dirty = false;
+        ++m->version; // captured evaluation graphs hold the old image pointers
+    }
     // the training forward (trace) on the SIMT path neither needs nor
     // refreshes the tensor-core images (they are repacked on first use)
     const bool simt_trace = trace && !(c->train_tc && m->tc.zh == 160);

@@ -299,3 +299,45 @@ def test_gradient_buckets_match_train_grad(oracle, frozen, n):
         assert all(a[1] == b[0] for a, b in zip(covered, covered[1:]))
         assert spans[0][1] == total  # the top layers come first
     torch.cuda.set_stream(torch.cuda.default_stream())
+
+
+def test_group_masked_model_trains_on_dense_device_images(oracle):
+    """A group-pruned model (configs 3/4: compacted tcgen05 images at upload)
+    that is then trained on the device switches to the dense images of W (.) M,
+    repacked on the device after every Adam step: its gradient matches the
+    oracle's masked batch_gradient (kernels.cpp:160-200, model.cpp:58-80), and
+    evaluating it after training steps agrees with a freshly uploaded
+    (compacted) model of the same weights."""
+    import torch
+    from paper_2003_09446_b200 import Context
+    from paper_2003_09446_b200 import workload as wl
+    K, N, L, n = 20, 30, 6, 700
+    Z, V = 8 * K, 2 * K
+    params = wl.xavier_params(K, L, seed=5)
+    masks = wl.group_masks(K, L, seed=31)
+    H, y, x = _inputs(oracle, n, K, N)
+    c = Context(0)
+    m = c.model(K, N, Z, V, params, masks=masks)
+    before = m.batch_evaluate(H, y, x)
+    ev, g = m.batch_gradient(H, y, x, 2, 0.0, 1e-3, 0.0)
+    om = OModel(K, N, Z, V, L, params, masks=masks)
+    ref = oracle.batch_gradient(om, H.astype(np.float64), y.astype(np.float64),
+                                x.astype(np.float64), 2, 0.0, 1e-3, 0.0)
+    scale = np.max(np.abs(ref["grads"]))
+    assert np.max(np.abs(g - ref["grads"])) <= 2e-4 * scale
+    assert np.all(g[masks == 0.0] == 0.0)
+    assert abs(ev.data_loss - ref["data_loss"]) <= 1e-4 * abs(ref["data_loss"])
+    assert abs(ev.data_loss - before.data_loss) <= 1e-5 * abs(before.data_loss)
+    Hd, yd, xd = (torch.tensor(a, device="cuda") for a in (H, y, x))
+    raw = m.new_raw()
+    for _ in range(3):
+        m.train_grad(n, Hd, yd, xd, raw, want_eval=False)
+        m.train_apply(raw, n, kind=2, lam1=1e-3, lr0=1e-3)
+    p = m.get_params()
+    assert np.all(p[masks == 0.0] == params[masks == 0.0])
+    after = m.batch_evaluate(H, y, x)                                   # dense device images
+    fresh = c.model(K, N, Z, V, p, masks=masks).batch_evaluate(H, y, x)  # compacted host pack
+    assert abs(after.symbol_errors - fresh.symbol_errors) <= 1
+    assert abs(after.data_loss - fresh.data_loss) <= 1e-5 * abs(fresh.data_loss)
+    assert after.data_loss < before.data_loss
+    c.close()

@@ -433,7 +433,7 @@ bool use_jit(const detnet_model *m) {
     if (path != 3 || std::getenv("DETNET_NO_JIT")) return false;
     // weights changed on the device since pack time (training, pruning in
     // progress) bump the version: the kernel no longer matches them
-    if (m->tc_stale || m->jit_src_version != m->version) return false;
+    if (m->jit_src_version != m->version) return false; // (a device prune re-records the source)
     if (m->jit_params.empty()) return false;
     return true;
 }
@@ -582,8 +582,9 @@ int run_stack(detnet_model *m, cudaStream_t st, long t0, long nt, long n_local, 
     // per weight version and have no training-trace variant, which put the training
     // forward of such models on the CUDA-core kernel (0.76 vs 0.22 ms at batch 5000).
     // A later detnet_model_update / detnet_model_prune compacts again.
-    if (trace && c->train_tc && c->path != 1 && c->path != 3 && m->tc.ready && m->tc.zh != 160 &&
-        m->K == 20 && m->Z == 160 && m->V == 40 && m->train_ready) {
+    if (trace && c->train_tc && c->path != 1 && c->path != 3 && m->tc.ready &&
+        (m->tc.zh != 160 || m->tc_stale) && m->K == 20 && m->Z == 160 && m->V == 40 &&
+        m->train_ready) { // tc_stale: pruned on the device since the images were packed
         LaunchScope ls(c, DETNET_K_OTHER, st);
         if (int rc = tc_pack_dense_device(m->tc, m->K, m->Z, m->V, m->L, m->tparams.as<double>(),
                                           m->tmasks.as<double>(), st))

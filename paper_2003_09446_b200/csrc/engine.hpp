@@ -333,6 +333,7 @@ struct TraceBufs {
 };
 int ensure_ws(detnet_ctx *c, long n, int K);
 int upload_model(detnet_model *m, const detnet_model_desc *d);
+void prepare_jit(detnet_model *m, const double *params, const double *masks);
 int reset_sing(detnet_ctx *c, cudaStream_t st);
 // exact: the reference's FP64 LU for every sample (training: each sample's
 // gradient is weighted by 1 / denom, so it gets the reference's denominators)

@@ -832,12 +832,31 @@ int detnet_model_prune(detnet_model *m, int kind, double eta, double eta1, doubl
     CK(cudaStreamSynchronize(m->ctx->stream));
     CK(cudaMemcpy(params.data(), m->tparams.p, sizeof(double) * total, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(masks.data(), m->tmasks.p, sizeof(double) * total, cudaMemcpyDeviceToHost));
-    const int64_t step = m->adam_step;
-    detnet_model_desc d{m->K, m->N, m->Z, m->V, m->L, m->frozen, params.data(), masks.data()};
-    if (int rc = upload_model(m, &d)) return rc;
+    // The device master copy already holds the pruned weights and masks: the SIMT
+    // records are repacked from it on the device; the tcgen05 images are marked
+    // stale, so the next tensor-core evaluation compacts them from the host copy
+    // (refresh_tc) while a training step switches to the dense device-packed images
+    // instead (run_stack) -- the ~10-20 ms of host packing are paid only if and
+    // when a compacted evaluation follows, not by every prune.
+    m->params_host = std::move(params);
+    m->masks_host = std::move(masks);
+    m->has_masks = true;
+    if (int rc = pack_simt_device(m)) return rc;
+    m->tc_stale = true;
+    m->tc_dev_dirty = false;
+    m->sparse_ready = false;
+    if (std::getenv("DETNET_SPARSE_CSR")) { // the table-driven stream is built only on request
+        detnet_model_desc d{m->K, m->N, m->Z, m->V, m->L, m->frozen, m->params_host.data(),
+                            m->masks_host.data()};
+        const int64_t step = m->adam_step;
+        if (int rc = upload_model(m, &d)) return rc;
+        m->train_ready = true; // device params / masks already hold exactly these values
+        m->adam_step = step;
+    } else {
+        prepare_jit(m, m->params_host.data(), m->masks_host.data());
+    }
     m->replicas_stale = !m->replicas.empty();
-    m->train_ready = true; // device params / masks already hold exactly these values
-    m->adam_step = step;
+    CK(cudaStreamSynchronize(m->ctx->stream));
     drain_times(m->ctx);
     return 0;
 }

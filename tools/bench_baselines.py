@@ -19,11 +19,16 @@ from oracle.oracle import Oracle, RefLib  # noqa: E402
 
 
 def timed(f, reps):
+    """Median of per-call wall times (a few ms each: a mean over 5 calls moved
+    4x between runs on a busy host), after one warm-up call."""
     f()
-    t0 = time.perf_counter()
+    ts = []
     for _ in range(reps):
+        t0 = time.perf_counter()
         out = f()
-    return (time.perf_counter() - t0) / reps, out
+        ts.append(time.perf_counter() - t0)
+    ts.sort()
+    return ts[len(ts) // 2], out
 
 
 def main():
@@ -31,8 +36,8 @@ def main():
     cases = [("zf", 0, 20, 30, 1 << 16), ("ml", 1, 8, 16, 1 << 14), ("ml", 1, 12, 16, 1 << 11)]
     for name, kind, K, N, n in cases:
         H, x, y, _ = orc.generate_batch(orc.rng(3, 0), N, K, n, 0.0, 12.0)
-        tg, (eg, sg) = timed(lambda: ctx.baseline_errors(kind, H, y, x), 5)
-        tr, (st, er, sr) = timed(lambda: ref.baseline_errors(kind, H, y, x), 2)
+        tg, (eg, sg) = timed(lambda: ctx.baseline_errors(kind, H, y, x), 21)
+        tr, (st, er, sr) = timed(lambda: ref.baseline_errors(kind, H, y, x), 3)
         assert st == 0 and (eg, sg) == (er, sr), (eg, er)
         print(json.dumps({"baseline": name, "K": K, "N": N, "samples": n,
                           "b200_detections_per_s": n / tg, "reference_detections_per_s": n / tr,

@@ -29,6 +29,7 @@
 #ifndef DETNET_B200_H
 #define DETNET_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -66,6 +67,15 @@ void detnet_ctx_destroy(detnet_ctx *ctx);
 int detnet_ctx_create_group(const int *devices, int count, detnet_ctx **out);
 int detnet_ctx_group_size(const detnet_ctx *ctx);
 const char *detnet_last_error(void);
+
+/* Page-locked host memory for sample / output buffers. detnet_batch_evaluate,
+ * detnet_batch_gradient and detnet_generate_host move pinned buffers at the full
+ * PCIe rate, asynchronously and overlapped with compute; pageable buffers are
+ * staged by the driver at a fraction of it. What the reference's callers do with
+ * their std::vector<ChannelSample> batches (kernels.hpp:34-47) the seam does by
+ * converting into buffers from here. bytes = 0 returns a null pointer. */
+int detnet_host_alloc(void **ptr, size_t bytes);
+int detnet_host_free(void *ptr);
 /* Kernel-path selection: 0 auto (tcgen05 split-FP16 where compiled, with
  * 3xTF32 recompute of out-of-range tiles; else 3xTF32; else SIMT), 1 SIMT
  * FP32, 2 tcgen05 3xTF32 only, 3 sparse (the model-specialised kernel,

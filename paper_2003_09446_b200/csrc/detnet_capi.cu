@@ -778,6 +778,25 @@ extern "C" {
 
 const char *detnet_last_error(void) { return g_err.c_str(); }
 
+int detnet_host_alloc(void **ptr, size_t bytes) {
+    if (!ptr) return fail(DETNET_ERR_CONTRACT, "null argument");
+    *ptr = nullptr;
+    if (bytes == 0) return 0;
+    if (cudaMallocHost(ptr, bytes) != cudaSuccess) {
+        *ptr = nullptr;
+        return fail(DETNET_ERR_CUDA, "pinned host allocation of %zu bytes failed: %s", bytes,
+                    cudaGetErrorString(cudaGetLastError()));
+    }
+    return 0;
+}
+
+int detnet_host_free(void *ptr) {
+    if (!ptr) return 0;
+    if (cudaFreeHost(ptr) != cudaSuccess)
+        return fail(DETNET_ERR_CUDA, "cudaFreeHost: %s", cudaGetErrorString(cudaGetLastError()));
+    return 0;
+}
+
 long detnet_record_size(int n_tx, int z_dim, int v_dim) { return record_size(n_tx, z_dim, v_dim); }
 
 int detnet_ctx_create(int device, detnet_ctx **out) {

@@ -157,18 +157,40 @@ detnet_model *model_for(const ModelParams &p) {
     return c.m;
 }
 
+// FP32 staging of a batch in page-locked memory (detnet_host_alloc): the engine's
+// chunked copies then run asynchronously at the PCIe rate instead of being staged
+// by the driver from pageable vectors. Grow-only, owned by the seam, reused by
+// every call (calls are serialised by the engine mutex).
+struct PinnedBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    void *ensure(size_t bytes) {
+        if (bytes > cap) {
+            if (p) detnet_host_free(p);
+            p = nullptr;
+            cap = 0;
+            check(detnet_host_alloc(&p, bytes + bytes / 4));
+            cap = bytes + bytes / 4;
+        }
+        return p;
+    }
+    // static lifetime: released with the process (a destructor would run after
+    // the CUDA runtime has begun unloading)
+};
+
 struct Packed {
-    std::vector<float> H, y;
-    std::vector<int8_t> x;
+    float *H, *y;
+    int8_t *x;
 };
 
 Packed pack_samples(const ModelParams &p, std::span<const ChannelSample> batch) {
-    Packed s;
+    static PinnedBuf bH, by, bx; // under engine().mu
     const int N = p.n_rx, K = p.n_tx;
     const size_t n = batch.size();
-    s.H.resize(n * N * K);
-    s.y.resize(n * N);
-    s.x.resize(n * K);
+    float *H = static_cast<float *>(bH.ensure(n * N * K * sizeof(float)));
+    float *y = static_cast<float *>(by.ensure(n * N * sizeof(float)));
+    int8_t *x = static_cast<int8_t *>(bx.ensure(n * K));
+    Packed s{H, y, x};
     for (size_t i = 0; i < n; ++i) {
         const ChannelSample &c = batch[i];
         if (c.H.rows != N || c.H.cols != K || static_cast<int>(c.y.size()) != N ||
@@ -178,9 +200,9 @@ Packed pack_samples(const ModelParams &p, std::span<const ChannelSample> batch) 
 #pragma omp parallel for schedule(static)
     for (long i = 0; i < static_cast<long>(n); ++i) {
         const ChannelSample &c = batch[i];
-        for (int j = 0; j < N * K; ++j) s.H[i * N * K + j] = static_cast<float>(c.H.data[j]);
-        for (int j = 0; j < N; ++j) s.y[i * N + j] = static_cast<float>(c.y[j]);
-        for (int j = 0; j < K; ++j) s.x[i * K + j] = c.x[j] >= 0.0 ? 1 : -1;
+        for (int j = 0; j < N * K; ++j) H[i * N * K + j] = static_cast<float>(c.H.data[j]);
+        for (int j = 0; j < N; ++j) y[i * N + j] = static_cast<float>(c.y[j]);
+        for (int j = 0; j < K; ++j) x[i * K + j] = c.x[j] >= 0.0 ? 1 : -1;
     }
     return s;
 }
@@ -237,8 +259,8 @@ BatchEval batch_evaluate(const ModelParams &params, std::span<const ChannelSampl
     if (batch.empty()) return BatchEval{};
     Packed s = pack_samples(params, batch);
     detnet_eval ev{};
-    check(detnet_batch_evaluate(m, static_cast<long>(batch.size()), s.H.data(), s.y.data(),
-                                s.x.data(), loss_layers == LossLayers::trainable_only, nullptr, &ev));
+    check(detnet_batch_evaluate(m, static_cast<long>(batch.size()), s.H, s.y,
+                                s.x, loss_layers == LossLayers::trainable_only, nullptr, &ev));
     return to_eval(ev);
 }
 
@@ -254,8 +276,8 @@ BatchEval batch_gradient(const ModelParams &params, std::span<const ChannelSampl
     detnet_loss_spec ls{spec.kind == LossKind::plain ? 0 : (spec.kind == LossKind::element_l1 ? 1 : 2),
                         spec.lambda, spec.lambda1, spec.lambda2};
     detnet_eval ev{};
-    check(detnet_batch_gradient(m, static_cast<long>(batch.size()), s.H.data(), s.y.data(),
-                                s.x.data(), &ls, loss_layers == LossLayers::trainable_only,
+    check(detnet_batch_gradient(m, static_cast<long>(batch.size()), s.H, s.y,
+                                s.x, &ls, loss_layers == LossLayers::trainable_only,
                                 g.data(), &ev));
     grads.set_zero();
     for (int l = params.frozen_prefix; l < params.depth(); ++l) {

@@ -106,3 +106,41 @@ def test_training_steps_without_waits(setup):
             m.train_apply(raw, n, kind=2, lam1=1e-4, lr0=1e-3)
         out.append(m.get_params())
     assert np.array_equal(out[0], out[1])
+
+
+def test_pinned_host_buffers_from_the_c_abi():
+    """detnet_host_alloc / detnet_host_free: page-locked sample buffers give the
+    same BatchEval as pageable ones (the seam stages its FP32 batches there)."""
+    import ctypes as C
+    import numpy as np
+    from paper_2003_09446_b200 import Context, detnet as d
+    from paper_2003_09446_b200.workload import xavier_params
+    K, N, L, n = 20, 30, 4, 3000
+    rs = np.random.default_rng(5)
+    H = (rs.standard_normal((n, N, K)) / np.sqrt(N)).astype(np.float32)
+    x = np.where(rs.random((n, K)) < 0.5, -1, 1).astype(np.int8)
+    y = (np.einsum("sij,sj->si", H, x.astype(np.float32)) +
+         0.2 * rs.standard_normal((n, N)).astype(np.float32)).astype(np.float32)
+    lib = d._lib
+    lib.detnet_host_alloc.argtypes = [C.POINTER(C.c_void_p), C.c_size_t]
+    lib.detnet_host_free.argtypes = [C.c_void_p]
+    ptrs = []
+    for a in (H, y, x):
+        p = C.c_void_p()
+        assert lib.detnet_host_alloc(C.byref(p), a.nbytes) == 0 and p.value
+        C.memmove(p.value, a.ctypes.data, a.nbytes)
+        ptrs.append(p)
+    z = C.c_void_p(1)
+    assert lib.detnet_host_alloc(C.byref(z), 0) == 0 and not z.value
+    ctx = Context(0)
+    m = ctx.model(K, N, 8 * K, 2 * K, xavier_params(K, L, seed=9))
+    want = m.batch_evaluate(H, y, x)
+    ev = d._Eval()
+    d._check(lib.detnet_batch_evaluate(m._h, n, ptrs[0].value, ptrs[1].value, ptrs[2].value, 0, None,
+                                       C.byref(ev)))
+    assert (ev.data_loss, ev.symbol_errors, ev.flagged) == (want.data_loss, want.symbol_errors,
+                                                            want.flagged)
+    for p in ptrs:
+        assert lib.detnet_host_free(p) == 0
+    assert lib.detnet_host_free(None) == 0
+    ctx.close()
